@@ -1,0 +1,122 @@
+"""Generate the golden fixtures that pin oracle/ringseq_np.py to the reference.
+
+Run in the build container, where the reference is importable:
+
+    RINGSEQ_SRC=/root/reference/pkg/src python tests/golden/make_golden.py
+
+It imports the UNMODIFIED reference package ``ringseq`` and records its
+outputs for seeded inputs drawn exactly as the reference tests draw them
+(make_rng(seed).standard_normal for q, k, v, grad in that order --
+tests/test_acceptance.py:59-67).  Inputs are not stored: they are
+regenerated from the seed (PCG64 is platform-stable) on whatever host runs
+the tests.  Small cases store float64 results for bitwise pins; the two
+"mid" cases use bf16-rounded inputs at tensor-core-friendly shapes and store
+float32 results, so the same file also serves the GPU parity tests.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parent.parent))
+sys.path.insert(0, os.environ.get("RINGSEQ_SRC", "/root/reference/pkg/src"))
+
+import ringseq  # noqa: E402  (the reference itself)
+from oracle.ringseq_np import bf16_round  # noqa: E402
+
+RSA_SMALL = [  # (B, Z, L, A, N, seed)
+    (1, 2, 8, 4, 1, 7),
+    (1, 2, 12, 4, 3, 3),
+    (2, 2, 16, 4, 4, 104),
+    (1, 1, 8, 2, 2, 4),
+    (2, 1, 8, 2, 4, 5),
+    (2, 3, 40, 5, 4, 11),
+    (1, 2, 24, 3, 3, 9),
+]
+RSA_MID = [(1, 2, 256, 64, 2, 21), (1, 1, 512, 64, 4, 22)]
+SPARSE_SMALL = [  # (B, Z, L, A, K, N, seed)
+    (1, 2, 16, 2, 4, 1, 41),
+    (1, 2, 16, 2, 4, 2, 42),
+    (1, 2, 16, 2, 4, 4, 44),
+    (2, 3, 40, 5, 7, 4, 51),
+]
+SPARSE_MID = [(1, 2, 256, 64, 64, 2, 61)]
+
+
+def draw(shape, seed, n_tensors, rounded):
+    rng = ringseq.make_rng(seed)
+    out = [rng.standard_normal(shape) for _ in range(n_tensors)]
+    if rounded:
+        out = [bf16_round(x) for x in out]
+    return out, rng
+
+
+def rsa_case(b, z, seq, a, n, seed, rounded):
+    cfg = ringseq.AttentionConfig(batch_size=b, seq_len=seq, hidden_size=z * a,
+                                  num_heads=z, head_size=a, num_devices=n)
+    (q, k, v, g), _ = draw((b, z, seq, a), seed, 4, rounded)
+    split = lambda x: [np.ascontiguousarray(c) for c in np.split(x, n, axis=-2)]  # noqa: E731
+    fwd = ringseq.ring_attention_forward(split(q), split(k), split(v), cfg)
+    bwd = ringseq.ring_attention_backward(split(q), split(k), split(v), fwd.probs, split(g), cfg)
+    return {
+        "out": ringseq.gather_sequence(fwd.outputs),
+        "probs": np.stack(fwd.probs),
+        "dq": ringseq.gather_sequence(bwd.grad_q),
+        "dk": ringseq.gather_sequence(bwd.grad_k),
+        "dv": ringseq.gather_sequence(bwd.grad_v),
+        "ledger_fwd_ring": np.array([t.ring_p2p_elements for t in fwd.ledger.devices]),
+        "ledger_bwd_ring": np.array([t.ring_p2p_elements for t in bwd.ledger.devices]),
+        "ledger_bwd_ar": np.array([int(t.allreduce_elements) for t in bwd.ledger.devices]),
+    }
+
+
+def sparse_case(b, z, seq, a, kp, n, seed, rounded):
+    base = ringseq.AttentionConfig(batch_size=b, seq_len=seq, hidden_size=z * a,
+                                   num_heads=z, head_size=a, num_devices=n)
+    cfg = ringseq.SparseAttentionConfig(base=base, proj_dim=kp)
+    (q, k, v), rng = draw((b, z, seq, a), seed, 3, rounded)
+    w = ringseq.random_sparse_weights(seq, kp, rng)
+    if rounded:
+        w = ringseq.SparseWeights(bf16_round(w.key_proj), bf16_round(w.value_proj))
+    split = lambda x: [np.ascontiguousarray(c) for c in np.split(x, n, axis=-2)]  # noqa: E731
+    fwd = ringseq.sparse_ring_attention_forward(split(q), split(k), split(v), w, cfg)
+    return {
+        "out": ringseq.gather_sequence(fwd.outputs),
+        "ledger_ring": np.array([t.ring_p2p_elements for t in fwd.ledger.devices]),
+    }
+
+
+def main():
+    arrays = {}
+    for case in RSA_SMALL:
+        res = rsa_case(*case, rounded=False)
+        for key, val in res.items():
+            arrays["rsa_small/%s/%s" % ("_".join(map(str, case)), key)] = val
+    for case in RSA_MID:
+        res = rsa_case(*case, rounded=True)
+        for key, val in res.items():
+            if key == "probs" and case[2] > 256:
+                continue  # keep the fixture small; larger panels are checked against the oracle
+            arrays["rsa_mid/%s/%s" % ("_".join(map(str, case)), key)] = (
+                val.astype(np.float32) if val.dtype == np.float64 else val)
+    for case in SPARSE_SMALL:
+        res = sparse_case(*case, rounded=False)
+        for key, val in res.items():
+            arrays["sparse_small/%s/%s" % ("_".join(map(str, case)), key)] = val
+    for case in SPARSE_MID:
+        res = sparse_case(*case, rounded=True)
+        for key, val in res.items():
+            arrays["sparse_mid/%s/%s" % ("_".join(map(str, case)), key)] = (
+                val.astype(np.float32) if val.dtype == np.float64 else val)
+    out = HERE / "ringseq_golden.npz"
+    np.savez_compressed(out, **arrays)
+    print(f"wrote {out} ({out.stat().st_size} bytes, {len(arrays)} arrays)")
+
+
+if __name__ == "__main__":
+    main()
