@@ -1,0 +1,156 @@
+/*
+ * rsa_b200.h -- C ABI of librsa_b200.so, the sm_100a kernels behind the
+ * Ring Self-Attention (RSA) drop-in boundary.
+ *
+ * The reference (arXiv 2105.13120's `ringseq` package, a float64 NumPy
+ * simulator) has no FFI layer: its boundary is the Python API of
+ * ringseq.ring_attention / ringseq.sparse_attention / ringseq.tensor_ops.
+ * Each entry point below replaces the arithmetic of one reference function
+ * (cited per function); the host package paper_2105_13120_b200 binds them
+ * with ctypes and keeps the reference's Python names and signatures.
+ *
+ * Conventions
+ *   - Plain C types only.  Device buffers are raw pointers owned by the
+ *     caller (the torch caching allocator); nothing is allocated here.
+ *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous
+ *     on it and returns an int status (RSA_OK or an RSA_ERR_* code); no C++
+ *     exception crosses the ABI.  rsa_last_error() describes the last
+ *     failure on the calling thread.
+ *   - Element strides are in elements (not bytes); the innermost dimension
+ *     is always contiguous.
+ *   - Per-head tensors are addressed as [rank][b][z][row][col] through an
+ *     rsa_view, so the same kernels serve (a) N logical ranks resident in one
+ *     GPU's HBM and (b) one rank per GPU with ring-delivered chunks.
+ */
+#ifndef RSA_B200_H
+#define RSA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RSA_ABI_VERSION 1
+
+enum rsa_status {
+  RSA_OK = 0,
+  RSA_ERR_INVALID = 1,     /* bad argument (maps to ShapeError / ConfigError) */
+  RSA_ERR_UNSUPPORTED = 2, /* layout the requested kernel cannot tile         */
+  RSA_ERR_CUDA = 3,        /* CUDA runtime / launch failure                    */
+  RSA_ERR_NUMERIC = 4      /* non-finite input (maps to NumericError)          */
+};
+
+enum rsa_dtype { RSA_F32 = 0, RSA_BF16 = 1 };
+
+/* A strided 5-D view [rank][b][z][row][col] with unit column stride. */
+typedef struct rsa_view {
+  void* ptr;
+  int64_t s_rank; /* elements between consecutive ranks (or origin blocks) */
+  int64_t s_b;
+  int64_t s_z;
+  int64_t s_row;
+} rsa_view;
+
+/* Geometry shared by the fused RSA kernels. */
+typedef struct rsa_geom {
+  int32_t n_rank;    /* query ranks covered by this launch (1 per GPU, N when resident) */
+  int32_t batch;     /* B */
+  int32_t heads;     /* Z */
+  int32_t chunk;     /* c = L / N */
+  int32_t head_dim;  /* A */
+  int32_t seq_len;   /* L: width of the probability panel */
+  int32_t org_lo;    /* first origin chunk resident in this launch */
+  int32_t n_org;     /* number of consecutive origin chunks resident */
+  float scale;       /* 1/sqrt(A) */
+} rsa_geom;
+
+int rsa_abi_version(void);
+const char* rsa_last_error(void);
+int rsa_num_sms(void);
+
+/* ------------------------------------------------------------ primitives */
+
+/*
+ * Batched GEMM, C = alpha * op(A) * op(B) (+ C if accumulate).
+ * Replaces ringseq/tensor_ops.py:44-72 (`matmul`).  trans_a=0: A stored
+ * M x K; trans_a=1: A stored K x M.  trans_b=0: B stored K x N; trans_b=1:
+ * B stored N x K.  Batch index i = i1 * nb2 + i2 with strides (s1, s2) per
+ * operand; a zero stride broadcasts.  bf16 operands with 16-byte-aligned
+ * rows run on tcgen05 tensor cores (fp32 accumulation in TMEM); any other
+ * layout runs on the SIMT CUDA path.  c_dtype selects fp32 or bf16 output.
+ */
+int rsa_gemm(int M, int N, int K, const void* A, int a_dtype, int64_t lda, int trans_a, int64_t a_s1, int64_t a_s2,
+             const void* B, int b_dtype, int64_t ldb, int trans_b, int64_t b_s1, int64_t b_s2, void* C, int c_dtype,
+             int64_t ldc, int64_t c_s1, int64_t c_s2, int nb1, int nb2, float alpha, int accumulate, void* stream);
+
+/* Force one backend: 0 = auto, 1 = tcgen05 only (RSA_ERR_UNSUPPORTED if it
+ * cannot tile), 2 = SIMT only.  Used by the tests to cover both paths. */
+int rsa_gemm_set_backend(int backend);
+
+/*
+ * Row softmax y = exp(s*x - max(s*x)) / sum, over `cols` per row.
+ * Replaces ringseq/tensor_ops.py:75-84 (`softmax_rows`).  Any non-finite
+ * input sets *nonfinite_flag (device int) to 1; the host raises NumericError.
+ */
+int rsa_softmax_rows(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ld_x, float scale, void* y,
+                     int y_dtype, int64_t ld_y, int* nonfinite_flag, void* stream);
+
+/*
+ * Softmax Jacobian, ds = p * (dp - rowsum(dp * p)) * scale.
+ * Replaces ringseq/ring_attention.py:187-190 (and reference.py:99-100).
+ */
+int rsa_softmax_bwd(const void* p, int p_dtype, int64_t ld_p, const float* dp, int64_t ld_dp, int64_t rows,
+                    int64_t cols, float scale, void* ds, int ds_dtype, int64_t ld_ds, void* stream);
+
+/* out[r] = sum_c a[r,c] * b[r,c] (fp32 accumulate); a, b bf16. */
+int rsa_rowdot(const void* a, int64_t lda, const void* b, int64_t ldb, int64_t rows, int64_t cols, float* out,
+               void* stream);
+
+/* --------------------------------------------------- fused RSA kernels */
+
+/*
+ * Stage 1 of the RSA forward (ringseq/ring_attention.py:89-94): for every
+ * query row, the running max m and sum l of exp(scale * q.k) over the keys
+ * of origins [org_lo, org_lo + n_org).  stats is float2 [slot][rank][b][z][c]
+ * (slot stride = n_rank*B*Z*c); this launch writes slot `slot`.
+ */
+int rsa_fwd_stats(const rsa_geom* g, rsa_view q, rsa_view k, float* stats, int slot, void* stream);
+
+/*
+ * Stage 2 of the RSA forward (ringseq/ring_attention.py:97-103 plus the
+ * softmax normalisation): combines `n_slots` stat slots, recomputes the
+ * score tiles, writes the bf16 probability panel blocks of the resident
+ * origins, and accumulates O = sum_j P_j V_j in TMEM.  o_acc (fp32, may be
+ * NULL) is read-modify-written when accumulate != 0; o_out (bf16, may be
+ * NULL) receives the final output.
+ */
+int rsa_fwd_probs_pv(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, const float* stats, int n_slots,
+                     rsa_view panel, rsa_view o_acc, int accumulate, rsa_view o_out, void* stream);
+
+/*
+ * V-ring half of the RSA backward (ringseq/ring_attention.py:180-205):
+ * dP = dO V_j^T, dS = P (dP - D) scale written to the dS panel, and the
+ * key/value gradient contributions dK_j = dS_j^T Q, dV_j = P_j^T dO summed
+ * over the launch's query ranks.  D[row] = rowsum(dO * O) (see rsa_rowdot).
+ * dk/dv are fp32 (accumulate != 0 adds) or bf16 outputs per dkv_dtype.
+ */
+int rsa_bwd_dkdv(const rsa_geom* g, rsa_view q, rsa_view v, rsa_view dout, rsa_view panel, const float* dvec,
+                 rsa_view ds_panel, rsa_view dk, rsa_view dv, int dkv_dtype, int accumulate, void* stream);
+
+/*
+ * K-ring half of the RSA backward (ringseq/ring_attention.py:192-196):
+ * dQ = sum_j dS_j K_j over the resident origins.  dq_acc fp32 (optional,
+ * accumulate != 0 adds) and/or dq_out bf16.
+ */
+int rsa_bwd_dq(const rsa_geom* g, rsa_view ds_panel, rsa_view k, rsa_view dq_acc, int accumulate, rsa_view dq_out,
+               void* stream);
+
+/* Can the fused kernels tile this geometry (head_dim, chunk, alignment)? */
+int rsa_fused_supported(const rsa_geom* g);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RSA_B200_H */

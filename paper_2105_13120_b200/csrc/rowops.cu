@@ -1,0 +1,265 @@
+// Row-wise kernels of the staged RSA path: softmax, softmax Jacobian, row dot.
+//
+// One warp per row.  The softmax makes one online pass (running max and
+// rescaled sum, ringseq/tensor_ops.py:82-84 restated as a single sweep) and
+// one write pass; with 16-byte vector loads a row of L fp32 scores is read
+// from HBM once and re-read from L1/L2.  The Jacobian
+// (ringseq/ring_attention.py:187-190) is the same skeleton: one reduction
+// pass for rowsum(dP * P), one write pass.
+#include "common.h"
+#include "ptx.cuh"
+
+namespace rsa {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float ld1(const T* p, int64_t i);
+template <>
+__device__ __forceinline__ float ld1<float>(const float* p, int64_t i) {
+  return p[i];
+}
+template <>
+__device__ __forceinline__ float ld1<__nv_bfloat16>(const __nv_bfloat16* p, int64_t i) {
+  return __bfloat162float(p[i]);
+}
+
+// Load 4 consecutive elements as floats (caller guarantees alignment).
+template <typename T>
+__device__ __forceinline__ void ld4(const T* p, float* v);
+template <>
+__device__ __forceinline__ void ld4<float>(const float* p, float* v) {
+  float4 x = *reinterpret_cast<const float4*>(p);
+  v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+}
+template <>
+__device__ __forceinline__ void ld4<__nv_bfloat16>(const __nv_bfloat16* p, float* v) {
+  uint2 x = *reinterpret_cast<const uint2*>(p);
+  __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&x.x);
+  __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&x.y);
+  float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+  v[0] = fa.x, v[1] = fa.y, v[2] = fb.x, v[3] = fb.y;
+}
+
+template <typename T>
+__device__ __forceinline__ void st1(T* p, int64_t i, float v);
+template <>
+__device__ __forceinline__ void st1<float>(float* p, int64_t i, float v) {
+  p[i] = v;
+}
+template <>
+__device__ __forceinline__ void st1<__nv_bfloat16>(__nv_bfloat16* p, int64_t i, float v) {
+  p[i] = __float2bfloat16_rn(v);
+}
+
+template <typename T>
+__device__ __forceinline__ void st4(T* p, const float* v);
+template <>
+__device__ __forceinline__ void st4<float>(float* p, const float* v) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+template <>
+__device__ __forceinline__ void st4<__nv_bfloat16>(__nv_bfloat16* p, const float* v) {
+  *reinterpret_cast<uint2*>(p) = make_uint2(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]));
+}
+
+constexpr float LOG2E = 1.4426950408889634f;
+
+template <typename TI, typename TO, bool VEC>
+__global__ void __launch_bounds__(256) softmax_rows_kernel(const TI* __restrict__ x, int64_t rows, int64_t cols,
+                                                           int64_t ldx, float scale, TO* __restrict__ y, int64_t ldy,
+                                                           int* flag) {
+  const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const TI* xr = x + row * ldx;
+  TO* yr = y + row * ldy;
+  const float sl = scale * LOG2E;  // work in base 2: exp(s*x - m) = 2^(sl*x - m2)
+  float m = -INFINITY, s = 0.f;
+  bool bad = false;
+  if (VEC) {
+    for (int64_t c = int64_t(lane) * 4; c < cols; c += 128) {
+      float v[4];
+      ld4<TI>(xr + c, v);
+      float lm = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        bad |= !isfinite(v[i]);
+        lm = fmaxf(lm, __fmul_rn(v[i], sl));
+      }
+      if (lm > m) {
+        s *= exp2f(m - lm);
+        m = lm;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s += exp2f(__fmul_rn(v[i], sl) - m);
+    }
+  } else {
+    for (int64_t c = lane; c < cols; c += 32) {
+      const float v = ld1<TI>(xr, c);
+      bad |= !isfinite(v);
+      const float t = __fmul_rn(v, sl);
+      if (t > m) {
+        s *= exp2f(m - t);
+        m = t;
+      }
+      s += exp2f(t - m);
+    }
+  }
+  // warp-combine (m, s) in base 2
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, off);
+    const float mn = fmaxf(m, m2);
+    if (mn != -INFINITY) {
+      s = s * exp2f(m - mn) + s2 * exp2f(m2 - mn);
+      m = mn;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad)) {
+    if (lane == 0) atomicExch(flag, 1);
+  }
+  const float inv = 1.f / s;
+  if (VEC) {
+    for (int64_t c = int64_t(lane) * 4; c < cols; c += 128) {
+      float v[4];
+      ld4<TI>(xr + c, v);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = exp2f(__fmul_rn(v[i], sl) - m) * inv;
+      st4<TO>(yr + c, v);
+    }
+  } else {
+    for (int64_t c = lane; c < cols; c += 32) st1<TO>(yr, c, exp2f(__fmul_rn(ld1<TI>(xr, c), sl) - m) * inv);
+  }
+}
+
+template <typename TP, typename TD, bool VEC>
+__global__ void __launch_bounds__(256) softmax_bwd_kernel(const TP* __restrict__ p, int64_t ldp,
+                                                          const float* __restrict__ dp, int64_t lddp, int64_t rows,
+                                                          int64_t cols, float scale, TD* __restrict__ ds, int64_t ldds) {
+  const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const TP* pr = p + row * ldp;
+  const float* dr = dp + row * lddp;
+  TD* sr = ds + row * ldds;
+  float acc = 0.f;
+  if (VEC) {
+    for (int64_t c = int64_t(lane) * 4; c < cols; c += 128) {
+      float a[4], b[4];
+      ld4<TP>(pr + c, a);
+      ld4<float>(dr + c, b);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc += a[i] * b[i];
+    }
+  } else {
+    for (int64_t c = lane; c < cols; c += 32) acc += ld1<TP>(pr, c) * dr[c];
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (VEC) {
+    for (int64_t c = int64_t(lane) * 4; c < cols; c += 128) {
+      float a[4], b[4], o[4];
+      ld4<TP>(pr + c, a);
+      ld4<float>(dr + c, b);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[i] = a[i] * (b[i] - acc) * scale;
+      st4<TD>(sr + c, o);
+    }
+  } else {
+    for (int64_t c = lane; c < cols; c += 32) st1<TD>(sr, c, ld1<TP>(pr, c) * (dr[c] - acc) * scale);
+  }
+}
+
+__global__ void __launch_bounds__(256) rowdot_kernel(const __nv_bfloat16* __restrict__ a, int64_t lda,
+                                                     const __nv_bfloat16* __restrict__ b, int64_t ldb, int64_t rows,
+                                                     int64_t cols, float* __restrict__ out) {
+  const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  float acc = 0.f;
+  for (int64_t c = lane; c < cols; c += 32) acc += __bfloat162float(a[row * lda + c]) * __bfloat162float(b[row * ldb + c]);
+#pragma unroll
+  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) out[row] = acc;
+}
+
+template <typename T>
+bool vec_ok(const void* ptr, int64_t ld, int64_t cols) {
+  const int64_t esz = sizeof(T);
+  const int64_t need = 4 * esz;  // 4 elements per vector access
+  return (reinterpret_cast<uintptr_t>(ptr) % need) == 0 && (ld * esz) % need == 0 && cols % 4 == 0;
+}
+
+template <typename TI, typename TO>
+int softmax_launch(const void* x, int64_t rows, int64_t cols, int64_t ldx, float scale, void* y, int64_t ldy, int* flag,
+                   cudaStream_t st) {
+  const dim3 grid((rows + 7) / 8);
+  const bool v = vec_ok<TI>(x, ldx, cols) && vec_ok<TO>(y, ldy, cols);
+  if (v)
+    softmax_rows_kernel<TI, TO, true><<<grid, 256, 0, st>>>(static_cast<const TI*>(x), rows, cols, ldx, scale,
+                                                            static_cast<TO*>(y), ldy, flag);
+  else
+    softmax_rows_kernel<TI, TO, false><<<grid, 256, 0, st>>>(static_cast<const TI*>(x), rows, cols, ldx, scale,
+                                                             static_cast<TO*>(y), ldy, flag);
+  return check_launch("softmax_rows_kernel");
+}
+
+template <typename TP, typename TD>
+int softmax_bwd_launch(const void* p, int64_t ldp, const float* dp, int64_t lddp, int64_t rows, int64_t cols,
+                       float scale, void* ds, int64_t ldds, cudaStream_t st) {
+  const dim3 grid((rows + 7) / 8);
+  const bool v = vec_ok<TP>(p, ldp, cols) && vec_ok<float>(dp, lddp, cols) && vec_ok<TD>(ds, ldds, cols);
+  if (v)
+    softmax_bwd_kernel<TP, TD, true><<<grid, 256, 0, st>>>(static_cast<const TP*>(p), ldp, dp, lddp, rows, cols, scale,
+                                                           static_cast<TD*>(ds), ldds);
+  else
+    softmax_bwd_kernel<TP, TD, false><<<grid, 256, 0, st>>>(static_cast<const TP*>(p), ldp, dp, lddp, rows, cols,
+                                                            scale, static_cast<TD*>(ds), ldds);
+  return check_launch("softmax_bwd_kernel");
+}
+
+}  // namespace
+}  // namespace rsa
+
+extern "C" {
+
+int rsa_softmax_rows(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ld_x, float scale, void* y,
+                     int y_dtype, int64_t ld_y, int* nonfinite_flag, void* stream) {
+  using namespace rsa;
+  if (rows < 0 || cols < 1 || ld_x < cols || ld_y < cols || !nonfinite_flag)
+    return fail(RSA_ERR_INVALID, "softmax_rows: bad sizes");
+  if (rows == 0) return RSA_OK;
+  if ((rows + 7) / 8 > 0x7fffffff) return fail(RSA_ERR_INVALID, "softmax_rows: too many rows");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool xb = x_dtype == RSA_BF16, yb = y_dtype == RSA_BF16;
+  if (!xb && !yb) return softmax_launch<float, float>(x, rows, cols, ld_x, scale, y, ld_y, nonfinite_flag, st);
+  if (!xb && yb) return softmax_launch<float, __nv_bfloat16>(x, rows, cols, ld_x, scale, y, ld_y, nonfinite_flag, st);
+  if (xb && !yb) return softmax_launch<__nv_bfloat16, float>(x, rows, cols, ld_x, scale, y, ld_y, nonfinite_flag, st);
+  return softmax_launch<__nv_bfloat16, __nv_bfloat16>(x, rows, cols, ld_x, scale, y, ld_y, nonfinite_flag, st);
+}
+
+int rsa_softmax_bwd(const void* p, int p_dtype, int64_t ld_p, const float* dp, int64_t ld_dp, int64_t rows,
+                    int64_t cols, float scale, void* ds, int ds_dtype, int64_t ld_ds, void* stream) {
+  using namespace rsa;
+  if (rows < 0 || cols < 1) return fail(RSA_ERR_INVALID, "softmax_bwd: bad sizes");
+  if (rows == 0) return RSA_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool pb = p_dtype == RSA_BF16, db = ds_dtype == RSA_BF16;
+  if (!pb && !db) return softmax_bwd_launch<float, float>(p, ld_p, dp, ld_dp, rows, cols, scale, ds, ld_ds, st);
+  if (!pb && db) return softmax_bwd_launch<float, __nv_bfloat16>(p, ld_p, dp, ld_dp, rows, cols, scale, ds, ld_ds, st);
+  if (pb && !db) return softmax_bwd_launch<__nv_bfloat16, float>(p, ld_p, dp, ld_dp, rows, cols, scale, ds, ld_ds, st);
+  return softmax_bwd_launch<__nv_bfloat16, __nv_bfloat16>(p, ld_p, dp, ld_dp, rows, cols, scale, ds, ld_ds, st);
+}
+
+int rsa_rowdot(const void* a, int64_t lda, const void* b, int64_t ldb, int64_t rows, int64_t cols, float* out,
+               void* stream) {
+  using namespace rsa;
+  if (rows < 0 || cols < 0) return fail(RSA_ERR_INVALID, "rowdot: bad sizes");
+  if (rows == 0) return RSA_OK;
+  rowdot_kernel<<<(rows + 7) / 8, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(a), lda, static_cast<const __nv_bfloat16*>(b), ldb, rows, cols, out);
+  return check_launch("rowdot_kernel");
+}
+
+}  // extern "C"
