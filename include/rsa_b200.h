@@ -113,9 +113,12 @@ int rsa_rowdot(const void* a, int64_t lda, const void* b, int64_t ldb, int64_t r
  * Stage 1 of the RSA forward (ringseq/ring_attention.py:89-94): for every
  * query row, the running max m and sum l of exp(scale * q.k) over the keys
  * of origins [org_lo, org_lo + n_org).  stats is float2 [slot][rank][b][z][c]
- * (slot stride = n_rank*B*Z*c); this launch writes slot `slot`.
+ * (slot stride = n_rank*B*Z*c); this launch writes slot `slot`.  Stats are
+ * kept in base 2: m = max(scale*log2(e)*s), l = sum 2^(scale*log2(e)*s - m).
+ * A non-finite score sets *nonfinite_flag (device int, may be NULL).
  */
-int rsa_fwd_stats(const rsa_geom* g, rsa_view q, rsa_view k, float* stats, int slot, void* stream);
+int rsa_fwd_stats(const rsa_geom* g, rsa_view q, rsa_view k, float* stats, int slot, int* nonfinite_flag,
+                  void* stream);
 
 /*
  * Stage 2 of the RSA forward (ringseq/ring_attention.py:97-103 plus the

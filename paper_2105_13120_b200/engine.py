@@ -1,0 +1,198 @@
+"""Device orchestration of the RSA protocol on stacked chunk tensors.
+
+Every tensor here is stacked over ring ranks: per-head chunks are
+``[N][B][Z][c][A]`` and probability / dS panels ``[N][B][Z][c][L]`` (bf16).
+Rank d's slice is exactly the chunk / panel the reference keeps on device d
+(ringseq/ring_attention.py:43-60), so the list API in ``ring_attention.py``
+returns views of these stacks.
+
+Two device paths compute the same protocol:
+
+* ``fused`` (A = 64, c % 8 == 0): the four tcgen05 kernels of
+  csrc/fused.cu.  With all N ranks resident in one GPU's HBM a ring hop is a
+  pointer rotation, so one launch per stage covers every (rank, origin)
+  pair: the K-ring stage is rsa_fwd_stats, the V-ring stage
+  rsa_fwd_probs_pv, and the backward's V ring / K ring are rsa_bwd_dkdv /
+  rsa_bwd_dq.  dK/dV are reduced over ranks inside rsa_bwd_dkdv (the CTA
+  for a key tile walks every rank's query rows), which is the all-reduce of
+  ringseq/ring_attention.py:206-209 done in TMEM.
+* ``staged``: the reference's own stage structure built from the primitive
+  kernels -- per-origin score GEMMs into an fp32 panel, row softmax, per-
+  origin PV GEMMs summed in ascending origin order; backward dP panel,
+  softmax Jacobian, dQ / dK / dV GEMMs with the dK/dV partials summed over
+  ranks in ascending order (ringseq/cluster.py:346-349).  Any shape.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import tensor_ops as ops
+from ._native import BF16, F32, RsaGeom, RsaView, check, lib
+from .errors import ShapeError
+
+__all__ = ["fused_supported", "forward", "backward", "recompute_outputs", "NULL_VIEW"]
+
+NULL_VIEW = RsaView(None, 0, 0, 0, 0)
+
+
+def _stream(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _view(t: torch.Tensor | None) -> RsaView:
+    if t is None:
+        return NULL_VIEW
+    if t.dim() != 5 or t.stride(-1) != 1:
+        raise ShapeError(f"expected a [rank][b][z][row][col] tensor with unit column stride, got {tuple(t.shape)}")
+    return RsaView(t.data_ptr(), t.stride(0), t.stride(1), t.stride(2), t.stride(3))
+
+
+def _geom(n_rank, b, z, c, a, seq, org_lo, n_org) -> RsaGeom:
+    return RsaGeom(n_rank, b, z, c, a, seq, org_lo, n_org, 1.0 / math.sqrt(a))
+
+
+def fused_supported(n: int, b: int, z: int, c: int, a: int) -> bool:
+    g = _geom(n, b, z, c, a, n * c, 0, n)
+    return bool(lib().rsa_fused_supported(ctypes.byref(g)))
+
+
+def _pick(path: str, n, b, z, c, a) -> str:
+    if path == "auto":
+        return "fused" if fused_supported(n, b, z, c, a) else "staged"
+    if path not in ("fused", "staged"):
+        raise ValueError(f"unknown path {path!r}")
+    if path == "fused" and not fused_supported(n, b, z, c, a):
+        raise ShapeError(f"fused kernels cannot tile N={n} B={b} Z={z} c={c} A={a} (need A=64, c%8==0)")
+    return path
+
+
+# ----------------------------------------------------------------- forward
+
+def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, path: str = "auto",
+            flag: torch.Tensor | None = None, out: torch.Tensor | None = None,
+            panel: torch.Tensor | None = None):
+    """RSA forward on stacked [N][B][Z][c][A] bf16 chunks.
+
+    Returns (outputs [N][B][Z][c][A] bf16, panels [N][B][Z][c][L] bf16,
+    nonfinite flag tensor).  The flag is a device int set by the kernels when
+    a score is non-finite; callers decide when to read it.
+    """
+    n, b, z, c, a = q.shape
+    seq = n * c
+    dev = q.device
+    if flag is None:
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    if out is None:
+        out = torch.empty((n, b, z, c, a), dtype=torch.bfloat16, device=dev)
+    if panel is None:
+        panel = torch.empty((n, b, z, c, seq), dtype=torch.bfloat16, device=dev)
+    which = _pick(path, n, b, z, c, a)
+    if which == "fused":
+        L = lib()
+        st = _stream(q)
+        g = _geom(n, b, z, c, a, seq, 0, n)
+        stats = torch.empty((n * b * z * c * 2,), dtype=torch.float32, device=dev)
+        check(L.rsa_fwd_stats(ctypes.byref(g), _view(q), _view(k), stats.data_ptr(), 0, flag.data_ptr(), st),
+              "rsa_fwd_stats")
+        check(L.rsa_fwd_probs_pv(ctypes.byref(g), _view(q), _view(k), _view(v), stats.data_ptr(), 1, _view(panel),
+                                 NULL_VIEW, 0, _view(out), st), "rsa_fwd_probs_pv")
+        return out, panel, flag
+    _forward_staged(q, k, v, out, panel, flag)
+    return out, panel, flag
+
+
+def _softmax_into(x: torch.Tensor, y: torch.Tensor, scale: float, flag: torch.Tensor) -> None:
+    cols = x.shape[-1]
+    rows = x.numel() // cols
+    check(lib().rsa_softmax_rows(x.data_ptr(), F32, rows, cols, cols, float(scale), y.data_ptr(), BF16, cols,
+                                 flag.data_ptr(), _stream(x)), "rsa_softmax_rows")
+
+
+def _forward_staged(q, k, v, out, panel, flag) -> None:
+    n, b, z, c, a = q.shape
+    scale = 1.0 / math.sqrt(a)
+    scores = torch.empty((b, z, c, n * c), dtype=torch.float32, device=q.device)
+    acc = torch.empty((b, z, c, a), dtype=torch.float32, device=q.device)
+    for d in range(n):
+        # stage 1: score row blocks in ring arrival order (origin d, d-1, ...)
+        for h in range(n):
+            j = (d - h) % n
+            ops.matmul(q[d], k[j].transpose(-1, -2), out=scores[..., j * c:(j + 1) * c])
+        _softmax_into(scores, panel[d], scale, flag)
+        # stage 2: O = sum_j P_j V_j in ascending origin order
+        for j in range(n):
+            ops.matmul(panel[d][..., j * c:(j + 1) * c], v[j], out=acc, accumulate=j > 0)
+        out[d].copy_(acc)
+
+
+# ---------------------------------------------------------------- backward
+
+def recompute_outputs(panel: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
+    """O = P V from saved panels (used when the caller's panels carry no O)."""
+    n, b, z, c, _ = panel.shape
+    a = v.shape[-1]
+    out = torch.empty((n, b, z, c, a), dtype=torch.bfloat16, device=panel.device)
+    acc = torch.empty((b, z, c, a), dtype=torch.float32, device=panel.device)
+    for d in range(n):
+        for j in range(n):
+            ops.matmul(panel[d][..., j * c:(j + 1) * c], v[j], out=acc, accumulate=j > 0)
+        out[d].copy_(acc)
+    return out
+
+
+def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path: str = "auto"):
+    """RSA backward on stacked chunks; returns (dq, dk, dv) as [N][B][Z][c][A] bf16."""
+    n, b, z, c, a = q.shape
+    seq = n * c
+    dev = q.device
+    dq = torch.empty((n, b, z, c, a), dtype=torch.bfloat16, device=dev)
+    dk = torch.empty_like(dq)
+    dv = torch.empty_like(dq)
+    which = _pick(path, n, b, z, c, a)
+    if which == "fused":
+        if outputs is None:
+            outputs = recompute_outputs(panel, v)
+        dvec = ops.rowdot(grad, outputs)  # D = rowsum(dO * O) = rowsum(dP * P)
+        ds = torch.empty((n, b, z, c, seq), dtype=torch.bfloat16, device=dev)
+        L = lib()
+        st = _stream(q)
+        g = _geom(n, b, z, c, a, seq, 0, n)
+        check(L.rsa_bwd_dkdv(ctypes.byref(g), _view(q), _view(v), _view(grad), _view(panel), dvec.data_ptr(),
+                             _view(ds), _view(dk), _view(dv), BF16, 0, st), "rsa_bwd_dkdv")
+        check(L.rsa_bwd_dq(ctypes.byref(g), _view(ds), _view(k), NULL_VIEW, 0, _view(dq), st), "rsa_bwd_dq")
+        return dq, dk, dv
+    _backward_staged(q, k, v, panel, grad, dq, dk, dv)
+    return dq, dk, dv
+
+
+def _backward_staged(q, k, v, panel, grad, dq, dk, dv) -> None:
+    n, b, z, c, a = q.shape
+    seq = n * c
+    scale = 1.0 / math.sqrt(a)
+    dev = q.device
+    dp = torch.empty((b, z, c, seq), dtype=torch.float32, device=dev)
+    ds = torch.empty((b, z, c, seq), dtype=torch.bfloat16, device=dev)
+    acc = torch.empty((b, z, c, a), dtype=torch.float32, device=dev)
+    dk_acc = torch.empty((n, b, z, c, a), dtype=torch.float32, device=dev)
+    dv_acc = torch.empty_like(dk_acc)
+    for d in range(n):
+        # V ring: dP row blocks (ringseq/ring_attention.py:181-184)
+        for h in range(n):
+            j = (d - h) % n
+            ops.matmul(grad[d], v[j].transpose(-1, -2), out=dp[..., j * c:(j + 1) * c])
+        ops.softmax_backward(panel[d], dp, scale, out=ds)
+        # K ring: dQ in ascending origin order (ringseq/ring_attention.py:193-196)
+        for j in range(n):
+            ops.matmul(ds[..., j * c:(j + 1) * c], k[j], out=acc, accumulate=j > 0)
+        dq[d].copy_(acc)
+        # full-length partials, summed over ranks in ascending order
+        for j in range(n):
+            blk = slice(j * c, (j + 1) * c)
+            ops.matmul(ds[..., blk].transpose(-1, -2), q[d], out=dk_acc[j], accumulate=d > 0)
+            ops.matmul(panel[d][..., blk].transpose(-1, -2), grad[d], out=dv_acc[j], accumulate=d > 0)
+    dk.copy_(dk_acc)
+    dv.copy_(dv_acc)

@@ -1,0 +1,232 @@
+"""Ring Self-Attention (RSA) behind the reference API of ``ringseq.ring_attention``.
+
+Drop-in counterparts of ringseq/ring_attention.py:124-241 with the same
+names, positional/keyword signatures, result dataclasses and exceptions:
+
+* ``ring_attention_forward(q_chunks, k_chunks, v_chunks, cfg, *, executor=None)``
+  -> ``RingAttentionForward(outputs, probs, ledger)``
+* ``ring_attention_backward(q_chunks, k_chunks, v_chunks, probs, grad_chunks, cfg, *, executor=None)``
+  -> ``RingAttentionBackward(grad_q, grad_k, grad_v, ledger)``
+* ``sequence_parallel_attention(x_chunks, weights, cfg, *, executor=None)``
+  -> ``(results, ledger)``
+
+Chunks may be NumPy arrays (any float dtype) or torch tensors; they are
+moved to the GPU as bf16.  Results are CUDA tensors (bf16), one per ring
+rank, in the reference's layout: outputs (B, Z, L/N, A), probability panels
+(B, Z, L/N, L) whose column block j belongs to origin j.
+
+The ring itself: when every rank's chunk sits in one GPU's HBM (this
+single-controller API), a hop is a pointer rotation, and the kernels in
+``engine`` read each origin's chunk in place.  The ledger charges exactly
+what the reference's simulated ring charges (ringseq/cluster.py:130-135):
+2(N-1)*C elements per rank forward; 2(N-1)*C ring plus two all-reduces of
+N*C elements backward.  Multi-GPU rings (one process per GPU, NCCL) live in
+``distributed.py`` and reuse the same kernels hop by hop.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import engine
+from . import tensor_ops as ops
+from .cluster import CommLedger, resolve_executor
+from .config import AttentionConfig
+from .errors import NumericError, ShapeError, StateError
+
+__all__ = [
+    "RingAttentionForward",
+    "RingAttentionBackward",
+    "ring_attention_forward",
+    "ring_attention_backward",
+    "sequence_parallel_attention",
+    "ProbPanels",
+]
+
+
+@dataclass
+class RingAttentionForward:
+    """Per-rank outputs (B, Z, L/N, A), saved probability panels (B, Z, L/N, L), ledger."""
+
+    outputs: list
+    probs: list
+    ledger: CommLedger
+
+
+@dataclass
+class RingAttentionBackward:
+    """Per-rank gradient chunks for queries, keys and values, plus the ledger."""
+
+    grad_q: list
+    grad_k: list
+    grad_v: list
+    ledger: CommLedger
+
+
+class ProbPanels(list):
+    """The ``probs`` list returned by the forward: per-rank panel views into one
+    stacked [N][B][Z][c][L] tensor, which also remembers the stacked outputs.
+
+    Passing it back to ``ring_attention_backward`` (as the reference's callers
+    do with ``fwd.probs``) lets the backward reuse the stacked panel without a
+    copy and form D = rowsum(dO * O) from the saved O instead of recomputing
+    P V.  Any other list of panels works too, at the cost of one staging copy.
+    """
+
+    def __init__(self, stacked: torch.Tensor, outputs: torch.Tensor):
+        super().__init__(stacked[d] for d in range(stacked.shape[0]))
+        self.stacked = stacked
+        self.outputs = outputs
+
+
+def _shape_of(x) -> tuple:
+    return tuple(x.shape) if hasattr(x, "shape") else tuple(__import__("numpy").asarray(x).shape)
+
+
+def _check_chunks(name: str, chunks, cfg: AttentionConfig, expect: tuple) -> list:
+    """ringseq/ring_attention.py:106-117: count and shape of the per-rank chunks."""
+    chunks = chunks if isinstance(chunks, list) else list(chunks)  # keep ProbPanels intact
+    if len(chunks) != cfg.num_devices:
+        raise ShapeError(f"{name}: got {len(chunks)} chunks for {cfg.num_devices} devices")
+    for i, c in enumerate(chunks):
+        if _shape_of(c) != expect:
+            raise ShapeError(f"{name}[{i}] has shape {_shape_of(c)}, expected {expect}")
+    return chunks
+
+
+def _device_of(*lists):
+    for lst in lists:
+        for x in lst:
+            if isinstance(x, torch.Tensor) and x.is_cuda:
+                return x.device
+    return ops.default_device()
+
+
+def _stack(chunks: list, device) -> torch.Tensor:
+    """Stack per-rank chunks into one contiguous bf16 [N][...] device tensor."""
+    if isinstance(chunks, ProbPanels) and chunks.stacked.device == device:
+        return chunks.stacked
+    first = chunks[0]
+    out = torch.empty((len(chunks),) + _shape_of(first), dtype=torch.bfloat16, device=device)
+    for d, c in enumerate(chunks):
+        out[d].copy_(ops.to_device(c, device))
+    return out
+
+
+def _chunk_elements(cfg: AttentionConfig) -> int:
+    return cfg.batch_size * cfg.num_heads * cfg.chunk_len * cfg.head_size
+
+
+def forward_ledger(cfg: AttentionConfig) -> CommLedger:
+    """Keys then values circulate N-1 hops each (ringseq/ring_attention.py:124-130)."""
+    n = cfg.num_devices
+    ledger = CommLedger(n)
+    if n > 1:
+        for d in range(n):
+            ledger.record_ring_send(d, 2 * (n - 1) * _chunk_elements(cfg))
+    return ledger
+
+
+def backward_ledger(cfg: AttentionConfig) -> CommLedger:
+    """One V and one K circulation plus two all-reduces of (B, Z, L, A) partials
+    (ringseq/ring_attention.py:150-156, 206-207)."""
+    n = cfg.num_devices
+    ledger = CommLedger(n)
+    if n > 1:
+        full = cfg.batch_size * cfg.num_heads * cfg.seq_len * cfg.head_size
+        for d in range(n):
+            ledger.record_ring_send(d, 2 * (n - 1) * _chunk_elements(cfg))
+            ledger.record_allreduce(d, full)
+            ledger.record_allreduce(d, full)
+    return ledger
+
+
+def ring_attention_forward(q_chunks, k_chunks, v_chunks, cfg: AttentionConfig, *, executor: str | None = None,
+                           path: str = "auto") -> RingAttentionForward:
+    """Distributed attention forward over per-rank (B, Z, L/N, A) chunks.
+
+    ringseq/ring_attention.py:124-147.  ``path`` ('auto' | 'fused' | 'staged')
+    selects the device implementation; both compute the same protocol.
+    """
+    resolve_executor(executor)
+    shape = cfg.chunk_shape()
+    q_chunks = _check_chunks("q_chunks", q_chunks, cfg, shape)
+    k_chunks = _check_chunks("k_chunks", k_chunks, cfg, shape)
+    v_chunks = _check_chunks("v_chunks", v_chunks, cfg, shape)
+    dev = _device_of(q_chunks, k_chunks, v_chunks)
+    q, k, v = (_stack(x, dev) for x in (q_chunks, k_chunks, v_chunks))
+    out, panel, flag = engine.forward(q, k, v, path=path)
+    if int(flag.item()):
+        raise NumericError("softmax_rows requires finite inputs")
+    return RingAttentionForward(
+        outputs=[out[d] for d in range(cfg.num_devices)],
+        probs=ProbPanels(panel, out),
+        ledger=forward_ledger(cfg),
+    )
+
+
+def ring_attention_backward(q_chunks, k_chunks, v_chunks, probs, grad_chunks, cfg: AttentionConfig, *,
+                            executor: str | None = None, path: str = "auto") -> RingAttentionBackward:
+    """Gradients of ring_attention_forward w.r.t. the q/k/v chunks.
+
+    ringseq/ring_attention.py:150-217.  ``probs`` are the panels saved by the
+    forward (StateError when missing, ShapeError when mis-shaped).
+    """
+    resolve_executor(executor)
+    shape = cfg.chunk_shape()
+    q_chunks = _check_chunks("q_chunks", q_chunks, cfg, shape)
+    k_chunks = _check_chunks("k_chunks", k_chunks, cfg, shape)
+    v_chunks = _check_chunks("v_chunks", v_chunks, cfg, shape)
+    grad_chunks = _check_chunks("grad_chunks", grad_chunks, cfg, shape)
+    if probs is None:
+        raise StateError("ring_attention_backward needs the probability panels saved by ring_attention_forward")
+    probs = _check_chunks("probs", probs, cfg, cfg.panel_shape())
+    dev = _device_of(q_chunks, k_chunks, v_chunks, grad_chunks, probs)
+    q, k, v, g = (_stack(x, dev) for x in (q_chunks, k_chunks, v_chunks, grad_chunks))
+    panel = _stack(probs, dev)
+    outputs = probs.outputs if isinstance(probs, ProbPanels) and panel is probs.stacked else None
+    if outputs is not None and (outputs.shape != q.shape or outputs.device != dev):
+        outputs = None
+    dq, dk, dv = engine.backward(q, k, v, panel, g, outputs=outputs, path=path)
+    n = cfg.num_devices
+    return RingAttentionBackward(
+        grad_q=[dq[d] for d in range(n)],
+        grad_k=[dk[d] for d in range(n)],
+        grad_v=[dv[d] for d in range(n)],
+        ledger=backward_ledger(cfg),
+    )
+
+
+def sequence_parallel_attention(x_chunks, weights, cfg: AttentionConfig, *, executor: str | None = None,
+                                path: str = "auto"):
+    """Multi-head attention layer on sequence-partitioned (B, L/N, H) inputs.
+
+    ringseq/ring_attention.py:220-241: replicated projections are local
+    GEMMs, only the attention stages ring.  Returns (per-rank outputs, ledger).
+    """
+    resolve_executor(executor)
+    expect = (cfg.batch_size, cfg.chunk_len, cfg.hidden_size)
+    x_chunks = _check_chunks("x_chunks", x_chunks, cfg, expect)
+    h, za = cfg.hidden_size, cfg.num_heads * cfg.head_size
+    for name, expect_w in (("wq", (h, za)), ("wk", (h, za)), ("wv", (h, za)), ("wo", (za, h))):
+        if _shape_of(getattr(weights, name)) != expect_w:
+            raise ShapeError(f"{name} has shape {_shape_of(getattr(weights, name))}, expected {expect_w}")
+    dev = _device_of(x_chunks)
+    x = _stack(x_chunks, dev)  # [N][B][c][H]
+    wq, wk, wv, wo = (ops.to_device(getattr(weights, n), dev) for n in ("wq", "wk", "wv", "wo"))
+    n, b, c, z, a = cfg.num_devices, cfg.batch_size, cfg.chunk_len, cfg.num_heads, cfg.head_size
+
+    def project(w):
+        y = ops.matmul(x, w, out_dtype=torch.bfloat16)  # [N][B][c][Z*A]
+        return y.view(n, b, c, z, a).permute(0, 1, 3, 2, 4).contiguous()  # split_heads per rank
+
+    q, k, v = project(wq), project(wk), project(wv)
+    out, _, flag = engine.forward(q, k, v, path=path)
+    if int(flag.item()):
+        raise NumericError("softmax_rows requires finite inputs")
+    merged = out.permute(0, 1, 3, 2, 4).reshape(n, b, c, z * a)  # merge_heads per rank
+    y = ops.matmul(merged, wo)
+    return [y[d] for d in range(n)], forward_ledger(cfg)
+

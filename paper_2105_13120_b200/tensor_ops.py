@@ -15,8 +15,6 @@ helpers are only used at the API surface.
 
 from __future__ import annotations
 
-import math
-
 import numpy as np
 import torch
 

@@ -1,0 +1,261 @@
+"""GPU parity of the RSA path against the CPU oracle and the reference goldens.
+
+Inputs are drawn exactly like the reference tests (make_rng(seed) normals,
+q, k, v, grad in that order -- tests/test_acceptance.py:59-67), rounded to
+bf16, and fed to both the device path and the float64 oracle, so the gates
+measure kernel error only.
+
+Tolerances (bf16 operands, fp32 accumulation, bf16 P and dS; derivation in
+SURVEY.md section 8c and DESIGN.md "Numerics"):
+  outputs / dq / dk / dv : relative Frobenius error <= 1e-2 and
+                           max |diff| <= 2e-2 * max(1, max |ref|)
+  probability panels     : max |diff| <= 4e-3 (one bf16 ulp at 1.0)
+Ledgers are integers and must match exactly.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_cases
+from oracle import ringseq_np as orc
+
+pytestmark = pytest.mark.gpu
+
+REL_F = 1e-2
+MAX_ABS = 2e-2
+PROB_ABS = 4e-3
+
+
+@pytest.fixture(scope="module")
+def rsa():
+    import paper_2105_13120_b200 as pkg
+    from paper_2105_13120_b200 import ring_attention as ra
+
+    return pkg, ra
+
+
+def _cfg(pkg, b, z, seq, a, n):
+    return pkg.AttentionConfig(batch_size=b, seq_len=seq, hidden_size=z * a, num_heads=z, head_size=a, num_devices=n)
+
+
+def _inputs(b, z, seq, a, seed):
+    rng = orc.make_rng(seed)
+    return [orc.bf16_round(rng.standard_normal((b, z, seq, a))) for _ in range(4)]
+
+
+def _np(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def _gate(name, got, want):
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    assert got.shape == want.shape, (name, got.shape, want.shape)
+    rel = np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30)
+    mx = np.max(np.abs(got - want))
+    assert rel <= REL_F, f"{name}: relative Frobenius error {rel:.3e}"
+    assert mx <= MAX_ABS * max(1.0, np.max(np.abs(want))), f"{name}: max |diff| {mx:.3e}"
+
+
+def _run(pkg, ra, q, k, v, g, n, path):
+    b, z, seq, a = q.shape
+    cfg = _cfg(pkg, b, z, seq, a, n)
+    ch = lambda x: orc.chunks_of(x, n)  # noqa: E731
+    fwd = ra.ring_attention_forward(ch(q), ch(k), ch(v), cfg, path=path)
+    bwd = ra.ring_attention_backward(ch(q), ch(k), ch(v), fwd.probs, ch(g), cfg, path=path)
+    torch.cuda.synchronize()
+    return cfg, fwd, bwd
+
+
+def _oracle(q, k, v, g, n):
+    ch = lambda x: orc.chunks_of(x, n)  # noqa: E731
+    outs, probs, _ = orc.ring_forward(ch(q), ch(k), ch(v), exact=False)
+    dq, dk, dv, _ = orc.ring_backward(ch(q), ch(k), ch(v), probs, ch(g), exact=False)
+    cat = lambda xs: np.concatenate(xs, axis=-2)  # noqa: E731
+    return cat(outs), probs, cat(dq), cat(dk), cat(dv)
+
+
+def _check_all(pkg, fwd, bwd, want):
+    out, probs, dq, dk, dv = want
+    _gate("out", _np(pkg.gather_sequence(fwd.outputs)), out)
+    for d, p in enumerate(fwd.probs):
+        diff = np.max(np.abs(_np(p) - probs[d]))
+        assert diff <= PROB_ABS, f"probs[{d}] max |diff| {diff:.3e}"
+    _gate("dq", _np(pkg.gather_sequence(bwd.grad_q)), dq)
+    _gate("dk", _np(pkg.gather_sequence(bwd.grad_k)), dk)
+    _gate("dv", _np(pkg.gather_sequence(bwd.grad_v)), dv)
+
+
+@pytest.mark.parametrize("path", ["fused", "staged"])
+def test_matches_reference_goldens(rsa, golden, path):
+    """Device results vs outputs of the unmodified reference on the same bf16 inputs."""
+    pkg, ra = rsa
+    for case, want in golden_cases(golden, "rsa_mid").items():
+        b, z, seq, a, n, seed = (int(t) for t in case.split("_"))
+        q, k, v, g = _inputs(b, z, seq, a, seed)
+        _, fwd, bwd = _run(pkg, ra, q, k, v, g, n, path)
+        _gate("out", _np(pkg.gather_sequence(fwd.outputs)), want["out"])
+        _gate("dq", _np(pkg.gather_sequence(bwd.grad_q)), want["dq"])
+        _gate("dk", _np(pkg.gather_sequence(bwd.grad_k)), want["dk"])
+        _gate("dv", _np(pkg.gather_sequence(bwd.grad_v)), want["dv"])
+        if "probs" in want:
+            got = np.stack([_np(p) for p in fwd.probs])
+            assert np.max(np.abs(got - want["probs"])) <= PROB_ABS
+
+
+# (B, Z, L, A, N): BERT-base heads at config-1 length, ragged chunk tails
+# (c = 200, 24), c = 64 (N = 8), and a single rank.
+FUSED_SHAPES = [
+    (2, 3, 512, 64, 4),
+    (1, 2, 400, 64, 2),
+    (1, 2, 512, 64, 8),
+    (2, 1, 96, 64, 4),
+    (1, 2, 384, 64, 1),
+]
+
+
+@pytest.mark.parametrize("shape", FUSED_SHAPES)
+@pytest.mark.parametrize("path", ["fused", "staged"])
+def test_matches_oracle(rsa, shape, path):
+    pkg, ra = rsa
+    b, z, seq, a, n = shape
+    q, k, v, g = _inputs(b, z, seq, a, seed=sum(shape))
+    _, fwd, bwd = _run(pkg, ra, q, k, v, g, n, path)
+    _check_all(pkg, fwd, bwd, _oracle(q, k, v, g, n))
+
+
+# The reference's own small grid (tests/test_acceptance.py:44-50 style shapes,
+# head sizes 2..8) runs on the staged path (SIMT GEMM for unaligned heads).
+SMALL_SHAPES = [(1, 2, 8, 4, 1), (1, 2, 12, 4, 3), (2, 2, 16, 4, 4), (1, 1, 8, 2, 2), (2, 3, 40, 5, 4),
+                (2, 4, 32, 8, 8), (1, 2, 24, 3, 3)]
+
+
+@pytest.mark.parametrize("shape", SMALL_SHAPES)
+def test_small_reference_shapes(rsa, shape):
+    pkg, ra = rsa
+    b, z, seq, a, n = shape
+    q, k, v, g = _inputs(b, z, seq, a, seed=7 + seq)
+    _, fwd, bwd = _run(pkg, ra, q, k, v, g, n, "auto")
+    _check_all(pkg, fwd, bwd, _oracle(q, k, v, g, n))
+
+
+def test_fused_and_staged_agree(rsa):
+    pkg, ra = rsa
+    q, k, v, g = _inputs(2, 2, 256, 64, seed=5)
+    _, f1, b1 = _run(pkg, ra, q, k, v, g, 2, "fused")
+    _, f2, b2 = _run(pkg, ra, q, k, v, g, 2, "staged")
+    for x, y in zip(f1.probs, f2.probs):
+        assert np.max(np.abs(_np(x) - _np(y))) <= PROB_ABS
+    for xs, ys in ((f1.outputs, f2.outputs), (b1.grad_q, b2.grad_q), (b1.grad_k, b2.grad_k), (b1.grad_v, b2.grad_v)):
+        _gate("fused-vs-staged", _np(pkg.gather_sequence(xs)), _np(pkg.gather_sequence(ys)))
+
+
+def test_probability_panels_are_rank_invariant(rsa):
+    """ringseq tests/test_ring_attention.py:67-76: each rank's panel equals the
+    matching rows of the single-device panel.  With c a multiple of the
+    128-key tile the fused kernels reduce in the same order for every N, so the
+    panels agree bitwise."""
+    pkg, ra = rsa
+    q, k, v, g = _inputs(1, 2, 512, 64, seed=3)
+    _, f1, _ = _run(pkg, ra, q, k, v, g, 1, "fused")
+    _, f4, _ = _run(pkg, ra, q, k, v, g, 4, "fused")
+    full = f1.probs[0]
+    for d in range(4):
+        assert torch.equal(f4.probs[d], full[..., d * 128:(d + 1) * 128, :])
+
+
+def test_single_rank_matches_attention_oracle(rsa):
+    pkg, ra = rsa
+    q, k, v, g = _inputs(1, 2, 256, 64, seed=11)
+    _, fwd, bwd = _run(pkg, ra, q, k, v, g, 1, "auto")
+    _gate("out", _np(fwd.outputs[0]), orc.attention_forward(q, k, v, exact=False))
+    want = orc.attention_backward(q, k, v, g, exact=False)
+    for got, ref, name in zip((bwd.grad_q[0], bwd.grad_k[0], bwd.grad_v[0]), want, "qkv"):
+        _gate("d" + name, _np(got), ref)
+
+
+def test_ledgers_are_exact(rsa):
+    pkg, ra = rsa
+    # tests/test_acceptance.py:183-204: B2 Z12 L512 A64 N4
+    q, k, v, g = _inputs(2, 12, 512, 64, seed=0)
+    _, fwd, bwd = _run(pkg, ra, q, k, v, g, 4, "auto")
+    for t in fwd.ledger.devices:
+        assert t.total_elements() == 1_179_648
+    for t in bwd.ledger.devices:
+        assert t.total_elements() == 3_538_944
+        assert t.ring_p2p_elements == 2 * 3 * 2 * 12 * 128 * 64
+    # tests/test_ring_attention.py:78-84
+    q, k, v, g = _inputs(1, 2, 8, 4, seed=1)
+    _, fwd, _ = _run(pkg, ra, q, k, v, g, 4, "auto")
+    assert all(t.ring_p2p_elements == 96 for t in fwd.ledger.devices)
+    _, fwd1, bwd1 = _run(pkg, ra, q, k, v, g, 1, "auto")
+    assert fwd1.ledger.total_elements() == 0 and bwd1.ledger.total_elements() == 0
+
+
+def test_errors_match_reference(rsa):
+    pkg, ra = rsa
+    cfg = _cfg(pkg, 1, 1, 8, 2, 4)
+    x = orc.make_rng(0).standard_normal((1, 1, 8, 2))
+    halves = orc.chunks_of(x, 2)
+    with pytest.raises(pkg.ShapeError, match="chunks"):
+        ra.ring_attention_forward(halves, halves, halves, cfg)
+    cfg2 = _cfg(pkg, 1, 1, 8, 2, 2)
+    good = orc.chunks_of(np.zeros((1, 1, 8, 2)), 2)
+    bad = orc.chunks_of(np.zeros((1, 1, 8, 3)), 2)
+    with pytest.raises(pkg.ShapeError, match="expected"):
+        ra.ring_attention_forward(good, bad, good, cfg2)
+    cfg3 = _cfg(pkg, 1, 1, 4, 2, 2)
+    ch = orc.chunks_of(np.zeros((1, 1, 4, 2)), 2)
+    with pytest.raises(pkg.StateError, match="saved"):
+        ra.ring_attention_backward(ch, ch, ch, None, ch, cfg3)
+    with pytest.raises(pkg.ShapeError, match="probs"):
+        ra.ring_attention_backward(ch, ch, ch, [np.zeros((1, 1, 2, 2))] * 2, ch, cfg3)
+    with pytest.raises(pkg.ConfigError):
+        ra.ring_attention_forward(ch, ch, ch, cfg3, executor="bogus")
+
+
+@pytest.mark.parametrize("path", ["fused", "staged"])
+def test_nonfinite_input_raises_numeric_error(rsa, path):
+    pkg, ra = rsa
+    q, k, v, _ = _inputs(1, 1, 128, 64, seed=2)
+    q[0, 0, 3, 5] = np.inf
+    cfg = _cfg(pkg, 1, 1, 128, 64, 2)
+    ch = lambda x: orc.chunks_of(x, 2)  # noqa: E731
+    with pytest.raises(pkg.NumericError):
+        ra.ring_attention_forward(ch(q), ch(k), ch(v), cfg, path=path)
+
+
+def test_executor_choice_does_not_change_results(rsa):
+    pkg, ra = rsa
+    q, k, v, _ = _inputs(1, 2, 256, 64, seed=4)
+    cfg = _cfg(pkg, 1, 2, 256, 64, 4)
+    ch = lambda x: orc.chunks_of(x, 4)  # noqa: E731
+    a = ra.ring_attention_forward(ch(q), ch(k), ch(v), cfg, executor="sequential")
+    b = ra.ring_attention_forward(ch(q), ch(k), ch(v), cfg, executor="concurrent")
+    for x, y in zip(a.outputs + list(a.probs), b.outputs + list(b.probs)):
+        assert torch.equal(x, y)
+    assert a.ledger == b.ledger
+
+
+def test_layer_wrapper_matches_multi_head_oracle(rsa):
+    pkg, ra = rsa
+    b, seq, z, a, n = 2, 256, 2, 64, 4
+    h = z * a
+    rng = orc.make_rng(60)
+    x = orc.bf16_round(rng.standard_normal((b, seq, h)))
+    s = 1.0 / math.sqrt(h)
+    ws = [orc.bf16_round(rng.standard_normal((h, h)) * s) for _ in range(4)]
+    cfg = pkg.AttentionConfig(batch_size=b, seq_len=seq, hidden_size=h, num_heads=z, head_size=a, num_devices=n)
+    w = pkg.AttentionWeights(*ws)
+    results, ledger = ra.sequence_parallel_attention(orc.chunks_of(x, n), w, cfg)
+    want = orc.multi_head_forward(x, *ws, num_heads=z, exact=False)
+    # two extra bf16 roundings (projections, merged heads) before the output GEMM
+    got = _np(pkg.gather_sequence(results))
+    rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert rel <= 2e-2, rel
+    assert all(t.ring_p2p_elements == 2 * (n - 1) * b * z * (seq // n) * a for t in ledger.devices)
