@@ -1,0 +1,292 @@
+"""RSA across real ranks: one process per GPU, rings over torch.distributed (NCCL).
+
+This is the multi-GPU form of ringseq/ring_attention.py:124-217.  Rank d
+holds only its own (B, Z, c, A) chunks; keys and values travel d -> d+1 by
+NCCL send/recv (``batch_isend_irecv``), exactly the reference's ring
+(ringseq/ring_attention.py:67-79, ringseq/cluster.py:293-318), and the
+per-hop arithmetic runs in the same sm_100a kernels the single-GPU path
+uses, launched with ``n_org = 1`` for the origin that just arrived.
+
+Schedule per rank (h = hop, origin j = (d - h) mod N):
+
+  forward   K ring: hop h+1 is posted before hop h's rsa_fwd_stats runs, so
+            the transfer overlaps the kernel; received chunks land directly
+            in a per-origin slot (no copies).  V ring: rsa_fwd_probs_pv per
+            hop -- it needs K_j again, taken from the slots filled by the K
+            ring (the reference discards them; keeping them costs L*A per
+            head and no extra communication).
+  backward  V ring: rsa_bwd_dkdv per hop writes this rank's dK/dV
+            contribution for origin j into full-length fp32 partials and the
+            dS panel block j.  K ring: rsa_bwd_dq accumulates dQ.  The two
+            partials are then summed across ranks: ``reduce_scatter`` by
+            default (each rank receives only its own rows -- half the bytes
+            of the reference's all-reduce + slice), ``all_reduce`` in
+            ``mode="paper"``.
+
+The ledger charges what the reference charges (element counts, all-reduce
+convention); ``wire_bytes`` records the bytes actually sent.
+
+The per-hop kernels are injected (``HopKernels``) so the schedule can be
+tested on CPU with the gloo backend (tests/test_distributed_gloo.py) using a
+test-only implementation; the product path always uses ``CudaHopKernels``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import torch
+import torch.distributed as dist
+
+from .cluster import CommLedger
+
+__all__ = ["SpmdRing", "CudaHopKernels", "RingContext", "bench_main"]
+
+
+def _acc_dtype(t: torch.Tensor) -> torch.dtype:
+    """Cross-hop accumulators: fp32 for bf16 chunks, else the chunk dtype."""
+    return torch.float32 if t.dtype == torch.bfloat16 else t.dtype
+
+
+class CudaHopKernels:
+    """Per-hop launches of the fused kernels (librsa_b200.so)."""
+
+    def __init__(self):
+        from . import engine
+        from ._native import BF16, RsaGeom, check, lib
+
+        self.engine, self.BF16, self.RsaGeom, self.check, self.lib = engine, BF16, RsaGeom, check, lib
+
+    def _g(self, q, seq, origin):
+        _, b, z, c, a = q.shape
+        return self.RsaGeom(1, b, z, c, a, seq, origin, 1, 1.0 / math.sqrt(a))
+
+    def _st(self, t):
+        return torch.cuda.current_stream(t.device).cuda_stream
+
+    def new_stats(self, q, n):
+        _, b, z, c, _ = q.shape
+        return torch.empty((n * b * z * c * 2,), dtype=torch.float32, device=q.device)
+
+    def stats(self, q, k_j, origin, seq, stats, flag):
+        g = self._g(q, seq, origin)
+        v = self.engine._view
+        self.check(self.lib().rsa_fwd_stats(ctypes.byref(g), v(q), v(k_j), stats.data_ptr(), origin,
+                                            flag.data_ptr(), self._st(q)), "rsa_fwd_stats")
+
+    def probs_pv(self, q, k_j, v_j, origin, seq, stats, n_slots, panel, o_acc, accumulate, o_out):
+        g = self._g(q, seq, origin)
+        v = self.engine._view
+        self.check(self.lib().rsa_fwd_probs_pv(ctypes.byref(g), v(q), v(k_j), v(v_j), stats.data_ptr(), n_slots,
+                                               v(panel), v(o_acc), int(accumulate), v(o_out), self._st(q)),
+                   "rsa_fwd_probs_pv")
+
+    def rowdot(self, grad, out):
+        from . import tensor_ops
+
+        return tensor_ops.rowdot(grad, out)
+
+    def dkdv(self, q, v_j, grad, panel, dvec, ds, origin, seq, dk_j, dv_j):
+        g = self._g(q, seq, origin)
+        v = self.engine._view
+        self.check(self.lib().rsa_bwd_dkdv(ctypes.byref(g), v(q), v(v_j), v(grad), v(panel), dvec.data_ptr(), v(ds),
+                                           v(dk_j), v(dv_j), 0, 0, self._st(q)), "rsa_bwd_dkdv")
+
+    def dq(self, ds, k_j, origin, seq, dq_acc, accumulate, dq_out):
+        g = self._g(k_j, seq, origin)
+        v = self.engine._view
+        self.check(self.lib().rsa_bwd_dq(ctypes.byref(g), v(ds), v(k_j), v(dq_acc), int(accumulate), v(dq_out),
+                                         self._st(k_j)), "rsa_bwd_dq")
+
+
+@dataclass
+class RingContext:
+    """What the forward keeps for the backward (the reference keeps only probs)."""
+
+    q: torch.Tensor
+    k_slots: torch.Tensor
+    panel: torch.Tensor
+    out: torch.Tensor
+    v_local: torch.Tensor
+    extra: dict = field(default_factory=dict)
+
+
+class SpmdRing:
+    """One rank's view of the RSA ring over a torch.distributed process group."""
+
+    def __init__(self, group=None, kernels=None, mode: str = "reduce_scatter", overlap: bool = True):
+        if mode not in ("reduce_scatter", "paper"):
+            raise ValueError(f"unknown mode {mode!r}")
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.kernels = kernels or CudaHopKernels()
+        self.mode = mode
+        self.overlap = overlap
+        self.ledger = CommLedger(self.world)
+
+    # ---- communication -------------------------------------------------
+
+    def _post(self, send: torch.Tensor, recv: torch.Tensor):
+        """Post one ring hop (send to rank+1, receive from rank-1); returns works."""
+        n = self.world
+        nxt = dist.get_global_rank(self.group, (self.rank + 1) % n) if self.group else (self.rank + 1) % n
+        prv = dist.get_global_rank(self.group, (self.rank - 1) % n) if self.group else (self.rank - 1) % n
+        ops = [dist.P2POp(dist.isend, send, nxt, self.group), dist.P2POp(dist.irecv, recv, prv, self.group)]
+        self.ledger.record_ring_send(self.rank, send.numel(), send.numel() * send.element_size())
+        return dist.batch_isend_irecv(ops)
+
+    @staticmethod
+    def _wait(works):
+        for w in works or ():
+            w.wait()
+
+    def _circulate(self, slots: torch.Tensor, on_arrival):
+        """Run the ring over per-origin ``slots`` ([N][...]); slot d must hold
+        the local chunk.  ``on_arrival(h, j)`` runs once slot j is valid."""
+        n, d = self.world, self.rank
+        pending = self._post(slots[d], slots[(d - 1) % n]) if n > 1 and self.overlap else None
+        for h in range(n):
+            j = (d - h) % n
+            if h > 0:
+                if not self.overlap:
+                    pending = self._post(slots[(j + 1) % n], slots[j])
+                self._wait(pending)
+                pending = None
+                if self.overlap and h + 1 < n:
+                    pending = self._post(slots[j], slots[(j - 1) % n])
+            on_arrival(h, j)
+        self._wait(pending)
+
+    # ---- protocol --------------------------------------------------------
+
+    def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, flag: torch.Tensor | None = None):
+        """q/k/v: this rank's [1][B][Z][c][A] chunks.  Returns (out, ctx)."""
+        kern = self.kernels
+        n, d = self.world, self.rank
+        _, b, z, c, a = q.shape
+        seq = n * c
+        dev = q.device
+        if flag is None:
+            flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        k_slots = torch.empty((n, b, z, c, a), dtype=k.dtype, device=dev)
+        k_slots[d].copy_(k[0])
+        stats = kern.new_stats(q, n)
+        self._circulate(k_slots, lambda h, j: kern.stats(q, k_slots[j:j + 1], j, seq, stats, flag))
+        v_slots = torch.empty((n, b, z, c, a), dtype=v.dtype, device=dev)
+        v_slots[d].copy_(v[0])
+        panel = torch.empty((1, b, z, c, seq), dtype=q.dtype, device=dev)
+        o_acc = torch.empty((1, b, z, c, a), dtype=_acc_dtype(q), device=dev)
+        out = torch.empty((1, b, z, c, a), dtype=q.dtype, device=dev)
+
+        def pv(h, j):
+            kern.probs_pv(q, k_slots[j:j + 1], v_slots[j:j + 1], j, seq, stats, n, panel, o_acc, h > 0,
+                          out if h == n - 1 else None)
+
+        self._circulate(v_slots, pv)
+        return out, RingContext(q=q, k_slots=k_slots, panel=panel, out=out, v_local=v, extra={"flag": flag})
+
+    def backward(self, ctx: RingContext, grad: torch.Tensor):
+        """grad: this rank's [1][B][Z][c][A] dO.  Returns (dq, dk, dv) chunks."""
+        kern = self.kernels
+        n, d = self.world, self.rank
+        _, b, z, c, a = grad.shape
+        seq = n * c
+        dev = grad.device
+        dvec = kern.rowdot(grad, ctx.out)
+        ds = torch.empty_like(ctx.panel)
+        dk_part = torch.empty((n, b, z, c, a), dtype=_acc_dtype(grad), device=dev)
+        dv_part = torch.empty_like(dk_part)
+        v_slots = torch.empty((n, b, z, c, a), dtype=ctx.v_local.dtype, device=dev)
+        v_slots[d].copy_(ctx.v_local[0])
+        self._circulate(v_slots, lambda h, j: kern.dkdv(ctx.q, v_slots[j:j + 1], grad, ctx.panel, dvec, ds, j, seq,
+                                                        dk_part[j:j + 1], dv_part[j:j + 1]))
+        # K ring (the reference re-circulates keys: ringseq/ring_attention.py:192-196)
+        k_slots = torch.empty_like(ctx.k_slots)
+        k_slots[d].copy_(ctx.k_slots[d])
+        dq_acc = torch.empty((1, b, z, c, a), dtype=_acc_dtype(grad), device=dev)
+        dq = torch.empty((1, b, z, c, a), dtype=grad.dtype, device=dev)
+        self._circulate(k_slots, lambda h, j: kern.dq(ds, k_slots[j:j + 1], j, seq, dq_acc, h > 0,
+                                                      dq if h == n - 1 else None))
+        dk = self._reduce(dk_part)
+        dv = self._reduce(dv_part)
+        return dq, dk.to(grad.dtype), dv.to(grad.dtype)
+
+    def _reduce(self, part: torch.Tensor) -> torch.Tensor:
+        """Sum full-length partials over ranks; return this rank's [1][...] rows."""
+        n, d = self.world, self.rank
+        self.ledger.record_allreduce(d, part.numel())
+        if n == 1:
+            return part[d:d + 1]
+        use_rs = self.mode == "reduce_scatter" and dist.get_backend(self.group) == "nccl"
+        if use_rs:
+            out = torch.empty_like(part[0:1])
+            dist.reduce_scatter_tensor(out, part, group=self.group)
+            self.ledger.devices[d].wire_bytes += part.numel() * part.element_size() * (n - 1) // n
+            return out
+        dist.all_reduce(part, group=self.group)
+        self.ledger.devices[d].wire_bytes += 2 * part.numel() * part.element_size() * (n - 1) // n
+        return part[d:d + 1].clone()
+
+
+# ------------------------------------------------------------------ bench
+
+def bench_main(args, metric, unit, config):
+    """Multi-GPU arm of bench.py (launched under torchrun, one rank per GPU)."""
+    import json
+    import os
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, rank = dist.get_world_size(), dist.get_rank()
+    dev = torch.device("cuda", local)
+    B, Z, L, A, LAYERS = args.batch * n, args.heads, args.seq, args.head_size, args.layers
+    if L % n:
+        raise SystemExit(f"seq {L} not divisible by {n} ranks")
+    c = L // n
+    ring = SpmdRing()
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+
+    def rnd():
+        return torch.randn((1, B, Z, c, A), generator=gen, device=dev).to(torch.bfloat16)
+
+    layers = [dict(q=rnd(), k=rnd(), v=rnd(), g=rnd()) for _ in range(LAYERS)]
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def step():
+        ctxs = []
+        for ly in layers:
+            _, ctx = ring.forward(ly["q"], ly["k"], ly["v"], flag)
+            ctxs.append(ctx)
+        for ly, ctx in zip(reversed(layers), reversed(ctxs)):
+            ring.backward(ctx, ly["g"])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    if rank == 0:
+        value = B * L / (ms / 1e3)
+        print(json.dumps({
+            "metric": metric, "value": value, "unit": unit, "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic N(0,1) bf16 inputs, per-layer q/k/v/dO", "config": config,
+            "gpu_launches": (LAYERS * (2 * n + 2 * n + 1)) * args.steps,
+            "comm": {"mode": ring.mode, "wire_bytes_per_rank_per_step":
+                     ring.ledger.devices[rank].wire_bytes // max(1, args.steps + args.warmup)},
+        }), flush=True)
+    dist.destroy_process_group()

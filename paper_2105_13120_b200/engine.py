@@ -34,9 +34,66 @@ from . import tensor_ops as ops
 from ._native import BF16, F32, RsaGeom, RsaView, check, lib
 from .errors import ShapeError
 
-__all__ = ["fused_supported", "forward", "backward", "recompute_outputs", "NULL_VIEW"]
+__all__ = ["fused_supported", "forward", "backward", "recompute_outputs", "NULL_VIEW", "KernelTimer"]
 
 NULL_VIEW = RsaView(None, 0, 0, 0, 0)
+
+
+class KernelTimer:
+    """Per-kernel CUDA-event timing on the launching stream (bench instrumentation).
+
+    ``with timer("fwd_pv"): launch(...)`` records an event pair around the
+    launch; ``totals()`` returns {name: (launches, total_ms)} after a sync.
+    """
+
+    def __init__(self):
+        self.events: dict[str, list] = {}
+        self.enabled = True
+
+    def __call__(self, name: str):
+        return _Span(self, name)
+
+    def totals(self) -> dict:
+        torch.cuda.synchronize()
+        return {k: (len(v), sum(a.elapsed_time(b) for a, b in v)) for k, v in self.events.items()}
+
+    def reset(self) -> None:
+        self.events.clear()
+
+
+class _Span:
+    __slots__ = ("t", "name", "a")
+
+    def __init__(self, t, name):
+        self.t, self.name = t, name
+
+    def __enter__(self):
+        if self.t.enabled:
+            self.a = torch.cuda.Event(enable_timing=True)
+            self.a.record()
+
+    def __exit__(self, *exc):
+        if self.t.enabled:
+            b = torch.cuda.Event(enable_timing=True)
+            b.record()
+            self.t.events.setdefault(self.name, []).append((self.a, b))
+
+
+class _NoTimer:
+    def __call__(self, name):
+        return _NULL_SPAN
+
+
+class _NullSpan:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *exc):
+        return False
+
+
+_NULL_SPAN = _NullSpan()
+_NO_TIMER = _NoTimer()
 
 
 def _stream(t: torch.Tensor) -> int:
@@ -74,7 +131,7 @@ def _pick(path: str, n, b, z, c, a) -> str:
 
 def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, path: str = "auto",
             flag: torch.Tensor | None = None, out: torch.Tensor | None = None,
-            panel: torch.Tensor | None = None):
+            panel: torch.Tensor | None = None, stats: torch.Tensor | None = None, timer=None):
     """RSA forward on stacked [N][B][Z][c][A] bf16 chunks.
 
     Returns (outputs [N][B][Z][c][A] bf16, panels [N][B][Z][c][L] bf16,
@@ -92,14 +149,18 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, path: str = "a
         panel = torch.empty((n, b, z, c, seq), dtype=torch.bfloat16, device=dev)
     which = _pick(path, n, b, z, c, a)
     if which == "fused":
+        tm = timer or _NO_TIMER
         L = lib()
         st = _stream(q)
         g = _geom(n, b, z, c, a, seq, 0, n)
-        stats = torch.empty((n * b * z * c * 2,), dtype=torch.float32, device=dev)
-        check(L.rsa_fwd_stats(ctypes.byref(g), _view(q), _view(k), stats.data_ptr(), 0, flag.data_ptr(), st),
-              "rsa_fwd_stats")
-        check(L.rsa_fwd_probs_pv(ctypes.byref(g), _view(q), _view(k), _view(v), stats.data_ptr(), 1, _view(panel),
-                                 NULL_VIEW, 0, _view(out), st), "rsa_fwd_probs_pv")
+        if stats is None:
+            stats = torch.empty((n * b * z * c * 2,), dtype=torch.float32, device=dev)
+        with tm("fwd_stats"):
+            check(L.rsa_fwd_stats(ctypes.byref(g), _view(q), _view(k), stats.data_ptr(), 0, flag.data_ptr(), st),
+                  "rsa_fwd_stats")
+        with tm("fwd_probs_pv"):
+            check(L.rsa_fwd_probs_pv(ctypes.byref(g), _view(q), _view(k), _view(v), stats.data_ptr(), 1,
+                                     _view(panel), NULL_VIEW, 0, _view(out), st), "rsa_fwd_probs_pv")
         return out, panel, flag
     _forward_staged(q, k, v, out, panel, flag)
     return out, panel, flag
@@ -144,26 +205,41 @@ def recompute_outputs(panel: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path: str = "auto"):
-    """RSA backward on stacked chunks; returns (dq, dk, dv) as [N][B][Z][c][A] bf16."""
+def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path: str = "auto",
+             grads: tuple | None = None, ds: torch.Tensor | None = None, dvec: torch.Tensor | None = None,
+             timer=None):
+    """RSA backward on stacked chunks; returns (dq, dk, dv) as [N][B][Z][c][A] bf16.
+
+    ``grads`` / ``ds`` / ``dvec`` optionally supply preallocated output,
+    dS-panel and D buffers (the bench reuses them across layers)."""
     n, b, z, c, a = q.shape
     seq = n * c
     dev = q.device
-    dq = torch.empty((n, b, z, c, a), dtype=torch.bfloat16, device=dev)
-    dk = torch.empty_like(dq)
-    dv = torch.empty_like(dq)
+    if grads is None:
+        dq = torch.empty((n, b, z, c, a), dtype=torch.bfloat16, device=dev)
+        dk = torch.empty_like(dq)
+        dv = torch.empty_like(dq)
+    else:
+        dq, dk, dv = grads
     which = _pick(path, n, b, z, c, a)
     if which == "fused":
+        tm = timer or _NO_TIMER
         if outputs is None:
             outputs = recompute_outputs(panel, v)
-        dvec = ops.rowdot(grad, outputs)  # D = rowsum(dO * O) = rowsum(dP * P)
-        ds = torch.empty((n, b, z, c, seq), dtype=torch.bfloat16, device=dev)
+        if dvec is None:
+            dvec = torch.empty((n, b, z, c), dtype=torch.float32, device=dev)
+        with tm("rowdot"):
+            ops.rowdot(grad, outputs, out=dvec)  # D = rowsum(dO * O) = rowsum(dP * P)
+        if ds is None:
+            ds = torch.empty((n, b, z, c, seq), dtype=torch.bfloat16, device=dev)
         L = lib()
         st = _stream(q)
         g = _geom(n, b, z, c, a, seq, 0, n)
-        check(L.rsa_bwd_dkdv(ctypes.byref(g), _view(q), _view(v), _view(grad), _view(panel), dvec.data_ptr(),
-                             _view(ds), _view(dk), _view(dv), BF16, 0, st), "rsa_bwd_dkdv")
-        check(L.rsa_bwd_dq(ctypes.byref(g), _view(ds), _view(k), NULL_VIEW, 0, _view(dq), st), "rsa_bwd_dq")
+        with tm("bwd_dkdv"):
+            check(L.rsa_bwd_dkdv(ctypes.byref(g), _view(q), _view(v), _view(grad), _view(panel), dvec.data_ptr(),
+                                 _view(ds), _view(dk), _view(dv), BF16, 0, st), "rsa_bwd_dkdv")
+        with tm("bwd_dq"):
+            check(L.rsa_bwd_dq(ctypes.byref(g), _view(ds), _view(k), NULL_VIEW, 0, _view(dq), st), "rsa_bwd_dq")
         return dq, dk, dv
     _backward_staged(q, k, v, panel, grad, dq, dk, dv)
     return dq, dk, dv
