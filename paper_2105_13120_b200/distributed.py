@@ -94,6 +94,24 @@ class CudaHopKernels:
         self.check(self.lib().rsa_bwd_dkdv(ctypes.byref(g), v(q), v(v_j), v(grad), v(panel), dvec.data_ptr(), v(ds),
                                            v(dk_j), v(dv_j), 0, 0, self._st(q)), "rsa_bwd_dkdv")
 
+    def project_pair(self, e_cols, k, f_cols, v):
+        """[E_d K_d ; F_d V_d] as one fp32 [2][B][Z][K][A] buffer (tcgen05 GEMMs)."""
+        from . import tensor_ops
+
+        b, z, _, a = k.shape
+        out = torch.empty((2, b, z, e_cols.shape[0], a), dtype=torch.float32, device=k.device)
+        tensor_ops.matmul(e_cols, k, out=out[0])
+        tensor_ops.matmul(f_cols, v, out=out[1])
+        return out
+
+    def low_rank_attention(self, q, k_low, v_low):
+        """softmax(Q K'^T / sqrt(A)) V' with rows fully local."""
+        from . import tensor_ops
+
+        scores = tensor_ops.matmul(q, k_low.to(torch.bfloat16).transpose(-1, -2))
+        probs = tensor_ops.softmax_rows(scores, scale=1.0 / math.sqrt(q.shape[-1]), out_dtype=torch.bfloat16)
+        return tensor_ops.matmul(probs, v_low.to(torch.bfloat16), out_dtype=torch.bfloat16)
+
     def dq(self, ds, k_j, origin, seq, dq_acc, accumulate, dq_out):
         g = self._g(k_j, seq, origin)
         v = self.engine._view
@@ -213,6 +231,27 @@ class SpmdRing:
         dk = self._reduce(dk_part)
         dv = self._reduce(dv_part)
         return dq, dk.to(grad.dtype), dv.to(grad.dtype)
+
+    def linformer_forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, e_cols: torch.Tensor,
+                          f_cols: torch.Tensor) -> torch.Tensor:
+        """Sequence-sharded Linformer forward (ringseq/sparse_attention.py:74-133).
+
+        q/k/v: this rank's [1][B][Z][c][A] chunks; e_cols/f_cols: this rank's
+        (K, c) column blocks of the projections.  The two partial projections
+        are summed across ranks with ONE all-reduce of the concatenated
+        [K'; V'] buffer (the reference spells it as 2(N-1) ring hops; the
+        ledger charges that convention, wire_bytes the all-reduce).
+        """
+        kern = self.kernels
+        n, d = self.world, self.rank
+        _, b, z, c, a = q.shape
+        kdim = e_cols.shape[0]
+        low = kern.project_pair(e_cols, k[0], f_cols, v[0])  # [2][B][Z][K][A] accumulator dtype
+        self.ledger.record_ring_send(d, 2 * (n - 1) * b * z * kdim * a)
+        if n > 1:
+            dist.all_reduce(low, group=self.group)
+            self.ledger.devices[d].wire_bytes += 2 * low.numel() * low.element_size() * (n - 1) // n
+        return kern.low_rank_attention(q, low[0], low[1])
 
     def _reduce(self, part: torch.Tensor) -> torch.Tensor:
         """Sum full-length partials over ranks; return this rank's [1][...] rows."""

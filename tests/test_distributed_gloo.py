@@ -124,3 +124,50 @@ def test_spmd_ring_matches_oracle(world, mode, overlap):
         # forward K+V rings, backward V+K rings: 4(N-1) chunks; two all-reduces
         assert r["ring"] == ring_f + ring_b
         assert r["ar"] == ar_b
+
+
+class CpuLinformerKernels(CpuHopKernels):
+    def project_pair(self, e_cols, k, f_cols, v):
+        return torch.stack([e_cols @ k, f_cols @ v])
+
+    def low_rank_attention(self, q, k_low, v_low):
+        s = q @ k_low.transpose(-1, -2) / math.sqrt(q.shape[-1])
+        return torch.softmax(s, -1) @ v_low
+
+
+def _lin_worker(rank, world, port, shape, seed, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2105_13120_b200.distributed import SpmdRing
+
+        b, z, seq, a, kp = shape
+        rng = orc.make_rng(seed)
+        q, k, v = (rng.standard_normal((b, z, seq, a)) for _ in range(3))
+        e, f = rng.standard_normal((kp, seq)), rng.standard_normal((kp, seq))
+        ch = lambda x: torch.from_numpy(orc.chunks_of(x, world)[rank][None].copy())  # noqa: E731
+        c = seq // world
+        ring = SpmdRing(kernels=CpuLinformerKernels())
+        out = ring.linformer_forward(ch(q), ch(k), ch(v), torch.from_numpy(e[:, rank * c:(rank + 1) * c].copy()),
+                                     torch.from_numpy(f[:, rank * c:(rank + 1) * c].copy()))
+        results[rank] = {"out": out[0].numpy(), "ring": ring.ledger.devices[rank].ring_p2p_elements}
+    finally:
+        dist.destroy_process_group()
+
+
+def test_spmd_linformer_matches_oracle():
+    world, shape, seed = 2, (2, 3, 40, 5, 7), 51
+    mgr = mp.get_context("spawn").Manager()
+    results = mgr.dict()
+    mp.start_processes(_lin_worker, args=(world, _free_port(), shape, seed, results), nprocs=world, join=True,
+                       start_method="spawn")
+    b, z, seq, a, kp = shape
+    rng = orc.make_rng(seed)
+    q, k, v = (rng.standard_normal((b, z, seq, a)) for _ in range(3))
+    e, f = rng.standard_normal((kp, seq)), rng.standard_normal((kp, seq))
+    ch = lambda x: orc.chunks_of(x, world)  # noqa: E731
+    outs, ring = orc.sparse_ring_forward(ch(q), ch(k), ch(v), e, f, exact=False)
+    for d in range(world):
+        assert np.max(np.abs(results[d]["out"] - outs[d])) <= 1e-12
+        assert results[d]["ring"] == ring
