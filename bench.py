@@ -205,10 +205,12 @@ def kernel_model(name, n, b, z, c, seq, a):
         return 2 * 2 * ce, 2 * pe * a                 # read Q, K; S = QK^T
     if name == "fwd_probs_pv":
         return 2 * pe + 2 * 4 * ce, 4 * pe * a        # write P; read Q,K,V, write O
+    if name == "fwd_resident":
+        return 2 * pe + 2 * 4 * ce, 6 * pe * a        # write P; Q,K,V in, O out; QK^T twice + PV
     if name == "bwd_dkdv":
-        return 4 * pe + 2 * 5 * ce, 6 * pe * a        # read P, write dS; dO,Q,V in, dK,dV out
+        return 2 * pe + 2 * 5 * ce, 6 * pe * a        # read P; dO,Q,V in, dK,dV out; dO V^T, P^T dO, dS^T Q
     if name == "bwd_dq":
-        return 2 * pe + 2 * 2 * ce, 2 * pe * a        # read dS; K in, dQ out
+        return 2 * pe + 2 * 4 * ce, 4 * pe * a        # read P; dO,K,V in, dQ out; dO V^T, dS K
     if name == "rowdot":
         return 2 * 2 * ce + 4 * n * b * z * c, 2 * ce
     return 0, 0
@@ -240,19 +242,16 @@ def ours(args):
         ly["o"] = torch.empty_like(ly["q"])
         ly["p"] = torch.empty((1, B, Z, c, L), dtype=torch.bfloat16, device=dev)
         ly["grads"] = (torch.empty_like(ly["q"]), torch.empty_like(ly["q"]), torch.empty_like(ly["q"]))
-    ds = torch.empty((1, B, Z, c, L), dtype=torch.bfloat16, device=dev)
-    stats = torch.empty((B * Z * c * 2,), dtype=torch.float32, device=dev)
     dvec = torch.empty((1, B, Z, c), dtype=torch.float32, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     timer = engine.KernelTimer()
 
     def step(tm=None):
         for ly in layers:
-            engine.forward(ly["q"], ly["k"], ly["v"], path="fused", flag=flag, out=ly["o"], panel=ly["p"],
-                           stats=stats, timer=tm)
+            engine.forward(ly["q"], ly["k"], ly["v"], path="fused", flag=flag, out=ly["o"], panel=ly["p"], timer=tm)
         for ly in reversed(layers):
             engine.backward(ly["q"], ly["k"], ly["v"], ly["p"], ly["g"], outputs=ly["o"], path="fused",
-                            grads=ly["grads"], ds=ds, dvec=dvec, timer=tm)
+                            grads=ly["grads"], dvec=dvec, timer=tm)
 
     for _ in range(args.warmup):
         step()

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define RSA_ABI_VERSION 1
+#define RSA_ABI_VERSION 2
 
 enum rsa_status {
   RSA_OK = 0,
@@ -132,22 +132,35 @@ int rsa_fwd_probs_pv(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, cons
                      rsa_view panel, rsa_view o_acc, int accumulate, rsa_view o_out, void* stream);
 
 /*
- * V-ring half of the RSA backward (ringseq/ring_attention.py:180-205):
- * dP = dO V_j^T, dS = P (dP - D) scale written to the dS panel, and the
- * key/value gradient contributions dK_j = dS_j^T Q, dV_j = P_j^T dO summed
- * over the launch's query ranks.  D[row] = rowsum(dO * O) (see rsa_rowdot).
- * dk/dv are fp32 (accumulate != 0 adds) or bf16 outputs per dkv_dtype.
+ * Both forward stages in one launch when every origin is resident (N logical
+ * ranks in one GPU's HBM, or N = 1): per query tile a statistics pass over
+ * all keys, then the probability/PV pass; replaces _score_panel +
+ * _apply_values (ringseq/ring_attention.py:89-103) for all ranks at once.
+ */
+int rsa_fwd_resident(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view panel, rsa_view o_out,
+                     int* nonfinite_flag, void* stream);
+
+/*
+ * V-ring half of the RSA backward (ringseq/ring_attention.py:180-205) for
+ * the resident origins: per key tile, dP = dO V_j^T and the softmax Jacobian
+ * dS = P (dP - D) scale (kept in shared memory, never written to HBM), then
+ * the key/value gradient contributions dK_j = dS_j^T Q, dV_j = P_j^T dO
+ * summed over the launch's query ranks (the all-reduce of
+ * ringseq/ring_attention.py:206-209 when the ranks are resident).
+ * D[row] = rowsum(dO * O) = rowsum(dP * P) (see rsa_rowdot).  dk/dv are fp32
+ * (accumulate != 0 adds) or bf16 outputs per dkv_dtype.
  */
 int rsa_bwd_dkdv(const rsa_geom* g, rsa_view q, rsa_view v, rsa_view dout, rsa_view panel, const float* dvec,
-                 rsa_view ds_panel, rsa_view dk, rsa_view dv, int dkv_dtype, int accumulate, void* stream);
+                 rsa_view dk, rsa_view dv, int dkv_dtype, int accumulate, void* stream);
 
 /*
  * K-ring half of the RSA backward (ringseq/ring_attention.py:192-196):
- * dQ = sum_j dS_j K_j over the resident origins.  dq_acc fp32 (optional,
- * accumulate != 0 adds) and/or dq_out bf16.
+ * dQ = sum_j dS_j K_j over the resident origins, with dS recomputed from
+ * P, dO V_j^T and D exactly as in rsa_bwd_dkdv (so no dS panel exists).
+ * dq_acc fp32 (optional, accumulate != 0 adds) and/or dq_out bf16.
  */
-int rsa_bwd_dq(const rsa_geom* g, rsa_view ds_panel, rsa_view k, rsa_view dq_acc, int accumulate, rsa_view dq_out,
-               void* stream);
+int rsa_bwd_dq(const rsa_geom* g, rsa_view dout, rsa_view k, rsa_view v, rsa_view panel, const float* dvec,
+               rsa_view dq_acc, int accumulate, rsa_view dq_out, void* stream);
 
 /* Can the fused kernels tile this geometry (head_dim, chunk, alignment)? */
 int rsa_fused_supported(const rsa_geom* g);

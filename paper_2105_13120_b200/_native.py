@@ -21,7 +21,7 @@ from .errors import NativeError, NativeUnavailable, NumericError, ShapeError
 __all__ = ["lib", "check", "RsaView", "RsaGeom", "LIB_PATH", "ABI_VERSION", "F32", "BF16", "EXPORTS"]
 
 LIB_PATH = Path(os.environ.get("RSA_B200_LIB", Path(__file__).resolve().parent / "librsa_b200.so"))
-ABI_VERSION = 1
+ABI_VERSION = 2
 F32, BF16 = 0, 1
 
 RSA_OK, RSA_ERR_INVALID, RSA_ERR_UNSUPPORTED, RSA_ERR_CUDA, RSA_ERR_NUMERIC = 0, 1, 2, 3, 4
@@ -84,8 +84,9 @@ EXPORTS = {
     "rsa_rowdot": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p]),
     "rsa_fwd_stats": (c_int, [_GEOM, _V, _V, c_void_p, c_int, c_void_p, c_void_p]),
     "rsa_fwd_probs_pv": (c_int, [_GEOM, _V, _V, _V, c_void_p, c_int, _V, _V, c_int, _V, c_void_p]),
-    "rsa_bwd_dkdv": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, _V, _V, _V, c_int, c_int, c_void_p]),
-    "rsa_bwd_dq": (c_int, [_GEOM, _V, _V, _V, c_int, _V, c_void_p]),
+    "rsa_fwd_resident": (c_int, [_GEOM, _V, _V, _V, _V, _V, c_void_p, c_void_p]),
+    "rsa_bwd_dkdv": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, _V, _V, c_int, c_int, c_void_p]),
+    "rsa_bwd_dq": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, _V, c_int, _V, c_void_p]),
     "rsa_fused_supported": (c_int, [_GEOM]),
 }
 

@@ -1,66 +1,78 @@
 // Fused Ring Self-Attention kernels for sm_100a (head size A = 64).
 //
-// Tensor layout (all bf16 unless noted): per-head tensors are addressed as
-// [rank][b][z][row][a] and probability / dS panels as [rank][b][z][row][col]
-// with col = origin * c + key (ringseq/ring_attention.py:91-94: column block
-// j of the panel belongs to origin j).  TMA moves 128-row x 64-column tiles
-// (one 128-byte swizzle row per tile row); every tile lives in shared memory
-// in the SWIZZLE_128B layout the UMMA descriptors read, and the same bytes are
-// read as K-major or MN-major operands as each product needs.
+// Tensor layout (bf16 unless noted): per-head tensors are [rank][b][z][row][a];
+// probability panels are [rank][b][z][row][col] with col = origin * c + key
+// (ringseq/ring_attention.py:91-94: column block j of a panel is origin j).
+// TMA moves 128-row x 64-column tiles (one 128-byte swizzle row per tile
+// row).  In shared memory every tile uses the SWIZZLE_128B layout the UMMA
+// descriptors read, and the same bytes serve as K-major or MN-major
+// operands as each product needs (P is K-major A of P.V and MN-major A of
+// P^T.dO; dO is K-major A of dO.V^T and MN-major B of P^T.dO; ...).
 //
-// Each kernel is warp-specialised, 6 warps:
-//   warp 0      TMA producer (one elected lane)
-//   warp 1      tcgen05.mma issuer (one elected lane); owns TMEM alloc
-//   warps 2..5  epilogue: warp w reads TMEM lanes 32*(w%4).. (= tile rows),
-//               so every row-wise reduction is thread-local (no shuffles)
+// All kernels are persistent (one CTA per SM walking a static work list)
+// and warp-specialised, 10 warps:
+//   warp 0      TMA producer (one lane)
+//   warp 1      tcgen05.mma issuer (one lane); owns the TMEM allocation
+//   warps 2..9  epilogue: warp w reads TMEM lanes 32*(w%4).. (tile rows) and
+//               the column half (w-2)/4 of each 128-column tile, so row
+//               reductions are thread-local plus one smem exchange.
+// Accumulators and smem tiles are double-buffered, so the MMAs of tile i+1
+// and the TMA loads of the next work item overlap the epilogue of tile i.
 //
-// rsa_fwd_stats    stage 1 (K ring): S = Q K_j^T per key tile, online row
-//                  max / sum of exp2 kept in registers -> (m, l) per row.
-// rsa_fwd_probs_pv stage 2 (V ring): S recomputed, P = 2^(S' - m) / l written
-//                  once to the bf16 panel (TMA store) and fed from smem to a
-//                  second UMMA, O += P V_j accumulating in TMEM.
-// rsa_bwd_dkdv     V-ring half of the backward, one CTA per key tile of an
-//                  origin: dP = dO V^T (TMEM), dS = P (dP - D) scale (smem +
-//                  TMA store), dV += P^T dO and dK += dS^T Q (TMEM).
-// rsa_bwd_dq       K-ring half: dQ += dS K_j.
+// rsa_fwd          K ring stage (pass A: S = Q K^T, running row max / sum of
+//                  exp2) and V ring stage (pass B: S recomputed, P = 2^(S'-m)/l
+//                  to smem -> TMA store to the bf16 panel and UMMA O += P V).
+//                  Passes A+B in one launch when every key is resident.
+// rsa_bwd_dkdv     per key tile: dP = dO V^T, dS = P (dP - D) scale (smem
+//                  only), dV += P^T dO, dK += dS^T Q over all query rows.
+// rsa_bwd_dq       per query row tile: dP, dS recomputed the same way,
+//                  dQ += dS K.  dS never goes to HBM.
 #include "common.h"
 #include "ptx.cuh"
 
 namespace rsa {
 namespace {
 
-constexpr int HD = 64;                          // head size the fused kernels tile
-constexpr int TR = 128;                         // rows per tile (UMMA M)
-constexpr int TKEYS = 128;                      // keys per tile
-constexpr uint32_t TILE = TR * HD * 2;          // 16 KB: 128 x 64 bf16
-constexpr uint32_t PTILE = TR * TKEYS * 2;      // 32 KB: 128 x 128 bf16 (two 64-key atoms)
-constexpr uint32_t ATOM = TR * 128;             // 16 KB: one 128-row x 128-byte swizzle atom column
+constexpr int HD = 64;                      // head size the fused kernels tile
+constexpr int TR = 128;                     // rows per tile (UMMA M)
+constexpr int TK = 128;                     // keys per tile
+constexpr uint32_t TILE = TR * HD * 2;      // 16 KB: 128 x 64 bf16
+constexpr uint32_t PTILE = TR * TK * 2;     // 32 KB: 128 x 128 bf16 (two 64-key atoms)
+constexpr uint32_t ATOM = TR * 128;         // 16 KB: one 128-row x 128-byte swizzle column
 constexpr float LOG2E = 1.4426950408889634f;
-constexpr int NTHREADS = 192;
+constexpr int EPI_WARPS = 8;
+constexpr int NTHREADS = 64 + 32 * EPI_WARPS;  // 320
+constexpr int EPI_THREADS = 32 * EPI_WARPS;    // 256
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+enum { MODE_PASS_A = 1, MODE_PASS_B = 2, MODE_EXT_STATS = 4, MODE_WRITE_STATS = 8 };
 
-// Write 32 consecutive fp32 values (key columns col0..col0+31 of row r) as
-// bf16 into a [key atom][128 rows][128 B] SWIZZLE_128B tile.
-__device__ __forceinline__ void st_row32_sw128(uint32_t tile_base, uint32_t r, int col0, const float* v) {
-  const uint32_t atom = col0 >> 6;
-  const uint32_t chunk0 = (col0 & 63) >> 3;
+__device__ __forceinline__ void bar_epi() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void bar_half(int h) { asm volatile("bar.sync %0, 128;" ::"r"(2 + h) : "memory"); }
+
+// Pipeline position: slot and phase of the i-th use of an n-deep ring.
+struct Pos {
+  uint32_t i = 0;
+  __device__ __forceinline__ uint32_t slot(uint32_t n) const { return i % n; }
+  __device__ __forceinline__ uint32_t phase(uint32_t n) const { return (i / n) & 1u; }
+};
+
+// 32 fp32 values of row r, columns col0..col0+31, as bf16 into a
+// [64-col atom][128 rows][128 B] SWIZZLE_128B tile.
+__device__ __forceinline__ void st_row32_sw128(uint32_t tile, uint32_t r, int col0, const float* v) {
+  const uint32_t atom = col0 >> 6, chunk0 = (col0 & 63) >> 3;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const uint32_t addr = tile_base + atom * ATOM + sw128_offset(r, chunk0 + q);
-    st_shared_v4(addr, pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
-                 pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
-  }
+  for (int q = 0; q < 4; ++q)
+    st_shared_v4(tile + atom * ATOM + sw128_offset(r, chunk0 + q), pack_bf16(v[8 * q], v[8 * q + 1]),
+                 pack_bf16(v[8 * q + 2], v[8 * q + 3]), pack_bf16(v[8 * q + 4], v[8 * q + 5]),
+                 pack_bf16(v[8 * q + 6], v[8 * q + 7]));
 }
 
-// Read 32 consecutive bf16 (columns col0..col0+31 of row r) from the same layout.
-__device__ __forceinline__ void ld_row32_sw128(uint32_t tile_base, uint32_t r, int col0, float* v) {
-  const uint32_t atom = col0 >> 6;
-  const uint32_t chunk0 = (col0 & 63) >> 3;
+__device__ __forceinline__ void ld_row32_sw128(uint32_t tile, uint32_t r, int col0, float* v) {
+  const uint32_t atom = col0 >> 6, chunk0 = (col0 & 63) >> 3;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     uint32_t w[4];
-    ld_shared_v4(tile_base + atom * ATOM + sw128_offset(r, chunk0 + q), w[0], w[1], w[2], w[3]);
+    ld_shared_v4(tile + atom * ATOM + sw128_offset(r, chunk0 + q), w[0], w[1], w[2], w[3]);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float2 f = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[e]));
@@ -70,7 +82,7 @@ __device__ __forceinline__ void ld_row32_sw128(uint32_t tile_base, uint32_t r, i
   }
 }
 
-struct OutView {  // generic strided output [rank][b][z][row][a]
+struct OutView {  // strided output [rank][b][z][row][a]
   void* ptr;
   int64_t s_rank, s_b, s_z, s_row;
 };
@@ -79,13 +91,14 @@ __device__ __forceinline__ int64_t out_off(const OutView& o, int rank, int b, in
   return int64_t(rank) * o.s_rank + int64_t(b) * o.s_b + int64_t(z) * o.s_z + int64_t(row) * o.s_row;
 }
 
-// Store 64 fp32 values of one row (fp32 accumulate and/or bf16 final).
-__device__ __forceinline__ void store_row64(const OutView& acc, const OutView& fin, int accumulate, int rank, int b,
-                                            int z, int row, float* v) {
+// Store 32 fp32 values (columns col0..col0+31 of one row): fp32 (optionally
+// accumulating) and/or bf16.
+__device__ __forceinline__ void store_row32(const OutView& acc, const OutView& fin, int accumulate, int rank, int b,
+                                            int z, int row, int col0, float* v) {
   if (acc.ptr) {
-    float* p = reinterpret_cast<float*>(acc.ptr) + out_off(acc, rank, b, z, row);
+    float* p = reinterpret_cast<float*>(acc.ptr) + out_off(acc, rank, b, z, row) + col0;
 #pragma unroll
-    for (int i = 0; i < 64; i += 4) {
+    for (int i = 0; i < 32; i += 4) {
       float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
       if (accumulate) {
         const float4 old = *reinterpret_cast<const float4*>(p + i);
@@ -96,9 +109,9 @@ __device__ __forceinline__ void store_row64(const OutView& acc, const OutView& f
     }
   }
   if (fin.ptr) {
-    __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(fin.ptr) + out_off(fin, rank, b, z, row);
+    __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(fin.ptr) + out_off(fin, rank, b, z, row) + col0;
 #pragma unroll
-    for (int i = 0; i < 64; i += 8)
+    for (int i = 0; i < 32; i += 8)
       *reinterpret_cast<uint4*>(p + i) = make_uint4(pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]),
                                                     pack_bf16(v[i + 4], v[i + 5]), pack_bf16(v[i + 6], v[i + 7]));
   }
@@ -109,190 +122,67 @@ struct Geo {
   float scale;
 };
 
-// =================================================================== stats
-
-struct StatsArgs {
-  CUtensorMap tq, tk;
-  Geo g;
-  float sl;  // scale * log2(e)
-  float2* stats;
-  int64_t slot_off;
-  int* flag;
-};
-
-constexpr int ST_STAGES = 4;
-constexpr uint32_t ST_SMEM = TILE + ST_STAGES * TILE + 256 + 1024;
-
-__global__ void __launch_bounds__(NTHREADS, 1) fwd_stats_kernel(const __grid_constant__ StatsArgs p) {
+__device__ __forceinline__ uint8_t* smem_base() {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sq = smem;
-  uint8_t* sk = smem + TILE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TILE + ST_STAGES * TILE);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;
-  uint64_t* k_empty = k_full + ST_STAGES;
-  uint64_t* s_full = k_empty + ST_STAGES;
-  uint64_t* s_empty = s_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_empty + 2);
-
-  const Geo& g = p.g;
-  const int rt = blockIdx.x, bz = blockIdx.y, d = blockIdx.z;
-  const int b = bz / g.Z, z = bz % g.Z;
-  const int r0 = rt * TR;
-  const int ntk = (g.c + TKEYS - 1) / TKEYS;
-  const int T = g.n_org * ntk;
-  const uint32_t warp = warp_id(), lane = lane_id();
-
-  if (warp == 1) tmem_alloc(tmem_slot, 256);
-  if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    for (int s = 0; s < ST_STAGES; ++s) mbar_init(&k_full[s], 1), mbar_init(&k_empty[s], 1);
-    for (int s = 0; s < 2; ++s) mbar_init(&s_full[s], 1), mbar_init(&s_empty[s], 4);
-    fence_barrier_init();
-    tma_prefetch(&p.tq);
-    tma_prefetch(&p.tk);
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, TILE);
-      tma_load_4d(sq, &p.tq, q_full, 0, r0, z, d * g.B + b);
-      for (int i = 0; i < T; ++i) {
-        const int s = i % ST_STAGES;
-        mbar_wait(&k_empty[s], ((i / ST_STAGES) & 1) ^ 1);
-        mbar_arrive_expect_tx(&k_full[s], TILE);
-        const int jo = i / ntk, k0 = (i % ntk) * TKEYS;
-        tma_load_4d(sk + s * TILE, &p.tk, &k_full[s], 0, k0, z, jo * g.B + b);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32(TR, TKEYS, 0, 0);
-      mbar_wait(q_full, 0);
-      const uint32_t qa = smem_u32(sq);
-      for (int i = 0; i < T; ++i) {
-        const int s = i % ST_STAGES, buf = i & 1;
-        mbar_wait(&k_full[s], (i / ST_STAGES) & 1);
-        mbar_wait(&s_empty[buf], ((i >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t ka = smem_u32(sk + s * TILE);
-#pragma unroll
-        for (int k = 0; k < HD / 16; ++k)
-          umma_bf16(tmem + buf * TKEYS, smem_desc_sw128(qa + k * 32, 0, 1024), smem_desc_sw128(ka + k * 32, 0, 1024),
-                    idesc, k > 0);
-        umma_commit(&k_empty[s]);
-        umma_commit(&s_full[buf]);
-      }
-    }
-  } else {
-    const uint32_t quad = warp & 3;
-    const int r = quad * 32 + lane;
-    float m = -INFINITY, l = 0.f;
-    bool bad = false;
-    for (int i = 0; i < T; ++i) {
-      const int buf = i & 1;
-      mbar_wait(&s_full[buf], (i >> 1) & 1);
-      tc_fence_after();
-      const int nvalid = min(TKEYS, g.c - (i % ntk) * TKEYS);
-#pragma unroll 1
-      for (int cc = 0; cc < TKEYS / 32; ++cc) {
-        float v[32];
-        __syncwarp();
-        tmem_ld32(tmem + ((quad * 32u) << 16) + buf * TKEYS + cc * 32, v);
-        tmem_ld_wait();
-        float cm = -INFINITY;
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float t = __fmul_rn(v[e], p.sl);
-          v[e] = (cc * 32 + e < nvalid) ? t : -INFINITY;
-          bad |= !isfinite(t);
-          cm = fmaxf(cm, v[e]);
-        }
-        if (cm > m) {
-          l *= fast_exp2(m - cm);
-          m = cm;
-        }
-#pragma unroll
-        for (int e = 0; e < 32; ++e) l += fast_exp2(v[e] - m);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[buf]);
-    }
-    const int row = r0 + r;
-    if (row < g.c) {
-      const int64_t idx = (int64_t(d * g.B + b) * g.Z + z) * g.c + row;
-      p.stats[p.slot_off + idx] = make_float2(m, l);
-      if (bad && p.flag) atomicExch(p.flag, 1);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 256);
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 }
 
-// ======================================================== probs + PV
+// ================================================================ forward
 
-struct PvArgs {
+struct FwdArgs {
   CUtensorMap tq, tk, tv, tp;
   Geo g;
-  float sl;
-  const float2* stats;
+  int mode;
+  float sl;  // scale * log2(e)
+  float2* stats;
+  int slot;
   int n_slots;
   int64_t slot_stride;
+  int* flag;
   OutView o_acc, o_out;
   int accumulate;
 };
 
-constexpr int PV_STAGES = 3;
-constexpr uint32_t PV_OFF_K = TILE;
-constexpr uint32_t PV_OFF_V = PV_OFF_K + PV_STAGES * TILE;
-constexpr uint32_t PV_OFF_P = PV_OFF_V + PV_STAGES * TILE;
-constexpr uint32_t PV_OFF_BAR = PV_OFF_P + 2 * PTILE;
-constexpr uint32_t PV_SMEM = PV_OFF_BAR + 256 + 1024;
+constexpr int FK_ST = 3, FV_ST = 2;
+constexpr uint32_t F_OFF_Q = 0;
+constexpr uint32_t F_OFF_K = F_OFF_Q + 2 * TILE;
+constexpr uint32_t F_OFF_V = F_OFF_K + FK_ST * TILE;
+constexpr uint32_t F_OFF_P = F_OFF_V + FV_ST * TILE;
+constexpr uint32_t F_OFF_X = F_OFF_P + 2 * PTILE;         // (m, l) exchange, 256 x float2
+constexpr uint32_t F_OFF_BAR = F_OFF_X + EPI_THREADS * 8;
+constexpr uint32_t F_SMEM = F_OFF_BAR + 512 + 1024;
 
-__global__ void __launch_bounds__(NTHREADS, 1) fwd_pv_kernel(const __grid_constant__ PvArgs p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + PV_OFF_BAR);
-  uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
-  uint64_t* kv_empty = kv_full + PV_STAGES;
-  uint64_t* s_full = kv_empty + PV_STAGES;
-  uint64_t* s_empty = s_full + 2;
-  uint64_t* p_full = s_empty + 2;
-  uint64_t* p_empty = p_full + 2;
-  uint64_t* o_full = p_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
+__global__ void __launch_bounds__(NTHREADS, 1) fwd_kernel(const __grid_constant__ FwdArgs p) {
+  uint8_t* smem = smem_base();
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + F_OFF_BAR);
+  uint64_t *q_full = bar, *q_empty = bar + 2, *k_full = bar + 4, *k_empty = k_full + FK_ST;
+  uint64_t *v_full = k_empty + FK_ST, *v_empty = v_full + FV_ST;
+  uint64_t *s_full = v_empty + FV_ST, *s_empty = s_full + 2, *p_full = s_empty + 2, *p_empty = p_full + 2;
+  uint64_t *o_full = p_empty + 2, *o_empty = o_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
 
   const Geo& g = p.g;
-  const int rt = blockIdx.x, bz = blockIdx.y, d = blockIdx.z;
-  const int b = bz / g.Z, z = bz % g.Z;
-  const int r0 = rt * TR;
-  const int ntk = (g.c + TKEYS - 1) / TKEYS;
+  const bool pass_a = p.mode & MODE_PASS_A, pass_b = p.mode & MODE_PASS_B;
+  const int ntk = (g.c + TK - 1) / TK, nrt = (g.c + TR - 1) / TR;
   const int T = g.n_org * ntk;
+  const int BZ = g.B * g.Z;
+  const int items = g.n_rank * BZ * nrt;
   const uint32_t warp = warp_id(), lane = lane_id();
-  constexpr uint32_t O_COL = 2 * TKEYS;
 
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    for (int s = 0; s < PV_STAGES; ++s) mbar_init(&kv_full[s], 1), mbar_init(&kv_empty[s], 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&s_full[s], 1), mbar_init(&s_empty[s], 4);
-      mbar_init(&p_full[s], 4), mbar_init(&p_empty[s], 1);
+      mbar_init(&q_full[s], 1), mbar_init(&q_empty[s], 1);
+      mbar_init(&s_full[s], 1), mbar_init(&s_empty[s], EPI_WARPS);
+      mbar_init(&p_full[s], EPI_WARPS), mbar_init(&p_empty[s], 1);
+      mbar_init(&o_full[s], 1), mbar_init(&o_empty[s], EPI_WARPS);
     }
-    mbar_init(o_full, 1);
+    for (int s = 0; s < FK_ST; ++s) mbar_init(&k_full[s], 1), mbar_init(&k_empty[s], 1);
+    for (int s = 0; s < FV_ST; ++s) mbar_init(&v_full[s], 1), mbar_init(&v_empty[s], 1);
     fence_barrier_init();
     tma_prefetch(&p.tq);
     tma_prefetch(&p.tk);
-    tma_prefetch(&p.tv);
-    tma_prefetch(&p.tp);
+    if (pass_b) tma_prefetch(&p.tv), tma_prefetch(&p.tp);
   }
   tc_fence_before();
   __syncthreads();
@@ -301,131 +191,254 @@ __global__ void __launch_bounds__(NTHREADS, 1) fwd_pv_kernel(const __grid_consta
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, TILE);
-      tma_load_4d(smem, &p.tq, q_full, 0, r0, z, d * g.B + b);
-      for (int i = 0; i < T; ++i) {
-        const int s = i % PV_STAGES;
-        mbar_wait(&kv_empty[s], ((i / PV_STAGES) & 1) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[s], 2 * TILE);
-        const int jo = i / ntk, k0 = (i % ntk) * TKEYS;
-        tma_load_4d(smem + PV_OFF_K + s * TILE, &p.tk, &kv_full[s], 0, k0, z, jo * g.B + b);
-        tma_load_4d(smem + PV_OFF_V + s * TILE, &p.tv, &kv_full[s], 0, k0, z, jo * g.B + b);
+      Pos kq, vq;
+      uint32_t it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        const int rt = item % nrt, bz = (item / nrt) % BZ, d = item / (nrt * BZ);
+        const int b = bz / g.Z, z = bz % g.Z;
+        const int qb = it & 1;
+        mbar_wait(&q_empty[qb], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qb], TILE);
+        tma_load_4d(smem + F_OFF_Q + qb * TILE, &p.tq, &q_full[qb], 0, rt * TR, z, d * g.B + b);
+        for (int pass = 0; pass < 2; ++pass) {
+          if ((pass == 0 && !pass_a) || (pass == 1 && !pass_b)) continue;
+          for (int t = 0; t < T; ++t) {
+            const int jo = t / ntk, k0 = (t % ntk) * TK;
+            const uint32_t ks = kq.slot(FK_ST);
+            mbar_wait(&k_empty[ks], kq.phase(FK_ST) ^ 1);
+            mbar_arrive_expect_tx(&k_full[ks], TILE);
+            tma_load_4d(smem + F_OFF_K + ks * TILE, &p.tk, &k_full[ks], 0, k0, z, jo * g.B + b);
+            ++kq.i;
+            if (pass == 1) {
+              const uint32_t vs = vq.slot(FV_ST);
+              mbar_wait(&v_empty[vs], vq.phase(FV_ST) ^ 1);
+              mbar_arrive_expect_tx(&v_full[vs], TILE);
+              tma_load_4d(smem + F_OFF_V + vs * TILE, &p.tv, &v_full[vs], 0, k0, z, jo * g.B + b);
+              ++vq.i;
+            }
+          }
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc_s = idesc_bf16_f32(TR, TKEYS, 0, 0);
+      const uint32_t idesc_s = idesc_bf16_f32(TR, TK, 0, 0);
       const uint32_t idesc_o = idesc_bf16_f32(TR, HD, 0, 1);
-      mbar_wait(q_full, 0);
-      const uint32_t qa = smem_u32(smem);
-      auto issue_s = [&](int i) {
-        const int s = i % PV_STAGES, buf = i & 1;
-        mbar_wait(&kv_full[s], (i / PV_STAGES) & 1);
-        mbar_wait(&s_empty[buf], ((i >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t ka = smem_u32(smem + PV_OFF_K + s * TILE);
+      Pos kq, vq, sq, pq;
+      uint32_t it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        const int qb = it & 1;
+        mbar_wait(&q_full[qb], (it >> 1) & 1);
+        const uint32_t qa = smem_u32(smem + F_OFF_Q + qb * TILE);
+        auto issue_s = [&]() {
+          const uint32_t ks = kq.slot(FK_ST), sb = sq.slot(2);
+          mbar_wait(&k_full[ks], kq.phase(FK_ST));
+          mbar_wait(&s_empty[sb], sq.phase(2) ^ 1);
+          tc_fence_after();
+          const uint32_t ka = smem_u32(smem + F_OFF_K + ks * TILE);
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k)
-          umma_bf16(tmem + buf * TKEYS, smem_desc_sw128(qa + k * 32, 0, 1024), smem_desc_sw128(ka + k * 32, 0, 1024),
-                    idesc_s, k > 0);
-        umma_commit(&s_full[buf]);
-      };
-      auto issue_pv = [&](int i) {
-        const int s = i % PV_STAGES, pb = i & 1;
-        mbar_wait(&p_full[pb], (i >> 1) & 1);
-        tc_fence_after();
-        const uint32_t pa = smem_u32(smem + PV_OFF_P + pb * PTILE);
-        const uint32_t va = smem_u32(smem + PV_OFF_V + s * TILE);
+          for (int k = 0; k < HD / 16; ++k)
+            umma_bf16(tmem + sb * TK, smem_desc_sw128(qa + k * 32, 0, 1024), smem_desc_sw128(ka + k * 32, 0, 1024),
+                      idesc_s, k > 0);
+          umma_commit(&k_empty[ks]);
+          umma_commit(&s_full[sb]);
+          ++kq.i, ++sq.i;
+        };
+        if (pass_a)
+          for (int t = 0; t < T; ++t) issue_s();
+        if (pass_b) {
+          const uint32_t ob = it & 1;
+          mbar_wait(&o_empty[ob], ((it >> 1) & 1) ^ 1);
+          if (T > 0) issue_s();
+          for (int t = 0; t < T; ++t) {
+            if (t + 1 < T) issue_s();
+            const uint32_t pb = pq.slot(2), vs = vq.slot(FV_ST);
+            mbar_wait(&p_full[pb], pq.phase(2));
+            mbar_wait(&v_full[vs], vq.phase(FV_ST));
+            tc_fence_after();
+            const uint32_t pa = smem_u32(smem + F_OFF_P + pb * PTILE);
+            const uint32_t va = smem_u32(smem + F_OFF_V + vs * TILE);
 #pragma unroll
-        for (int k = 0; k < TKEYS / 16; ++k)
-          umma_bf16(tmem + O_COL, smem_desc_sw128(pa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
-                    smem_desc_sw128(va + k * 2048, ATOM, 1024), idesc_o, (i | k) != 0);
-        umma_commit(&kv_empty[s]);
-        umma_commit(&p_empty[pb]);
-      };
-      if (T > 0) issue_s(0);
-      for (int i = 0; i < T; ++i) {
-        if (i + 1 < T) issue_s(i + 1);
-        issue_pv(i);
+            for (int k = 0; k < TK / 16; ++k)
+              umma_bf16(tmem + 2 * TK + ob * HD, smem_desc_sw128(pa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
+                        smem_desc_sw128(va + k * 2048, ATOM, 1024), idesc_o, (t | k) != 0);
+            umma_commit(&v_empty[vs]);
+            umma_commit(&p_empty[pb]);
+            ++pq.i, ++vq.i;
+          }
+          umma_commit(&o_full[ob]);
+        }
+        umma_commit(&q_empty[qb]);
       }
-      umma_commit(o_full);
     }
   } else {
     const uint32_t quad = warp & 3;
+    const int half = (warp - 2) >> 2;  // which 64-column half of each S tile
     const int r = quad * 32 + lane;
-    const int et = (warp - 2) * 32 + lane;
-    const int row = r0 + r;
-    const int head = (d * g.B + b) * g.Z + z;
-    float m = 0.f, inv_l = 1.f;
-    if (row < g.c) {
-      const int64_t idx = int64_t(head) * g.c + row;
-      float mm = -INFINITY, ll = 0.f;
-      for (int s = 0; s < p.n_slots; ++s) {
-        const float2 st = p.stats[s * p.slot_stride + idx];
-        const float mn = fmaxf(mm, st.x);
-        if (mn != -INFINITY) {
-          ll = ll * fast_exp2(mm - mn) + st.y * fast_exp2(st.x - mn);
-          mm = mn;
-        }
-      }
-      m = mm;
-      inv_l = 1.f / ll;
-    }
-    const uint32_t pbase = smem_u32(smem + PV_OFF_P);
-    for (int i = 0; i < T; ++i) {
-      const int buf = i & 1;
-      const int jo = i / ntk, k0 = (i % ntk) * TKEYS;
-      const int nvalid = min(TKEYS, g.c - k0);
-      mbar_wait(&s_full[buf], (i >> 1) & 1);
-      mbar_wait(&p_empty[buf], ((i >> 1) & 1) ^ 1);
-      if (et == 0 && i >= 2) tma_store_wait_read<1>();
-      epi_bar();
+    const int et = threadIdx.x - 64;   // 0..255
+    const bool storer = (lane == 0) && (quad == 2);  // first warp of each half issues its TMA stores
+    const uint32_t lane_base = (quad * 32u) << 16;
+    const uint32_t xbase = smem_u32(smem + F_OFF_X);
+    const uint32_t pbase = smem_u32(smem + F_OFF_P);
+    const float sl = p.sl;
+    Pos sq, pq;
+    uint32_t it = 0;
+    bool bad = false;
+    auto load_s = [&](float* v) {  // this thread's 64 columns of the next S tile, then free the buffer
+      const uint32_t sb = sq.slot(2);
+      mbar_wait(&s_full[sb], sq.phase(2));
       tc_fence_after();
-#pragma unroll 1
-      for (int cc = 0; cc < TKEYS / 32; ++cc) {
-        float v[32];
-        __syncwarp();
-        tmem_ld32(tmem + ((quad * 32u) << 16) + buf * TKEYS + cc * 32, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e)
-          v[e] = (cc * 32 + e < nvalid) ? fast_exp2(__fmul_rn(v[e], p.sl) - m) * inv_l : 0.f;
-        st_row32_sw128(pbase + buf * PTILE, r, cc * 32, v);
-      }
-      tc_fence_before();
-      fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&s_empty[buf]);
-        mbar_arrive(&p_full[buf]);
+      tmem_ld32(tmem + lane_base + sb * TK + half * 64, v);
+      tmem_ld32(tmem + lane_base + sb * TK + half * 64 + 32, v + 32);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[sb]);
+      ++sq.i;
+    };
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      const int rt = item % nrt, bz = (item / nrt) % BZ, d = item / (nrt * BZ);
+      const int b = bz / g.Z, z = bz % g.Z;
+      const int row = rt * TR + r;
+      const int64_t sidx = (int64_t(d * g.B + b) * g.Z + z) * g.c + row;
+      float bias = 0.f;  // pass B computes p = 2^(s*sl - bias), bias = m*sl + log2(l)
+      if (pass_a) {
+        float m = -INFINITY, l = 0.f;  // m: raw (unscaled) row max; l = sum 2^((s - m) * sl)
+        int k0 = 0;
+        for (int t = 0; t < T; ++t) {
+          float v[64];
+          load_s(v);
+          const int nvalid = min(TK, g.c - k0) - half * 64;
+          k0 = k0 + TK >= g.c ? 0 : k0 + TK;
+          if (nvalid <= 0) continue;
+          float cmax, cmin;
+          if (nvalid >= 64) {
+            float mx[8], mi[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) mx[e] = mi[e] = v[e];
+#pragma unroll
+            for (int e = 8; e < 64; ++e) mx[e & 7] = max_nan(mx[e & 7], v[e]), mi[e & 7] = min_nan(mi[e & 7], v[e]);
+#pragma unroll
+            for (int w = 4; w; w >>= 1)
+#pragma unroll
+              for (int e = 0; e < w; ++e) mx[e] = max_nan(mx[e], mx[e + w]), mi[e] = min_nan(mi[e], mi[e + w]);
+            cmax = mx[0], cmin = mi[0];
+          } else {
+            cmax = -INFINITY, cmin = INFINITY;
+#pragma unroll
+            for (int e = 0; e < 64; ++e)
+              if (e < nvalid) cmax = max_nan(cmax, v[e]), cmin = min_nan(cmin, v[e]);
+          }
+          bad |= !(fabsf(cmax) <= 3.402823466e38f) || !(fabsf(cmin) <= 3.402823466e38f);
+          const float mn = fmaxf(m, cmax);
+          if (mn > m) {
+            l *= fast_exp2((m - mn) * sl);
+            m = mn;
+          }
+          const float msl = m * sl;
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+          if (nvalid >= 64) {
+#pragma unroll
+            for (int e = 0; e < 64; ++e) {
+              const float x = fmaf(v[e], sl, -msl);
+              acc[e & 3] += (e & 3) == 3 ? exp2_poly<4>(x) : fast_exp2(x);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 64; ++e)
+              if (e < nvalid) acc[e & 3] += fast_exp2(fmaf(v[e], sl, -msl));
+          }
+          l += (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        }
+        // combine the two column halves of each row through shared memory
+        st_shared_f2(xbase + et * 8, m, l);
+        bar_epi();
+        const float2 o = ld_shared_f2(xbase + ((et + 128) & 255) * 8);
+        bar_epi();
+        const float mn = fmaxf(m, o.x);
+        if (mn != -INFINITY) {
+          l = l * fast_exp2((m - mn) * sl) + o.y * fast_exp2((o.x - mn) * sl);
+          m = mn;
+        }
+        if ((p.mode & MODE_WRITE_STATS) && half == 0 && row < g.c)
+          p.stats[int64_t(p.slot) * p.slot_stride + sidx] = make_float2(m * sl, l);
+        bias = (row < g.c && l > 0.f) ? m * sl + __log2f(l) : 0.f;
       }
-      epi_bar();
-      if (et == 0) {
-        const int jg = g.org_lo + jo;
-        tma_store_5d(&p.tp, smem + PV_OFF_P + buf * PTILE, k0, jg, r0, z, d * g.B + b);
-        if (nvalid > 64) tma_store_5d(&p.tp, smem + PV_OFF_P + buf * PTILE + ATOM, k0 + 64, jg, r0, z, d * g.B + b);
-        tma_store_commit();
+      if (!pass_b) continue;
+      if (p.mode & MODE_EXT_STATS) {  // stats slots hold (scaled max, sum), base 2
+        float msl = -INFINITY, l = 0.f;
+        if (row < g.c)
+          for (int s = 0; s < p.n_slots; ++s) {
+            const float2 st = p.stats[int64_t(s) * p.slot_stride + sidx];
+            const float mn = fmaxf(msl, st.x);
+            if (mn != -INFINITY) {
+              l = l * fast_exp2(msl - mn) + st.y * fast_exp2(st.x - mn);
+              msl = mn;
+            }
+          }
+        bias = (row < g.c && l > 0.f) ? msl + __log2f(l) : 0.f;  // padded rows: finite garbage, never stored
       }
+      int jo = 0, k0 = 0;
+      for (int t = 0; t < T; ++t) {
+        const uint32_t pb = pq.slot(2);
+        const int nvalid = min(TK, g.c - k0) - half * 64;
+        float v[64];
+        load_s(v);
+        if (nvalid >= 64) {
+#pragma unroll
+          for (int e = 0; e < 64; ++e) {
+            const float x = fmaf(v[e], sl, -bias);
+            v[e] = (e & 3) == 3 ? exp2_poly<3>(x) : fast_exp2(x);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 64; ++e) v[e] = e < nvalid ? fast_exp2(fmaf(v[e], sl, -bias)) : 0.f;
+        }
+        mbar_wait(&p_empty[pb], pq.phase(2) ^ 1);
+        if (storer && pq.i >= 2) tma_store_wait_read<1>();
+        bar_half(half);
+        const uint32_t ptile = pbase + pb * PTILE;
+        st_row32_sw128(ptile, r, half * 64, v);
+        st_row32_sw128(ptile, r, half * 64 + 32, v + 32);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[pb]);
+        bar_half(half);
+        if (storer) {
+          if (nvalid > 0)
+            tma_store_5d(&p.tp, smem + F_OFF_P + pb * PTILE + half * ATOM, k0 + half * 64, g.org_lo + jo, rt * TR,
+                         z, d * g.B + b);
+          tma_store_commit();
+        }
+        ++pq.i;
+        if (k0 + TK >= g.c) k0 = 0, ++jo;
+        else k0 += TK;
+      }
+      const uint32_t ob = it & 1;
+      mbar_wait(&o_full[ob], (it >> 1) & 1);
+      tc_fence_after();
+      float o[32];
+      __syncwarp();
+      tmem_ld32(tmem + lane_base + 2 * TK + ob * HD + half * 32, o);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[ob]);
+      if (row < g.c) store_row32(p.o_acc, p.o_out, p.accumulate, d, b, z, row, half * 32, o);
     }
-    mbar_wait(o_full, 0);
-    tc_fence_after();
-    float v[64];
-    __syncwarp();
-    tmem_ld32(tmem + ((quad * 32u) << 16) + O_COL, v);
-    tmem_ld32(tmem + ((quad * 32u) << 16) + O_COL + 32, v + 32);
-    tmem_ld_wait();
-    if (row < g.c) store_row64(p.o_acc, p.o_out, p.accumulate, d, b, z, row, v);
-    if (et == 0) tma_store_wait_all<0>();
+    if (bad && p.flag) atomicExch(p.flag, 1);
+    if (storer) tma_store_wait_all<0>();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
-// ================================================================ dK / dV
+// ============================================================== dK / dV
 
 struct DkdvArgs {
-  CUtensorMap tq, tv, tdo, tp, tds;
+  CUtensorMap tq, tv, tdo, tp;
   Geo g;
   const float* dvec;
   OutView dk, dv;
@@ -433,52 +446,43 @@ struct DkdvArgs {
   int accumulate;
 };
 
-constexpr int BK_STAGES = 2;
-constexpr uint32_t BK_STAGE = TILE /*dO*/ + TILE /*Q*/ + PTILE /*P*/;
-constexpr uint32_t BK_OFF_ST = TILE;  // after V
-constexpr uint32_t BK_OFF_DS = BK_OFF_ST + BK_STAGES * BK_STAGE;
-constexpr uint32_t BK_OFF_BAR = BK_OFF_DS + 2 * PTILE;
-constexpr uint32_t BK_SMEM = BK_OFF_BAR + 256 + 1024;
+// A stage holds dO, Q and the P tile; the epilogue overwrites P with dS in
+// place (each thread rewrites exactly the elements it read, after the
+// P^T dO product that also reads P has completed), so 3 stages fit.
+constexpr int BK_ST = 3;
+constexpr uint32_t BK_STAGE = TILE /*dO*/ + TILE /*Q*/ + PTILE /*P, then dS*/;
+constexpr uint32_t BK_OFF_V = 0;
+constexpr uint32_t BK_OFF_ST = TILE;
+constexpr uint32_t BK_OFF_BAR = BK_OFF_ST + BK_ST * BK_STAGE;
+constexpr uint32_t BK_SMEM = BK_OFF_BAR + 512 + 1024;
 
 __global__ void __launch_bounds__(NTHREADS, 1) bwd_dkdv_kernel(const __grid_constant__ DkdvArgs p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + BK_OFF_BAR);
-  uint64_t* v_full = bars;
-  uint64_t* ld_full = bars + 1;
-  uint64_t* ld_empty = ld_full + BK_STAGES;
-  uint64_t* dp_full = ld_empty + BK_STAGES;
-  uint64_t* dp_empty = dp_full + 2;
-  uint64_t* ds_full = dp_empty + 2;
-  uint64_t* ds_empty = ds_full + 2;
-  uint64_t* acc_full = ds_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint8_t* smem = smem_base();
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BK_OFF_BAR);
+  uint64_t *v_full = bar, *v_empty = bar + 1, *ld_full = bar + 2, *ld_empty = ld_full + BK_ST;
+  uint64_t *dp_full = ld_empty + BK_ST, *dp_empty = dp_full + 2, *ds_full = dp_empty + 2, *ds_empty = ds_full + 2;
+  uint64_t *acc_full = ds_empty + 2, *acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const Geo& g = p.g;
-  const int kt = blockIdx.x, bz = blockIdx.y, jo = blockIdx.z;
-  const int b = bz / g.Z, z = bz % g.Z;
-  const int k0 = kt * TKEYS;
-  const int jg = g.org_lo + jo;
-  const int nrt = (g.c + TR - 1) / TR;
-  const int T = g.n_rank * nrt;
+  const int ntk = (g.c + TK - 1) / TK, nrt = (g.c + TR - 1) / TR;
+  const int T = g.n_rank * nrt;  // query row tiles walked per key tile
+  const int BZ = g.B * g.Z;
+  const int items = g.n_org * BZ * ntk;
   const uint32_t warp = warp_id(), lane = lane_id();
-  constexpr uint32_t DV_COL = 2 * TKEYS, DK_COL = 2 * TKEYS + HD;
+  constexpr uint32_t ACC_COL = 2 * TK;  // [dV | dK] x 2 buffers, 128 columns each
 
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   if (threadIdx.x == 0) {
-    mbar_init(v_full, 1);
-    for (int s = 0; s < BK_STAGES; ++s) mbar_init(&ld_full[s], 1), mbar_init(&ld_empty[s], 1 + 4);
+    mbar_init(v_full, 1), mbar_init(v_empty, 1);
+    for (int s = 0; s < BK_ST; ++s) mbar_init(&ld_full[s], 1), mbar_init(&ld_empty[s], 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&dp_full[s], 1), mbar_init(&dp_empty[s], 4);
-      mbar_init(&ds_full[s], 4), mbar_init(&ds_empty[s], 1);
+      mbar_init(&dp_full[s], 1), mbar_init(&dp_empty[s], EPI_WARPS);
+      mbar_init(&ds_full[s], EPI_WARPS), mbar_init(&ds_empty[s], 1);
+      mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], EPI_WARPS);
     }
-    mbar_init(acc_full, 1);
     fence_barrier_init();
-    tma_prefetch(&p.tq);
-    tma_prefetch(&p.tv);
-    tma_prefetch(&p.tdo);
-    tma_prefetch(&p.tp);
-    tma_prefetch(&p.tds);
+    tma_prefetch(&p.tq), tma_prefetch(&p.tv), tma_prefetch(&p.tdo), tma_prefetch(&p.tp);
   }
   tc_fence_before();
   __syncthreads();
@@ -487,169 +491,201 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dkdv_kernel(const __grid_cons
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(v_full, TILE);
-      tma_load_4d(smem, &p.tv, v_full, 0, k0, z, jo * g.B + b);
-      for (int i = 0; i < T; ++i) {
-        const int s = i % BK_STAGES;
-        const int d = i / nrt, r0 = (i % nrt) * TR;
-        mbar_wait(&ld_empty[s], ((i / BK_STAGES) & 1) ^ 1);
-        mbar_arrive_expect_tx(&ld_full[s], BK_STAGE);
-        uint8_t* st = smem + BK_OFF_ST + s * BK_STAGE;
-        tma_load_4d(st, &p.tdo, &ld_full[s], 0, r0, z, d * g.B + b);
-        tma_load_4d(st + TILE, &p.tq, &ld_full[s], 0, r0, z, d * g.B + b);
-        tma_load_5d(st + 2 * TILE, &p.tp, &ld_full[s], k0, jg, r0, z, d * g.B + b);
-        tma_load_5d(st + 2 * TILE + ATOM, &p.tp, &ld_full[s], k0 + 64, jg, r0, z, d * g.B + b);
+      Pos lq;
+      uint32_t it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        const int kt = item % ntk, bz = (item / ntk) % BZ, jo = item / (ntk * BZ);
+        const int b = bz / g.Z, z = bz % g.Z, k0 = kt * TK, jg = g.org_lo + jo;
+        mbar_wait(v_empty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(v_full, TILE);
+        tma_load_4d(smem + BK_OFF_V, &p.tv, v_full, 0, k0, z, jo * g.B + b);
+        for (int t = 0; t < T; ++t) {
+          const int d = t / nrt, r0 = (t % nrt) * TR;
+          const uint32_t s = lq.slot(BK_ST);
+          mbar_wait(&ld_empty[s], lq.phase(BK_ST) ^ 1);
+          mbar_arrive_expect_tx(&ld_full[s], BK_STAGE);
+          uint8_t* st = smem + BK_OFF_ST + s * BK_STAGE;
+          tma_load_4d(st, &p.tdo, &ld_full[s], 0, r0, z, d * g.B + b);
+          tma_load_4d(st + TILE, &p.tq, &ld_full[s], 0, r0, z, d * g.B + b);
+          tma_load_5d(st + 2 * TILE, &p.tp, &ld_full[s], k0, jg, r0, z, d * g.B + b);
+          tma_load_5d(st + 2 * TILE + ATOM, &p.tp, &ld_full[s], k0 + 64, jg, r0, z, d * g.B + b);
+          ++lq.i;
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc_dp = idesc_bf16_f32(TR, TKEYS, 0, 0);  // dO (K-major) x V (K-major)
-      const uint32_t idesc_kv = idesc_bf16_f32(TKEYS, HD, 1, 1);  // P^T / dS^T (MN-major) x dO / Q (MN-major)
-      mbar_wait(v_full, 0);
-      const uint32_t va = smem_u32(smem);
-      for (int i = 0; i < T; ++i) {
-        const int s = i % BK_STAGES, buf = i & 1;
-        const uint32_t st = smem_u32(smem + BK_OFF_ST + s * BK_STAGE);
-        const uint32_t doa = st, qa = st + TILE, pa = st + 2 * TILE;
-        const uint32_t dsa = smem_u32(smem + BK_OFF_DS + buf * PTILE);
-        mbar_wait(&ld_full[s], (i / BK_STAGES) & 1);
-        mbar_wait(&dp_empty[buf], ((i >> 1) & 1) ^ 1);
-        tc_fence_after();
+      const uint32_t idesc_dp = idesc_bf16_f32(TR, TK, 0, 0);  // dO (K-major) x V (K-major)
+      const uint32_t idesc_kv = idesc_bf16_f32(TK, HD, 1, 1);  // P^T / dS^T (MN-major) x dO / Q (MN-major)
+      const uint32_t va = smem_u32(smem + BK_OFF_V);
+      Pos lq_a, dq_a, lq_b, dq_b;  // "a": dP/dV issue (runs one tile ahead), "b": dK issue
+      uint32_t it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        const uint32_t ab = it & 1;
+        const uint32_t dv_col = ACC_COL + ab * 128, dk_col = dv_col + HD;
+        mbar_wait(v_full, it & 1);
+        mbar_wait(&acc_empty[ab], ((it >> 1) & 1) ^ 1);
+        // dP(t) = dO V^T and dV += P^T dO need only the loaded stage; issuing
+        // them one tile ahead of dK(t) (which waits for the epilogue's dS)
+        // keeps the epilogue fed.
+        auto issue_dp = [&](int t) {
+          const uint32_t s = lq_a.slot(BK_ST), db = dq_a.slot(2);
+          const uint32_t st = smem_u32(smem + BK_OFF_ST + s * BK_STAGE);
+          const uint32_t doa = st, pa = st + 2 * TILE;
+          mbar_wait(&ld_full[s], lq_a.phase(BK_ST));
+          mbar_wait(&dp_empty[db], dq_a.phase(2) ^ 1);
+          tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k)
-          umma_bf16(tmem + buf * TKEYS, smem_desc_sw128(doa + k * 32, 0, 1024), smem_desc_sw128(va + k * 32, 0, 1024),
-                    idesc_dp, k > 0);
-        umma_commit(&dp_full[buf]);
-        // dV += P^T dO : contraction over the 128 query rows of this tile
+          for (int k = 0; k < HD / 16; ++k)
+            umma_bf16(tmem + db * TK, smem_desc_sw128(doa + k * 32, 0, 1024), smem_desc_sw128(va + k * 32, 0, 1024),
+                      idesc_dp, k > 0);
+          if (t == T - 1) umma_commit(v_empty);  // last read of V for this item
 #pragma unroll
-        for (int k = 0; k < TR / 16; ++k)
-          umma_bf16(tmem + DV_COL, smem_desc_sw128(pa + k * 2048, ATOM, 1024), smem_desc_sw128(doa + k * 2048, ATOM, 1024),
-                    idesc_kv, (i | k) != 0);
-        mbar_wait(&ds_full[buf], (i >> 1) & 1);
-        tc_fence_after();
-        // dK += dS^T Q
+          for (int k = 0; k < TR / 16; ++k)
+            umma_bf16(tmem + dv_col, smem_desc_sw128(pa + k * 2048, ATOM, 1024),
+                      smem_desc_sw128(doa + k * 2048, ATOM, 1024), idesc_kv, (t | k) != 0);
+          // dp_full also certifies that P^T dO has finished reading P, so the
+          // epilogue may overwrite P with dS in place.
+          umma_commit(&dp_full[db]);
+          ++lq_a.i, ++dq_a.i;
+        };
+        if (T > 0) issue_dp(0);
+        for (int t = 0; t < T; ++t) {
+          if (t + 1 < T) issue_dp(t + 1);
+          const uint32_t s = lq_b.slot(BK_ST), db = dq_b.slot(2);
+          const uint32_t qa = smem_u32(smem + BK_OFF_ST + s * BK_STAGE) + TILE;
+          const uint32_t dsa = qa + TILE;  // dS, written over P
+          mbar_wait(&ds_full[db], dq_b.phase(2));
+          tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < TR / 16; ++k)
-          umma_bf16(tmem + DK_COL, smem_desc_sw128(dsa + k * 2048, ATOM, 1024), smem_desc_sw128(qa + k * 2048, ATOM, 1024),
-                    idesc_kv, (i | k) != 0);
-        umma_commit(&ld_empty[s]);
-        umma_commit(&ds_empty[buf]);
+          for (int k = 0; k < TR / 16; ++k)
+            umma_bf16(tmem + dk_col, smem_desc_sw128(dsa + k * 2048, ATOM, 1024),
+                      smem_desc_sw128(qa + k * 2048, ATOM, 1024), idesc_kv, (t | k) != 0);
+          umma_commit(&ld_empty[s]);
+          ++lq_b.i, ++dq_b.i;
+        }
+        umma_commit(&acc_full[ab]);
       }
-      umma_commit(acc_full);
     }
   } else {
     const uint32_t quad = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int r = quad * 32 + lane;
-    const int et = (warp - 2) * 32 + lane;
-    const uint32_t dsbase = smem_u32(smem + BK_OFF_DS);
-    for (int i = 0; i < T; ++i) {
-      const int s = i % BK_STAGES, buf = i & 1;
-      const int d = i / nrt, r0 = (i % nrt) * TR;
-      const int row = r0 + r;
-      const float dval = row < g.c ? p.dvec[(int64_t((d * g.B + b) * g.Z + z)) * g.c + row] : 0.f;
-      const uint32_t pbase = smem_u32(smem + BK_OFF_ST + s * BK_STAGE + 2 * TILE);
-      mbar_wait(&ld_full[s], (i / BK_STAGES) & 1);
-      mbar_wait(&dp_full[buf], (i >> 1) & 1);
-      mbar_wait(&ds_empty[buf], ((i >> 1) & 1) ^ 1);
-      if (et == 0 && i >= 2) tma_store_wait_read<1>();
-      epi_bar();
-      tc_fence_after();
-#pragma unroll 1
-      for (int cc = 0; cc < TKEYS / 32; ++cc) {
-        float v[32], pv[32];
-        __syncwarp();
-        tmem_ld32(tmem + ((quad * 32u) << 16) + buf * TKEYS + cc * 32, v);
-        ld_row32_sw128(pbase, r, cc * 32, pv);
-        tmem_ld_wait();
+    const uint32_t lane_base = (quad * 32u) << 16;
+    Pos lq, dq_;
+    uint32_t it = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      const int kt = item % ntk, bz = (item / ntk) % BZ, jo = item / (ntk * BZ);
+      const int b = bz / g.Z, z = bz % g.Z, k0 = kt * TK;
+      int d = 0, r0 = 0;
+      for (int t = 0; t < T; ++t) {
+        const int row = r0 + r;
+        const uint32_t s = lq.slot(BK_ST), db = dq_.slot(2);
+        const float dval = row < g.c ? p.dvec[(int64_t(d * g.B + b) * g.Z + z) * g.c + row] : 0.f;
+        if (r0 + TR >= g.c) r0 = 0, ++d;
+        else r0 += TR;
+        const uint32_t pt = smem_u32(smem + BK_OFF_ST + s * BK_STAGE + 2 * TILE);
+        const uint32_t dst = pt;  // dS overwrites P in place
+        mbar_wait(&ld_full[s], lq.phase(BK_ST));
+        mbar_wait(&dp_full[db], dq_.phase(2));
+        tc_fence_after();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = pv[e] * (v[e] - dval) * g.scale;
-        st_row32_sw128(dsbase + buf * PTILE, r, cc * 32, v);
+        for (int cc = 0; cc < 2; ++cc) {
+          float v[32], pv[32];
+          const int col = half * 64 + cc * 32;
+          __syncwarp();
+          tmem_ld32(tmem + lane_base + db * TK + col, v);
+          ld_row32_sw128(pt, r, col, pv);
+          tmem_ld_wait();
+          // dS' = P (dP - D); the 1/sqrt(A) scale is applied to dK once, at the end
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = pv[e] * (v[e] - dval);
+          st_row32_sw128(dst, r, col, v);
+        }
+        tc_fence_before();
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&dp_empty[db]);
+          mbar_arrive(&ds_full[db]);
+        }
+        ++lq.i, ++dq_.i;
       }
-      tc_fence_before();
-      fence_proxy_async_smem();
+      const uint32_t ab = it & 1;
+      mbar_wait(&acc_full[ab], (it >> 1) & 1);
+      tc_fence_after();
+      float dvv[32], dkv[32];
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&dp_empty[buf]);
-        mbar_arrive(&ld_empty[s]);
-        mbar_arrive(&ds_full[buf]);
+      tmem_ld32(tmem + lane_base + ACC_COL + ab * 128 + half * 32, dvv);
+      tmem_ld32(tmem + lane_base + ACC_COL + ab * 128 + HD + half * 32, dkv);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[ab]);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) dkv[e] *= g.scale;
+      const int key = k0 + r;
+      if (key < g.c) {
+        const OutView none{nullptr, 0, 0, 0, 0};
+        if (p.dkv_bf16) {
+          store_row32(none, p.dv, 0, jo, b, z, key, half * 32, dvv);
+          store_row32(none, p.dk, 0, jo, b, z, key, half * 32, dkv);
+        } else {
+          store_row32(p.dv, none, p.accumulate, jo, b, z, key, half * 32, dvv);
+          store_row32(p.dk, none, p.accumulate, jo, b, z, key, half * 32, dkv);
+        }
       }
-      epi_bar();
-      if (et == 0) {
-        tma_store_5d(&p.tds, smem + BK_OFF_DS + buf * PTILE, k0, jg, r0, z, d * g.B + b);
-        if (g.c - k0 > 64) tma_store_5d(&p.tds, smem + BK_OFF_DS + buf * PTILE + ATOM, k0 + 64, jg, r0, z, d * g.B + b);
-        tma_store_commit();
-      }
     }
-    mbar_wait(acc_full, 0);
-    tc_fence_after();
-    const int key = k0 + r;
-    float v[64];
-    __syncwarp();
-    tmem_ld32(tmem + ((quad * 32u) << 16) + DV_COL, v);
-    tmem_ld32(tmem + ((quad * 32u) << 16) + DV_COL + 32, v + 32);
-    tmem_ld_wait();
-    const OutView none{nullptr, 0, 0, 0, 0};
-    if (key < g.c) {
-      if (p.dkv_bf16)
-        store_row64(none, p.dv, 0, jo, b, z, key, v);
-      else
-        store_row64(p.dv, none, p.accumulate, jo, b, z, key, v);
-    }
-    __syncwarp();
-    tmem_ld32(tmem + ((quad * 32u) << 16) + DK_COL, v);
-    tmem_ld32(tmem + ((quad * 32u) << 16) + DK_COL + 32, v + 32);
-    tmem_ld_wait();
-    if (key < g.c) {
-      if (p.dkv_bf16)
-        store_row64(none, p.dk, 0, jo, b, z, key, v);
-      else
-        store_row64(p.dk, none, p.accumulate, jo, b, z, key, v);
-    }
-    if (et == 0) tma_store_wait_all<0>();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
-// ===================================================================== dQ
+// =================================================================== dQ
 
 struct DqArgs {
-  CUtensorMap tds, tk;
+  CUtensorMap tdo, tk, tv, tp;
   Geo g;
+  const float* dvec;
   OutView dq_acc, dq_out;
   int accumulate;
 };
 
-constexpr int DQ_STAGES = 4;
-constexpr uint32_t DQ_STAGE = PTILE + TILE;
-constexpr uint32_t DQ_OFF_BAR = DQ_STAGES * DQ_STAGE;
-constexpr uint32_t DQ_SMEM = DQ_OFF_BAR + 256 + 1024;
+constexpr int DQ_ST = 3;  // dS overwrites P inside the stage, as in bwd_dkdv
+constexpr uint32_t DQ_STAGE = TILE /*V*/ + TILE /*K*/ + PTILE /*P, then dS*/;
+constexpr uint32_t DQ_OFF_DO = 0;
+constexpr uint32_t DQ_OFF_ST = 2 * TILE;
+constexpr uint32_t DQ_OFF_BAR = DQ_OFF_ST + DQ_ST * DQ_STAGE;
+constexpr uint32_t DQ_SMEM = DQ_OFF_BAR + 512 + 1024;
 
 __global__ void __launch_bounds__(NTHREADS, 1) bwd_dq_kernel(const __grid_constant__ DqArgs p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + DQ_OFF_BAR);
-  uint64_t* ld_full = bars;
-  uint64_t* ld_empty = ld_full + DQ_STAGES;
-  uint64_t* acc_full = ld_empty + DQ_STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint8_t* smem = smem_base();
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + DQ_OFF_BAR);
+  uint64_t *do_full = bar, *do_empty = bar + 2, *ld_full = bar + 4, *ld_empty = ld_full + DQ_ST;
+  uint64_t *dp_full = ld_empty + DQ_ST, *dp_empty = dp_full + 2, *ds_full = dp_empty + 2, *ds_empty = ds_full + 2;
+  uint64_t *acc_full = ds_empty + 2, *acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const Geo& g = p.g;
-  const int rt = blockIdx.x, bz = blockIdx.y, d = blockIdx.z;
-  const int b = bz / g.Z, z = bz % g.Z;
-  const int r0 = rt * TR;
-  const int ntk = (g.c + TKEYS - 1) / TKEYS;
+  const int ntk = (g.c + TK - 1) / TK, nrt = (g.c + TR - 1) / TR;
   const int T = g.n_org * ntk;
+  const int BZ = g.B * g.Z;
+  const int items = g.n_rank * BZ * nrt;
   const uint32_t warp = warp_id(), lane = lane_id();
+  constexpr uint32_t ACC_COL = 2 * TK;
 
-  if (warp == 1) tmem_alloc(tmem_slot, 64);
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < DQ_STAGES; ++s) mbar_init(&ld_full[s], 1), mbar_init(&ld_empty[s], 1);
-    mbar_init(acc_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&do_full[s], 1), mbar_init(&do_empty[s], 1);
+      mbar_init(&dp_full[s], 1), mbar_init(&dp_empty[s], EPI_WARPS);
+      mbar_init(&ds_full[s], EPI_WARPS), mbar_init(&ds_empty[s], 1);
+      mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], EPI_WARPS);
+    }
+    for (int s = 0; s < DQ_ST; ++s) mbar_init(&ld_full[s], 1), mbar_init(&ld_empty[s], 1);
     fence_barrier_init();
-    tma_prefetch(&p.tds);
-    tma_prefetch(&p.tk);
+    tma_prefetch(&p.tdo), tma_prefetch(&p.tk), tma_prefetch(&p.tv), tma_prefetch(&p.tp);
   }
   tc_fence_before();
   __syncthreads();
@@ -658,48 +694,129 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dq_kernel(const __grid_consta
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int i = 0; i < T; ++i) {
-        const int s = i % DQ_STAGES;
-        const int jo = i / ntk, k0 = (i % ntk) * TKEYS;
-        mbar_wait(&ld_empty[s], ((i / DQ_STAGES) & 1) ^ 1);
-        mbar_arrive_expect_tx(&ld_full[s], DQ_STAGE);
-        uint8_t* st = smem + s * DQ_STAGE;
-        tma_load_5d(st, &p.tds, &ld_full[s], k0, g.org_lo + jo, r0, z, d * g.B + b);
-        tma_load_5d(st + ATOM, &p.tds, &ld_full[s], k0 + 64, g.org_lo + jo, r0, z, d * g.B + b);
-        tma_load_4d(st + PTILE, &p.tk, &ld_full[s], 0, k0, z, jo * g.B + b);
+      Pos lq;
+      uint32_t it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        const int rt = item % nrt, bz = (item / nrt) % BZ, d = item / (nrt * BZ);
+        const int b = bz / g.Z, z = bz % g.Z, r0 = rt * TR;
+        const uint32_t ob = it & 1;
+        mbar_wait(&do_empty[ob], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&do_full[ob], TILE);
+        tma_load_4d(smem + DQ_OFF_DO + ob * TILE, &p.tdo, &do_full[ob], 0, r0, z, d * g.B + b);
+        for (int t = 0; t < T; ++t) {
+          const int jo = t / ntk, k0 = (t % ntk) * TK;
+          const uint32_t s = lq.slot(DQ_ST);
+          mbar_wait(&ld_empty[s], lq.phase(DQ_ST) ^ 1);
+          mbar_arrive_expect_tx(&ld_full[s], DQ_STAGE);
+          uint8_t* st = smem + DQ_OFF_ST + s * DQ_STAGE;
+          tma_load_4d(st, &p.tv, &ld_full[s], 0, k0, z, jo * g.B + b);
+          tma_load_4d(st + TILE, &p.tk, &ld_full[s], 0, k0, z, jo * g.B + b);
+          tma_load_5d(st + 2 * TILE, &p.tp, &ld_full[s], k0, g.org_lo + jo, r0, z, d * g.B + b);
+          tma_load_5d(st + 2 * TILE + ATOM, &p.tp, &ld_full[s], k0 + 64, g.org_lo + jo, r0, z, d * g.B + b);
+          ++lq.i;
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32(TR, HD, 0, 1);  // dS (K-major over keys) x K (MN-major)
-      for (int i = 0; i < T; ++i) {
-        const int s = i % DQ_STAGES;
-        mbar_wait(&ld_full[s], (i / DQ_STAGES) & 1);
-        tc_fence_after();
-        const uint32_t dsa = smem_u32(smem + s * DQ_STAGE), ka = dsa + PTILE;
+      const uint32_t idesc_dp = idesc_bf16_f32(TR, TK, 0, 0);  // dO x V^T
+      const uint32_t idesc_dq = idesc_bf16_f32(TR, HD, 0, 1);  // dS (K-major over keys) x K (MN-major)
+      Pos lq_a, dq_a, lq_b, dq_b;  // "a": dP issue (one tile ahead), "b": dQ issue
+      uint32_t it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        const uint32_t ob = it & 1;
+        const uint32_t doa = smem_u32(smem + DQ_OFF_DO + ob * TILE);
+        mbar_wait(&do_full[ob], (it >> 1) & 1);
+        mbar_wait(&acc_empty[ob], ((it >> 1) & 1) ^ 1);
+        auto issue_dp = [&](int t) {
+          const uint32_t s = lq_a.slot(DQ_ST), db = dq_a.slot(2);
+          const uint32_t va = smem_u32(smem + DQ_OFF_ST + s * DQ_STAGE);
+          mbar_wait(&ld_full[s], lq_a.phase(DQ_ST));
+          mbar_wait(&dp_empty[db], dq_a.phase(2) ^ 1);
+          tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < TKEYS / 16; ++k)
-          umma_bf16(tmem, smem_desc_sw128(dsa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
-                    smem_desc_sw128(ka + k * 2048, ATOM, 1024), idesc, (i | k) != 0);
-        umma_commit(&ld_empty[s]);
+          for (int k = 0; k < HD / 16; ++k)
+            umma_bf16(tmem + db * TK, smem_desc_sw128(doa + k * 32, 0, 1024), smem_desc_sw128(va + k * 32, 0, 1024),
+                      idesc_dp, k > 0);
+          umma_commit(&dp_full[db]);
+          if (t == T - 1) umma_commit(&do_empty[ob]);
+          ++lq_a.i, ++dq_a.i;
+        };
+        if (T > 0) issue_dp(0);
+        for (int t = 0; t < T; ++t) {
+          if (t + 1 < T) issue_dp(t + 1);
+          const uint32_t s = lq_b.slot(DQ_ST), db = dq_b.slot(2);
+          const uint32_t ka = smem_u32(smem + DQ_OFF_ST + s * DQ_STAGE) + TILE;
+          const uint32_t dsa = ka + TILE;  // dS, written over P
+          mbar_wait(&ds_full[db], dq_b.phase(2));
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < TK / 16; ++k)
+            umma_bf16(tmem + ACC_COL + ob * HD, smem_desc_sw128(dsa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
+                      smem_desc_sw128(ka + k * 2048, ATOM, 1024), idesc_dq, (t | k) != 0);
+          umma_commit(&ld_empty[s]);
+          ++lq_b.i, ++dq_b.i;
+        }
+        umma_commit(&acc_full[ob]);
       }
-      umma_commit(acc_full);
     }
   } else {
     const uint32_t quad = warp & 3;
-    const int row = r0 + quad * 32 + lane;
-    mbar_wait(acc_full, 0);
-    tc_fence_after();
-    float v[64];
-    __syncwarp();
-    tmem_ld32(tmem + ((quad * 32u) << 16), v);
-    tmem_ld32(tmem + ((quad * 32u) << 16) + 32, v + 32);
-    tmem_ld_wait();
-    if (row < g.c) store_row64(p.dq_acc, p.dq_out, p.accumulate, d, b, z, row, v);
+    const int half = (warp - 2) >> 2;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_base = (quad * 32u) << 16;
+    Pos lq, dq_;
+    uint32_t it = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      const int rt = item % nrt, bz = (item / nrt) % BZ, d = item / (nrt * BZ);
+      const int b = bz / g.Z, z = bz % g.Z, row = rt * TR + r;
+      const float dval = row < g.c ? p.dvec[(int64_t(d * g.B + b) * g.Z + z) * g.c + row] : 0.f;
+      for (int t = 0; t < T; ++t) {
+        const uint32_t s = lq.slot(DQ_ST), db = dq_.slot(2);
+        const uint32_t pt = smem_u32(smem + DQ_OFF_ST + s * DQ_STAGE + 2 * TILE);
+        const uint32_t dst = pt;  // dS overwrites P in place (no MMA reads this P tile)
+        mbar_wait(&ld_full[s], lq.phase(DQ_ST));
+        mbar_wait(&dp_full[db], dq_.phase(2));
+        tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          float v[32], pv[32];
+          const int col = half * 64 + cc * 32;
+          __syncwarp();
+          tmem_ld32(tmem + lane_base + db * TK + col, v);
+          ld_row32_sw128(pt, r, col, pv);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = pv[e] * (v[e] - dval);  // dS' = P (dP - D); scale applied to dQ
+          st_row32_sw128(dst, r, col, v);
+        }
+        tc_fence_before();
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&dp_empty[db]);
+          mbar_arrive(&ds_full[db]);
+        }
+        ++lq.i, ++dq_.i;
+      }
+      const uint32_t ob = it & 1;
+      mbar_wait(&acc_full[ob], (it >> 1) & 1);
+      tc_fence_after();
+      float o[32];
+      __syncwarp();
+      tmem_ld32(tmem + lane_base + ACC_COL + ob * HD + half * 32, o);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[ob]);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) o[e] *= g.scale;
+      if (row < g.c) store_row32(p.dq_acc, p.dq_out, p.accumulate, d, b, z, row, half * 32, o);
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 64);
+  if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
 // ================================================================== host
@@ -707,18 +824,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dq_kernel(const __grid_consta
 bool geom_ok(const rsa_geom* g) {
   return g && g->n_rank >= 1 && g->batch >= 1 && g->heads >= 1 && g->chunk >= 1 && g->head_dim == HD &&
          g->n_org >= 1 && g->org_lo >= 0 && g->seq_len % g->chunk == 0 && g->chunk % 8 == 0 &&
-         g->org_lo + g->n_org <= g->seq_len / g->chunk && int64_t(g->batch) * g->heads <= 65535 &&
-         g->n_rank <= 65535 && g->n_org <= 65535;
+         g->org_lo + g->n_org <= g->seq_len / g->chunk;
 }
 
 Geo to_geo(const rsa_geom* g) {
   return Geo{g->n_rank, g->batch, g->heads, g->chunk, g->seq_len, g->org_lo, g->n_org, g->scale};
 }
 
-// [rank][b][z][row][a] with a = 64 contiguous, `nrank` ranks merged into b.
+// [rank][b][z][row][a] with a = 64 contiguous; `nrank` ranks merged into b.
 bool head_map(CUtensorMap* m, const rsa_view& v, const rsa_geom* g, int nrank) {
   if (!v.ptr || !aligned16(v.ptr)) return fail(RSA_ERR_UNSUPPORTED, "fused: tensor not 16-byte aligned"), false;
-  if (nrank > 1 && v.s_rank != int64_t(g->batch) * v.s_b && g->batch > 1)
+  if (nrank > 1 && g->batch > 1 && v.s_rank != int64_t(g->batch) * v.s_b)
     return fail(RSA_ERR_UNSUPPORTED, "fused: rank stride must equal B * batch stride"), false;
   const int64_t sb = (g->batch == 1 && nrank > 1) ? v.s_rank : v.s_b;
   if (!stride_ok(v.s_row * 2) || !stride_ok(v.s_z * 2) || !stride_ok(sb * 2))
@@ -732,7 +848,7 @@ bool head_map(CUtensorMap* m, const rsa_view& v, const rsa_geom* g, int nrank) {
 // [rank][b][z][row][col], col = blk * c + key: 5-D (key, blk, row, z, b*rank).
 bool panel_map(CUtensorMap* m, const rsa_view& v, const rsa_geom* g, int nrank) {
   if (!v.ptr || !aligned16(v.ptr)) return fail(RSA_ERR_UNSUPPORTED, "fused: panel not 16-byte aligned"), false;
-  if (nrank > 1 && v.s_rank != int64_t(g->batch) * v.s_b && g->batch > 1)
+  if (nrank > 1 && g->batch > 1 && v.s_rank != int64_t(g->batch) * v.s_b)
     return fail(RSA_ERR_UNSUPPORTED, "fused: panel rank stride must equal B * batch stride"), false;
   const int64_t sb = (g->batch == 1 && nrank > 1) ? v.s_rank : v.s_b;
   if (!stride_ok(v.s_row * 2) || !stride_ok(v.s_z * 2) || !stride_ok(sb * 2))
@@ -754,10 +870,37 @@ bool out_ok(const rsa_view& v, int esz) {
 }
 
 template <typename K, typename A>
-int launch(K kernel, dim3 grid, uint32_t smem, const A& args, void* stream, const char* name) {
+int launch(K kernel, int items, uint32_t smem, const A& args, void* stream, const char* name) {
+  if (items <= 0) return RSA_OK;
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int grid = items < num_sms() ? items : num_sms();
   kernel<<<grid, NTHREADS, smem, reinterpret_cast<cudaStream_t>(stream)>>>(args);
   return check_launch(name);
+}
+
+int fwd_launch(const rsa_geom* g, int mode, rsa_view q, rsa_view k, rsa_view v, float* stats, int slot, int n_slots,
+               rsa_view panel, rsa_view o_acc, int accumulate, rsa_view o_out, int* flag, void* stream) {
+  if (!geom_ok(g)) return fail(RSA_ERR_INVALID, "rsa_fwd: unsupported geometry");
+  if ((mode & (MODE_WRITE_STATS | MODE_EXT_STATS)) && !stats) return fail(RSA_ERR_INVALID, "rsa_fwd: stats missing");
+  if (!out_ok(o_acc, 4) || !out_ok(o_out, 2)) return fail(RSA_ERR_UNSUPPORTED, "rsa_fwd: output alignment");
+  FwdArgs a{};
+  if (!head_map(&a.tq, q, g, g->n_rank) || !head_map(&a.tk, k, g, g->n_org)) return RSA_ERR_UNSUPPORTED;
+  if (mode & MODE_PASS_B) {
+    if (!head_map(&a.tv, v, g, g->n_org) || !panel_map(&a.tp, panel, g, g->n_rank)) return RSA_ERR_UNSUPPORTED;
+  }
+  a.g = to_geo(g);
+  a.mode = mode;
+  a.sl = g->scale * LOG2E;
+  a.stats = reinterpret_cast<float2*>(stats);
+  a.slot = slot;
+  a.n_slots = n_slots;
+  a.slot_stride = int64_t(g->n_rank) * g->batch * g->heads * g->chunk;
+  a.flag = flag;
+  a.o_acc = to_out(o_acc);
+  a.o_out = to_out(o_out);
+  a.accumulate = accumulate;
+  const int items = g->n_rank * g->batch * g->heads * ((g->chunk + TR - 1) / TR);
+  return launch(fwd_kernel, items, F_SMEM, a, stream, "fwd_kernel");
 }
 
 }  // namespace
@@ -767,44 +910,33 @@ extern "C" {
 
 int rsa_fused_supported(const rsa_geom* g) { return rsa::geom_ok(g) ? 1 : 0; }
 
+int rsa_fwd_resident(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view panel, rsa_view o_out,
+                     int* nonfinite_flag, void* stream) {
+  using namespace rsa;
+  const rsa_view none{nullptr, 0, 0, 0, 0};
+  return fwd_launch(g, MODE_PASS_A | MODE_PASS_B, q, k, v, nullptr, 0, 0, panel, none, 0, o_out, nonfinite_flag,
+                    stream);
+}
+
 int rsa_fwd_stats(const rsa_geom* g, rsa_view q, rsa_view k, float* stats, int slot, int* nonfinite_flag,
                   void* stream) {
   using namespace rsa;
-  if (!geom_ok(g) || !stats || slot < 0) return fail(RSA_ERR_INVALID, "rsa_fwd_stats: unsupported geometry");
-  StatsArgs a{};
-  if (!head_map(&a.tq, q, g, g->n_rank) || !head_map(&a.tk, k, g, g->n_org)) return RSA_ERR_UNSUPPORTED;
-  a.g = to_geo(g);
-  a.sl = g->scale * LOG2E;
-  a.stats = reinterpret_cast<float2*>(stats);
-  a.slot_off = int64_t(slot) * g->n_rank * g->batch * g->heads * g->chunk;
-  a.flag = nonfinite_flag;
-  dim3 grid((g->chunk + TR - 1) / TR, g->batch * g->heads, g->n_rank);
-  return launch(fwd_stats_kernel, grid, ST_SMEM, a, stream, "fwd_stats_kernel");
+  const rsa_view none{nullptr, 0, 0, 0, 0};
+  if (slot < 0) return fail(RSA_ERR_INVALID, "rsa_fwd_stats: bad slot");
+  return fwd_launch(g, MODE_PASS_A | MODE_WRITE_STATS, q, k, none, stats, slot, 0, none, none, 0, none,
+                    nonfinite_flag, stream);
 }
 
 int rsa_fwd_probs_pv(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, const float* stats, int n_slots,
                      rsa_view panel, rsa_view o_acc, int accumulate, rsa_view o_out, void* stream) {
   using namespace rsa;
-  if (!geom_ok(g) || !stats || n_slots < 1) return fail(RSA_ERR_INVALID, "rsa_fwd_probs_pv: unsupported geometry");
-  if (!out_ok(o_acc, 4) || !out_ok(o_out, 2)) return fail(RSA_ERR_UNSUPPORTED, "rsa_fwd_probs_pv: output alignment");
-  PvArgs a{};
-  if (!head_map(&a.tq, q, g, g->n_rank) || !head_map(&a.tk, k, g, g->n_org) || !head_map(&a.tv, v, g, g->n_org) ||
-      !panel_map(&a.tp, panel, g, g->n_rank))
-    return RSA_ERR_UNSUPPORTED;
-  a.g = to_geo(g);
-  a.sl = g->scale * LOG2E;
-  a.stats = reinterpret_cast<const float2*>(stats);
-  a.n_slots = n_slots;
-  a.slot_stride = int64_t(g->n_rank) * g->batch * g->heads * g->chunk;
-  a.o_acc = to_out(o_acc);
-  a.o_out = to_out(o_out);
-  a.accumulate = accumulate;
-  dim3 grid((g->chunk + TR - 1) / TR, g->batch * g->heads, g->n_rank);
-  return launch(fwd_pv_kernel, grid, PV_SMEM, a, stream, "fwd_pv_kernel");
+  if (n_slots < 1) return fail(RSA_ERR_INVALID, "rsa_fwd_probs_pv: n_slots must be >= 1");
+  return fwd_launch(g, MODE_PASS_B | MODE_EXT_STATS, q, k, v, const_cast<float*>(stats), 0, n_slots, panel, o_acc,
+                    accumulate, o_out, nullptr, stream);
 }
 
 int rsa_bwd_dkdv(const rsa_geom* g, rsa_view q, rsa_view v, rsa_view dout, rsa_view panel, const float* dvec,
-                 rsa_view ds_panel, rsa_view dk, rsa_view dv, int dkv_dtype, int accumulate, void* stream) {
+                 rsa_view dk, rsa_view dv, int dkv_dtype, int accumulate, void* stream) {
   using namespace rsa;
   if (!geom_ok(g) || !dvec) return fail(RSA_ERR_INVALID, "rsa_bwd_dkdv: unsupported geometry");
   const int esz = dkv_dtype == RSA_BF16 ? 2 : 4;
@@ -812,7 +944,7 @@ int rsa_bwd_dkdv(const rsa_geom* g, rsa_view q, rsa_view v, rsa_view dout, rsa_v
     return fail(RSA_ERR_UNSUPPORTED, "rsa_bwd_dkdv: output alignment");
   DkdvArgs a{};
   if (!head_map(&a.tq, q, g, g->n_rank) || !head_map(&a.tdo, dout, g, g->n_rank) || !head_map(&a.tv, v, g, g->n_org) ||
-      !panel_map(&a.tp, panel, g, g->n_rank) || !panel_map(&a.tds, ds_panel, g, g->n_rank))
+      !panel_map(&a.tp, panel, g, g->n_rank))
     return RSA_ERR_UNSUPPORTED;
   a.g = to_geo(g);
   a.dvec = dvec;
@@ -820,23 +952,26 @@ int rsa_bwd_dkdv(const rsa_geom* g, rsa_view q, rsa_view v, rsa_view dout, rsa_v
   a.dv = to_out(dv);
   a.dkv_bf16 = dkv_dtype == RSA_BF16;
   a.accumulate = accumulate;
-  dim3 grid((g->chunk + TKEYS - 1) / TKEYS, g->batch * g->heads, g->n_org);
-  return launch(bwd_dkdv_kernel, grid, BK_SMEM, a, stream, "bwd_dkdv_kernel");
+  const int items = g->n_org * g->batch * g->heads * ((g->chunk + TK - 1) / TK);
+  return launch(bwd_dkdv_kernel, items, BK_SMEM, a, stream, "bwd_dkdv_kernel");
 }
 
-int rsa_bwd_dq(const rsa_geom* g, rsa_view ds_panel, rsa_view k, rsa_view dq_acc, int accumulate, rsa_view dq_out,
-               void* stream) {
+int rsa_bwd_dq(const rsa_geom* g, rsa_view dout, rsa_view k, rsa_view v, rsa_view panel, const float* dvec,
+               rsa_view dq_acc, int accumulate, rsa_view dq_out, void* stream) {
   using namespace rsa;
-  if (!geom_ok(g)) return fail(RSA_ERR_INVALID, "rsa_bwd_dq: unsupported geometry");
+  if (!geom_ok(g) || !dvec) return fail(RSA_ERR_INVALID, "rsa_bwd_dq: unsupported geometry");
   if (!out_ok(dq_acc, 4) || !out_ok(dq_out, 2)) return fail(RSA_ERR_UNSUPPORTED, "rsa_bwd_dq: output alignment");
   DqArgs a{};
-  if (!panel_map(&a.tds, ds_panel, g, g->n_rank) || !head_map(&a.tk, k, g, g->n_org)) return RSA_ERR_UNSUPPORTED;
+  if (!head_map(&a.tdo, dout, g, g->n_rank) || !head_map(&a.tk, k, g, g->n_org) || !head_map(&a.tv, v, g, g->n_org) ||
+      !panel_map(&a.tp, panel, g, g->n_rank))
+    return RSA_ERR_UNSUPPORTED;
   a.g = to_geo(g);
+  a.dvec = dvec;
   a.dq_acc = to_out(dq_acc);
   a.dq_out = to_out(dq_out);
   a.accumulate = accumulate;
-  dim3 grid((g->chunk + TR - 1) / TR, g->batch * g->heads, g->n_rank);
-  return launch(bwd_dq_kernel, grid, DQ_SMEM, a, stream, "bwd_dq_kernel");
+  const int items = g->n_rank * g->batch * g->heads * ((g->chunk + TR - 1) / TR);
+  return launch(bwd_dq_kernel, items, DQ_SMEM, a, stream, "bwd_dq_kernel");
 }
 
 }  // extern "C"

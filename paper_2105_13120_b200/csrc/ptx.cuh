@@ -250,6 +250,50 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// 2^x on the FMA/ALU pipes (no MUFU): round-to-nearest split x = n + f with
+// f in [-0.5, 0.5] via the 1.5*2^23 trick, a minimax polynomial for 2^f,
+// and n added straight into the exponent field.  Valid for x in [-125, 1];
+// the caller only passes x <= ~0 (softmax arguments).  Max relative error
+// 2.0e-4 (DEG 3, enough for a bf16 result) or 5.1e-6 (DEG 4).
+template <int DEG>
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float r = x + 12582912.f;   // round(x) lands in the low mantissa bits
+  const float n = r - 12582912.f;
+  const float f = x - n;
+  float p;
+  if constexpr (DEG == 3) {
+    p = fmaf(fmaf(fmaf(0.05314989015460014f, f, 0.2425033301115036f), f, 0.693769097328186f), f, 1.f);
+  } else {
+    p = fmaf(fmaf(fmaf(fmaf(0.009625268168747425f, f, 0.05598338693380356f), f, 0.24023357033729553f), f,
+                  0.6931096315383911f),
+             f, 1.f);
+  }
+  return __int_as_float(__float_as_int(p) + (__float_as_int(r) << 23));
+}
+
+// NaN-propagating min/max (plain fmaxf drops NaNs, which would hide a
+// non-finite score from the NumericError check).
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float y;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(y) : "f"(a), "f"(b));
+  return y;
+}
+__device__ __forceinline__ float min_nan(float a, float b) {
+  float y;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(y) : "f"(a), "f"(b));
+  return y;
+}
+
+__device__ __forceinline__ void st_shared_f2(uint32_t addr, float a, float b) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
+}
+__device__ __forceinline__ float2 ld_shared_f2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+
 // Byte offset of the 16-byte chunk `chunk` (0..7) of row `row` inside a
 // SWIZZLE_128B tile whose rows are 128 B (the TMA/UMMA 128B swizzle: the
 // 16-byte chunk index is XORed with the row index mod 8).

@@ -88,10 +88,10 @@ class CudaHopKernels:
 
         return tensor_ops.rowdot(grad, out)
 
-    def dkdv(self, q, v_j, grad, panel, dvec, ds, origin, seq, dk_j, dv_j):
+    def dkdv(self, q, v_j, grad, panel, dvec, origin, seq, dk_j, dv_j):
         g = self._g(q, seq, origin)
         v = self.engine._view
-        self.check(self.lib().rsa_bwd_dkdv(ctypes.byref(g), v(q), v(v_j), v(grad), v(panel), dvec.data_ptr(), v(ds),
+        self.check(self.lib().rsa_bwd_dkdv(ctypes.byref(g), v(q), v(v_j), v(grad), v(panel), dvec.data_ptr(),
                                            v(dk_j), v(dv_j), 0, 0, self._st(q)), "rsa_bwd_dkdv")
 
     def project_pair(self, e_cols, k, f_cols, v):
@@ -112,11 +112,11 @@ class CudaHopKernels:
         probs = tensor_ops.softmax_rows(scores, scale=1.0 / math.sqrt(q.shape[-1]), out_dtype=torch.bfloat16)
         return tensor_ops.matmul(probs, v_low.to(torch.bfloat16), out_dtype=torch.bfloat16)
 
-    def dq(self, ds, k_j, origin, seq, dq_acc, accumulate, dq_out):
-        g = self._g(k_j, seq, origin)
+    def dq(self, grad, k_j, v_j, panel, dvec, origin, seq, dq_acc, accumulate, dq_out):
+        g = self._g(grad, seq, origin)
         v = self.engine._view
-        self.check(self.lib().rsa_bwd_dq(ctypes.byref(g), v(ds), v(k_j), v(dq_acc), int(accumulate), v(dq_out),
-                                         self._st(k_j)), "rsa_bwd_dq")
+        self.check(self.lib().rsa_bwd_dq(ctypes.byref(g), v(grad), v(k_j), v(v_j), v(panel), dvec.data_ptr(),
+                                         v(dq_acc), int(accumulate), v(dq_out), self._st(grad)), "rsa_bwd_dq")
 
 
 @dataclass
@@ -214,20 +214,20 @@ class SpmdRing:
         seq = n * c
         dev = grad.device
         dvec = kern.rowdot(grad, ctx.out)
-        ds = torch.empty_like(ctx.panel)
         dk_part = torch.empty((n, b, z, c, a), dtype=_acc_dtype(grad), device=dev)
         dv_part = torch.empty_like(dk_part)
         v_slots = torch.empty((n, b, z, c, a), dtype=ctx.v_local.dtype, device=dev)
         v_slots[d].copy_(ctx.v_local[0])
-        self._circulate(v_slots, lambda h, j: kern.dkdv(ctx.q, v_slots[j:j + 1], grad, ctx.panel, dvec, ds, j, seq,
+        self._circulate(v_slots, lambda h, j: kern.dkdv(ctx.q, v_slots[j:j + 1], grad, ctx.panel, dvec, j, seq,
                                                         dk_part[j:j + 1], dv_part[j:j + 1]))
-        # K ring (the reference re-circulates keys: ringseq/ring_attention.py:192-196)
+        # K ring (the reference re-circulates keys: ringseq/ring_attention.py:192-196).  dS for origin j is
+        # recomputed from P, dO V_j^T and D with V_j from the V ring's slots, so no dS panel is kept.
         k_slots = torch.empty_like(ctx.k_slots)
         k_slots[d].copy_(ctx.k_slots[d])
         dq_acc = torch.empty((1, b, z, c, a), dtype=_acc_dtype(grad), device=dev)
         dq = torch.empty((1, b, z, c, a), dtype=grad.dtype, device=dev)
-        self._circulate(k_slots, lambda h, j: kern.dq(ds, k_slots[j:j + 1], j, seq, dq_acc, h > 0,
-                                                      dq if h == n - 1 else None))
+        self._circulate(k_slots, lambda h, j: kern.dq(grad, k_slots[j:j + 1], v_slots[j:j + 1], ctx.panel, dvec, j,
+                                                      seq, dq_acc, h > 0, dq if h == n - 1 else None))
         dk = self._reduce(dk_part)
         dv = self._reduce(dv_part)
         return dq, dk.to(grad.dtype), dv.to(grad.dtype)

@@ -153,14 +153,17 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, path: str = "a
         L = lib()
         st = _stream(q)
         g = _geom(n, b, z, c, a, seq, 0, n)
-        if stats is None:
-            stats = torch.empty((n * b * z * c * 2,), dtype=torch.float32, device=dev)
-        with tm("fwd_stats"):
-            check(L.rsa_fwd_stats(ctypes.byref(g), _view(q), _view(k), stats.data_ptr(), 0, flag.data_ptr(), st),
-                  "rsa_fwd_stats")
-        with tm("fwd_probs_pv"):
-            check(L.rsa_fwd_probs_pv(ctypes.byref(g), _view(q), _view(k), _view(v), stats.data_ptr(), 1,
-                                     _view(panel), NULL_VIEW, 0, _view(out), st), "rsa_fwd_probs_pv")
+        if stats is not None:  # two-launch form (K-ring stats, then V-ring probs/PV)
+            with tm("fwd_stats"):
+                check(L.rsa_fwd_stats(ctypes.byref(g), _view(q), _view(k), stats.data_ptr(), 0, flag.data_ptr(),
+                                      st), "rsa_fwd_stats")
+            with tm("fwd_probs_pv"):
+                check(L.rsa_fwd_probs_pv(ctypes.byref(g), _view(q), _view(k), _view(v), stats.data_ptr(), 1,
+                                         _view(panel), NULL_VIEW, 0, _view(out), st), "rsa_fwd_probs_pv")
+            return out, panel, flag
+        with tm("fwd_resident"):
+            check(L.rsa_fwd_resident(ctypes.byref(g), _view(q), _view(k), _view(v), _view(panel), _view(out),
+                                     flag.data_ptr(), st), "rsa_fwd_resident")
         return out, panel, flag
     _forward_staged(q, k, v, out, panel, flag)
     return out, panel, flag
@@ -206,7 +209,7 @@ def recompute_outputs(panel: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
 
 
 def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path: str = "auto",
-             grads: tuple | None = None, ds: torch.Tensor | None = None, dvec: torch.Tensor | None = None,
+             grads: tuple | None = None, dvec: torch.Tensor | None = None,
              timer=None):
     """RSA backward on stacked chunks; returns (dq, dk, dv) as [N][B][Z][c][A] bf16.
 
@@ -230,16 +233,15 @@ def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path:
             dvec = torch.empty((n, b, z, c), dtype=torch.float32, device=dev)
         with tm("rowdot"):
             ops.rowdot(grad, outputs, out=dvec)  # D = rowsum(dO * O) = rowsum(dP * P)
-        if ds is None:
-            ds = torch.empty((n, b, z, c, seq), dtype=torch.bfloat16, device=dev)
         L = lib()
         st = _stream(q)
         g = _geom(n, b, z, c, a, seq, 0, n)
         with tm("bwd_dkdv"):
             check(L.rsa_bwd_dkdv(ctypes.byref(g), _view(q), _view(v), _view(grad), _view(panel), dvec.data_ptr(),
-                                 _view(ds), _view(dk), _view(dv), BF16, 0, st), "rsa_bwd_dkdv")
+                                 _view(dk), _view(dv), BF16, 0, st), "rsa_bwd_dkdv")
         with tm("bwd_dq"):
-            check(L.rsa_bwd_dq(ctypes.byref(g), _view(ds), _view(k), NULL_VIEW, 0, _view(dq), st), "rsa_bwd_dq")
+            check(L.rsa_bwd_dq(ctypes.byref(g), _view(grad), _view(k), _view(v), _view(panel), dvec.data_ptr(),
+                               NULL_VIEW, 0, _view(dq), st), "rsa_bwd_dq")
         return dq, dk, dv
     _backward_staged(q, k, v, panel, grad, dq, dk, dv)
     return dq, dk, dv

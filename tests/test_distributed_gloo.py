@@ -52,19 +52,21 @@ class CpuHopKernels:
     def rowdot(self, grad, out):
         return (grad * out).sum(-1)
 
-    def dkdv(self, q, v_j, grad, panel, dvec, ds, origin, seq, dk_j, dv_j):
-        c = q.shape[-2]
-        blk = slice(origin * c, (origin + 1) * c)
-        p = panel[0][..., blk]
+    @staticmethod
+    def _ds(grad, v_j, panel, dvec, origin):
+        c = v_j.shape[-2]
+        p = panel[0][..., origin * c:(origin + 1) * c]
         dp = grad[0] @ v_j[0].transpose(-1, -2)
-        dsb = p * (dp - dvec[0][..., None]) / math.sqrt(q.shape[-1])
-        ds[0][..., blk] = dsb
+        return p, p * (dp - dvec[0][..., None]) / math.sqrt(grad.shape[-1])
+
+    def dkdv(self, q, v_j, grad, panel, dvec, origin, seq, dk_j, dv_j):
+        p, dsb = self._ds(grad, v_j, panel, dvec, origin)
         dk_j[0] = dsb.transpose(-1, -2) @ q[0]
         dv_j[0] = p.transpose(-1, -2) @ grad[0]
 
-    def dq(self, ds, k_j, origin, seq, dq_acc, accumulate, dq_out):
-        c = k_j.shape[-2]
-        t = ds[0][..., origin * c:(origin + 1) * c] @ k_j[0]
+    def dq(self, grad, k_j, v_j, panel, dvec, origin, seq, dq_acc, accumulate, dq_out):
+        _, dsb = self._ds(grad, v_j, panel, dvec, origin)
+        t = dsb @ k_j[0]
         dq_acc[0] = dq_acc[0] + t if accumulate else t
         if dq_out is not None:
             dq_out.copy_(dq_acc)
