@@ -209,6 +209,8 @@ def kernel_model(name, n, b, z, c, seq, a):
         return 2 * pe + 2 * 4 * ce, 6 * pe * a        # write P; Q,K,V in, O out; QK^T twice + PV
     if name == "bwd_dkdv":
         return 2 * pe + 2 * 5 * ce, 6 * pe * a        # read P; dO,Q,V in, dK,dV out; dO V^T, P^T dO, dS^T Q
+    if name == "bwd_fused":
+        return 2 * pe + 2 * 7 * ce, 8 * pe * a        # read P; Q,K,V,dO in, dQ,dK,dV out; dO V^T, P^T dO, dS^T Q, dS K
     if name == "bwd_dq":
         return 2 * pe + 2 * 4 * ce, 4 * pe * a        # read P; dO,K,V in, dQ out; dO V^T, dS K
     if name == "rowdot":

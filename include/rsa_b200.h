@@ -165,6 +165,23 @@ int rsa_bwd_dq(const rsa_geom* g, rsa_view dout, rsa_view k, rsa_view v, rsa_vie
 /* Can the fused kernels tile this geometry (head_dim, chunk, alignment)? */
 int rsa_fused_supported(const rsa_geom* g);
 
+/*
+ * Whole RSA backward of ringseq/ring_attention.py:168-209 in ONE pass over
+ * the probability panel: per head, dP = dO V_j^T, dS = P (dP - D) scale
+ * (shared memory only), dV_j = P_j^T dO and dK_j = dS_j^T Q summed over the
+ * launch's query ranks (the all-reduce of :206-209 when resident), and
+ * dQ = sum_j dS_j K_j (the K ring of :192-196), all accumulated in TMEM.
+ * Replaces the rsa_bwd_dkdv + rsa_bwd_dq pair (which read the panel twice)
+ * when a head's query rows fit four 128-row tiles:
+ * n_rank * ceil(chunk / 128) <= 4 (rsa_bwd_fused_supported).
+ * dq: fp32 dq_acc (accumulate_dq != 0 adds) and/or bf16 dq_out; dk/dv:
+ * bf16 or fp32 per dkv_dtype (fp32 with accumulate_dkv != 0 adds).
+ */
+int rsa_bwd_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view dout, rsa_view panel,
+                  const float* dvec, rsa_view dq_acc, int accumulate_dq, rsa_view dq_out, rsa_view dk, rsa_view dv,
+                  int dkv_dtype, int accumulate_dkv, void* stream);
+int rsa_bwd_fused_supported(const rsa_geom* g);
+
 #ifdef __cplusplus
 }
 #endif

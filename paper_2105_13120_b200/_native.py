@@ -88,6 +88,8 @@ EXPORTS = {
     "rsa_bwd_dkdv": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, _V, _V, c_int, c_int, c_void_p]),
     "rsa_bwd_dq": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, _V, c_int, _V, c_void_p]),
     "rsa_fused_supported": (c_int, [_GEOM]),
+    "rsa_bwd_fused": (c_int, [_GEOM, _V, _V, _V, _V, _V, c_void_p, _V, c_int, _V, _V, _V, c_int, c_int, c_void_p]),
+    "rsa_bwd_fused_supported": (c_int, [_GEOM]),
 }
 
 _lib = None

@@ -1,0 +1,394 @@
+// Single-pass RSA backward for sm_100a (head size A = 64): dQ, dK and dV of a
+// head from ONE read of its probability panel.
+//
+// Replaces the V-ring / K-ring pair of ringseq/ring_attention.py:168-209:
+//   dP = dO V_j^T                       (V ring, :181-184)
+//   dS = P (dP - rowsum(dP P)) scale    (:186-189; rowsum(dP P) = rowsum(dO O) = D, supplied)
+//   dQ = sum_j dS_j K_j                 (K ring, :192-196)
+//   dK_j = dS_j^T Q,  dV_j = P_j^T dO   (full-length partials, :198-205)
+// for every (query tile, key tile) pair of one head inside one CTA, so the
+// panel tile P(qt, kt) is loaded once and dS never leaves shared memory.
+//
+// A CTA owns a whole head (b, z): the outer loop walks key tiles kt (any
+// number: all resident origins), the inner loop the head's query tiles qt
+// (at most 4 -- n_rank * ceil(c / 128) <= 4, e.g. L <= 512 resident, or
+// c <= 512 per ring hop).  TMEM (512 columns) holds
+//   [  0,128)  dP of the current step
+//   [128,192)  dV of the current key tile      (M = keys)
+//   [192,256)  dK of the current key tile
+//   [256,512)  dQ of each query tile, 64 columns per tile, live for the head
+// so dK/dV are final when a key tile's inner loop ends and dQ when the last
+// key tile has been applied -- every sum is accumulated in TMEM in a fixed
+// order (deterministic, no atomics).
+//
+// Warp roles (10 warps): warp 0 TMA producer, warp 1 tcgen05.mma issuer
+// (owns TMEM), warps 2..9 epilogue (warp w reads TMEM lanes 32*(w%4)..,
+// column half (w-2)/4).  Rings: K, V, dO, Q tiles 2 deep each, panel
+// tiles 3 deep (the only HBM stream that matters; dO/Q re-reads are L2 hits).  dS overwrites P in place once P^T dO has consumed it.
+#include "fused_common.cuh"
+
+namespace rsa {
+namespace {
+
+constexpr int MAX_QT = 4;  // query tiles per head that fit the dQ columns of TMEM
+
+struct BwdArgs {
+  CUtensorMap tq, tk, tv, tdo, tp;
+  Geo g;
+  const float* dvec;
+  OutView dq_acc, dq_out, dk, dv;
+  int accumulate_dq;
+  int dkv_bf16;
+  int accumulate_dkv;
+};
+
+// Ring depths.  Each operand is released as soon as its last MMA has read it
+// (dO after P^T dO, V after the key tile's last dO V^T, Q / P / K after the
+// dS products), so the producer runs 1-2 steps ahead of the tensor pipe.
+constexpr int BF_DO = 2, BF_Q = 2, BF_P = 3, BF_K = 2, BF_V = 2;
+constexpr uint32_t BF_OFF_DO = 0;
+constexpr uint32_t BF_OFF_Q = BF_OFF_DO + BF_DO * TILE;
+constexpr uint32_t BF_OFF_K = BF_OFF_Q + BF_Q * TILE;
+constexpr uint32_t BF_OFF_V = BF_OFF_K + BF_K * TILE;
+constexpr uint32_t BF_OFF_P = BF_OFF_V + BF_V * TILE;  // [slot] P, then dS in place
+constexpr uint32_t BF_OFF_BAR = BF_OFF_P + BF_P * PTILE;
+constexpr uint32_t BF_SMEM = BF_OFF_BAR + 512 + 1024;
+static_assert(BF_SMEM <= 232448, "bwd_fused smem over the sm_100 per-CTA limit");
+
+constexpr uint32_t COL_DP = 0, COL_DV = 128, COL_DK = 192, COL_DQ = 256;
+
+struct Ring {  // full/empty barrier pair array of one operand ring
+  uint64_t *full, *empty;
+};
+
+__global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_constant__ BwdArgs p) {
+  uint8_t* smem = smem_base();
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BF_OFF_BAR);
+  const Ring rdo{bar, bar + BF_DO};
+  const Ring rq{rdo.empty + BF_DO, rdo.empty + BF_DO + BF_Q};
+  const Ring rk{rq.empty + BF_Q, rq.empty + BF_Q + BF_K};
+  const Ring rv{rk.empty + BF_K, rk.empty + BF_K + BF_V};
+  const Ring rp{rv.empty + BF_V, rv.empty + BF_V + BF_P};
+  uint64_t* ds_full = rp.empty + BF_P;
+  uint64_t* p_read = ds_full + BF_P;  // P^T dO has consumed the P slot (dS may overwrite it)
+  uint64_t *dp_full = p_read + BF_P, *dp_empty = dp_full + 1, *acc_full = dp_empty + 1, *acc_empty = acc_full + 1;
+  uint64_t *dq_full = acc_empty + 1, *dq_empty = dq_full + MAX_QT;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_empty + MAX_QT);
+
+  const Geo& g = p.g;
+  const int nrt = (g.c + TR - 1) / TR, ntk = (g.c + TK - 1) / TK;
+  const int NQ = g.n_rank * nrt;  // query tiles of a head (<= MAX_QT)
+  const int NK = g.n_org * ntk;   // key tiles of a head
+  const int T = NQ * NK;
+  const int items = g.B * g.Z;
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (threadIdx.x == 0) {
+    auto init = [](const Ring& r, int n) {
+      for (int s = 0; s < n; ++s) mbar_init(&r.full[s], 1), mbar_init(&r.empty[s], 1);
+    };
+    init(rdo, BF_DO), init(rq, BF_Q), init(rk, BF_K), init(rv, BF_V), init(rp, BF_P);
+    for (int s = 0; s < BF_P; ++s) mbar_init(&ds_full[s], EPI_WARPS), mbar_init(&p_read[s], 1);
+    mbar_init(dp_full, 1), mbar_init(dp_empty, EPI_WARPS);
+    mbar_init(acc_full, 1), mbar_init(acc_empty, EPI_WARPS);
+    for (int s = 0; s < MAX_QT; ++s) mbar_init(&dq_full[s], 1), mbar_init(&dq_empty[s], EPI_WARPS);
+    fence_barrier_init();
+    tma_prefetch(&p.tq), tma_prefetch(&p.tk), tma_prefetch(&p.tv), tma_prefetch(&p.tdo), tma_prefetch(&p.tp);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      Pos dq_, qq, kq, vq, pq;
+      // one 16 KB head tile (rows r0.. of rank/origin `blk`) into ring slot
+      auto load_tile = [&](const Ring& r, Pos& pos, int depth, uint32_t off, const CUtensorMap* map, int r0, int z,
+                           int blk) {
+        const uint32_t s = pos.slot(depth);
+        mbar_wait(&r.empty[s], pos.phase(depth) ^ 1);
+        mbar_arrive_expect_tx(&r.full[s], TILE);
+        tma_load_4d(smem + off + s * TILE, map, &r.full[s], 0, r0, z, blk);
+        ++pos.i;
+      };
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int b = item / g.Z, z = item % g.Z;
+        for (int kk = 0; kk < NK; ++kk) {
+          const int jo = kk / ntk, k0 = (kk % ntk) * TK;
+          for (int qt = 0; qt < NQ; ++qt) {
+            const int d = qt / nrt, r0 = (qt % nrt) * TR;
+            // consumption order: V (first dO V^T of the key tile), dO, P, then K, Q (dS products)
+            if (qt == 0) load_tile(rv, vq, BF_V, BF_OFF_V, &p.tv, k0, z, jo * g.B + b);
+            load_tile(rdo, dq_, BF_DO, BF_OFF_DO, &p.tdo, r0, z, d * g.B + b);
+            const uint32_t s = pq.slot(BF_P);
+            mbar_wait(&rp.empty[s], pq.phase(BF_P) ^ 1);
+            mbar_arrive_expect_tx(&rp.full[s], PTILE);
+            uint8_t* pt = smem + BF_OFF_P + s * PTILE;
+            tma_load_5d(pt, &p.tp, &rp.full[s], k0, g.org_lo + jo, r0, z, d * g.B + b);
+            tma_load_5d(pt + ATOM, &p.tp, &rp.full[s], k0 + 64, g.org_lo + jo, r0, z, d * g.B + b);
+            ++pq.i;
+            if (qt == 0) load_tile(rk, kq, BF_K, BF_OFF_K, &p.tk, k0, z, jo * g.B + b);
+            load_tile(rq, qq, BF_Q, BF_OFF_Q, &p.tq, r0, z, d * g.B + b);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc_dp = idesc_bf16_f32(TR, TK, 0, 0);  // dO (K-major) x V (K-major)     -> 128 x 128
+      const uint32_t idesc_kv = idesc_bf16_f32(TK, HD, 1, 1);  // P^T / dS^T (MN) x dO / Q (MN) -> 128 x 64
+      const uint32_t idesc_dq = idesc_bf16_f32(TR, HD, 0, 1);  // dS (K-major) x K (MN-major)   -> 128 x 64
+      Pos v_a, do_a, p_a, k_b, q_b, p_b, dpq, accq;
+      uint32_t head_it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++head_it) {
+        // dP(t) = dO V^T into the single dP buffer (after the epilogue has read dP(t-1))
+        auto issue_dp = [&](int t) {
+          const int qt = t % NQ;
+          const uint32_t vs = v_a.slot(BF_V), ds = do_a.slot(BF_DO);
+          if (qt == 0) mbar_wait(&rv.full[vs], v_a.phase(BF_V));
+          mbar_wait(&rdo.full[ds], do_a.phase(BF_DO));
+          mbar_wait(dp_empty, dpq.phase(1) ^ 1);
+          tc_fence_after();
+          const uint32_t doa = smem_u32(smem + BF_OFF_DO + ds * TILE);
+          const uint32_t va = smem_u32(smem + BF_OFF_V + vs * TILE);
+#pragma unroll
+          for (int k = 0; k < HD / 16; ++k)
+            umma_bf16(tmem + COL_DP, smem_desc_sw128(doa + k * 32, 0, 1024), smem_desc_sw128(va + k * 32, 0, 1024),
+                      idesc_dp, k > 0);
+          if (qt == NQ - 1) {
+            umma_commit(&rv.empty[vs]);
+            ++v_a.i;
+          }
+          umma_commit(dp_full);
+          ++dpq.i;
+        };
+        // dV += P^T dO; p_read certifies P has been consumed, so dS may overwrite it
+        auto issue_dv = [&](int t) {
+          const int qt = t % NQ;
+          const uint32_t ds = do_a.slot(BF_DO), ps = p_a.slot(BF_P);
+          if (qt == 0) mbar_wait(acc_empty, accq.phase(1) ^ 1);
+          mbar_wait(&rp.full[ps], p_a.phase(BF_P));
+          tc_fence_after();
+          const uint32_t doa = smem_u32(smem + BF_OFF_DO + ds * TILE);
+          const uint32_t pa = smem_u32(smem + BF_OFF_P + ps * PTILE);
+#pragma unroll
+          for (int k = 0; k < TR / 16; ++k)
+            umma_bf16(tmem + COL_DV, smem_desc_sw128(pa + k * 2048, ATOM, 1024),
+                      smem_desc_sw128(doa + k * 2048, ATOM, 1024), idesc_kv, (qt | k) != 0);
+          umma_commit(&rdo.empty[ds]);
+          umma_commit(&p_read[ps]);
+          ++do_a.i, ++p_a.i;
+          if (qt == NQ - 1) ++accq.i;
+        };
+        // dK += dS^T Q and dQ(qt) += dS K once the epilogue has written dS(t)
+        auto issue_b = [&](int t) {
+          const int kk = t / NQ, qt = t % NQ;
+          const uint32_t ks = k_b.slot(BF_K), qs = q_b.slot(BF_Q), ps = p_b.slot(BF_P);
+          if (qt == 0) mbar_wait(&rk.full[ks], k_b.phase(BF_K));
+          mbar_wait(&rq.full[qs], q_b.phase(BF_Q));
+          mbar_wait(&ds_full[ps], p_b.phase(BF_P));
+          tc_fence_after();
+          const uint32_t qa = smem_u32(smem + BF_OFF_Q + qs * TILE);
+          const uint32_t dsa = smem_u32(smem + BF_OFF_P + ps * PTILE);
+          const uint32_t ka = smem_u32(smem + BF_OFF_K + ks * TILE);
+#pragma unroll
+          for (int k = 0; k < TR / 16; ++k)
+            umma_bf16(tmem + COL_DK, smem_desc_sw128(dsa + k * 2048, ATOM, 1024),
+                      smem_desc_sw128(qa + k * 2048, ATOM, 1024), idesc_kv, (qt | k) != 0);
+          if (kk == 0) {
+            mbar_wait(&dq_empty[qt], (head_it & 1) ^ 1);
+            tc_fence_after();
+          }
+#pragma unroll
+          for (int k = 0; k < TK / 16; ++k)
+            umma_bf16(tmem + COL_DQ + qt * HD, smem_desc_sw128(dsa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
+                      smem_desc_sw128(ka + k * 2048, ATOM, 1024), idesc_dq, (kk | k) != 0);
+          umma_commit(&rp.empty[ps]);
+          umma_commit(&rq.empty[qs]);
+          if (qt == NQ - 1) {
+            umma_commit(acc_full);
+            umma_commit(&rk.empty[ks]);
+            ++k_b.i;
+          }
+          if (kk == NK - 1) umma_commit(&dq_full[qt]);
+          ++q_b.i, ++p_b.i;
+        };
+        issue_dp(0);
+        issue_dv(0);
+        for (int t = 0; t < T; ++t) {
+          const bool next = t + 1 < T;
+          const bool new_kt = next && (t + 1) % NQ == 0;
+          if (next) issue_dp(t + 1);
+          if (next && !new_kt) issue_dv(t + 1);
+          issue_b(t);
+          if (new_kt) issue_dv(t + 1);  // its dV overwrites the key tile just finished: after acc_empty
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    // Readouts of finished accumulators are deferred by one step: a key
+    // tile's dK/dV are read while the next step's dS is in registers (before
+    // its P slot is overwritten, since the next P^T dO waits for them), and a
+    // query tile's dQ after the next step's dS is stored.  So the epilogue
+    // never waits on the MMAs its own dS has just enabled.
+    const uint32_t quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_base = (quad * 32u) << 16;
+    Pos pq, dpq, accq;
+    uint32_t head_it = 0;
+    // pending readouts: key tile (jo, k0) of head (kb, kz); query tile qqt of head (qb, qz)
+    bool kv_on = false, q_on = false;
+    int kjo = 0, kk0 = 0, kb = 0, kz = 0, qqt = 0, qd = 0, qrow = 0, qb = 0, qz = 0;
+    uint32_t qphase = 0;
+    auto read_kv = [&](float* dvv, float* dkv) {
+      mbar_wait(acc_full, accq.phase(1));
+      tc_fence_after();
+      __syncwarp();
+      tmem_ld32(tmem + lane_base + COL_DV + half * 32, dvv);
+      tmem_ld32(tmem + lane_base + COL_DK + half * 32, dkv);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);
+      ++accq.i;
+    };
+    auto store_kv = [&](float* dvv, float* dkv) {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) dkv[e] *= g.scale;
+      const int key = kk0 + r;
+      if (key < g.c) {
+        const OutView none{nullptr, 0, 0, 0, 0};
+        if (p.dkv_bf16) {
+          store_row32(none, p.dv, 0, kjo, kb, kz, key, half * 32, dvv);
+          store_row32(none, p.dk, 0, kjo, kb, kz, key, half * 32, dkv);
+        } else {
+          store_row32(p.dv, none, p.accumulate_dkv, kjo, kb, kz, key, half * 32, dvv);
+          store_row32(p.dk, none, p.accumulate_dkv, kjo, kb, kz, key, half * 32, dkv);
+        }
+      }
+      kv_on = false;
+    };
+    auto flush_q = [&]() {
+      float o[32];
+      mbar_wait(&dq_full[qqt], qphase);
+      tc_fence_after();
+      __syncwarp();
+      tmem_ld32(tmem + lane_base + COL_DQ + qqt * HD + half * 32, o);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dq_empty[qqt]);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) o[e] *= g.scale;
+      if (qrow < g.c) store_row32(p.dq_acc, p.dq_out, p.accumulate_dq, qd, qb, qz, qrow, half * 32, o);
+      q_on = false;
+    };
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++head_it) {
+      const int b = item / g.Z, z = item % g.Z;
+      for (int t = 0; t < T; ++t) {
+        const int kk = t / NQ, qt = t % NQ;
+        const int d = qt / nrt, row = (qt % nrt) * TR + r;
+        const float dval = row < g.c ? p.dvec[(int64_t(d * g.B + b) * g.Z + z) * g.c + row] : 0.f;
+        const uint32_t ps = pq.slot(BF_P);
+        const uint32_t pt = smem_u32(smem + BF_OFF_P + ps * PTILE);
+        float dp[64];
+        mbar_wait(&rp.full[ps], pq.phase(BF_P));
+        mbar_wait(dp_full, dpq.phase(1));
+        tc_fence_after();
+        __syncwarp();
+        tmem_ld32(tmem + lane_base + COL_DP + half * 64, dp);
+        tmem_ld32(tmem + lane_base + COL_DP + half * 64 + 32, dp + 32);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dp_empty);
+        ++dpq.i;
+        // dS' = P (dP - D) as packed bf16 (the 1/sqrt(A) scale is applied to dQ / dK at the end)
+        uint32_t dsw[32];
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          float pv[32];
+          ld_row32_sw128(pt, r, half * 64 + cc * 32, pv);
+#pragma unroll
+          for (int e = 0; e < 32; e += 2)
+            dsw[cc * 16 + e / 2] = pack_bf16(pv[e] * (dp[cc * 32 + e] - dval), pv[e + 1] * (dp[cc * 32 + e + 1] - dval));
+        }
+        if (kv_on) {  // frees dK/dV for this step's P^T dO
+          float dvv[32], dkv[32];
+          read_kv(dvv, dkv);
+          store_kv(dvv, dkv);
+        }
+        mbar_wait(&p_read[ps], pq.phase(BF_P));
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const uint32_t atom = (half * 64 + cc * 32) >> 6, chunk0 = ((half * 64 + cc * 32) & 63) >> 3;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4)
+            st_shared_v4(pt + atom * ATOM + sw128_offset(r, chunk0 + q4), dsw[cc * 16 + q4 * 4],
+                         dsw[cc * 16 + q4 * 4 + 1], dsw[cc * 16 + q4 * 4 + 2], dsw[cc * 16 + q4 * 4 + 3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ds_full[ps]);
+        ++pq.i;
+        if (q_on) flush_q();
+        if (qt == NQ - 1) kv_on = true, kjo = kk / ntk, kk0 = (kk % ntk) * TK, kb = b, kz = z;
+        if (kk == NK - 1) q_on = true, qqt = qt, qd = d, qrow = row, qb = b, qz = z, qphase = head_it & 1;
+      }
+    }
+    if (kv_on) {
+      float dvv[32], dkv[32];
+      read_kv(dvv, dkv);
+      store_kv(dvv, dkv);
+    }
+    if (q_on) flush_q();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+bool bwd_fused_geom_ok(const rsa_geom* g) {
+  return geom_ok(g) && g->n_rank * ((g->chunk + TR - 1) / TR) <= MAX_QT;
+}
+
+}  // namespace
+}  // namespace rsa
+
+extern "C" {
+
+int rsa_bwd_fused_supported(const rsa_geom* g) { return rsa::bwd_fused_geom_ok(g) ? 1 : 0; }
+
+int rsa_bwd_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view dout, rsa_view panel,
+                  const float* dvec, rsa_view dq_acc, int accumulate_dq, rsa_view dq_out, rsa_view dk, rsa_view dv,
+                  int dkv_dtype, int accumulate_dkv, void* stream) {
+  using namespace rsa;
+  if (!bwd_fused_geom_ok(g) || !dvec)
+    return fail(RSA_ERR_INVALID, "rsa_bwd_fused: unsupported geometry (need A=64, c%%8==0, n_rank*ceil(c/128)<=4)");
+  const int esz = dkv_dtype == RSA_BF16 ? 2 : 4;
+  if (!dk.ptr || !dv.ptr || !out_ok(dk, esz) || !out_ok(dv, esz) || !out_ok(dq_acc, 4) || !out_ok(dq_out, 2) ||
+      (!dq_acc.ptr && !dq_out.ptr))
+    return fail(RSA_ERR_UNSUPPORTED, "rsa_bwd_fused: output views missing or misaligned");
+  BwdArgs a{};
+  if (!head_map(&a.tq, q, g, g->n_rank) || !head_map(&a.tdo, dout, g, g->n_rank) ||
+      !head_map(&a.tk, k, g, g->n_org) || !head_map(&a.tv, v, g, g->n_org) || !panel_map(&a.tp, panel, g, g->n_rank))
+    return RSA_ERR_UNSUPPORTED;
+  a.g = to_geo(g);
+  a.dvec = dvec;
+  a.dq_acc = to_out(dq_acc);
+  a.dq_out = to_out(dq_out);
+  a.dk = to_out(dk);
+  a.dv = to_out(dv);
+  a.accumulate_dq = accumulate_dq;
+  a.dkv_bf16 = dkv_dtype == RSA_BF16;
+  a.accumulate_dkv = accumulate_dkv;
+  return launch(bwd_fused_kernel, g->batch * g->heads, BF_SMEM, a, stream, "bwd_fused_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,166 @@
+// Shared pieces of the fused RSA kernels (fused.cu, bwd_fused.cu): tile
+// constants, pipeline positions, swizzled smem row moves, strided outputs,
+// and the host-side TMA map builders.  Everything is internal linkage.
+#pragma once
+
+#include "common.h"
+#include "ptx.cuh"
+
+namespace rsa {
+namespace {
+
+constexpr int HD = 64;                      // head size the fused kernels tile
+constexpr int TR = 128;                     // rows per tile (UMMA M)
+constexpr int TK = 128;                     // keys per tile
+constexpr uint32_t TILE = TR * HD * 2;      // 16 KB: 128 x 64 bf16
+constexpr uint32_t PTILE = TR * TK * 2;     // 32 KB: 128 x 128 bf16 (two 64-key atoms)
+constexpr uint32_t ATOM = TR * 128;         // 16 KB: one 128-row x 128-byte swizzle column
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr int EPI_WARPS = 8;
+constexpr int NTHREADS = 64 + 32 * EPI_WARPS;  // 320
+constexpr int EPI_THREADS = 32 * EPI_WARPS;    // 256
+
+enum { MODE_PASS_A = 1, MODE_PASS_B = 2, MODE_EXT_STATS = 4, MODE_WRITE_STATS = 8 };
+
+__device__ __forceinline__ void bar_epi() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void bar_half(int h) { asm volatile("bar.sync %0, 128;" ::"r"(2 + h) : "memory"); }
+
+// Pipeline position: slot and phase of the i-th use of an n-deep ring.
+struct Pos {
+  uint32_t i = 0;
+  __device__ __forceinline__ uint32_t slot(uint32_t n) const { return i % n; }
+  __device__ __forceinline__ uint32_t phase(uint32_t n) const { return (i / n) & 1u; }
+};
+
+// 32 fp32 values of row r, columns col0..col0+31, as bf16 into a
+// [64-col atom][128 rows][128 B] SWIZZLE_128B tile.
+__device__ __forceinline__ void st_row32_sw128(uint32_t tile, uint32_t r, int col0, const float* v) {
+  const uint32_t atom = col0 >> 6, chunk0 = (col0 & 63) >> 3;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    st_shared_v4(tile + atom * ATOM + sw128_offset(r, chunk0 + q), pack_bf16(v[8 * q], v[8 * q + 1]),
+                 pack_bf16(v[8 * q + 2], v[8 * q + 3]), pack_bf16(v[8 * q + 4], v[8 * q + 5]),
+                 pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+}
+
+__device__ __forceinline__ void ld_row32_sw128(uint32_t tile, uint32_t r, int col0, float* v) {
+  const uint32_t atom = col0 >> 6, chunk0 = (col0 & 63) >> 3;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t w[4];
+    ld_shared_v4(tile + atom * ATOM + sw128_offset(r, chunk0 + q), w[0], w[1], w[2], w[3]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[e]));
+      v[8 * q + 2 * e] = f.x;
+      v[8 * q + 2 * e + 1] = f.y;
+    }
+  }
+}
+
+struct OutView {  // strided output [rank][b][z][row][a]
+  void* ptr;
+  int64_t s_rank, s_b, s_z, s_row;
+};
+
+__device__ __forceinline__ int64_t out_off(const OutView& o, int rank, int b, int z, int row) {
+  return int64_t(rank) * o.s_rank + int64_t(b) * o.s_b + int64_t(z) * o.s_z + int64_t(row) * o.s_row;
+}
+
+// Store 32 fp32 values (columns col0..col0+31 of one row): fp32 (optionally
+// accumulating) and/or bf16.
+__device__ __forceinline__ void store_row32(const OutView& acc, const OutView& fin, int accumulate, int rank, int b,
+                                            int z, int row, int col0, float* v) {
+  if (acc.ptr) {
+    float* p = reinterpret_cast<float*>(acc.ptr) + out_off(acc, rank, b, z, row) + col0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      if (accumulate) {
+        const float4 old = *reinterpret_cast<const float4*>(p + i);
+        o.x += old.x, o.y += old.y, o.z += old.z, o.w += old.w;
+        v[i] = o.x, v[i + 1] = o.y, v[i + 2] = o.z, v[i + 3] = o.w;
+      }
+      *reinterpret_cast<float4*>(p + i) = o;
+    }
+  }
+  if (fin.ptr) {
+    __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(fin.ptr) + out_off(fin, rank, b, z, row) + col0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 8)
+      *reinterpret_cast<uint4*>(p + i) = make_uint4(pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]),
+                                                    pack_bf16(v[i + 4], v[i + 5]), pack_bf16(v[i + 6], v[i + 7]));
+  }
+}
+
+struct Geo {
+  int n_rank, B, Z, c, L, org_lo, n_org;
+  float scale;
+};
+
+__device__ __forceinline__ uint8_t* smem_base() {
+  extern __shared__ uint8_t smem_raw[];
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+}
+
+// ------------------------------------------------------------ host side
+
+inline bool geom_ok(const rsa_geom* g) {
+  return g && g->n_rank >= 1 && g->batch >= 1 && g->heads >= 1 && g->chunk >= 1 && g->head_dim == HD &&
+         g->n_org >= 1 && g->org_lo >= 0 && g->seq_len % g->chunk == 0 && g->chunk % 8 == 0 &&
+         g->org_lo + g->n_org <= g->seq_len / g->chunk;
+}
+
+inline Geo to_geo(const rsa_geom* g) {
+  return Geo{g->n_rank, g->batch, g->heads, g->chunk, g->seq_len, g->org_lo, g->n_org, g->scale};
+}
+
+// [rank][b][z][row][a] with a = 64 contiguous; `nrank` ranks merged into b.
+inline bool head_map(CUtensorMap* m, const rsa_view& v, const rsa_geom* g, int nrank) {
+  if (!v.ptr || !aligned16(v.ptr)) return fail(RSA_ERR_UNSUPPORTED, "fused: tensor not 16-byte aligned"), false;
+  if (nrank > 1 && g->batch > 1 && v.s_rank != int64_t(g->batch) * v.s_b)
+    return fail(RSA_ERR_UNSUPPORTED, "fused: rank stride must equal B * batch stride"), false;
+  const int64_t sb = (g->batch == 1 && nrank > 1) ? v.s_rank : v.s_b;
+  if (!stride_ok(v.s_row * 2) || !stride_ok(v.s_z * 2) || !stride_ok(sb * 2))
+    return fail(RSA_ERR_UNSUPPORTED, "fused: strides must be multiples of 8 elements"), false;
+  uint64_t dims[4] = {uint64_t(HD), uint64_t(g->chunk), uint64_t(g->heads), uint64_t(g->batch) * nrank};
+  uint64_t str[3] = {uint64_t(v.s_row) * 2, uint64_t(v.s_z) * 2, uint64_t(sb) * 2};
+  uint32_t box[4] = {64, TR, 1, 1};
+  return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, v.ptr, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// [rank][b][z][row][col], col = blk * c + key: 5-D (key, blk, row, z, b*rank).
+inline bool panel_map(CUtensorMap* m, const rsa_view& v, const rsa_geom* g, int nrank) {
+  if (!v.ptr || !aligned16(v.ptr)) return fail(RSA_ERR_UNSUPPORTED, "fused: panel not 16-byte aligned"), false;
+  if (nrank > 1 && g->batch > 1 && v.s_rank != int64_t(g->batch) * v.s_b)
+    return fail(RSA_ERR_UNSUPPORTED, "fused: panel rank stride must equal B * batch stride"), false;
+  const int64_t sb = (g->batch == 1 && nrank > 1) ? v.s_rank : v.s_b;
+  if (!stride_ok(v.s_row * 2) || !stride_ok(v.s_z * 2) || !stride_ok(sb * 2))
+    return fail(RSA_ERR_UNSUPPORTED, "fused: panel strides must be multiples of 8 elements"), false;
+  const int nblk = g->seq_len / g->chunk;
+  uint64_t dims[5] = {uint64_t(g->chunk), uint64_t(nblk), uint64_t(g->chunk), uint64_t(g->heads),
+                      uint64_t(g->batch) * nrank};
+  uint64_t str[4] = {uint64_t(g->chunk) * 2, uint64_t(v.s_row) * 2, uint64_t(v.s_z) * 2, uint64_t(sb) * 2};
+  uint32_t box[5] = {64, 1, TR, 1, 1};
+  return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, v.ptr, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+inline OutView to_out(const rsa_view& v) { return OutView{v.ptr, v.s_rank, v.s_b, v.s_z, v.s_row}; }
+
+inline bool out_ok(const rsa_view& v, int esz) {
+  if (!v.ptr) return true;
+  return aligned16(v.ptr) && (v.s_row * esz) % 16 == 0 && (v.s_z * esz) % 16 == 0 && (v.s_b * esz) % 16 == 0 &&
+         (v.s_rank * esz) % 16 == 0;
+}
+
+template <typename K, typename A>
+int launch(K kernel, int items, uint32_t smem, const A& args, void* stream, const char* name) {
+  if (items <= 0) return RSA_OK;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int grid = items < num_sms() ? items : num_sms();
+  kernel<<<grid, NTHREADS, smem, reinterpret_cast<cudaStream_t>(stream)>>>(args);
+  return check_launch(name);
+}
+
+}  // namespace
+}  // namespace rsa

@@ -208,13 +208,21 @@ def recompute_outputs(panel: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def single_pass_supported(n: int, b: int, z: int, c: int, a: int) -> bool:
+    """Does rsa_bwd_fused cover this geometry (a head's query rows in <= 4 tiles)?"""
+    g = _geom(n, b, z, c, a, n * c, 0, n)
+    return bool(lib().rsa_bwd_fused_supported(ctypes.byref(g)))
+
+
 def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path: str = "auto",
              grads: tuple | None = None, dvec: torch.Tensor | None = None,
-             timer=None):
+             timer=None, single_pass: bool | None = None):
     """RSA backward on stacked chunks; returns (dq, dk, dv) as [N][B][Z][c][A] bf16.
 
-    ``grads`` / ``ds`` / ``dvec`` optionally supply preallocated output,
-    dS-panel and D buffers (the bench reuses them across layers)."""
+    ``grads`` / ``dvec`` optionally supply preallocated output and D buffers
+    (the bench reuses them across layers).  On the fused path,
+    ``single_pass`` picks rsa_bwd_fused (one panel read; default when the
+    geometry allows) or the rsa_bwd_dkdv + rsa_bwd_dq pair."""
     n, b, z, c, a = q.shape
     seq = n * c
     dev = q.device
@@ -236,6 +244,14 @@ def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path:
         L = lib()
         st = _stream(q)
         g = _geom(n, b, z, c, a, seq, 0, n)
+        if single_pass is None:
+            single_pass = bool(L.rsa_bwd_fused_supported(ctypes.byref(g)))
+        if single_pass:
+            with tm("bwd_fused"):
+                check(L.rsa_bwd_fused(ctypes.byref(g), _view(q), _view(k), _view(v), _view(grad), _view(panel),
+                                      dvec.data_ptr(), NULL_VIEW, 0, _view(dq), _view(dk), _view(dv), BF16, 0, st),
+                      "rsa_bwd_fused")
+            return dq, dk, dv
         with tm("bwd_dkdv"):
             check(L.rsa_bwd_dkdv(ctypes.byref(g), _view(q), _view(v), _view(grad), _view(panel), dvec.data_ptr(),
                                  _view(dk), _view(dv), BF16, 0, st), "rsa_bwd_dkdv")

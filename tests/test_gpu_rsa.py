@@ -259,3 +259,52 @@ def test_layer_wrapper_matches_multi_head_oracle(rsa):
     rel = np.linalg.norm(got - want) / np.linalg.norm(want)
     assert rel <= 2e-2, rel
     assert all(t.ring_p2p_elements == 2 * (n - 1) * b * z * (seq // n) * a for t in ledger.devices)
+
+
+# Single-pass backward (rsa_bwd_fused) vs the split rsa_bwd_dkdv + rsa_bwd_dq
+# pair, both against the oracle: every geometry with <= 4 query tiles per head
+# (resident N ranks x ceil(c/128)), including ragged tails and the bench shape.
+SINGLE_PASS_SHAPES = [
+    (2, 2, 512, 64, 1),   # bench geometry: 4 row tiles of one rank
+    (2, 3, 512, 64, 4),   # c = 128: 4 ranks x 1 tile
+    (1, 2, 400, 64, 2),   # c = 200: ragged second tile
+    (2, 1, 96, 64, 4),    # c = 24: mostly padding
+    (1, 3, 384, 64, 1),   # 3 tiles
+    (3, 2, 128, 64, 1),   # one tile, several heads per CTA walk
+]
+
+
+@pytest.mark.parametrize("shape", SINGLE_PASS_SHAPES)
+@pytest.mark.parametrize("single_pass", [True, False])
+def test_backward_kernels_match_oracle(rsa, shape, single_pass):
+    from paper_2105_13120_b200 import engine
+
+    b, z, seq, a, n = shape
+    c = seq // n
+    assert engine.single_pass_supported(n, b, z, c, a)
+    q, k, v, g = _inputs(b, z, seq, a, seed=31 + sum(shape))
+    dev = torch.device("cuda", 0)
+    stack = lambda x: torch.from_numpy(np.stack(orc.chunks_of(x, n))).to(dev, torch.bfloat16)  # noqa: E731
+    tq, tk, tv, tg = (stack(x) for x in (q, k, v, g))
+    out, panel, _ = engine.forward(tq, tk, tv, path="fused")
+    dq, dk, dv = engine.backward(tq, tk, tv, panel, tg, outputs=out, path="fused", single_pass=single_pass)
+    torch.cuda.synchronize()
+    _, _, wdq, wdk, wdv = _oracle(q, k, v, g, n)
+    cat = lambda t: np.concatenate([_np(t[d]) for d in range(n)], axis=-2)  # noqa: E731
+    _gate("dq", cat(dq), wdq)
+    _gate("dk", cat(dk), wdk)
+    _gate("dv", cat(dv), wdv)
+
+
+def test_single_pass_backward_is_deterministic(rsa):
+    from paper_2105_13120_b200 import engine
+
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev).manual_seed(4)
+    tq, tk, tv, tg = (torch.randn((1, 4, 3, 512, 64), generator=gen, device=dev).to(torch.bfloat16) for _ in range(4))
+    out, panel, _ = engine.forward(tq, tk, tv, path="fused")
+    r1 = engine.backward(tq, tk, tv, panel, tg, outputs=out, path="fused", single_pass=True)
+    r2 = engine.backward(tq, tk, tv, panel, tg, outputs=out, path="fused", single_pass=True)
+    torch.cuda.synchronize()
+    for x, y in zip(r1, r2):
+        assert torch.equal(x, y)
