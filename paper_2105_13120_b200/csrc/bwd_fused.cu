@@ -138,7 +138,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    // The whole warp runs this loop (warp-uniform state); elect.sync inside
+    // umma_bf16_ws / umma_commit_ws picks the issuing lane.
+    {
       const uint32_t idesc_dp = idesc_bf16_f32(TR, TK, 0, 0);  // dO (K-major) x V (K-major)     -> 128 x 128
       const uint32_t idesc_kv = idesc_bf16_f32(TK, HD, 1, 1);  // P^T / dS^T (MN) x dO / Q (MN) -> 128 x 64
       const uint32_t idesc_dq = idesc_bf16_f32(TR, HD, 0, 1);  // dS (K-major) x K (MN-major)   -> 128 x 64
@@ -153,17 +155,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
           mbar_wait(&rdo.full[ds], do_a.phase(BF_DO));
           mbar_wait(dp_empty, dpq.phase(1) ^ 1);
           tc_fence_after();
-          const uint32_t doa = smem_u32(smem + BF_OFF_DO + ds * TILE);
-          const uint32_t va = smem_u32(smem + BF_OFF_V + vs * TILE);
+          const uint64_t da = smem_desc_sw128(smem_u32(smem + BF_OFF_DO + ds * TILE), 0, 1024);
+          const uint64_t db = smem_desc_sw128(smem_u32(smem + BF_OFF_V + vs * TILE), 0, 1024);
 #pragma unroll
-          for (int k = 0; k < HD / 16; ++k)
-            umma_bf16(tmem + COL_DP, smem_desc_sw128(doa + k * 32, 0, 1024), smem_desc_sw128(va + k * 32, 0, 1024),
-                      idesc_dp, k > 0);
+          for (int k = 0; k < HD / 16; ++k)  // K-major: +32 B per 16-wide k step
+            umma_bf16_ws(tmem + COL_DP, da + 2 * k, db + 2 * k, idesc_dp, k > 0);
           if (qt == NQ - 1) {
-            umma_commit(&rv.empty[vs]);
+            umma_commit_ws(&rv.empty[vs]);
             ++v_a.i;
           }
-          umma_commit(dp_full);
+          umma_commit_ws(dp_full);
           ++dpq.i;
         };
         // dV += P^T dO; p_read certifies P has been consumed, so dS may overwrite it
@@ -173,14 +174,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
           if (qt == 0) mbar_wait(acc_empty, accq.phase(1) ^ 1);
           mbar_wait(&rp.full[ps], p_a.phase(BF_P));
           tc_fence_after();
-          const uint32_t doa = smem_u32(smem + BF_OFF_DO + ds * TILE);
-          const uint32_t pa = smem_u32(smem + BF_OFF_P + ps * PTILE);
+          const uint64_t da = smem_desc_sw128(smem_u32(smem + BF_OFF_P + ps * PTILE), ATOM, 1024);
+          const uint64_t db = smem_desc_sw128(smem_u32(smem + BF_OFF_DO + ds * TILE), ATOM, 1024);
 #pragma unroll
-          for (int k = 0; k < TR / 16; ++k)
-            umma_bf16(tmem + COL_DV, smem_desc_sw128(pa + k * 2048, ATOM, 1024),
-                      smem_desc_sw128(doa + k * 2048, ATOM, 1024), idesc_kv, (qt | k) != 0);
-          umma_commit(&rdo.empty[ds]);
-          umma_commit(&p_read[ps]);
+          for (int k = 0; k < TR / 16; ++k)  // MN-major: +16 rows (2048 B) per k step
+            umma_bf16_ws(tmem + COL_DV, da + 128 * k, db + 128 * k, idesc_kv, (qt | k) != 0);
+          umma_commit_ws(&rdo.empty[ds]);
+          umma_commit_ws(&p_read[ps]);
           ++do_a.i, ++p_a.i;
           if (qt == NQ - 1) ++accq.i;
         };
@@ -192,29 +192,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
           mbar_wait(&rq.full[qs], q_b.phase(BF_Q));
           mbar_wait(&ds_full[ps], p_b.phase(BF_P));
           tc_fence_after();
-          const uint32_t qa = smem_u32(smem + BF_OFF_Q + qs * TILE);
           const uint32_t dsa = smem_u32(smem + BF_OFF_P + ps * PTILE);
-          const uint32_t ka = smem_u32(smem + BF_OFF_K + ks * TILE);
+          const uint64_t dmn = smem_desc_sw128(dsa, ATOM, 1024);  // dS^T: MN-major A
+          const uint64_t dkm = smem_desc_sw128(dsa, 0, 1024);     // dS: K-major A
+          const uint64_t qd = smem_desc_sw128(smem_u32(smem + BF_OFF_Q + qs * TILE), ATOM, 1024);
+          const uint64_t kd = smem_desc_sw128(smem_u32(smem + BF_OFF_K + ks * TILE), ATOM, 1024);
 #pragma unroll
           for (int k = 0; k < TR / 16; ++k)
-            umma_bf16(tmem + COL_DK, smem_desc_sw128(dsa + k * 2048, ATOM, 1024),
-                      smem_desc_sw128(qa + k * 2048, ATOM, 1024), idesc_kv, (qt | k) != 0);
+            umma_bf16_ws(tmem + COL_DK, dmn + 128 * k, qd + 128 * k, idesc_kv, (qt | k) != 0);
           if (kk == 0) {
             mbar_wait(&dq_empty[qt], (head_it & 1) ^ 1);
             tc_fence_after();
           }
 #pragma unroll
-          for (int k = 0; k < TK / 16; ++k)
-            umma_bf16(tmem + COL_DQ + qt * HD, smem_desc_sw128(dsa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
-                      smem_desc_sw128(ka + k * 2048, ATOM, 1024), idesc_dq, (kk | k) != 0);
-          umma_commit(&rp.empty[ps]);
-          umma_commit(&rq.empty[qs]);
+          for (int k = 0; k < TK / 16; ++k)  // dS K-major over keys: 64-key atoms ATOM apart, +32 B per k
+            umma_bf16_ws(tmem + COL_DQ + qt * HD, dkm + (k >> 2) * (ATOM >> 4) + 2 * (k & 3), kd + 128 * k, idesc_dq,
+                         (kk | k) != 0);
+          umma_commit_ws(&rp.empty[ps]);
+          umma_commit_ws(&rq.empty[qs]);
           if (qt == NQ - 1) {
-            umma_commit(acc_full);
-            umma_commit(&rk.empty[ks]);
+            umma_commit_ws(acc_full);
+            umma_commit_ws(&rk.empty[ks]);
             ++k_b.i;
           }
-          if (kk == NK - 1) umma_commit(&dq_full[qt]);
+          if (kk == NK - 1) umma_commit_ws(&dq_full[qt]);
           ++q_b.i, ++p_b.i;
         };
         issue_dp(0);

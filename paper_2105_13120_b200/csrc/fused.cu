@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fwd_kernel(const __grid_constant_
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp; elect.sync inside the _ws issue helpers
       const uint32_t idesc_s = idesc_bf16_f32(TR, TK, 0, 0);
       const uint32_t idesc_o = idesc_bf16_f32(TR, HD, 0, 1);
       Pos kq, vq, sq, pq;
@@ -143,10 +143,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fwd_kernel(const __grid_constant_
           const uint32_t ka = smem_u32(smem + F_OFF_K + ks * TILE);
 #pragma unroll
           for (int k = 0; k < HD / 16; ++k)
-            umma_bf16(tmem + sb * TK, smem_desc_sw128(qa + k * 32, 0, 1024), smem_desc_sw128(ka + k * 32, 0, 1024),
+            umma_bf16_ws(tmem + sb * TK, smem_desc_sw128(qa + k * 32, 0, 1024), smem_desc_sw128(ka + k * 32, 0, 1024),
                       idesc_s, k > 0);
-          umma_commit(&k_empty[ks]);
-          umma_commit(&s_full[sb]);
+          umma_commit_ws(&k_empty[ks]);
+          umma_commit_ws(&s_full[sb]);
           ++kq.i, ++sq.i;
         };
         if (pass_a)
@@ -165,15 +165,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) fwd_kernel(const __grid_constant_
             const uint32_t va = smem_u32(smem + F_OFF_V + vs * TILE);
 #pragma unroll
             for (int k = 0; k < TK / 16; ++k)
-              umma_bf16(tmem + 2 * TK + ob * HD, smem_desc_sw128(pa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
+              umma_bf16_ws(tmem + 2 * TK + ob * HD, smem_desc_sw128(pa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
                         smem_desc_sw128(va + k * 2048, ATOM, 1024), idesc_o, (t | k) != 0);
-            umma_commit(&v_empty[vs]);
-            umma_commit(&p_empty[pb]);
+            umma_commit_ws(&v_empty[vs]);
+            umma_commit_ws(&p_empty[pb]);
             ++pq.i, ++vq.i;
           }
-          umma_commit(&o_full[ob]);
+          umma_commit_ws(&o_full[ob]);
         }
-        umma_commit(&q_empty[qb]);
+        umma_commit_ws(&q_empty[qb]);
       }
     }
   } else {
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dkdv_kernel(const __grid_cons
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp; elect.sync inside the _ws issue helpers
       const uint32_t idesc_dp = idesc_bf16_f32(TR, TK, 0, 0);  // dO (K-major) x V (K-major)
       const uint32_t idesc_kv = idesc_bf16_f32(TK, HD, 1, 1);  // P^T / dS^T (MN-major) x dO / Q (MN-major)
       const uint32_t va = smem_u32(smem + BK_OFF_V);
@@ -442,16 +442,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dkdv_kernel(const __grid_cons
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < HD / 16; ++k)
-            umma_bf16(tmem + db * TK, smem_desc_sw128(doa + k * 32, 0, 1024), smem_desc_sw128(va + k * 32, 0, 1024),
+            umma_bf16_ws(tmem + db * TK, smem_desc_sw128(doa + k * 32, 0, 1024), smem_desc_sw128(va + k * 32, 0, 1024),
                       idesc_dp, k > 0);
-          if (t == T - 1) umma_commit(v_empty);  // last read of V for this item
+          if (t == T - 1) umma_commit_ws(v_empty);  // last read of V for this item
 #pragma unroll
           for (int k = 0; k < TR / 16; ++k)
-            umma_bf16(tmem + dv_col, smem_desc_sw128(pa + k * 2048, ATOM, 1024),
+            umma_bf16_ws(tmem + dv_col, smem_desc_sw128(pa + k * 2048, ATOM, 1024),
                       smem_desc_sw128(doa + k * 2048, ATOM, 1024), idesc_kv, (t | k) != 0);
           // dp_full also certifies that P^T dO has finished reading P, so the
           // epilogue may overwrite P with dS in place.
-          umma_commit(&dp_full[db]);
+          umma_commit_ws(&dp_full[db]);
           ++lq_a.i, ++dq_a.i;
         };
         if (T > 0) issue_dp(0);
@@ -464,12 +464,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dkdv_kernel(const __grid_cons
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < TR / 16; ++k)
-            umma_bf16(tmem + dk_col, smem_desc_sw128(dsa + k * 2048, ATOM, 1024),
+            umma_bf16_ws(tmem + dk_col, smem_desc_sw128(dsa + k * 2048, ATOM, 1024),
                       smem_desc_sw128(qa + k * 2048, ATOM, 1024), idesc_kv, (t | k) != 0);
-          umma_commit(&ld_empty[s]);
+          umma_commit_ws(&ld_empty[s]);
           ++lq_b.i, ++dq_b.i;
         }
-        umma_commit(&acc_full[ab]);
+        umma_commit_ws(&acc_full[ab]);
       }
     }
   } else {
@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dq_kernel(const __grid_consta
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp; elect.sync inside the _ws issue helpers
       const uint32_t idesc_dp = idesc_bf16_f32(TR, TK, 0, 0);  // dO x V^T
       const uint32_t idesc_dq = idesc_bf16_f32(TR, HD, 0, 1);  // dS (K-major over keys) x K (MN-major)
       Pos lq_a, dq_a, lq_b, dq_b;  // "a": dP issue (one tile ahead), "b": dQ issue
@@ -641,10 +641,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dq_kernel(const __grid_consta
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < HD / 16; ++k)
-            umma_bf16(tmem + db * TK, smem_desc_sw128(doa + k * 32, 0, 1024), smem_desc_sw128(va + k * 32, 0, 1024),
+            umma_bf16_ws(tmem + db * TK, smem_desc_sw128(doa + k * 32, 0, 1024), smem_desc_sw128(va + k * 32, 0, 1024),
                       idesc_dp, k > 0);
-          umma_commit(&dp_full[db]);
-          if (t == T - 1) umma_commit(&do_empty[ob]);
+          umma_commit_ws(&dp_full[db]);
+          if (t == T - 1) umma_commit_ws(&do_empty[ob]);
           ++lq_a.i, ++dq_a.i;
         };
         if (T > 0) issue_dp(0);
@@ -657,12 +657,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dq_kernel(const __grid_consta
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < TK / 16; ++k)
-            umma_bf16(tmem + ACC_COL + ob * HD, smem_desc_sw128(dsa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
+            umma_bf16_ws(tmem + ACC_COL + ob * HD, smem_desc_sw128(dsa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
                       smem_desc_sw128(ka + k * 2048, ATOM, 1024), idesc_dq, (t | k) != 0);
-          umma_commit(&ld_empty[s]);
+          umma_commit_ws(&ld_empty[s]);
           ++lq_b.i, ++dq_b.i;
         }
-        umma_commit(&acc_full[ob]);
+        umma_commit_ws(&acc_full[ob]);
       }
     }
   } else {
