@@ -201,12 +201,15 @@ def kernel_model(name, n, b, z, c, seq, a):
     """Algorithmic (bytes, flops) per launch of one fused kernel at one layer."""
     pe = n * b * z * c * seq  # panel elements in the launch
     ce = n * b * z * c * a    # chunk elements
+    rows = n * b * z * c      # query rows
     if name == "fwd_stats":
         return 2 * 2 * ce, 2 * pe * a                 # read Q, K; S = QK^T
     if name == "fwd_probs_pv":
         return 2 * pe + 2 * 4 * ce, 4 * pe * a        # write P; read Q,K,V, write O
     if name == "fwd_resident":
         return 2 * pe + 2 * 4 * ce, 6 * pe * a        # write P; Q,K,V in, O out; QK^T twice + PV
+    if name == "fwd_factored":
+        return 2 * pe + 2 * 4 * ce + 4 * rows, 4 * pe * a  # write P~ and r; Q,K,V in, O out; QK^T, PV (algorithmic)
     if name == "bwd_dkdv":
         return 2 * pe + 2 * 5 * ce, 6 * pe * a        # read P; dO,Q,V in, dK,dV out; dO V^T, P^T dO, dS^T Q
     if name == "bwd_fused":
@@ -214,7 +217,7 @@ def kernel_model(name, n, b, z, c, seq, a):
     if name == "bwd_dq":
         return 2 * pe + 2 * 4 * ce, 4 * pe * a        # read P; dO,K,V in, dQ out; dO V^T, dS K
     if name == "rowdot":
-        return 2 * 2 * ce + 4 * n * b * z * c, 2 * ce
+        return 2 * 3 * ce + 8 * rows, 3 * ce            # read dO, O, r; write D*r, dO*r
     return 0, 0
 
 
@@ -243,17 +246,20 @@ def ours(args):
     for ly in layers:
         ly["o"] = torch.empty_like(ly["q"])
         ly["p"] = torch.empty((1, B, Z, c, L), dtype=torch.bfloat16, device=dev)
+        ly["r"] = torch.empty((1, B, Z, c), dtype=torch.float32, device=dev)
         ly["grads"] = (torch.empty_like(ly["q"]), torch.empty_like(ly["q"]), torch.empty_like(ly["q"]))
     dvec = torch.empty((1, B, Z, c), dtype=torch.float32, device=dev)
+    g_scaled = torch.empty((1, B, Z, c, A), dtype=torch.bfloat16, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     timer = engine.KernelTimer()
 
     def step(tm=None):
         for ly in layers:
-            engine.forward(ly["q"], ly["k"], ly["v"], path="fused", flag=flag, out=ly["o"], panel=ly["p"], timer=tm)
+            engine.forward(ly["q"], ly["k"], ly["v"], path="fused", flag=flag, out=ly["o"], panel=ly["p"],
+                           rowscale=ly["r"], timer=tm)
         for ly in reversed(layers):
             engine.backward(ly["q"], ly["k"], ly["v"], ly["p"], ly["g"], outputs=ly["o"], path="fused",
-                            grads=ly["grads"], dvec=dvec, timer=tm)
+                            grads=ly["grads"], dvec=dvec, rowscale=ly["r"], grad_scaled=g_scaled, timer=tm)
 
     for _ in range(args.warmup):
         step()

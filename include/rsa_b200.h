@@ -107,6 +107,25 @@ int rsa_softmax_bwd(const void* p, int p_dtype, int64_t ld_p, const float* dp, i
 int rsa_rowdot(const void* a, int64_t lda, const void* b, int64_t ldb, int64_t rows, int64_t cols, float* out,
                void* stream);
 
+/*
+ * Backward prologue for a factored panel (see rsa_fwd_factored):
+ * out[r] = scale[r] * sum_c a[r,c] * b[r,c] and a_scaled[r,:] = bf16(scale[r] * a[r,:]).
+ * With a = dO, b = O and scale = the panel's row scale this gives D*r and
+ * dO*r, which let rsa_bwd_fused / rsa_bwd_dkdv / rsa_bwd_dq consume the
+ * factored panel P~ unchanged: P (dP - D) = P~ (dO*r V^T - D*r) and
+ * P^T dO = P~^T (dO*r)  (ringseq/ring_attention.py:180-205).
+ */
+int rsa_rowdot_scale(const void* a, int64_t lda, const void* b, int64_t ldb, const float* scale, int64_t rows,
+                     int64_t cols, float* out, void* a_scaled, int64_t ld_as, void* stream);
+
+/*
+ * Materialise probabilities from a factored panel: y[r,c] = scale[r] * p[r,c]
+ * (p bf16; y fp32 or bf16 per y_dtype).  The reference's probs
+ * (ringseq/ring_attention.py:89-94) on demand; not on the fwd/bwd path.
+ */
+int rsa_panel_normalize(const void* p, int64_t ld_p, const float* scale, int64_t rows, int64_t cols, void* y,
+                        int y_dtype, int64_t ld_y, void* stream);
+
 /* --------------------------------------------------- fused RSA kernels */
 
 /*
@@ -139,6 +158,19 @@ int rsa_fwd_probs_pv(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, cons
  */
 int rsa_fwd_resident(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view panel, rsa_view o_out,
                      int* nonfinite_flag, void* stream);
+
+/*
+ * Single-launch forward with a FACTORED probability panel, every origin
+ * resident (org_lo = 0, n_org = L / c): panel = bf16(P~), P~ = 2^(s*sl - m)
+ * with m the row max, and rowscale[row] = 1 / sum_k P~[row, k] (fp32,
+ * [rank][b][z][c]), so the reference's probs are P = rowscale * P~
+ * (ringseq/ring_attention.py:89-94) and o_out = P V (:97-103).  One exp2 per
+ * panel element (rsa_fwd_resident spends two); the row sum is accumulated by
+ * the tensor core from a block of ones next to V.  Backward consumers take
+ * the factored panel through rsa_rowdot_scale.
+ */
+int rsa_fwd_factored(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view panel, rsa_view o_out,
+                     float* rowscale, int* nonfinite_flag, void* stream);
 
 /*
  * V-ring half of the RSA backward (ringseq/ring_attention.py:180-205) for

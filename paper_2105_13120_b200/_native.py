@@ -82,9 +82,15 @@ EXPORTS = {
         [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int64, c_int64, c_float, c_void_p, c_int, c_int64, c_void_p],
     ),
     "rsa_rowdot": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p]),
+    "rsa_rowdot_scale": (
+        c_int,
+        [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_int64, c_void_p],
+    ),
+    "rsa_panel_normalize": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_int, c_int64, c_void_p]),
     "rsa_fwd_stats": (c_int, [_GEOM, _V, _V, c_void_p, c_int, c_void_p, c_void_p]),
     "rsa_fwd_probs_pv": (c_int, [_GEOM, _V, _V, _V, c_void_p, c_int, _V, _V, c_int, _V, c_void_p]),
     "rsa_fwd_resident": (c_int, [_GEOM, _V, _V, _V, _V, _V, c_void_p, c_void_p]),
+    "rsa_fwd_factored": (c_int, [_GEOM, _V, _V, _V, _V, _V, c_void_p, c_void_p, c_void_p]),
     "rsa_bwd_dkdv": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, _V, _V, c_int, c_int, c_void_p]),
     "rsa_bwd_dq": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, _V, c_int, _V, c_void_p]),
     "rsa_fused_supported": (c_int, [_GEOM]),

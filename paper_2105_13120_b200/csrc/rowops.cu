@@ -211,6 +211,74 @@ __global__ void __launch_bounds__(256) rowdot64_kernel(const __nv_bfloat16* __re
   if (row < rows && sub == 0) out[row] = acc;
 }
 
+
+// rowdot with a per-row scale, and the scaled copy of `a` (bf16): cols == 64,
+// 16-byte aligned rows, 8 lanes per row (one 16-byte load of a and of b, one
+// 16-byte store of a * scale per lane).
+__global__ void __launch_bounds__(256) rowdot64_scale_kernel(const __nv_bfloat16* __restrict__ a, int64_t lda,
+                                                             const __nv_bfloat16* __restrict__ b, int64_t ldb,
+                                                             const float* __restrict__ scale, int64_t rows,
+                                                             float* __restrict__ out, __nv_bfloat16* __restrict__ as,
+                                                             int64_t ldas) {
+  const int64_t row = int64_t(blockIdx.x) * 32 + (threadIdx.x >> 3);
+  const int sub = threadIdx.x & 7;
+  float acc = 0.f, sc = 0.f;
+  if (row < rows) {
+    sc = __ldg(scale + row);
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(a + row * lda) + sub);
+    const uint4 y = __ldg(reinterpret_cast<const uint4*>(b + row * ldb) + sub);
+    const uint32_t* xs = reinterpret_cast<const uint32_t*>(&x);
+    const uint32_t* ys = reinterpret_cast<const uint32_t*>(&y);
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 fx = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[i]));
+      const float2 fy = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ys[i]));
+      acc = fmaf(fx.x, fy.x, acc);
+      acc = fmaf(fx.y, fy.y, acc);
+      w[i] = pack_bf16(fx.x * sc, fx.y * sc);
+    }
+    *(reinterpret_cast<uint4*>(as + row * ldas) + sub) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+  if (row < rows && sub == 0) out[row] = acc * sc;
+}
+
+// Generic shape: one warp per row.
+__global__ void __launch_bounds__(256) rowdot_scale_kernel(const __nv_bfloat16* __restrict__ a, int64_t lda,
+                                                           const __nv_bfloat16* __restrict__ b, int64_t ldb,
+                                                           const float* __restrict__ scale, int64_t rows, int64_t cols,
+                                                           float* __restrict__ out, __nv_bfloat16* __restrict__ as,
+                                                           int64_t ldas) {
+  const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float sc = scale[row];
+  float acc = 0.f;
+  for (int64_t c = lane; c < cols; c += 32) {
+    const float x = __bfloat162float(a[row * lda + c]);
+    acc += x * __bfloat162float(b[row * ldb + c]);
+    as[row * ldas + c] = __float2bfloat16_rn(x * sc);
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) out[row] = acc * sc;
+}
+
+// y[r, c] = scale[r] * p[r, c]; one warp per row.
+template <typename TO>
+__global__ void __launch_bounds__(256) panel_normalize_kernel(const __nv_bfloat16* __restrict__ p, int64_t ldp,
+                                                              const float* __restrict__ scale, int64_t rows,
+                                                              int64_t cols, TO* __restrict__ y, int64_t ldy) {
+  const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float sc = scale[row];
+  for (int64_t c = lane; c < cols; c += 32) y[row * ldy + c] = TO(__bfloat162float(p[row * ldp + c]) * sc);
+}
+
 template <typename T>
 bool vec_ok(const void* ptr, int64_t ld, int64_t cols) {
   const int64_t esz = sizeof(T);
@@ -292,6 +360,42 @@ int rsa_rowdot(const void* a, int64_t lda, const void* b, int64_t ldb, int64_t r
   rowdot_kernel<<<(rows + 7) / 8, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16*>(a), lda, static_cast<const __nv_bfloat16*>(b), ldb, rows, cols, out);
   return check_launch("rowdot_kernel");
+}
+
+int rsa_rowdot_scale(const void* a, int64_t lda, const void* b, int64_t ldb, const float* scale, int64_t rows,
+                     int64_t cols, float* out, void* a_scaled, int64_t ld_as, void* stream) {
+  using namespace rsa;
+  if (rows < 0 || cols < 0 || !scale || !out || !a_scaled) return fail(RSA_ERR_INVALID, "rowdot_scale: bad arguments");
+  if (rows == 0) return RSA_OK;
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  const auto* pa = static_cast<const __nv_bfloat16*>(a);
+  const auto* pb = static_cast<const __nv_bfloat16*>(b);
+  auto* ps = static_cast<__nv_bfloat16*>(a_scaled);
+  if (cols == 64 && aligned16(a) && aligned16(b) && aligned16(a_scaled) && lda % 8 == 0 && ldb % 8 == 0 &&
+      ld_as % 8 == 0) {
+    rowdot64_scale_kernel<<<(rows + 31) / 32, 256, 0, st>>>(pa, lda, pb, ldb, scale, rows, out, ps, ld_as);
+    return check_launch("rowdot64_scale_kernel");
+  }
+  rowdot_scale_kernel<<<(rows + 7) / 8, 256, 0, st>>>(pa, lda, pb, ldb, scale, rows, cols, out, ps, ld_as);
+  return check_launch("rowdot_scale_kernel");
+}
+
+int rsa_panel_normalize(const void* p, int64_t ld_p, const float* scale, int64_t rows, int64_t cols, void* y,
+                        int y_dtype, int64_t ld_y, void* stream) {
+  using namespace rsa;
+  if (rows < 0 || cols < 0 || !scale) return fail(RSA_ERR_INVALID, "panel_normalize: bad arguments");
+  if (rows == 0) return RSA_OK;
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  const auto* pp = static_cast<const __nv_bfloat16*>(p);
+  const dim3 grid((rows + 7) / 8);
+  if (y_dtype == RSA_F32)
+    panel_normalize_kernel<float><<<grid, 256, 0, st>>>(pp, ld_p, scale, rows, cols, static_cast<float*>(y), ld_y);
+  else if (y_dtype == RSA_BF16)
+    panel_normalize_kernel<__nv_bfloat16>
+        <<<grid, 256, 0, st>>>(pp, ld_p, scale, rows, cols, static_cast<__nv_bfloat16*>(y), ld_y);
+  else
+    return fail(RSA_ERR_INVALID, "panel_normalize: bad output dtype");
+  return check_launch("panel_normalize_kernel");
 }
 
 }  // extern "C"

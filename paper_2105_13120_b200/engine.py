@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+from typing import NamedTuple
 
 import torch
 
@@ -34,7 +35,7 @@ from . import tensor_ops as ops
 from ._native import BF16, F32, RsaGeom, RsaView, check, lib
 from .errors import ShapeError
 
-__all__ = ["fused_supported", "forward", "backward", "recompute_outputs", "NULL_VIEW", "KernelTimer"]
+__all__ = ["fused_supported", "forward", "backward", "Forward", "normalized_panel", "recompute_outputs", "NULL_VIEW", "KernelTimer"]
 
 NULL_VIEW = RsaView(None, 0, 0, 0, 0)
 
@@ -129,14 +130,34 @@ def _pick(path: str, n, b, z, c, a) -> str:
 
 # ----------------------------------------------------------------- forward
 
+class Forward(NamedTuple):
+    """Result of ``forward``: outputs and the saved probability panel.
+
+    ``rowscale`` is None for a normalised panel (panel = P).  For a factored
+    panel (rsa_fwd_factored) it is the fp32 [N][B][Z][c] row scale r with
+    P = r * panel; ``backward`` and ``ring_attention.ProbPanels`` take either.
+    """
+
+    out: torch.Tensor
+    panel: torch.Tensor
+    rowscale: torch.Tensor | None
+    flag: torch.Tensor
+
+
 def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, path: str = "auto",
             flag: torch.Tensor | None = None, out: torch.Tensor | None = None,
-            panel: torch.Tensor | None = None, stats: torch.Tensor | None = None, timer=None):
+            panel: torch.Tensor | None = None, stats: torch.Tensor | None = None,
+            rowscale: torch.Tensor | None = None, factored: bool = True, timer=None) -> Forward:
     """RSA forward on stacked [N][B][Z][c][A] bf16 chunks.
 
-    Returns (outputs [N][B][Z][c][A] bf16, panels [N][B][Z][c][L] bf16,
-    nonfinite flag tensor).  The flag is a device int set by the kernels when
-    a score is non-finite; callers decide when to read it.
+    Returns ``Forward(out, panel, rowscale, flag)``: outputs [N][B][Z][c][A]
+    bf16, the panel [N][B][Z][c][L] bf16 (factored when ``rowscale`` is not
+    None), and the non-finite flag, a device int set by the kernels when a
+    score is non-finite (callers decide when to read it).
+
+    Fused path: ``factored`` (default) runs rsa_fwd_factored (one exp2 per
+    panel element); ``factored=False`` the normalised rsa_fwd_resident, and a
+    ``stats`` buffer the two-launch K-ring / V-ring form.
     """
     n, b, z, c, a = q.shape
     seq = n * c
@@ -160,13 +181,27 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, path: str = "a
             with tm("fwd_probs_pv"):
                 check(L.rsa_fwd_probs_pv(ctypes.byref(g), _view(q), _view(k), _view(v), stats.data_ptr(), 1,
                                          _view(panel), NULL_VIEW, 0, _view(out), st), "rsa_fwd_probs_pv")
-            return out, panel, flag
+            return Forward(out, panel, None, flag)
+        if factored:
+            if rowscale is None:
+                rowscale = torch.empty((n, b, z, c), dtype=torch.float32, device=dev)
+            with tm("fwd_factored"):
+                check(L.rsa_fwd_factored(ctypes.byref(g), _view(q), _view(k), _view(v), _view(panel), _view(out),
+                                         rowscale.data_ptr(), flag.data_ptr(), st), "rsa_fwd_factored")
+            return Forward(out, panel, rowscale, flag)
         with tm("fwd_resident"):
             check(L.rsa_fwd_resident(ctypes.byref(g), _view(q), _view(k), _view(v), _view(panel), _view(out),
                                      flag.data_ptr(), st), "rsa_fwd_resident")
-        return out, panel, flag
+        return Forward(out, panel, None, flag)
     _forward_staged(q, k, v, out, panel, flag)
-    return out, panel, flag
+    return Forward(out, panel, None, flag)
+
+
+def normalized_panel(panel: torch.Tensor, rowscale: torch.Tensor | None, dtype=torch.float32) -> torch.Tensor:
+    """The reference's probs from a saved panel: rowscale * panel (or the panel itself when normalised)."""
+    if rowscale is None:
+        return panel if panel.dtype == dtype else panel.to(dtype)
+    return ops.panel_normalize(panel, rowscale, out_dtype=dtype)
 
 
 def _softmax_into(x: torch.Tensor, y: torch.Tensor, scale: float, flag: torch.Tensor) -> None:
@@ -215,14 +250,19 @@ def single_pass_supported(n: int, b: int, z: int, c: int, a: int) -> bool:
 
 
 def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path: str = "auto",
-             grads: tuple | None = None, dvec: torch.Tensor | None = None,
-             timer=None, single_pass: bool | None = None):
+             grads: tuple | None = None, dvec: torch.Tensor | None = None, rowscale: torch.Tensor | None = None,
+             grad_scaled: torch.Tensor | None = None, timer=None, single_pass: bool | None = None):
     """RSA backward on stacked chunks; returns (dq, dk, dv) as [N][B][Z][c][A] bf16.
 
     ``grads`` / ``dvec`` optionally supply preallocated output and D buffers
     (the bench reuses them across layers).  On the fused path,
     ``single_pass`` picks rsa_bwd_fused (one panel read; default when the
-    geometry allows) or the rsa_bwd_dkdv + rsa_bwd_dq pair."""
+    geometry allows) or the rsa_bwd_dkdv + rsa_bwd_dq pair.
+
+    ``rowscale`` marks ``panel`` as factored (P = rowscale * panel, see
+    ``forward``): rsa_rowdot_scale then forms D*r and dO*r (``grad_scaled``
+    optionally preallocates the latter) and the same kernels consume the
+    factored panel unchanged."""
     n, b, z, c, a = q.shape
     seq = n * c
     dev = q.device
@@ -236,11 +276,15 @@ def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path:
     if which == "fused":
         tm = timer or _NO_TIMER
         if outputs is None:
-            outputs = recompute_outputs(panel, v)
+            outputs = recompute_outputs(normalized_panel(panel, rowscale, torch.bfloat16), v)
         if dvec is None:
             dvec = torch.empty((n, b, z, c), dtype=torch.float32, device=dev)
-        with tm("rowdot"):
-            ops.rowdot(grad, outputs, out=dvec)  # D = rowsum(dO * O) = rowsum(dP * P)
+        if rowscale is None:
+            with tm("rowdot"):
+                ops.rowdot(grad, outputs, out=dvec)  # D = rowsum(dO * O) = rowsum(dP * P)
+        else:  # factored panel: D*r and dO*r, so P (dP - D) = P~ (dO*r V^T - D*r) and P^T dO = P~^T (dO*r)
+            with tm("rowdot"):
+                dvec, grad = ops.rowdot_scale(grad, outputs, rowscale, out=dvec, a_scaled=grad_scaled)
         L = lib()
         st = _stream(q)
         g = _geom(n, b, z, c, a, seq, 0, n)
@@ -259,6 +303,8 @@ def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path:
             check(L.rsa_bwd_dq(ctypes.byref(g), _view(grad), _view(k), _view(v), _view(panel), dvec.data_ptr(),
                                NULL_VIEW, 0, _view(dq), st), "rsa_bwd_dq")
         return dq, dk, dv
+    if rowscale is not None:
+        panel = normalized_panel(panel, rowscale, torch.bfloat16)
     _backward_staged(q, k, v, panel, grad, dq, dk, dv)
     return dq, dk, dv
 

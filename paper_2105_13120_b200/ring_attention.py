@@ -66,19 +66,42 @@ class RingAttentionBackward:
 
 
 class ProbPanels(list):
-    """The ``probs`` list returned by the forward: per-rank panel views into one
-    stacked [N][B][Z][c][L] tensor, which also remembers the stacked outputs.
+    """The ``probs`` list returned by the forward: one (B, Z, c, L) panel per rank.
 
-    Passing it back to ``ring_attention_backward`` (as the reference's callers
-    do with ``fwd.probs``) lets the backward reuse the stacked panel without a
-    copy and form D = rowsum(dO * O) from the saved O instead of recomputing
-    P V.  Any other list of panels works too, at the cost of one staging copy.
+    Backed by one stacked [N][B][Z][c][L] bf16 panel plus, for the fused path,
+    an fp32 row scale r (``engine.Forward``): the saved state is the factored
+    panel P~ with P = r * P~.  Indexing or iterating materialises rank d's
+    probabilities on demand (``engine.normalized_panel``, fp32; a bf16 view
+    when the panel is already normalised) and caches them.  Passing the object
+    back to ``ring_attention_backward`` (as the reference's callers do with
+    ``fwd.probs``) hands the factored panel and the saved outputs straight to
+    the kernels -- nothing is materialised or copied.  Any other list of
+    panels works too, at the cost of one staging copy.
     """
 
-    def __init__(self, stacked: torch.Tensor, outputs: torch.Tensor):
-        super().__init__(stacked[d] for d in range(stacked.shape[0]))
+    def __init__(self, stacked: torch.Tensor, outputs: torch.Tensor, rowscale: torch.Tensor | None = None):
+        super().__init__([None] * stacked.shape[0])
         self.stacked = stacked
         self.outputs = outputs
+        self.rowscale = rowscale
+        self.panel_shape = tuple(stacked.shape[1:])
+
+    def _get(self, d: int):
+        item = list.__getitem__(self, d)
+        if item is None:
+            scale = None if self.rowscale is None else self.rowscale[d]
+            item = engine.normalized_panel(self.stacked[d], scale, torch.float32 if scale is not None else
+                                           self.stacked.dtype)
+            list.__setitem__(self, d, item)
+        return item
+
+    def __getitem__(self, i):
+        idx = range(len(self))[i]
+        return [self._get(d) for d in idx] if isinstance(i, slice) else self._get(idx)
+
+    def __iter__(self):
+        for d in range(len(self)):
+            yield self._get(d)
 
 
 def _shape_of(x) -> tuple:
@@ -90,6 +113,10 @@ def _check_chunks(name: str, chunks, cfg: AttentionConfig, expect: tuple) -> lis
     chunks = chunks if isinstance(chunks, list) else list(chunks)  # keep ProbPanels intact
     if len(chunks) != cfg.num_devices:
         raise ShapeError(f"{name}: got {len(chunks)} chunks for {cfg.num_devices} devices")
+    if isinstance(chunks, ProbPanels):  # shape check without materialising the panels
+        if chunks.panel_shape != expect:
+            raise ShapeError(f"{name}[0] has shape {chunks.panel_shape}, expected {expect}")
+        return chunks
     for i, c in enumerate(chunks):
         if _shape_of(c) != expect:
             raise ShapeError(f"{name}[{i}] has shape {_shape_of(c)}, expected {expect}")
@@ -157,12 +184,12 @@ def ring_attention_forward(q_chunks, k_chunks, v_chunks, cfg: AttentionConfig, *
     v_chunks = _check_chunks("v_chunks", v_chunks, cfg, shape)
     dev = _device_of(q_chunks, k_chunks, v_chunks)
     q, k, v = (_stack(x, dev) for x in (q_chunks, k_chunks, v_chunks))
-    out, panel, flag = engine.forward(q, k, v, path=path)
+    out, panel, rowscale, flag = engine.forward(q, k, v, path=path)
     if int(flag.item()):
         raise NumericError("softmax_rows requires finite inputs")
     return RingAttentionForward(
         outputs=[out[d] for d in range(cfg.num_devices)],
-        probs=ProbPanels(panel, out),
+        probs=ProbPanels(panel, out, rowscale),
         ledger=forward_ledger(cfg),
     )
 
@@ -186,10 +213,12 @@ def ring_attention_backward(q_chunks, k_chunks, v_chunks, probs, grad_chunks, cf
     dev = _device_of(q_chunks, k_chunks, v_chunks, grad_chunks, probs)
     q, k, v, g = (_stack(x, dev) for x in (q_chunks, k_chunks, v_chunks, grad_chunks))
     panel = _stack(probs, dev)
-    outputs = probs.outputs if isinstance(probs, ProbPanels) and panel is probs.stacked else None
+    own = isinstance(probs, ProbPanels) and panel is probs.stacked
+    outputs = probs.outputs if own else None
+    rowscale = probs.rowscale if own else None
     if outputs is not None and (outputs.shape != q.shape or outputs.device != dev):
         outputs = None
-    dq, dk, dv = engine.backward(q, k, v, panel, g, outputs=outputs, path=path)
+    dq, dk, dv = engine.backward(q, k, v, panel, g, outputs=outputs, rowscale=rowscale, path=path)
     n = cfg.num_devices
     return RingAttentionBackward(
         grad_q=[dq[d] for d in range(n)],
@@ -223,7 +252,7 @@ def sequence_parallel_attention(x_chunks, weights, cfg: AttentionConfig, *, exec
         return y.view(n, b, c, z, a).permute(0, 1, 3, 2, 4).contiguous()  # split_heads per rank
 
     q, k, v = project(wq), project(wk), project(wv)
-    out, _, flag = engine.forward(q, k, v, path=path)
+    out, _, _, flag = engine.forward(q, k, v, path=path)
     if int(flag.item()):
         raise NumericError("softmax_rows requires finite inputs")
     merged = out.permute(0, 1, 3, 2, 4).reshape(n, b, c, z * a)  # merge_heads per rank

@@ -28,6 +28,8 @@ __all__ = [
     "softmax_rows",
     "softmax_backward",
     "rowdot",
+    "rowdot_scale",
+    "panel_normalize",
     "split_heads",
     "merge_heads",
     "set_gemm_backend",
@@ -215,6 +217,38 @@ def rowdot(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) ->
     if out is None:
         out = torch.empty(a.shape[:-1], dtype=torch.float32, device=a.device)
     check(lib().rsa_rowdot(a.data_ptr(), cols, b.data_ptr(), cols, rows, cols, out.data_ptr(), _stream(a)), "rsa_rowdot")
+    return out
+
+
+def rowdot_scale(a: torch.Tensor, b: torch.Tensor, scale: torch.Tensor, out: torch.Tensor | None = None,
+                 a_scaled: torch.Tensor | None = None):
+    """(scale * rowsum(a * b), bf16(scale[..., None] * a)) for bf16 a, b and fp32 per-row scale."""
+    if a.shape != b.shape or a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
+        raise ShapeError("rowdot_scale needs two bf16 tensors of the same shape")
+    if scale.dtype != torch.float32 or scale.shape != a.shape[:-1]:
+        raise ShapeError(f"rowdot_scale: scale must be fp32 of shape {tuple(a.shape[:-1])}")
+    cols = a.shape[-1]
+    a, b, scale = a.contiguous(), b.contiguous(), scale.contiguous()
+    rows = a.numel() // max(cols, 1)
+    if out is None:
+        out = torch.empty(a.shape[:-1], dtype=torch.float32, device=a.device)
+    if a_scaled is None:
+        a_scaled = torch.empty_like(a)
+    check(lib().rsa_rowdot_scale(a.data_ptr(), cols, b.data_ptr(), cols, scale.data_ptr(), rows, cols, out.data_ptr(),
+                                 a_scaled.data_ptr(), cols, _stream(a)), "rsa_rowdot_scale")
+    return out, a_scaled
+
+
+def panel_normalize(panel: torch.Tensor, scale: torch.Tensor, out_dtype=torch.float32) -> torch.Tensor:
+    """Probabilities from a factored panel: scale[..., None] * panel (bf16 panel, fp32 row scale)."""
+    if panel.dtype != torch.bfloat16 or scale.dtype != torch.float32 or scale.shape != panel.shape[:-1]:
+        raise ShapeError("panel_normalize needs a bf16 panel and an fp32 scale per row")
+    cols = panel.shape[-1]
+    panel, scale = panel.contiguous(), scale.contiguous()
+    rows = panel.numel() // max(cols, 1)
+    out = torch.empty(panel.shape, dtype=out_dtype, device=panel.device)
+    check(lib().rsa_panel_normalize(panel.data_ptr(), cols, scale.data_ptr(), rows, cols, out.data_ptr(),
+                                    _DT[out_dtype], cols, _stream(panel)), "rsa_panel_normalize")
     return out
 
 

@@ -276,7 +276,8 @@ SINGLE_PASS_SHAPES = [
 
 @pytest.mark.parametrize("shape", SINGLE_PASS_SHAPES)
 @pytest.mark.parametrize("single_pass", [True, False])
-def test_backward_kernels_match_oracle(rsa, shape, single_pass):
+@pytest.mark.parametrize("factored", [True, False])
+def test_backward_kernels_match_oracle(rsa, shape, single_pass, factored):
     from paper_2105_13120_b200 import engine
 
     b, z, seq, a, n = shape
@@ -286,10 +287,16 @@ def test_backward_kernels_match_oracle(rsa, shape, single_pass):
     dev = torch.device("cuda", 0)
     stack = lambda x: torch.from_numpy(np.stack(orc.chunks_of(x, n))).to(dev, torch.bfloat16)  # noqa: E731
     tq, tk, tv, tg = (stack(x) for x in (q, k, v, g))
-    out, panel, _ = engine.forward(tq, tk, tv, path="fused")
-    dq, dk, dv = engine.backward(tq, tk, tv, panel, tg, outputs=out, path="fused", single_pass=single_pass)
+    out, panel, rowscale, _ = engine.forward(tq, tk, tv, path="fused", factored=factored)
+    assert (rowscale is not None) == factored
+    dq, dk, dv = engine.backward(tq, tk, tv, panel, tg, outputs=out, rowscale=rowscale, path="fused",
+                                 single_pass=single_pass)
     torch.cuda.synchronize()
-    _, _, wdq, wdk, wdv = _oracle(q, k, v, g, n)
+    wout, wprobs, wdq, wdk, wdv = _oracle(q, k, v, g, n)
+    _gate("out", np.concatenate([_np(out[d]) for d in range(n)], axis=-2), wout)
+    for d in range(n):
+        got = _np(engine.normalized_panel(panel[d], None if rowscale is None else rowscale[d]))
+        assert np.max(np.abs(got - wprobs[d])) <= PROB_ABS
     cat = lambda t: np.concatenate([_np(t[d]) for d in range(n)], axis=-2)  # noqa: E731
     _gate("dq", cat(dq), wdq)
     _gate("dk", cat(dk), wdk)
@@ -302,9 +309,49 @@ def test_single_pass_backward_is_deterministic(rsa):
     dev = torch.device("cuda", 0)
     gen = torch.Generator(device=dev).manual_seed(4)
     tq, tk, tv, tg = (torch.randn((1, 4, 3, 512, 64), generator=gen, device=dev).to(torch.bfloat16) for _ in range(4))
-    out, panel, _ = engine.forward(tq, tk, tv, path="fused")
-    r1 = engine.backward(tq, tk, tv, panel, tg, outputs=out, path="fused", single_pass=True)
-    r2 = engine.backward(tq, tk, tv, panel, tg, outputs=out, path="fused", single_pass=True)
+    out, panel, rowscale, _ = engine.forward(tq, tk, tv, path="fused")
+    r1 = engine.backward(tq, tk, tv, panel, tg, outputs=out, rowscale=rowscale, path="fused", single_pass=True)
+    r2 = engine.backward(tq, tk, tv, panel, tg, outputs=out, rowscale=rowscale, path="fused", single_pass=True)
     torch.cuda.synchronize()
     for x, y in zip(r1, r2):
         assert torch.equal(x, y)
+
+
+def test_factored_panel_matches_normalised_kernel(rsa):
+    """rsa_fwd_factored vs rsa_fwd_resident on the same inputs: r * P~ equals the
+    normalised panel to bf16 rounding, outputs agree, and every factored row
+    sums to one (the tensor-core row sum counts exactly the stored values)."""
+    from paper_2105_13120_b200 import engine
+
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev).manual_seed(9)
+    tq, tk, tv = (torch.randn((2, 2, 3, 256, 64), generator=gen, device=dev).to(torch.bfloat16) for _ in range(3))
+    f = engine.forward(tq, tk, tv, path="fused", factored=True)
+    n = engine.forward(tq, tk, tv, path="fused", factored=False)
+    torch.cuda.synchronize()
+    assert f.rowscale is not None and n.rowscale is None
+    p_f = engine.normalized_panel(f.panel, f.rowscale)
+    assert float((p_f - n.panel.float()).abs().max()) <= PROB_ABS
+    assert float((f.out.float() - n.out.float()).abs().max()) <= 2e-2
+    rows = (f.panel.float().sum(-1) * f.rowscale)
+    assert float((rows - 1).abs().max()) <= 1e-4
+    assert float(f.panel.float().max()) == 1.0  # the row max maps to 2^0 exactly
+
+
+def test_rowdot_scale_and_panel_normalize(rsa):
+    from paper_2105_13120_b200 import tensor_ops as ops
+
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev).manual_seed(5)
+    for cols in (64, 40):
+        a = torch.randn((3, 37, cols), generator=gen, device=dev).to(torch.bfloat16)
+        b = torch.randn((3, 37, cols), generator=gen, device=dev).to(torch.bfloat16)
+        s = torch.rand((3, 37), generator=gen, device=dev) + 0.5
+        d, a_s = ops.rowdot_scale(a, b, s)
+        want = (a.float() * b.float()).sum(-1) * s
+        assert torch.allclose(d, want, rtol=1e-5, atol=1e-5)
+        assert torch.equal(a_s, (a.float() * s[..., None]).to(torch.bfloat16))
+    p = torch.rand((5, 64, 96), generator=gen, device=dev).to(torch.bfloat16)
+    s = torch.rand((5, 64), generator=gen, device=dev)
+    assert torch.equal(ops.panel_normalize(p, s), p.float() * s[..., None])
+    assert torch.equal(ops.panel_normalize(p, s, torch.bfloat16), (p.float() * s[..., None]).to(torch.bfloat16))

@@ -16,7 +16,7 @@ dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev).manual_seed(0)
 q, k, v, dO = (torch.randn((1, B, Z, L, A), generator=g, device=dev).to(torch.bfloat16) for _ in range(4))
 for _ in range(iters):
-    out, panel, flag = engine.forward(q, k, v, path="fused")
-    engine.backward(q, k, v, panel, dO, outputs=out, path="fused")
+    out, panel, rowscale, flag = engine.forward(q, k, v, path="fused")
+    engine.backward(q, k, v, panel, dO, outputs=out, rowscale=rowscale, path="fused")
 torch.cuda.synchronize()
 print("done")
