@@ -15,10 +15,20 @@
 // written to the panel.  The panel bytes are the same as the normalised
 // panel's (2 per element) plus 4 bytes per row.
 //
-// Roles and buffers follow fwd_kernel (fused.cu): warp 0 TMA producer, warp 1
-// tcgen05.mma issuer (owns TMEM), warps 2..9 epilogue (TMEM lane quarter
-// w % 4, column half (w - 2) / 4).  TMEM: S double buffer [0, 256), O double
-// buffer at 256 + 128 * ob (80 columns each).
+// A CTA work unit is a PAIR of 128-row query tiles of one head (b, z) -- any
+// two of the head's n_rank * ceil(c/128) tiles, since every origin's keys are
+// resident -- so each K / V tile brought into shared memory feeds 256 query
+// rows.  18 warps:
+//   warp 0        TMA producer (one lane)
+//   warp 1        tcgen05.mma issuer (elect.sync); owns the TMEM allocation
+//   warps 2..17   two epilogue groups of 8 warps, group g = (w - 2) / 8 owns
+//                 query tile g of the unit; warp w reads TMEM lanes
+//                 32 * (w % 4).. (its tile rows) and column half ((w-2)/4) % 2
+// The groups run the same program on different tiles and drift apart, so
+// one group's exp2 work (MUFU) overlaps the other's shared-memory stores,
+// barriers and TMA stores.  TMEM: group g owns columns [256g, 256g+256):
+// S at +0 (128 columns, reloaded into registers at once, so single-buffered),
+// the O~ accumulator at +128 (80 columns).
 #include "fused_common.cuh"
 
 namespace rsa {
@@ -33,22 +43,23 @@ struct FfArgs {
   float* rowscale;  // [rank][b][z][c]
 };
 
-constexpr int FF_KST = 3, FF_VST = 2;
+constexpr int FF_GROUPS = 2;
+constexpr int FF_EPI_WARPS = 8 * FF_GROUPS;
+constexpr int FF_THREADS = 64 + 32 * FF_EPI_WARPS;  // 576
+constexpr int FF_KST = 4, FF_VST = 2;
 constexpr int PV_N = HD + 16;  // O columns + 16 row-sum columns
-constexpr uint32_t FF_OFF_Q = 0;
-constexpr uint32_t FF_OFF_K = FF_OFF_Q + 2 * TILE;
+constexpr uint32_t FF_OFF_Q = 0;                                  // one tile per group
+constexpr uint32_t FF_OFF_K = FF_OFF_Q + FF_GROUPS * TILE;
 constexpr uint32_t FF_OFF_V = FF_OFF_K + FF_KST * TILE;
-constexpr uint32_t FF_OFF_ONES = FF_OFF_V + FF_VST * TILE;  // 128 rows x 128 B of bf16 1.0
-constexpr uint32_t FF_OFF_P = FF_OFF_ONES + TILE;
-constexpr uint32_t FF_OFF_X = FF_OFF_P + 2 * PTILE;  // row-max exchange, 2 x 256 floats
-constexpr uint32_t FF_OFF_BAR = FF_OFF_X + 2 * EPI_THREADS * 4;
+constexpr uint32_t FF_OFF_ONES = FF_OFF_V + FF_VST * TILE;        // 128 rows x 128 B of bf16 1.0
+constexpr uint32_t FF_OFF_P = FF_OFF_ONES + TILE;                 // one P~ tile per group
+constexpr uint32_t FF_OFF_X = FF_OFF_P + FF_GROUPS * PTILE;       // row-max exchange [group][parity][256]
+constexpr uint32_t FF_OFF_BAR = FF_OFF_X + FF_GROUPS * 2 * 256 * 4;
 constexpr uint32_t FF_SMEM = FF_OFF_BAR + 512 + 1024;
-constexpr uint32_t COL_O = 2 * TK;
 static_assert(FF_SMEM <= 232448, "fwd_factored smem over the sm_100 per-CTA limit");
 
-// The two epilogue warps holding the two column halves of the same 32 rows.
-__device__ __forceinline__ void bar_rows(uint32_t quad) {
-  asm volatile("bar.sync %0, 64;" ::"r"(4 + quad) : "memory");
+__device__ __forceinline__ void bar_named(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
@@ -57,34 +68,51 @@ __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
   return __uint_as_float(r);
 }
 
-__global__ void __launch_bounds__(NTHREADS, 1) fwd_factored_kernel(const __grid_constant__ FfArgs p) {
+struct Unit {  // the query tiles of work unit u: head bz, tiles qi0 = 2p and qi1 = 2p + 1 (if it exists)
+  int bz, qi0, n;
+};
+
+__device__ __forceinline__ Unit unit_of(int u, int units_per_head, int nq) {
+  Unit r;
+  r.bz = u / units_per_head;
+  r.qi0 = 2 * (u % units_per_head);
+  r.n = min(2, nq - r.qi0);
+  return r;
+}
+
+// 96 registers: 18 warps put 5 warps on two SM sub-partitions, each with a 16K-register file.
+__global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfArgs p) {
   uint8_t* smem = smem_base();
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FF_OFF_BAR);
-  uint64_t *q_full = bar, *q_empty = bar + 2, *k_full = bar + 4, *k_empty = k_full + FF_KST;
+  uint64_t *q_full = bar, *q_empty = q_full + 2;
+  uint64_t *k_full = q_empty + 2, *k_empty = k_full + FF_KST;
   uint64_t *v_full = k_empty + FF_KST, *v_empty = v_full + FF_VST;
-  uint64_t *s_full = v_empty + FF_VST, *s_empty = s_full + 2, *p_full = s_empty + 2, *p_empty = p_full + 2;
+  uint64_t *s_full = v_empty + FF_VST, *s_empty = s_full + 2;
+  uint64_t *p_full = s_empty + 2, *p_empty = p_full + 2;
   uint64_t *o_full = p_empty + 2, *o_empty = o_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
 
   const Geo& g = p.g;
   const int ntk = (g.c + TK - 1) / TK, nrt = (g.c + TR - 1) / TR;
-  const int T = g.n_org * ntk;
-  const int BZ = g.B * g.Z;
-  const int items = g.n_rank * BZ * nrt;
+  const int T = g.n_org * ntk;   // key tiles per row
+  const int NQ = g.n_rank * nrt;  // query tiles per head
+  const int UH = (NQ + 1) / 2;    // units per head
+  const int units = g.B * g.Z * UH;
   const uint32_t warp = warp_id(), lane = lane_id();
 
   {  // constant B-operand block of ones (read by the async proxy)
     uint4* ones = reinterpret_cast<uint4*>(smem + FF_OFF_ONES);
-    for (uint32_t i = threadIdx.x; i < TILE / 16; i += NTHREADS) ones[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    for (uint32_t i = threadIdx.x; i < TILE / 16; i += FF_THREADS)
+      ones[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
     fence_proxy_async_smem();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(&q_full[s], 1), mbar_init(&q_empty[s], 1);
-      mbar_init(&s_full[s], 1), mbar_init(&s_empty[s], EPI_WARPS);
-      mbar_init(&p_full[s], EPI_WARPS), mbar_init(&p_empty[s], 1);
-      mbar_init(&o_full[s], 1), mbar_init(&o_empty[s], EPI_WARPS);
+      mbar_init(&s_full[s], 1), mbar_init(&s_empty[s], 8);
+      mbar_init(&p_full[s], 8), mbar_init(&p_empty[s], 1);
+      mbar_init(&o_full[s], 1), mbar_init(&o_empty[s], 8);
     }
     for (int s = 0; s < FF_KST; ++s) mbar_init(&k_full[s], 1), mbar_init(&k_empty[s], 1);
     for (int s = 0; s < FF_VST; ++s) mbar_init(&v_full[s], 1), mbar_init(&v_empty[s], 1);
@@ -100,14 +128,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) fwd_factored_kernel(const __grid_
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       Pos kq, vq;
-      uint32_t it = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-        const int rt = item % nrt, bz = (item / nrt) % BZ, d = item / (nrt * BZ);
-        const int b = bz / g.Z, z = bz % g.Z;
-        const int qb = it & 1;
-        mbar_wait(&q_empty[qb], ((it >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&q_full[qb], TILE);
-        tma_load_4d(smem + FF_OFF_Q + qb * TILE, &p.tq, &q_full[qb], 0, rt * TR, z, d * g.B + b);
+      uint32_t qn[2] = {0, 0};
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit un = unit_of(u, UH, NQ);
+        const int b = un.bz / g.Z, z = un.bz % g.Z;
+        for (int gi = 0; gi < un.n; ++gi) {
+          const int qi = un.qi0 + gi, d = qi / nrt, rt = qi % nrt;
+          mbar_wait(&q_empty[gi], (qn[gi] & 1) ^ 1);
+          mbar_arrive_expect_tx(&q_full[gi], TILE);
+          tma_load_4d(smem + FF_OFF_Q + gi * TILE, &p.tq, &q_full[gi], 0, rt * TR, z, d * g.B + b);
+          ++qn[gi];
+        }
         for (int pass = 0; pass < 2; ++pass) {
           for (int t = 0; t < T; ++t) {
             const int jo = t / ntk, k0 = (t % ntk) * TK;
@@ -131,116 +162,122 @@ __global__ void __launch_bounds__(NTHREADS, 1) fwd_factored_kernel(const __grid_
     // ---------------------------------------------------------- MMA issuer
     const uint32_t idesc_s = idesc_bf16_f32(TR, TK, 0, 0);
     const uint32_t idesc_o = idesc_bf16_f32(TR, PV_N, 0, 1);
-    Pos kq, vq, sq, pq;
-    uint32_t it = 0;
-    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-      const int qb = it & 1;
-      mbar_wait(&q_full[qb], (it >> 1) & 1);
-      const uint32_t qa = smem_u32(smem + FF_OFF_Q + qb * TILE);
-      auto issue_s = [&]() {
-        const uint32_t ks = kq.slot(FF_KST), sb = sq.slot(2);
+    Pos kq, vq;
+    uint32_t qn[2] = {0, 0}, sn[2] = {0, 0}, pn[2] = {0, 0}, on[2] = {0, 0};
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit un = unit_of(u, UH, NQ);
+      for (int gi = 0; gi < un.n; ++gi) mbar_wait(&q_full[gi], qn[gi] & 1);
+      // S(g) = Q_g K_t^T for both tiles of the unit from one K tile
+      auto issue_s = [&](bool last) {
+        const uint32_t ks = kq.slot(FF_KST);
         mbar_wait(&k_full[ks], kq.phase(FF_KST));
-        mbar_wait(&s_empty[sb], sq.phase(2) ^ 1);
-        tc_fence_after();
         const uint32_t ka = smem_u32(smem + FF_OFF_K + ks * TILE);
+        for (int gi = 0; gi < un.n; ++gi) {
+          mbar_wait(&s_empty[gi], (sn[gi] & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t qa = smem_u32(smem + FF_OFF_Q + gi * TILE);
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k)
-          umma_bf16_ws(tmem + sb * TK, smem_desc_sw128(qa + k * 32, 0, 1024), smem_desc_sw128(ka + k * 32, 0, 1024),
-                       idesc_s, k > 0);
+          for (int k = 0; k < HD / 16; ++k)
+            umma_bf16_ws(tmem + gi * 256, smem_desc_sw128(qa + k * 32, 0, 1024), smem_desc_sw128(ka + k * 32, 0, 1024),
+                         idesc_s, k > 0);
+          umma_commit_ws(&s_full[gi]);
+          if (last) umma_commit_ws(&q_empty[gi]), ++qn[gi];
+          ++sn[gi];
+        }
         umma_commit_ws(&k_empty[ks]);
-        umma_commit_ws(&s_full[sb]);
-        ++kq.i, ++sq.i;
+        ++kq.i;
       };
-      for (int t = 0; t < T; ++t) issue_s();  // pass A: row max
-      const uint32_t ob = it & 1;
-      mbar_wait(&o_empty[ob], ((it >> 1) & 1) ^ 1);
-      issue_s();
+      for (int t = 0; t < T; ++t) issue_s(false);  // pass A: row max
+      issue_s(T == 1);
       for (int t = 0; t < T; ++t) {  // pass B: P~ and O~ = P~ [V | 1]
-        if (t + 1 < T) issue_s();
-        const uint32_t pb = pq.slot(2), vs = vq.slot(FF_VST);
-        mbar_wait(&p_full[pb], pq.phase(2));
+        if (t + 1 < T) issue_s(t + 2 == T);
+        const uint32_t vs = vq.slot(FF_VST);
         mbar_wait(&v_full[vs], vq.phase(FF_VST));
-        tc_fence_after();
-        const uint32_t pa = smem_u32(smem + FF_OFF_P + pb * PTILE);
         const uint32_t va = smem_u32(smem + FF_OFF_V + vs * TILE);
         const uint32_t lbo = FF_OFF_ONES - (FF_OFF_V + vs * TILE);  // second 64-column atom: the ones block
+        for (int gi = 0; gi < un.n; ++gi) {
+          if (t == 0) mbar_wait(&o_empty[gi], (on[gi] & 1) ^ 1);
+          mbar_wait(&p_full[gi], pn[gi] & 1);
+          tc_fence_after();
+          const uint32_t pa = smem_u32(smem + FF_OFF_P + gi * PTILE);
 #pragma unroll
-        for (int k = 0; k < TK / 16; ++k)
-          umma_bf16_ws(tmem + COL_O + ob * 128, smem_desc_sw128(pa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
-                       smem_desc_sw128(va + k * 2048, lbo, 1024), idesc_o, (t | k) != 0);
+          for (int k = 0; k < TK / 16; ++k)
+            umma_bf16_ws(tmem + gi * 256 + 128, smem_desc_sw128(pa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
+                         smem_desc_sw128(va + k * 2048, lbo, 1024), idesc_o, (t | k) != 0);
+          umma_commit_ws(&p_empty[gi]);
+          ++pn[gi];
+        }
         umma_commit_ws(&v_empty[vs]);
-        umma_commit_ws(&p_empty[pb]);
-        ++pq.i, ++vq.i;
+        ++vq.i;
       }
-      umma_commit_ws(&o_full[ob]);
-      umma_commit_ws(&q_empty[qb]);
+      for (int gi = 0; gi < un.n; ++gi) umma_commit_ws(&o_full[gi]), ++on[gi];
     }
   } else {
     // ------------------------------------------------------------ epilogue
+    const uint32_t gi = (warp - 2) >> 3;
     const uint32_t quad = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int half = ((warp - 2) >> 2) & 1;
     const int r = quad * 32 + lane;
-    const int et = threadIdx.x - 64;  // 0..255
-    const bool storer = (lane == 0) && (quad == 2);
+    const int et = (threadIdx.x - 64) & 255;  // thread index within the group
+    const bool storer = (lane == 0) && (quad == 2);  // first warp of each (group, half)
     const uint32_t lane_base = (quad * 32u) << 16;
-    const uint32_t xbase = smem_u32(smem + FF_OFF_X);
-    const uint32_t pbase = smem_u32(smem + FF_OFF_P);
+    const uint32_t t_s = tmem + lane_base + gi * 256 + half * 64;
+    const uint32_t t_o = tmem + lane_base + gi * 256 + 128;
+    const uint32_t xbase = smem_u32(smem + FF_OFF_X) + gi * 2 * 256 * 4;
+    const uint32_t ptile = smem_u32(smem + FF_OFF_P + gi * PTILE);
+    uint8_t* ptile_gen = smem + FF_OFF_P + gi * PTILE + half * ATOM;
+    const uint32_t bar_half_id = 2 + gi * 2 + half, bar_rows_id = 6 + gi * 4 + quad;
     const float sl = p.sl;
     const OutView none{nullptr, 0, 0, 0, 0};
-    Pos sq, pq;
-    uint32_t it = 0;
+    uint32_t sn = 0, pn = 0, un_n = 0;
     bool bad = false;
-    auto load_s = [&](float* v) {
-      const uint32_t sb = sq.slot(2);
-      mbar_wait(&s_full[sb], sq.phase(2));
-      tc_fence_after();
-      __syncwarp();
-      tmem_ld32(tmem + lane_base + sb * TK + half * 64, v);
-      tmem_ld32(tmem + lane_base + sb * TK + half * 64 + 32, v + 32);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[sb]);
-      ++sq.i;
-    };
-    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-      const int rt = item % nrt, bz = (item / nrt) % BZ, d = item / (nrt * BZ);
-      const int b = bz / g.Z, z = bz % g.Z;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit un = unit_of(u, UH, NQ);
+      if (int(gi) >= un.n) continue;
+      const int b = un.bz / g.Z, z = un.bz % g.Z;
+      const int qi = un.qi0 + gi, d = qi / nrt, rt = qi % nrt;
       const int row = rt * TR + r;
       // ---- pass A: raw row max (and the non-finite check) over every key
       float m = -INFINITY;
       int k0 = 0;
       for (int t = 0; t < T; ++t) {
-        float v[64];
-        load_s(v);
         const int nvalid = min(TK, g.c - k0) - half * 64;
         k0 = k0 + TK >= g.c ? 0 : k0 + TK;
-        if (nvalid <= 0) continue;
-        float cmax, cmin;
-        if (nvalid >= 64) {
-          float mx[8], mi[8];
+        mbar_wait(&s_full[gi], sn & 1);
+        tc_fence_after();
+        __syncwarp();
+        float cmax = -INFINITY, cmin = INFINITY;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) mx[e] = mi[e] = v[e];
+        for (int cc = 0; cc < 2; ++cc) {  // two 32-column chunks (register budget of 18 warps)
+          float v[32];
+          tmem_ld32(t_s + cc * 32, v);
+          tmem_ld_wait();
+          if (nvalid >= 64) {
+            float mx[4], mi[4];
 #pragma unroll
-          for (int e = 8; e < 64; ++e) mx[e & 7] = max_nan(mx[e & 7], v[e]), mi[e & 7] = min_nan(mi[e & 7], v[e]);
+            for (int e = 0; e < 4; ++e) mx[e] = mi[e] = v[e];
 #pragma unroll
-          for (int w = 4; w; w >>= 1)
+            for (int e = 4; e < 32; ++e) mx[e & 3] = max_nan(mx[e & 3], v[e]), mi[e & 3] = min_nan(mi[e & 3], v[e]);
+            cmax = max_nan(cmax, max_nan(max_nan(mx[0], mx[1]), max_nan(mx[2], mx[3])));
+            cmin = min_nan(cmin, min_nan(min_nan(mi[0], mi[1]), min_nan(mi[2], mi[3])));
+          } else {
 #pragma unroll
-            for (int e = 0; e < w; ++e) mx[e] = max_nan(mx[e], mx[e + w]), mi[e] = min_nan(mi[e], mi[e + w]);
-          cmax = mx[0], cmin = mi[0];
-        } else {
-          cmax = -INFINITY, cmin = INFINITY;
-#pragma unroll
-          for (int e = 0; e < 64; ++e)
-            if (e < nvalid) cmax = max_nan(cmax, v[e]), cmin = min_nan(cmin, v[e]);
+            for (int e = 0; e < 32; ++e)
+              if (cc * 32 + e < nvalid) cmax = max_nan(cmax, v[e]), cmin = min_nan(cmin, v[e]);
+          }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[gi]);
+        ++sn;
+        if (nvalid <= 0) continue;
         bad |= !(fabsf(cmax) <= 3.402823466e38f) || !(fabsf(cmin) <= 3.402823466e38f);
         m = fmaxf(m, cmax);
       }
       {  // combine the two column halves of each row
-        const uint32_t slot = xbase + ((it & 1) * EPI_THREADS) * 4;
+        const uint32_t slot = xbase + (un_n & 1) * 256 * 4;
         asm volatile("st.shared.f32 [%0], %1;" ::"r"(slot + et * 4), "f"(m) : "memory");
-        bar_rows(quad);
+        bar_named(bar_rows_id, 64);
         float o;
         asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(slot + ((et + 128) & 255) * 4) : "memory");
         m = fmaxf(m, o);
@@ -250,49 +287,68 @@ __global__ void __launch_bounds__(NTHREADS, 1) fwd_factored_kernel(const __grid_
       int jo = 0;
       k0 = 0;
       for (int t = 0; t < T; ++t) {
-        const uint32_t pb = pq.slot(2);
         const int nvalid = min(TK, g.c - k0) - half * 64;
-        float v[64];
-        load_s(v);
-        if (nvalid >= 64) {
+        uint32_t w[32];
+        mbar_wait(&s_full[gi], sn & 1);
+        tc_fence_after();
+        __syncwarp();
 #pragma unroll
-          for (int e = 0; e < 64; ++e) v[e] = fast_exp2(fmaf(v[e], sl, -msl));
-        } else {
+        for (int cc = 0; cc < 2; ++cc) {
+          float v[32];
+          tmem_ld32(t_s + cc * 32, v);
+          tmem_ld_wait();
+          if (cc == 1) {  // both chunks are in registers: free the TMEM buffer for the next S
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[gi]);
+            ++sn;
+          }
+          if (nvalid >= 64) {
 #pragma unroll
-          for (int e = 0; e < 64; ++e) v[e] = e < nvalid ? fast_exp2(fmaf(v[e], sl, -msl)) : 0.f;
+            for (int e = 0; e < 16; ++e) {
+              const float x0 = fmaf(v[2 * e], sl, -msl), x1 = fmaf(v[2 * e + 1], sl, -msl);
+              w[cc * 16 + e] = pack_bf16(fast_exp2(x0), (e & 1) ? exp2_poly<3>(x1) : fast_exp2(x1));
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int c0 = cc * 32 + 2 * e;
+              w[cc * 16 + e] = pack_bf16(c0 < nvalid ? fast_exp2(fmaf(v[2 * e], sl, -msl)) : 0.f,
+                                         c0 + 1 < nvalid ? fast_exp2(fmaf(v[2 * e + 1], sl, -msl)) : 0.f);
+            }
+          }
         }
-        mbar_wait(&p_empty[pb], pq.phase(2) ^ 1);
-        if (storer && pq.i >= 2) tma_store_wait_read<1>();
-        bar_half(half);
-        const uint32_t ptile = pbase + pb * PTILE;
-        st_row32_sw128(ptile, r, half * 64, v);
-        st_row32_sw128(ptile, r, half * 64 + 32, v + 32);
+        mbar_wait(&p_empty[gi], (pn & 1) ^ 1);  // the previous P~ V product has read the tile
+        if (storer) tma_store_wait_read<0>();    // and the previous TMA store has read it
+        bar_named(bar_half_id, 128);
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4)
+          st_shared_v4(ptile + half * ATOM + sw128_offset(r, q4), w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2],
+                       w[4 * q4 + 3]);
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[pb]);
-        bar_half(half);
+        if (lane == 0) mbar_arrive(&p_full[gi]);
+        bar_named(bar_half_id, 128);
         if (storer) {
-          if (nvalid > 0)
-            tma_store_5d(&p.tp, smem + FF_OFF_P + pb * PTILE + half * ATOM, k0 + half * 64, g.org_lo + jo, rt * TR,
-                         z, d * g.B + b);
+          if (nvalid > 0) tma_store_5d(&p.tp, ptile_gen, k0 + half * 64, g.org_lo + jo, rt * TR, z, d * g.B + b);
           tma_store_commit();
         }
-        ++pq.i;
+        ++pn;
         if (k0 + TK >= g.c) k0 = 0, ++jo;
         else k0 += TK;
       }
       // ---- O = O~ / l, r = 1 / l (l >= 1: the max element contributes 2^0)
-      const uint32_t ob = it & 1;
-      mbar_wait(&o_full[ob], (it >> 1) & 1);
+      mbar_wait(&o_full[gi], un_n & 1);
       tc_fence_after();
       float o[32];
       __syncwarp();
-      tmem_ld32(tmem + lane_base + COL_O + ob * 128 + half * 32, o);
-      const float l = tmem_ld1(tmem + lane_base + COL_O + ob * 128 + HD);
+      tmem_ld32(t_o + half * 32, o);
+      const float l = tmem_ld1(t_o + HD);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&o_empty[ob]);
+      if (lane == 0) mbar_arrive(&o_empty[gi]);
+      ++un_n;
       const float rinv = 1.f / l;
 #pragma unroll
       for (int e = 0; e < 32; ++e) o[e] *= rinv;
@@ -331,8 +387,17 @@ int rsa_fwd_factored(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_
   a.flag = nonfinite_flag;
   a.o_out = to_out(o_out);
   a.rowscale = rowscale;
-  const int items = g->n_rank * g->batch * g->heads * ((g->chunk + TR - 1) / TR);
-  return launch(fwd_factored_kernel, items, FF_SMEM, a, stream, "fwd_factored_kernel");
+  const int nq = g->n_rank * ((g->chunk + TR - 1) / TR);
+  const int units = g->batch * g->heads * ((nq + 1) / 2);
+  if (units <= 0) return RSA_OK;
+  cudaFuncSetAttribute(fwd_factored_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FF_SMEM);
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, fwd_factored_kernel) == cudaSuccess && fa.maxThreadsPerBlock < FF_THREADS)
+    return fail(RSA_ERR_CUDA, "rsa_fwd_factored: %d registers/thread allow only %d threads per CTA (need %d)",
+                fa.numRegs, fa.maxThreadsPerBlock, FF_THREADS);
+  const int grid = units < num_sms() ? units : num_sms();
+  fwd_factored_kernel<<<grid, FF_THREADS, FF_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  return check_launch("fwd_factored_kernel");
 }
 
 }  // extern "C"
