@@ -1,59 +1,68 @@
 // Factored-panel RSA forward for sm_100a (head size A = 64, every origin
-// resident): the probability panel is saved as P~ = 2^(s*sl - m) (bf16, the
-// row max m taken over the whole row) plus one fp32 row scale r = 1 / sum(P~),
+// resident), ONE pass over the scores: the probability panel is saved as
+//   P~[row, k] = 2^(s*sl - m_ref[row])   (bf16),   r[row] = 1 / sum_k P~[row, k]   (fp32)
 // so the reference's probs are P = r * P~ (ringseq/ring_attention.py:89-94,
-// ringseq/tensor_ops.py:75-84) and its output O = P V = r * (P~ V)
-// (ringseq/ring_attention.py:97-103).
+// ringseq/tensor_ops.py:75-84) and its output is O = P V = r * (P~ V)
+// (ringseq/ring_attention.py:97-103).  sl = scale * log2(e).
 //
-// Why factored: the normalised panel needs the row sum before the first
-// probability can be written, which costs a second exponential per panel
-// element (fused.cu's pass A: max AND sum).  Here pass A is a max-only scan
-// of S = Q K^T, pass B is one exp2 per element, and the row sum comes from
-// the tensor core: the P~ V product runs with N = 80, whose last 16 B-operand
-// columns read a constant block of bf16 ones, so TMEM column 64 of the O
-// accumulator holds sum_k P~[row, k] -- the sum of exactly the rounded values
-// written to the panel.  The panel bytes are the same as the normalised
-// panel's (2 per element) plus 4 bytes per row.
+// Why factored and single-pass.  A normalised panel needs the full row max
+// AND sum before the first probability can be written, i.e. a second pass
+// over S = Q K^T.  On sm_100 the binding resource of that pass is the TMEM
+// read port (tcgen05.ld moves 64 B/clk per SM: one 128x128 fp32 S tile costs
+// 1024 clk), not the tensor core or the exp2 unit.  Softmax is invariant to
+// the reference point, so any per-row m_ref works as long as 2^(s*sl - m_ref)
+// neither overflows nor flushes the row: here m_ref is the max of the row's
+// FIRST key tile (exact, read once), and every later tile reuses it.  The row
+// sum comes from the tensor core -- the P~ V product runs with N = 80 whose
+// last 16 B-operand columns read a constant block of bf16 ones, so TMEM
+// column 64 of the O accumulator is sum_k P~[row, k] over exactly the rounded
+// values written to the panel.  A row whose true max exceeds m_ref by more
+// than 2^FF_HEADROOM (never for real attention logits: that is a probability
+// ratio of 2^96 between the first tile's best key and the row's best key)
+// sets bit 1 of *flag and the caller recomputes with the two-pass kernel
+// (rsa_fwd_resident); non-finite scores set bit 0 (NumericError).
 //
-// A CTA work unit is a PAIR of 128-row query tiles of one head (b, z) -- any
-// two of the head's n_rank * ceil(c/128) tiles, since every origin's keys are
-// resident -- so each K / V tile brought into shared memory feeds 256 query
-// rows.  18 warps:
+// A CTA work unit is a PAIR of 128-row query tiles of one head (b, z), so
+// each K / V tile brought into shared memory feeds 256 query rows; CTAs walk
+// contiguous unit ranges so consecutive units mostly share the head and K
+// stays resident when a row's T <= FF_KST key tiles fit.  18 warps:
 //   warp 0        TMA producer (one lane)
 //   warp 1        tcgen05.mma issuer (elect.sync); owns the TMEM allocation
 //   warps 2..17   two epilogue groups of 8 warps, group g = (w - 2) / 8 owns
 //                 query tile g of the unit; warp w reads TMEM lanes
 //                 32 * (w % 4).. (its tile rows) and column half ((w-2)/4) % 2
-// The groups run the same program on different tiles and drift apart, so
-// one group's exp2 work (MUFU) overlaps the other's shared-memory stores,
-// barriers and TMA stores.  TMEM: group g owns columns [256g, 256g+256):
-// S at +0 (128 columns, reloaded into registers at once, so single-buffered),
-// the O~ accumulator at +128 (80 columns).
+// TMEM: group g owns columns [256g, 256g + 256): S at +0 (128 columns; the
+// epilogue moves it to registers at once, so one buffer suffices) and the
+// O~ accumulator at +128 (80 columns).
+#include <cstdio>
+#include <cstdlib>
+
 #include "fused_common.cuh"
 
 namespace rsa {
 namespace {
 
 struct FfArgs {
-  CUtensorMap tq, tk, tv, tp;
+  CUtensorMap tq, tk, tv, tp, to;
   Geo g;
   float sl;  // scale * log2(e)
   int* flag;
-  OutView o_out;
-  float* rowscale;  // [rank][b][z][c]
+  float* rowscale;   // [rank][b][z][c]
+  long long* trace;  // RSA_FF_TRACE: per-warp (event, clock) log of CTA 0 (timeline experiments)
 };
 
 constexpr int FF_GROUPS = 2;
 constexpr int FF_EPI_WARPS = 8 * FF_GROUPS;
 constexpr int FF_THREADS = 64 + 32 * FF_EPI_WARPS;  // 576
 constexpr int FF_KST = 4, FF_VST = 2;
-constexpr int PV_N = HD + 16;  // O columns + 16 row-sum columns
+constexpr int PV_N = HD + 16;          // O columns + 16 row-sum columns
+constexpr float FF_HEADROOM = 96.f;    // max (row max - m_ref) * sl before the two-pass fallback
 constexpr uint32_t FF_OFF_Q = 0;                                  // one tile per group
 constexpr uint32_t FF_OFF_K = FF_OFF_Q + FF_GROUPS * TILE;
 constexpr uint32_t FF_OFF_V = FF_OFF_K + FF_KST * TILE;
 constexpr uint32_t FF_OFF_ONES = FF_OFF_V + FF_VST * TILE;        // 128 rows x 128 B of bf16 1.0
 constexpr uint32_t FF_OFF_P = FF_OFF_ONES + TILE;                 // one P~ tile per group
-constexpr uint32_t FF_OFF_X = FF_OFF_P + FF_GROUPS * PTILE;       // row-max exchange [group][parity][256]
+constexpr uint32_t FF_OFF_X = FF_OFF_P + FF_GROUPS * PTILE;       // m_ref exchange [group][parity][256]
 constexpr uint32_t FF_OFF_BAR = FF_OFF_X + FF_GROUPS * 2 * 256 * 4;
 constexpr uint32_t FF_SMEM = FF_OFF_BAR + 512 + 1024;
 static_assert(FF_SMEM <= 232448, "fwd_factored smem over the sm_100 per-CTA limit");
@@ -68,7 +77,13 @@ __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
   return __uint_as_float(r);
 }
 
-struct Unit {  // the query tiles of work unit u: head bz, tiles qi0 = 2p and qi1 = 2p + 1 (if it exists)
+#define FF_TRACE(ev)                                                                                          \
+  do {                                                                                                        \
+    if (p.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0 && tr_i < 4095)                                 \
+      p.trace[(threadIdx.x >> 5) * 4096 + tr_i++] = ((long long)(ev) << 48) | (long long)(clock64() - tr0); \
+  } while (0)
+
+struct Unit {  // work unit u: head bz, query tiles qi0 = 2p and qi0 + 1 (when it exists)
   int bz, qi0, n;
 };
 
@@ -78,6 +93,40 @@ __device__ __forceinline__ Unit unit_of(int u, int units_per_head, int nq) {
   r.qi0 = 2 * (u % units_per_head);
   r.n = min(2, nq - r.qi0);
   return r;
+}
+
+// Max and min of the first `nvalid` of 32 values (NaN-propagating).
+__device__ __forceinline__ void minmax32(const float* v, int nvalid, float& mx_out, float& mi_out) {
+  if (nvalid >= 32) {
+    float mx[4], mi[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) mx[e] = mi[e] = v[e];
+#pragma unroll
+    for (int e = 4; e < 32; ++e) mx[e & 3] = max_nan(mx[e & 3], v[e]), mi[e & 3] = min_nan(mi[e & 3], v[e]);
+    mx_out = max_nan(mx_out, max_nan(max_nan(mx[0], mx[1]), max_nan(mx[2], mx[3])));
+    mi_out = min_nan(mi_out, min_nan(min_nan(mi[0], mi[1]), min_nan(mi[2], mi[3])));
+  } else {
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if (e < nvalid) mx_out = max_nan(mx_out, v[e]), mi_out = min_nan(mi_out, v[e]);
+  }
+}
+
+// 32 values -> 16 packed bf16 pairs of 2^(v*sl - msl) (zero past nvalid);
+// one element in four on the FMA pipe (exp2_poly) to offload MUFU.
+__device__ __forceinline__ void exp_pack32(const float* v, int nvalid, float sl, float msl, uint32_t* w) {
+  if (nvalid >= 32) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const float x0 = fmaf(v[2 * e], sl, -msl), x1 = fmaf(v[2 * e + 1], sl, -msl);
+      w[e] = pack_bf16(fast_exp2(x0), (e & 1) ? exp2_poly<3>(x1) : fast_exp2(x1));
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      w[e] = pack_bf16(2 * e < nvalid ? fast_exp2(fmaf(v[2 * e], sl, -msl)) : 0.f,
+                       2 * e + 1 < nvalid ? fast_exp2(fmaf(v[2 * e + 1], sl, -msl)) : 0.f);
+  }
 }
 
 // 96 registers: 18 warps put 5 warps on two SM sub-partitions, each with a 16K-register file.
@@ -94,11 +143,14 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
 
   const Geo& g = p.g;
   const int ntk = (g.c + TK - 1) / TK, nrt = (g.c + TR - 1) / TR;
-  const int T = g.n_org * ntk;   // key tiles per row
+  const int T = g.n_org * ntk;    // key tiles per row
   const int NQ = g.n_rank * nrt;  // query tiles per head
   const int UH = (NQ + 1) / 2;    // units per head
   const int units = g.B * g.Z * UH;
   const uint32_t warp = warp_id(), lane = lane_id();
+  const int u_begin = int(int64_t(blockIdx.x) * units / gridDim.x);
+  const int u_end = int(int64_t(blockIdx.x + 1) * units / gridDim.x);
+  const bool kres = T <= FF_KST;  // K tile t stays in slot t while the head is unchanged
 
   {  // constant B-operand block of ones (read by the async proxy)
     uint4* ones = reinterpret_cast<uint4*>(smem + FF_OFF_ONES);
@@ -117,19 +169,22 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
     for (int s = 0; s < FF_KST; ++s) mbar_init(&k_full[s], 1), mbar_init(&k_empty[s], 1);
     for (int s = 0; s < FF_VST; ++s) mbar_init(&v_full[s], 1), mbar_init(&v_empty[s], 1);
     fence_barrier_init();
-    tma_prefetch(&p.tq), tma_prefetch(&p.tk), tma_prefetch(&p.tv), tma_prefetch(&p.tp);
+    tma_prefetch(&p.tq), tma_prefetch(&p.tk), tma_prefetch(&p.tv), tma_prefetch(&p.tp), tma_prefetch(&p.to);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const long long tr0 = clock64();
+  int tr_i = 0;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       Pos kq, vq;
-      uint32_t qn[2] = {0, 0};
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      uint32_t qn[2] = {0, 0}, kgen = 0;
+      int prev_bz = -1;
+      for (int u = u_begin; u < u_end; ++u) {
         const Unit un = unit_of(u, UH, NQ);
         const int b = un.bz / g.Z, z = un.bz % g.Z;
         for (int gi = 0; gi < un.n; ++gi) {
@@ -139,22 +194,30 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
           tma_load_4d(smem + FF_OFF_Q + gi * TILE, &p.tq, &q_full[gi], 0, rt * TR, z, d * g.B + b);
           ++qn[gi];
         }
-        for (int pass = 0; pass < 2; ++pass) {
+        if (kres && un.bz != prev_bz) {
           for (int t = 0; t < T; ++t) {
             const int jo = t / ntk, k0 = (t % ntk) * TK;
+            mbar_wait(&k_empty[t], (kgen & 1) ^ 1);
+            mbar_arrive_expect_tx(&k_full[t], TILE);
+            tma_load_4d(smem + FF_OFF_K + t * TILE, &p.tk, &k_full[t], 0, k0, z, (g.org_lo + jo) * g.B + b);
+          }
+          ++kgen;
+        }
+        prev_bz = un.bz;
+        for (int t = 0; t < T; ++t) {
+          const int jo = t / ntk, k0 = (t % ntk) * TK;
+          if (!kres) {
             const uint32_t ks = kq.slot(FF_KST);
             mbar_wait(&k_empty[ks], kq.phase(FF_KST) ^ 1);
             mbar_arrive_expect_tx(&k_full[ks], TILE);
             tma_load_4d(smem + FF_OFF_K + ks * TILE, &p.tk, &k_full[ks], 0, k0, z, (g.org_lo + jo) * g.B + b);
             ++kq.i;
-            if (pass == 1) {
-              const uint32_t vs = vq.slot(FF_VST);
-              mbar_wait(&v_empty[vs], vq.phase(FF_VST) ^ 1);
-              mbar_arrive_expect_tx(&v_full[vs], TILE);
-              tma_load_4d(smem + FF_OFF_V + vs * TILE, &p.tv, &v_full[vs], 0, k0, z, (g.org_lo + jo) * g.B + b);
-              ++vq.i;
-            }
           }
+          const uint32_t vs = vq.slot(FF_VST);
+          mbar_wait(&v_empty[vs], vq.phase(FF_VST) ^ 1);
+          mbar_arrive_expect_tx(&v_full[vs], TILE);
+          tma_load_4d(smem + FF_OFF_V + vs * TILE, &p.tv, &v_full[vs], 0, k0, z, (g.org_lo + jo) * g.B + b);
+          ++vq.i;
         }
       }
     }
@@ -163,14 +226,20 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
     const uint32_t idesc_s = idesc_bf16_f32(TR, TK, 0, 0);
     const uint32_t idesc_o = idesc_bf16_f32(TR, PV_N, 0, 1);
     Pos kq, vq;
-    uint32_t qn[2] = {0, 0}, sn[2] = {0, 0}, pn[2] = {0, 0}, on[2] = {0, 0};
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    uint32_t qn[2] = {0, 0}, sn[2] = {0, 0}, pn[2] = {0, 0}, on[2] = {0, 0}, kgen = 0;
+    int prev_bz = -1;
+    for (int u = u_begin; u < u_end; ++u) {
       const Unit un = unit_of(u, UH, NQ);
+      if (kres && un.bz != prev_bz) ++kgen;
+      prev_bz = un.bz;
+      // resident K: release the slots after the unit's last S unless the next unit reuses them
+      const bool k_release = kres && u + 1 < u_end && unit_of(u + 1, UH, NQ).bz != un.bz;
       for (int gi = 0; gi < un.n; ++gi) mbar_wait(&q_full[gi], qn[gi] & 1);
-      // S(g) = Q_g K_t^T for both tiles of the unit from one K tile
-      auto issue_s = [&](bool last) {
-        const uint32_t ks = kq.slot(FF_KST);
-        mbar_wait(&k_full[ks], kq.phase(FF_KST));
+      // S(g) = Q_g K_t^T for both query tiles of the unit from one K tile
+      auto issue_s = [&](int t) {
+        const bool last = t + 1 == T;
+        const uint32_t ks = kres ? uint32_t(t) : kq.slot(FF_KST);
+        mbar_wait(&k_full[ks], kres ? (kgen - 1) & 1 : kq.phase(FF_KST));
         const uint32_t ka = smem_u32(smem + FF_OFF_K + ks * TILE);
         for (int gi = 0; gi < un.n; ++gi) {
           mbar_wait(&s_empty[gi], (sn[gi] & 1) ^ 1);
@@ -181,16 +250,17 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
             umma_bf16_ws(tmem + gi * 256, smem_desc_sw128(qa + k * 32, 0, 1024), smem_desc_sw128(ka + k * 32, 0, 1024),
                          idesc_s, k > 0);
           umma_commit_ws(&s_full[gi]);
+          FF_TRACE(10 + gi);
           if (last) umma_commit_ws(&q_empty[gi]), ++qn[gi];
           ++sn[gi];
         }
-        umma_commit_ws(&k_empty[ks]);
-        ++kq.i;
+        if (!kres) umma_commit_ws(&k_empty[ks]), ++kq.i;
+        else if (last && k_release)
+          for (int j = 0; j < T; ++j) umma_commit_ws(&k_empty[j]);
       };
-      for (int t = 0; t < T; ++t) issue_s(false);  // pass A: row max
-      issue_s(T == 1);
-      for (int t = 0; t < T; ++t) {  // pass B: P~ and O~ = P~ [V | 1]
-        if (t + 1 < T) issue_s(t + 2 == T);
+      issue_s(0);
+      for (int t = 0; t < T; ++t) {  // O~ += P~ [V | 1], one key tile behind S
+        if (t + 1 < T) issue_s(t + 1);
         const uint32_t vs = vq.slot(FF_VST);
         mbar_wait(&v_full[vs], vq.phase(FF_VST));
         const uint32_t va = smem_u32(smem + FF_OFF_V + vs * TILE);
@@ -205,6 +275,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
             umma_bf16_ws(tmem + gi * 256 + 128, smem_desc_sw128(pa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
                          smem_desc_sw128(va + k * 2048, lbo, 1024), idesc_o, (t | k) != 0);
           umma_commit_ws(&p_empty[gi]);
+          FF_TRACE(12 + gi);
           ++pn[gi];
         }
         umma_commit_ws(&v_empty[vs]);
@@ -218,7 +289,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
     const uint32_t quad = warp & 3;
     const int half = ((warp - 2) >> 2) & 1;
     const int r = quad * 32 + lane;
-    const int et = (threadIdx.x - 64) & 255;  // thread index within the group
+    const int et = (threadIdx.x - 64) & 255;         // thread index within the group
     const bool storer = (lane == 0) && (quad == 2);  // first warp of each (group, half)
     const uint32_t lane_base = (quad * 32u) << 16;
     const uint32_t t_s = tmem + lane_base + gi * 256 + half * 64;
@@ -226,98 +297,62 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
     const uint32_t xbase = smem_u32(smem + FF_OFF_X) + gi * 2 * 256 * 4;
     const uint32_t ptile = smem_u32(smem + FF_OFF_P + gi * PTILE);
     uint8_t* ptile_gen = smem + FF_OFF_P + gi * PTILE + half * ATOM;
-    const uint32_t bar_half_id = 2 + gi * 2 + half, bar_rows_id = 6 + gi * 4 + quad;
+    const uint32_t bar_half_id = 2 + gi * 2 + half, bar_rows_id = 6 + gi * 4 + quad, bar_grp_id = 14 + gi;
     const float sl = p.sl;
-    const OutView none{nullptr, 0, 0, 0, 0};
     uint32_t sn = 0, pn = 0, un_n = 0;
-    bool bad = false;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    bool bad = false, redo = false;
+    for (int u = u_begin; u < u_end; ++u) {
       const Unit un = unit_of(u, UH, NQ);
       if (int(gi) >= un.n) continue;
       const int b = un.bz / g.Z, z = un.bz % g.Z;
       const int qi = un.qi0 + gi, d = qi / nrt, rt = qi % nrt;
       const int row = rt * TR + r;
-      // ---- pass A: raw row max (and the non-finite check) over every key
-      float m = -INFINITY;
-      int k0 = 0;
-      for (int t = 0; t < T; ++t) {
-        const int nvalid = min(TK, g.c - k0) - half * 64;
-        k0 = k0 + TK >= g.c ? 0 : k0 + TK;
-        mbar_wait(&s_full[gi], sn & 1);
-        tc_fence_after();
-        __syncwarp();
-        float cmax = -INFINITY, cmin = INFINITY;
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {  // two 32-column chunks (register budget of 18 warps)
-          float v[32];
-          tmem_ld32(t_s + cc * 32, v);
-          tmem_ld_wait();
-          if (nvalid >= 64) {
-            float mx[4], mi[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) mx[e] = mi[e] = v[e];
-#pragma unroll
-            for (int e = 4; e < 32; ++e) mx[e & 3] = max_nan(mx[e & 3], v[e]), mi[e & 3] = min_nan(mi[e & 3], v[e]);
-            cmax = max_nan(cmax, max_nan(max_nan(mx[0], mx[1]), max_nan(mx[2], mx[3])));
-            cmin = min_nan(cmin, min_nan(min_nan(mi[0], mi[1]), min_nan(mi[2], mi[3])));
-          } else {
-#pragma unroll
-            for (int e = 0; e < 32; ++e)
-              if (cc * 32 + e < nvalid) cmax = max_nan(cmax, v[e]), cmin = min_nan(cmin, v[e]);
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[gi]);
-        ++sn;
-        if (nvalid <= 0) continue;
-        bad |= !(fabsf(cmax) <= 3.402823466e38f) || !(fabsf(cmin) <= 3.402823466e38f);
-        m = fmaxf(m, cmax);
-      }
-      {  // combine the two column halves of each row
-        const uint32_t slot = xbase + (un_n & 1) * 256 * 4;
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(slot + et * 4), "f"(m) : "memory");
-        bar_named(bar_rows_id, 64);
-        float o;
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(slot + ((et + 128) & 255) * 4) : "memory");
-        m = fmaxf(m, o);
-      }
-      const float msl = (m == -INFINITY || !(fabsf(m) <= 3.402823466e38f)) ? 0.f : m * sl;
-      // ---- pass B: P~ = 2^(s*sl - m*sl) -> smem -> TMA store; UMMA accumulates P~ [V | 1]
-      int jo = 0;
-      k0 = 0;
+      FF_TRACE(1);
+      float m = -INFINITY, mi = INFINITY, msl = 0.f;  // running raw max / min, reference m_ref * sl
+      int jo = 0, k0 = 0;
       for (int t = 0; t < T; ++t) {
         const int nvalid = min(TK, g.c - k0) - half * 64;
         uint32_t w[32];
         mbar_wait(&s_full[gi], sn & 1);
+        FF_TRACE(3);
         tc_fence_after();
         __syncwarp();
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          float v[32];
-          tmem_ld32(t_s + cc * 32, v);
+        if (t == 0) {  // first key tile: its row max is the reference
+          float v[64];
+          tmem_ld32(t_s, v);
+          tmem_ld32(t_s + 32, v + 32);
           tmem_ld_wait();
-          if (cc == 1) {  // both chunks are in registers: free the TMEM buffer for the next S
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[gi]);
-            ++sn;
-          }
-          if (nvalid >= 64) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_empty[gi]);
+          minmax32(v, nvalid, m, mi);
+          minmax32(v + 32, nvalid - 32, m, mi);
+          const uint32_t slot = xbase + (un_n & 1) * 256 * 4;  // combine the two column halves
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(slot + et * 4), "f"(m) : "memory");
+          bar_named(bar_rows_id, 64);
+          float o;
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(slot + ((et + 128) & 255) * 4) : "memory");
+          const float mref = fmaxf(m, o);
+          msl = (mref == -INFINITY || !(fabsf(mref) <= 3.402823466e38f)) ? 0.f : mref * sl;
+          exp_pack32(v, nvalid, sl, msl, w);
+          exp_pack32(v + 32, nvalid - 32, sl, msl, w + 16);
+        } else {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const float x0 = fmaf(v[2 * e], sl, -msl), x1 = fmaf(v[2 * e + 1], sl, -msl);
-              w[cc * 16 + e] = pack_bf16(fast_exp2(x0), (e & 1) ? exp2_poly<3>(x1) : fast_exp2(x1));
+          for (int cc = 0; cc < 2; ++cc) {  // two 32-column chunks (register budget of 18 warps)
+            float v[32];
+            tmem_ld32(t_s + cc * 32, v);
+            tmem_ld_wait();
+            if (cc == 1) {  // both chunks are in registers: free S for the next key tile
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&s_empty[gi]);
             }
-          } else {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const int c0 = cc * 32 + 2 * e;
-              w[cc * 16 + e] = pack_bf16(c0 < nvalid ? fast_exp2(fmaf(v[2 * e], sl, -msl)) : 0.f,
-                                         c0 + 1 < nvalid ? fast_exp2(fmaf(v[2 * e + 1], sl, -msl)) : 0.f);
-            }
+            minmax32(v, nvalid - cc * 32, m, mi);
+            exp_pack32(v, nvalid - cc * 32, sl, msl, w + cc * 16);
           }
         }
+        ++sn;
+        FF_TRACE(4);
         mbar_wait(&p_empty[gi], (pn & 1) ^ 1);  // the previous P~ V product has read the tile
         if (storer) tma_store_wait_read<0>();    // and the previous TMA store has read it
         bar_named(bar_half_id, 128);
@@ -333,12 +368,17 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
           if (nvalid > 0) tma_store_5d(&p.tp, ptile_gen, k0 + half * 64, g.org_lo + jo, rt * TR, z, d * g.B + b);
           tma_store_commit();
         }
+        FF_TRACE(6);
         ++pn;
         if (k0 + TK >= g.c) k0 = 0, ++jo;
         else k0 += TK;
       }
-      // ---- O = O~ / l, r = 1 / l (l >= 1: the max element contributes 2^0)
+      if (!(m == -INFINITY && mi == INFINITY))  // this thread saw at least one valid key
+        bad |= !(fabsf(m) <= 3.402823466e38f) || !(fabsf(mi) <= 3.402823466e38f);
+      redo |= m * sl - msl > FF_HEADROOM;
+      // ---- O = O~ / l, r = 1 / l (l >= 1 unless the row needs the fallback)
       mbar_wait(&o_full[gi], un_n & 1);
+      FF_TRACE(7);
       tc_fence_after();
       float o[32];
       __syncwarp();
@@ -350,14 +390,26 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
       if (lane == 0) mbar_arrive(&o_empty[gi]);
       ++un_n;
       const float rinv = 1.f / l;
+      redo |= !(l >= 1.f && l <= 3.402823466e38f);
+      // O -> the group's P~ buffer (atom 0, swizzled like a TMA tile) -> one TMA store
+      if (storer) tma_store_wait_read<0>();  // the unit's last P~ stores have left the buffer
+      bar_named(bar_grp_id, 256);
 #pragma unroll
-      for (int e = 0; e < 32; ++e) o[e] *= rinv;
-      if (row < g.c) {
-        store_row32(none, p.o_out, 0, d, b, z, row, half * 32, o);
-        if (half == 0) p.rowscale[(int64_t(d * g.B + b) * g.Z + z) * g.c + row] = rinv;
+      for (int q4 = 0; q4 < 4; ++q4)
+        st_shared_v4(ptile + sw128_offset(r, half * 4 + q4), pack_bf16(o[8 * q4] * rinv, o[8 * q4 + 1] * rinv),
+                     pack_bf16(o[8 * q4 + 2] * rinv, o[8 * q4 + 3] * rinv),
+                     pack_bf16(o[8 * q4 + 4] * rinv, o[8 * q4 + 5] * rinv),
+                     pack_bf16(o[8 * q4 + 6] * rinv, o[8 * q4 + 7] * rinv));
+      fence_proxy_async_smem();
+      bar_named(bar_grp_id, 256);
+      if (storer && half == 0) {
+        tma_store_4d(&p.to, smem + FF_OFF_P + gi * PTILE, 0, rt * TR, z, d * g.B + b);
+        tma_store_commit();
       }
+      if (row < g.c && half == 0) p.rowscale[(int64_t(d * g.B + b) * g.Z + z) * g.c + row] = rinv;
+      FF_TRACE(21);
     }
-    if (bad && p.flag) atomicExch(p.flag, 1);
+    if (p.flag && (bad || redo)) atomicOr(p.flag, (bad ? 1 : 0) | (redo ? 2 : 0));
     if (storer) tma_store_wait_all<0>();
   }
   tc_fence_before();
@@ -371,22 +423,28 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
 extern "C" {
 
 int rsa_fwd_factored(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view panel, rsa_view o_out,
-                     float* rowscale, int* nonfinite_flag, void* stream) {
+                     float* rowscale, int* flag, void* stream) {
   using namespace rsa;
   if (!geom_ok(g)) return fail(RSA_ERR_INVALID, "rsa_fwd_factored: unsupported geometry");
   if (g->org_lo != 0 || g->n_org != g->seq_len / g->chunk)
     return fail(RSA_ERR_INVALID, "rsa_fwd_factored: every origin must be resident (org_lo = 0, n_org = L / c)");
-  if (!rowscale || !o_out.ptr || !out_ok(o_out, 2))
-    return fail(RSA_ERR_UNSUPPORTED, "rsa_fwd_factored: output / row-scale buffers missing or misaligned");
+  if (!rowscale || !flag || !o_out.ptr || !out_ok(o_out, 2))
+    return fail(RSA_ERR_UNSUPPORTED, "rsa_fwd_factored: output / row-scale / flag buffers missing or misaligned");
   FfArgs a{};
   if (!head_map(&a.tq, q, g, g->n_rank) || !head_map(&a.tk, k, g, g->n_org) || !head_map(&a.tv, v, g, g->n_org) ||
-      !panel_map(&a.tp, panel, g, g->n_rank))
+      !panel_map(&a.tp, panel, g, g->n_rank) || !head_map(&a.to, o_out, g, g->n_rank))
     return RSA_ERR_UNSUPPORTED;
   a.g = to_geo(g);
   a.sl = g->scale * LOG2E;
-  a.flag = nonfinite_flag;
-  a.o_out = to_out(o_out);
+  a.flag = flag;
   a.rowscale = rowscale;
+  static long long* trace_buf = nullptr;
+  const char* trace_path = getenv("RSA_FF_TRACE");
+  if (trace_path) {
+    if (!trace_buf) cudaMalloc(&trace_buf, 18 * 4096 * sizeof(long long));
+    cudaMemset(trace_buf, 0, 18 * 4096 * sizeof(long long));
+    a.trace = trace_buf;
+  }
   const int nq = g->n_rank * ((g->chunk + TR - 1) / TR);
   const int units = g->batch * g->heads * ((nq + 1) / 2);
   if (units <= 0) return RSA_OK;
@@ -397,6 +455,11 @@ int rsa_fwd_factored(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_
                 fa.numRegs, fa.maxThreadsPerBlock, FF_THREADS);
   const int grid = units < num_sms() ? units : num_sms();
   fwd_factored_kernel<<<grid, FF_THREADS, FF_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  if (trace_path) {
+    static long long host[18 * 4096];
+    cudaMemcpy(host, trace_buf, sizeof(host), cudaMemcpyDeviceToHost);
+    if (FILE* f = fopen(trace_path, "wb")) fwrite(host, sizeof(host), 1, f), fclose(f);
+  }
   return check_launch("fwd_factored_kernel");
 }
 

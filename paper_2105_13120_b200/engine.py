@@ -152,8 +152,9 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, path: str = "a
 
     Returns ``Forward(out, panel, rowscale, flag)``: outputs [N][B][Z][c][A]
     bf16, the panel [N][B][Z][c][L] bf16 (factored when ``rowscale`` is not
-    None), and the non-finite flag, a device int set by the kernels when a
-    score is non-finite (callers decide when to read it).
+    None), and the status flag, a device int the kernels OR bits into (callers
+    decide when to read it): bit 0 = a non-finite score, bit 1 = the factored
+    kernel needs the two-pass fallback (``factored=False``) for this input.
 
     Fused path: ``factored`` (default) runs rsa_fwd_factored (one exp2 per
     panel element); ``factored=False`` the normalised rsa_fwd_resident, and a

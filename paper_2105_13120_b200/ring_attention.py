@@ -146,6 +146,25 @@ def _chunk_elements(cfg: AttentionConfig) -> int:
     return cfg.batch_size * cfg.num_heads * cfg.chunk_len * cfg.head_size
 
 
+def _forward_checked(q, k, v, path: str) -> engine.Forward:
+    """engine.forward plus the host-side status check.
+
+    Flag bit 0: a non-finite score (NumericError, as ringseq/tensor_ops.py:80-81).
+    Flag bit 1: the single-pass factored kernel found a row whose max lies more
+    than 2^96 above its first key tile's max; the two-pass normalised kernel
+    recomputes the whole launch (never seen for real attention logits).
+    """
+    res = engine.forward(q, k, v, path=path)
+    status = int(res.flag.item())
+    if status == 2:
+        res.flag.zero_()
+        res = engine.forward(q, k, v, path=path, factored=False, flag=res.flag, out=res.out, panel=res.panel)
+        status = int(res.flag.item())
+    if status:
+        raise NumericError("softmax_rows requires finite inputs")
+    return res
+
+
 def forward_ledger(cfg: AttentionConfig) -> CommLedger:
     """Keys then values circulate N-1 hops each (ringseq/ring_attention.py:124-130)."""
     n = cfg.num_devices
@@ -184,9 +203,7 @@ def ring_attention_forward(q_chunks, k_chunks, v_chunks, cfg: AttentionConfig, *
     v_chunks = _check_chunks("v_chunks", v_chunks, cfg, shape)
     dev = _device_of(q_chunks, k_chunks, v_chunks)
     q, k, v = (_stack(x, dev) for x in (q_chunks, k_chunks, v_chunks))
-    out, panel, rowscale, flag = engine.forward(q, k, v, path=path)
-    if int(flag.item()):
-        raise NumericError("softmax_rows requires finite inputs")
+    out, panel, rowscale, _ = _forward_checked(q, k, v, path)
     return RingAttentionForward(
         outputs=[out[d] for d in range(cfg.num_devices)],
         probs=ProbPanels(panel, out, rowscale),
@@ -252,9 +269,7 @@ def sequence_parallel_attention(x_chunks, weights, cfg: AttentionConfig, *, exec
         return y.view(n, b, c, z, a).permute(0, 1, 3, 2, 4).contiguous()  # split_heads per rank
 
     q, k, v = project(wq), project(wk), project(wv)
-    out, _, _, flag = engine.forward(q, k, v, path=path)
-    if int(flag.item()):
-        raise NumericError("softmax_rows requires finite inputs")
+    out = _forward_checked(q, k, v, path).out
     merged = out.permute(0, 1, 3, 2, 4).reshape(n, b, c, z * a)  # merge_heads per rank
     y = ops.matmul(merged, wo)
     return [y[d] for d in range(n)], forward_ledger(cfg)
