@@ -25,6 +25,9 @@
 // (owns TMEM), warps 2..9 epilogue (warp w reads TMEM lanes 32*(w%4)..,
 // column half (w-2)/4).  Rings: K, V, dO, Q tiles 2 deep each, panel
 // tiles 3 deep (the only HBM stream that matters; dO/Q re-reads are L2 hits).  dS overwrites P in place once P^T dO has consumed it.
+#include <cstdio>
+#include <cstdlib>
+
 #include "fused_common.cuh"
 
 namespace rsa {
@@ -33,14 +36,22 @@ namespace {
 constexpr int MAX_QT = 4;  // query tiles per head that fit the dQ columns of TMEM
 
 struct BwdArgs {
-  CUtensorMap tq, tk, tv, tdo, tp;
+  CUtensorMap tq, tk, tv, tdo, tp, tdk, tdv;
+  int kv_tma;  // bf16, non-accumulating dK/dV: staged in the retiring P slot and TMA-stored
   Geo g;
   const float* dvec;
   OutView dq_acc, dq_out, dk, dv;
   int accumulate_dq;
   int dkv_bf16;
   int accumulate_dkv;
+  long long* trace;  // RSA_BF_TRACE: per-warp (event, clock) log of CTA 0 (timeline experiments)
 };
+
+#define BF_TRACE(ev)                                                                                          \
+  do {                                                                                                        \
+    if (p.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0 && tr_i < 4095)                                 \
+      p.trace[(threadIdx.x >> 5) * 4096 + tr_i++] = ((long long)(ev) << 48) | (long long)(clock64() - tr0); \
+  } while (0)
 
 // Ring depths.  Each operand is released as soon as its last MMA has read it
 // (dO after P^T dO, V after the key tile's last dO V^T, Q / P / K after the
@@ -95,11 +106,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
     for (int s = 0; s < MAX_QT; ++s) mbar_init(&dq_full[s], 1), mbar_init(&dq_empty[s], EPI_WARPS);
     fence_barrier_init();
     tma_prefetch(&p.tq), tma_prefetch(&p.tk), tma_prefetch(&p.tv), tma_prefetch(&p.tdo), tma_prefetch(&p.tp);
+    if (p.kv_tma) tma_prefetch(&p.tdk), tma_prefetch(&p.tdv);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const long long tr0 = clock64();
+  int tr_i = 0;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -114,14 +128,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
         tma_load_4d(smem + off + s * TILE, map, &r.full[s], 0, r0, z, blk);
         ++pos.i;
       };
+      // V and K tiles of (head item, key tile kk); issued one key tile ahead of use
+      auto load_vk = [&](int item, int kk) {
+        const int b = item / g.Z, z = item % g.Z;
+        const int jo = kk / ntk, k0 = (kk % ntk) * TK;
+        load_tile(rv, vq, BF_V, BF_OFF_V, &p.tv, k0, z, jo * g.B + b);
+        load_tile(rk, kq, BF_K, BF_OFF_K, &p.tk, k0, z, jo * g.B + b);
+      };
+      if (blockIdx.x < items) load_vk(blockIdx.x, 0);
       for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const int b = item / g.Z, z = item % g.Z;
         for (int kk = 0; kk < NK; ++kk) {
           const int jo = kk / ntk, k0 = (kk % ntk) * TK;
           for (int qt = 0; qt < NQ; ++qt) {
             const int d = qt / nrt, r0 = (qt % nrt) * TR;
-            // consumption order: V (first dO V^T of the key tile), dO, P, then K, Q (dS products)
-            if (qt == 0) load_tile(rv, vq, BF_V, BF_OFF_V, &p.tv, k0, z, jo * g.B + b);
             load_tile(rdo, dq_, BF_DO, BF_OFF_DO, &p.tdo, r0, z, d * g.B + b);
             const uint32_t s = pq.slot(BF_P);
             mbar_wait(&rp.empty[s], pq.phase(BF_P) ^ 1);
@@ -129,9 +149,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
             uint8_t* pt = smem + BF_OFF_P + s * PTILE;
             tma_load_5d(pt, &p.tp, &rp.full[s], k0, g.org_lo + jo, r0, z, d * g.B + b);
             tma_load_5d(pt + ATOM, &p.tp, &rp.full[s], k0 + 64, g.org_lo + jo, r0, z, d * g.B + b);
+            BF_TRACE(1);
             ++pq.i;
-            if (qt == 0) load_tile(rk, kq, BF_K, BF_OFF_K, &p.tk, k0, z, jo * g.B + b);
             load_tile(rq, qq, BF_Q, BF_OFF_Q, &p.tq, r0, z, d * g.B + b);
+            // the next key tile's V / K after this key tile's last step: their slots (key tile
+            // kk - 1) have retired by now, and they arrive a step earlier than in step order
+            if (qt == NQ - 1) {
+              if (kk + 1 < NK) load_vk(item, kk + 1);
+              else if (item + int(gridDim.x) < items) load_vk(item + gridDim.x, 0);
+            }
           }
         }
       }
@@ -165,6 +191,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
             ++v_a.i;
           }
           umma_commit_ws(dp_full);
+          BF_TRACE(10);
           ++dpq.i;
         };
         // dV += P^T dO; p_read certifies P has been consumed, so dS may overwrite it
@@ -181,6 +208,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
             umma_bf16_ws(tmem + COL_DV, da + 128 * k, db + 128 * k, idesc_kv, (qt | k) != 0);
           umma_commit_ws(&rdo.empty[ds]);
           umma_commit_ws(&p_read[ps]);
+          BF_TRACE(11);
           ++do_a.i, ++p_a.i;
           if (qt == NQ - 1) ++accq.i;
         };
@@ -208,7 +236,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
           for (int k = 0; k < TK / 16; ++k)  // dS K-major over keys: 64-key atoms ATOM apart, +32 B per k
             umma_bf16_ws(tmem + COL_DQ + qt * HD, dkm + (k >> 2) * (ATOM >> 4) + 2 * (k & 3), kd + 128 * k, idesc_dq,
                          (kk | k) != 0);
-          umma_commit_ws(&rp.empty[ps]);
+          if (!(p.kv_tma && qt == NQ - 1)) umma_commit_ws(&rp.empty[ps]);  // else the epilogue frees it
           umma_commit_ws(&rq.empty[qs]);
           if (qt == NQ - 1) {
             umma_commit_ws(acc_full);
@@ -216,6 +244,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
             ++k_b.i;
           }
           if (kk == NK - 1) umma_commit_ws(&dq_full[qt]);
+          BF_TRACE(12);
           ++q_b.i, ++p_b.i;
         };
         issue_dp(0);
@@ -245,6 +274,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
     uint32_t head_it = 0;
     // pending readouts: key tile (jo, k0) of head (kb, kz); query tile qqt of head (qb, qz)
     bool kv_on = false, q_on = false;
+    uint32_t kslot = 0;  // P slot of the pending key tile's last step
+    bool rel_pending = false;
+    uint32_t rel_slot = 0;
     int kjo = 0, kk0 = 0, kb = 0, kz = 0, qqt = 0, qd = 0, qrow = 0, qb = 0, qz = 0;
     uint32_t qphase = 0;
     auto read_kv = [&](float* dvv, float* dkv) {
@@ -262,6 +294,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
     auto store_kv = [&](float* dvv, float* dkv) {
 #pragma unroll
       for (int e = 0; e < 32; ++e) dkv[e] *= g.scale;
+      if (p.kv_tma) {
+        // dV -> atom 0, dK -> atom 1 of the key tile's last P slot (its products are done:
+        // read_kv waited for them), two TMA stores, then the slot goes back to the producer
+        const uint32_t st = smem_u32(smem + BF_OFF_P + kslot * PTILE);
+        st_row32_sw128(st, r, half * 32, dvv);
+        st_row32_sw128(st, r, 64 + half * 32, dkv);
+        fence_proxy_async_smem();
+        bar_epi();
+        if (threadIdx.x == 64) {
+          tma_store_4d(&p.tdv, smem + BF_OFF_P + kslot * PTILE, 0, kk0, kz, kjo * g.B + kb);
+          tma_store_4d(&p.tdk, smem + BF_OFF_P + kslot * PTILE + ATOM, 0, kk0, kz, kjo * g.B + kb);
+          tma_store_commit();
+        }
+        rel_pending = true, rel_slot = kslot;  // slot returns to the producer once the stores have read it
+        kv_on = false;
+        return;
+      }
       const int key = kk0 + r;
       if (key < g.c) {
         const OutView none{nullptr, 0, 0, 0, 0};
@@ -298,9 +347,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
         const float dval = row < g.c ? p.dvec[(int64_t(d * g.B + b) * g.Z + z) * g.c + row] : 0.f;
         const uint32_t ps = pq.slot(BF_P);
         const uint32_t pt = smem_u32(smem + BF_OFF_P + ps * PTILE);
+        BF_TRACE(20);
+        if (kv_on) {  // the finished key tile's dK / dV first: frees the accumulators for this step's P^T dO
+          float dvv[32], dkv[32];
+          read_kv(dvv, dkv);
+          store_kv(dvv, dkv);
+        }
         float dp[64];
         mbar_wait(&rp.full[ps], pq.phase(BF_P));
+        BF_TRACE(21);
         mbar_wait(dp_full, dpq.phase(1));
+        BF_TRACE(22);
         tc_fence_after();
         __syncwarp();
         tmem_ld32(tmem + lane_base + COL_DP + half * 64, dp);
@@ -320,12 +377,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
           for (int e = 0; e < 32; e += 2)
             dsw[cc * 16 + e / 2] = pack_bf16(pv[e] * (dp[cc * 32 + e] - dval), pv[e + 1] * (dp[cc * 32 + e + 1] - dval));
         }
-        if (kv_on) {  // frees dK/dV for this step's P^T dO
-          float dvv[32], dkv[32];
-          read_kv(dvv, dkv);
-          store_kv(dvv, dkv);
-        }
+        BF_TRACE(23);
         mbar_wait(&p_read[ps], pq.phase(BF_P));
+        BF_TRACE(24);
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const uint32_t atom = (half * 64 + cc * 32) >> 6, chunk0 = ((half * 64 + cc * 32) & 63) >> 3;
@@ -337,9 +391,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&ds_full[ps]);
+        BF_TRACE(25);
         ++pq.i;
+        if (rel_pending) {
+          if (threadIdx.x == 64) tma_store_wait_read<0>(), mbar_arrive(&rp.empty[rel_slot]);
+          rel_pending = false;
+        }
         if (q_on) flush_q();
-        if (qt == NQ - 1) kv_on = true, kjo = kk / ntk, kk0 = (kk % ntk) * TK, kb = b, kz = z;
+        if (qt == NQ - 1) kv_on = true, kjo = kk / ntk, kk0 = (kk % ntk) * TK, kb = b, kz = z, kslot = ps;
         if (kk == NK - 1) q_on = true, qqt = qt, qd = d, qrow = row, qb = b, qz = z, qphase = head_it & 1;
       }
     }
@@ -348,6 +407,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
       read_kv(dvv, dkv);
       store_kv(dvv, dkv);
     }
+    if (rel_pending && threadIdx.x == 64) mbar_arrive(&rp.empty[rel_slot]);
+    if (p.kv_tma && threadIdx.x == 64) tma_store_wait_all<0>();
     if (q_on) flush_q();
   }
   tc_fence_before();
@@ -389,7 +450,21 @@ int rsa_bwd_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_vie
   a.accumulate_dq = accumulate_dq;
   a.dkv_bf16 = dkv_dtype == RSA_BF16;
   a.accumulate_dkv = accumulate_dkv;
-  return launch(bwd_fused_kernel, g->batch * g->heads, BF_SMEM, a, stream, "bwd_fused_kernel");
+  a.kv_tma = dkv_dtype == RSA_BF16 && head_map(&a.tdk, dk, g, g->n_org) && head_map(&a.tdv, dv, g, g->n_org);
+  static long long* trace_buf = nullptr;
+  const char* trace_path = getenv("RSA_BF_TRACE");
+  if (trace_path) {
+    if (!trace_buf) cudaMalloc(&trace_buf, 10 * 4096 * sizeof(long long));
+    cudaMemset(trace_buf, 0, 10 * 4096 * sizeof(long long));
+    a.trace = trace_buf;
+  }
+  const int rc = launch(bwd_fused_kernel, g->batch * g->heads, BF_SMEM, a, stream, "bwd_fused_kernel");
+  if (trace_path) {
+    static long long host[10 * 4096];
+    cudaMemcpy(host, trace_buf, sizeof(host), cudaMemcpyDeviceToHost);
+    if (FILE* f = fopen(trace_path, "wb")) fwrite(host, sizeof(host), 1, f), fclose(f);
+  }
+  return rc;
 }
 
 }  // extern "C"

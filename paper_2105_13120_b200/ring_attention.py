@@ -79,12 +79,17 @@ class ProbPanels(list):
     panels works too, at the cost of one staging copy.
     """
 
-    def __init__(self, stacked: torch.Tensor, outputs: torch.Tensor, rowscale: torch.Tensor | None = None):
+    def __init__(self, stacked: torch.Tensor, outputs: torch.Tensor, rowscale: torch.Tensor | None = None,
+                 inputs: dict | None = None):
         super().__init__([None] * stacked.shape[0])
         self.stacked = stacked
         self.outputs = outputs
         self.rowscale = rowscale
         self.panel_shape = tuple(stacked.shape[1:])
+        # device copies of the forward's q / k / v chunks with the identities (object and
+        # in-place version) of the caller's torch chunks: a backward called with the same,
+        # unmodified tensors reuses them instead of uploading again
+        self.inputs = inputs or []
 
     def _get(self, d: int):
         item = list.__getitem__(self, d)
@@ -132,14 +137,36 @@ def _device_of(*lists):
 
 
 def _stack(chunks: list, device) -> torch.Tensor:
-    """Stack per-rank chunks into one contiguous bf16 [N][...] device tensor."""
+    """Stack per-rank chunks into one contiguous bf16 [N][...] device tensor.
+
+    bf16 torch chunks in pinned host memory are copied asynchronously on the
+    current stream; a single device chunk that is already bf16 and contiguous
+    is used in place (a view, no copy)."""
     if isinstance(chunks, ProbPanels) and chunks.stacked.device == device:
         return chunks.stacked
     first = chunks[0]
+    if (len(chunks) == 1 and isinstance(first, torch.Tensor) and first.device == device
+            and first.dtype == torch.bfloat16 and first.is_contiguous()):
+        return first.unsqueeze(0)
     out = torch.empty((len(chunks),) + _shape_of(first), dtype=torch.bfloat16, device=device)
     for d, c in enumerate(chunks):
-        out[d].copy_(ops.to_device(c, device))
+        if isinstance(c, torch.Tensor) and c.dtype == torch.bfloat16:
+            out[d].copy_(c, non_blocking=c.device.type == "cpu" and c.is_pinned())
+        else:
+            out[d].copy_(ops.to_device(c, device))
     return out
+
+
+def _chunk_key(chunks):
+    """Identity of a list of torch chunks (objects + in-place version counters), or None."""
+    if not all(isinstance(c, torch.Tensor) for c in chunks):
+        return None
+    return tuple((c, c._version) for c in chunks)
+
+
+def _same_chunks(key, chunks) -> bool:
+    return key is not None and len(key) == len(chunks) and all(
+        c is k and c._version == ver for (k, ver), c in zip(key, chunks))
 
 
 def _chunk_elements(cfg: AttentionConfig) -> int:
@@ -204,9 +231,10 @@ def ring_attention_forward(q_chunks, k_chunks, v_chunks, cfg: AttentionConfig, *
     dev = _device_of(q_chunks, k_chunks, v_chunks)
     q, k, v = (_stack(x, dev) for x in (q_chunks, k_chunks, v_chunks))
     out, panel, rowscale, _ = _forward_checked(q, k, v, path)
+    saved = [(_chunk_key(c), t) for c, t in ((q_chunks, q), (k_chunks, k), (v_chunks, v))]
     return RingAttentionForward(
         outputs=[out[d] for d in range(cfg.num_devices)],
-        probs=ProbPanels(panel, out, rowscale),
+        probs=ProbPanels(panel, out, rowscale, saved),
         ledger=forward_ledger(cfg),
     )
 
@@ -228,7 +256,16 @@ def ring_attention_backward(q_chunks, k_chunks, v_chunks, probs, grad_chunks, cf
         raise StateError("ring_attention_backward needs the probability panels saved by ring_attention_forward")
     probs = _check_chunks("probs", probs, cfg, cfg.panel_shape())
     dev = _device_of(q_chunks, k_chunks, v_chunks, grad_chunks, probs)
-    q, k, v, g = (_stack(x, dev) for x in (q_chunks, k_chunks, v_chunks, grad_chunks))
+    saved = probs.inputs if isinstance(probs, ProbPanels) else []
+
+    def stack_or_saved(chunks):
+        for key, t in saved:
+            if t.device == dev and _same_chunks(key, chunks):
+                return t
+        return _stack(chunks, dev)
+
+    q, k, v = (stack_or_saved(x) for x in (q_chunks, k_chunks, v_chunks))
+    g = _stack(grad_chunks, dev)
     panel = _stack(probs, dev)
     own = isinstance(probs, ProbPanels) and panel is probs.stacked
     outputs = probs.outputs if own else None

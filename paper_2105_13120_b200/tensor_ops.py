@@ -59,7 +59,8 @@ def to_device(x, device=None, dtype=torch.bfloat16) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         if x.dtype == torch.float64:
             x = x.to(torch.float32)
-        return x.to(device=device, dtype=dtype)
+        # pinned host memory: asynchronous on the current stream (callers may overlap layers on streams)
+        return x.to(device=device, dtype=dtype, non_blocking=x.device.type == "cpu" and x.is_pinned())
     arr = np.asarray(x)
     if arr.dtype != np.float32:
         arr = arr.astype(np.float32)

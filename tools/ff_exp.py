@@ -33,3 +33,20 @@ if os.environ.get("TRACE_OUT"):
     engine.forward(q, k, v, path="fused", out=out, panel=panel, rowscale=rs)
     torch.cuda.synchronize()
     del os.environ["RSA_FF_TRACE"]
+
+if os.environ.get("BF_TRACE_OUT"):
+    out2, panel2, rs2, _ = engine.forward(q, k, v, path="fused")
+    for _ in range(2):
+        engine.backward(q, k, v, panel2, dO, outputs=out2, rowscale=rs2, path="fused")
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        engine.backward(q, k, v, panel2, dO, outputs=out2, rowscale=rs2, path="fused")
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"bwd (rowdot + bwd_fused): {e0.elapsed_time(e1) / 10 * 1e3:.1f} us", flush=True)
+    os.environ["RSA_BF_TRACE"] = os.environ["BF_TRACE_OUT"]
+    engine.backward(q, k, v, panel2, dO, outputs=out2, rowscale=rs2, path="fused")
+    torch.cuda.synchronize()
+    del os.environ["RSA_BF_TRACE"]
