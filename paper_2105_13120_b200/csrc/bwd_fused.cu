@@ -252,10 +252,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
         for (int t = 0; t < T; ++t) {
           const bool next = t + 1 < T;
           const bool new_kt = next && (t + 1) % NQ == 0;
-          if (next) issue_dp(t + 1);
-          if (next && !new_kt) issue_dv(t + 1);
+          if (next && !new_kt) issue_dp(t + 1), issue_dv(t + 1);
           issue_b(t);
-          if (new_kt) issue_dv(t + 1);  // its dV overwrites the key tile just finished: after acc_empty
+          // key-tile boundary: the finished tile's dK products go first, so the epilogue's
+          // dK/dV readout (which frees the accumulators for the next dV) waits the least
+          if (new_kt) issue_dp(t + 1), issue_dv(t + 1);
         }
       }
     }
