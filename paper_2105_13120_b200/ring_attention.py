@@ -130,6 +130,10 @@ def _check_chunks(name: str, chunks, cfg: AttentionConfig, expect: tuple) -> lis
 
 def _device_of(*lists):
     for lst in lists:
+        if isinstance(lst, ProbPanels):  # never materialise the panels just to find the device
+            if lst.stacked.is_cuda:
+                return lst.stacked.device
+            continue
         for x in lst:
             if isinstance(x, torch.Tensor) and x.is_cuda:
                 return x.device

@@ -389,3 +389,14 @@ def test_factored_flag_clear_on_ordinary_inputs(rsa):
     res = engine.forward(tq, tk, tv, path="fused")
     torch.cuda.synchronize()
     assert int(res.flag.item()) == 0 and res.rowscale is not None
+
+
+def test_backward_does_not_materialise_saved_panels(rsa):
+    """Passing fwd.probs back hands the factored panel to the kernels; the
+    per-rank probabilities are only built when the caller looks at them."""
+    pkg, ra = rsa
+    b, z, seq, a, n = 1, 2, 256, 64, 2
+    q, k, v, g = _inputs(b, z, seq, a, seed=5)
+    _, fwd, _ = _run(pkg, ra, q, k, v, g, n, "fused")
+    assert all(list.__getitem__(fwd.probs, d) is None for d in range(n))
+    assert fwd.probs[1].dtype == torch.float32 and list.__getitem__(fwd.probs, 1) is not None
