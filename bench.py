@@ -83,7 +83,7 @@ def config_obj(args, n):
 # ------------------------------------------------------------------ clocks
 
 class ClockSampler:
-    """Samples SM clock and throttle reasons via NVML every 100 ms."""
+    """Samples SM clock and throttle reasons via NVML every 5 ms."""
 
     NAMES = {
         0x1: "gpu_idle", 0x2: "applications_clocks", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
@@ -115,7 +115,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.005)
 
     def __enter__(self):
         if self.nv:
@@ -195,6 +195,15 @@ def peaks():
         return json.loads(PEAKS_FILE.read_text())
     except Exception:
         return {}
+
+
+def traffic_of(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture."""
+    try:
+        t = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+        return t["bytes_per_launch"].get(kernel)
+    except Exception:
+        return None
 
 
 def kernel_model(name, n, b, z, c, seq, a):
@@ -299,7 +308,7 @@ def ours(args):
         roof = {"bound": "tensor", "achieved": flops / per_launch_s / 1e12, "peak": tc, "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["kernel"] = dom
-    roof["traffic"] = None
+    roof["traffic"] = traffic_of(dom)
     roof["peak_source"] = "MEASURED_PEAKS.json" if pk else "fallback (B200_PROFILING.md)"
     kernels = {}
     step_kernel_ms = sum(shares.values()) / max(1, min(args.steps, 3))

@@ -45,6 +45,7 @@ _LAZY = {
     "ring_attention_forward": "ring_attention",
     "ring_attention_backward": "ring_attention",
     "sequence_parallel_attention": "ring_attention",
+    "sequence_parallel_attention_backward": "ring_attention",
     "SparseRingForward": "sparse_attention",
     "sparse_ring_attention_forward": "sparse_attention",
     "split_projection_columns": "sparse_attention",

@@ -42,6 +42,7 @@ __all__ = [
     "ring_attention_forward",
     "ring_attention_backward",
     "sequence_parallel_attention",
+    "sequence_parallel_attention_backward",
     "ProbPanels",
 ]
 
@@ -286,6 +287,31 @@ def ring_attention_backward(q_chunks, k_chunks, v_chunks, probs, grad_chunks, cf
     )
 
 
+def _layer_weights(weights, cfg: AttentionConfig, dev):
+    h, za = cfg.hidden_size, cfg.num_heads * cfg.head_size
+    for name, expect_w in (("wq", (h, za)), ("wk", (h, za)), ("wv", (h, za)), ("wo", (za, h))):
+        if _shape_of(getattr(weights, name)) != expect_w:
+            raise ShapeError(f"{name} has shape {_shape_of(getattr(weights, name))}, expected {expect_w}")
+    return [ops.to_device(getattr(weights, n), dev) for n in ("wq", "wk", "wv", "wo")]
+
+
+def _split_heads(y, n, b, c, z, a):
+    """[N][B][c][Z*A] -> [N][B][Z][c][A] (split_heads per rank, ringseq/tensor_ops.py:93-110)."""
+    return y.view(n, b, c, z, a).permute(0, 1, 3, 2, 4).contiguous()
+
+
+def _merge_heads(t):
+    """[N][B][Z][c][A] -> [N][B][c][Z*A] (merge_heads per rank, ringseq/tensor_ops.py:113-119)."""
+    n, b, z, c, a = t.shape
+    return t.permute(0, 1, 3, 2, 4).reshape(n, b, c, z * a)
+
+
+def _layer_forward(x, ws, cfg: AttentionConfig, path: str):
+    n, b, c, z, a = cfg.num_devices, cfg.batch_size, cfg.chunk_len, cfg.num_heads, cfg.head_size
+    q, k, v = (_split_heads(ops.matmul(x, w, out_dtype=torch.bfloat16), n, b, c, z, a) for w in ws[:3])
+    return q, k, v, _forward_checked(q, k, v, path)
+
+
 def sequence_parallel_attention(x_chunks, weights, cfg: AttentionConfig, *, executor: str | None = None,
                                 path: str = "auto"):
     """Multi-head attention layer on sequence-partitioned (B, L/N, H) inputs.
@@ -296,22 +322,58 @@ def sequence_parallel_attention(x_chunks, weights, cfg: AttentionConfig, *, exec
     resolve_executor(executor)
     expect = (cfg.batch_size, cfg.chunk_len, cfg.hidden_size)
     x_chunks = _check_chunks("x_chunks", x_chunks, cfg, expect)
-    h, za = cfg.hidden_size, cfg.num_heads * cfg.head_size
-    for name, expect_w in (("wq", (h, za)), ("wk", (h, za)), ("wv", (h, za)), ("wo", (za, h))):
-        if _shape_of(getattr(weights, name)) != expect_w:
-            raise ShapeError(f"{name} has shape {_shape_of(getattr(weights, name))}, expected {expect_w}")
     dev = _device_of(x_chunks)
+    ws = _layer_weights(weights, cfg, dev)
     x = _stack(x_chunks, dev)  # [N][B][c][H]
-    wq, wk, wv, wo = (ops.to_device(getattr(weights, n), dev) for n in ("wq", "wk", "wv", "wo"))
-    n, b, c, z, a = cfg.num_devices, cfg.batch_size, cfg.chunk_len, cfg.num_heads, cfg.head_size
+    _, _, _, res = _layer_forward(x, ws, cfg, path)
+    y = ops.matmul(_merge_heads(res.out), ws[3])
+    return [y[d] for d in range(cfg.num_devices)], forward_ledger(cfg)
 
-    def project(w):
-        y = ops.matmul(x, w, out_dtype=torch.bfloat16)  # [N][B][c][Z*A]
-        return y.view(n, b, c, z, a).permute(0, 1, 3, 2, 4).contiguous()  # split_heads per rank
 
-    q, k, v = project(wq), project(wk), project(wv)
-    out = _forward_checked(q, k, v, path).out
-    merged = out.permute(0, 1, 3, 2, 4).reshape(n, b, c, z * a)  # merge_heads per rank
-    y = ops.matmul(merged, wo)
-    return [y[d] for d in range(n)], forward_ledger(cfg)
+def sequence_parallel_attention_backward(x_chunks, weights, cfg: AttentionConfig, grad_chunks, *,
+                                         executor: str | None = None, path: str = "auto"):
+    """Gradients of ``sequence_parallel_attention`` w.r.t. its inputs and weights.
 
+    The reference ships only the layer's forward (ringseq/ring_attention.py:220-241);
+    this follows its dense oracle ``multi_head_backward`` (ringseq/reference.py:133-174)
+    with the attention stages replaced by the ring backward.  Returns
+    ``(grad_x chunks (B, L/N, H) bf16, AttentionWeights(grad_wq, grad_wk, grad_wv,
+    grad_wo) fp32, ledger)``.  Weight gradients are sums over every rank's rows;
+    on N devices that is one all-reduce of the four replicated matrices, which the
+    ledger charges with the reference's all-reduce convention
+    (ringseq/cluster.py:320-359) on top of the ring backward's traffic.
+    """
+    from .weights import AttentionWeights
+
+    resolve_executor(executor)
+    expect = (cfg.batch_size, cfg.chunk_len, cfg.hidden_size)
+    x_chunks = _check_chunks("x_chunks", x_chunks, cfg, expect)
+    grad_chunks = _check_chunks("grad_chunks", grad_chunks, cfg, expect)
+    dev = _device_of(x_chunks, grad_chunks)
+    ws = _layer_weights(weights, cfg, dev)
+    wq, wk, wv, wo = ws
+    n, b, c, z, a, h = (cfg.num_devices, cfg.batch_size, cfg.chunk_len, cfg.num_heads, cfg.head_size,
+                        cfg.hidden_size)
+    za = z * a
+    x = _stack(x_chunks, dev)     # [N][B][c][H]
+    g = _stack(grad_chunks, dev)  # [N][B][c][H]
+    q, k, v, res = _layer_forward(x, ws, cfg, path)
+    # output projection (ringseq/reference.py:155-160): rows of every rank folded together
+    o2 = _merge_heads(res.out).reshape(-1, za)
+    g2 = g.reshape(-1, h)
+    grad_wo = ops.matmul(o2.transpose(0, 1), g2)
+    grad_o = _split_heads(ops.matmul(g, wo.transpose(0, 1), out_dtype=torch.bfloat16), n, b, c, z, a)
+    dq, dk, dv = engine.backward(q, k, v, res.panel, grad_o, outputs=res.out, rowscale=res.rowscale, path=path)
+    # input projections (ringseq/reference.py:162-173)
+    x2 = x.reshape(-1, h)
+    gq2, gk2, gv2 = (_merge_heads(t).reshape(-1, za) for t in (dq, dk, dv))
+    grad_wq, grad_wk, grad_wv = (ops.matmul(x2.transpose(0, 1), t) for t in (gq2, gk2, gv2))
+    gx = ops.matmul(gq2, wq.transpose(0, 1))
+    ops.matmul(gk2, wk.transpose(0, 1), out=gx, accumulate=True)
+    ops.matmul(gv2, wv.transpose(0, 1), out=gx, accumulate=True)
+    gx = gx.to(torch.bfloat16).view(n, b, c, h)
+    ledger = backward_ledger(cfg)
+    if n > 1:
+        for d in range(n):
+            ledger.record_allreduce(d, 2 * h * za + za * h + h * za)  # wq, wk, wv, wo gradients
+    return [gx[d] for d in range(n)], AttentionWeights(grad_wq, grad_wk, grad_wv, grad_wo), ledger

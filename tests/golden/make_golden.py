@@ -46,6 +46,8 @@ SPARSE_SMALL = [  # (B, Z, L, A, K, N, seed)
     (2, 3, 40, 5, 7, 4, 51),
 ]
 SPARSE_MID = [(1, 2, 256, 64, 64, 2, 61)]
+LAYER_SMALL = [(2, 12, 3, 4, 31)]      # (B, L, Z, A, seed): multi_head_forward / _backward, float64
+LAYER_MID = [(2, 256, 2, 64, 32)]      # bf16-rounded inputs at tensor-core shapes, float32 results
 
 
 def draw(shape, seed, n_tensors, rounded):
@@ -91,6 +93,22 @@ def sparse_case(b, z, seq, a, kp, n, seed, rounded):
     }
 
 
+def layer_case(b, seq, z, a, seed, rounded):
+    """The reference's dense multi-head layer and its backward (ringseq/reference.py:122-174)."""
+    cfg = ringseq.AttentionConfig(batch_size=b, seq_len=seq, hidden_size=z * a,
+                                  num_heads=z, head_size=a, num_devices=1)
+    rng = ringseq.make_rng(seed)
+    x = rng.standard_normal((b, seq, z * a))
+    g = rng.standard_normal((b, seq, z * a))
+    w = ringseq.random_attention_weights(cfg, rng)
+    if rounded:
+        x, g = bf16_round(x), bf16_round(g)
+        w = ringseq.AttentionWeights(*(bf16_round(m) for m in (w.wq, w.wk, w.wv, w.wo)))
+    y = ringseq.multi_head_forward(x, w, cfg)
+    gx, gw = ringseq.multi_head_backward(x, w, cfg, g)
+    return {"y": y, "grad_x": gx, "grad_wq": gw.wq, "grad_wk": gw.wk, "grad_wv": gw.wv, "grad_wo": gw.wo}
+
+
 def main():
     arrays = {}
     for case in RSA_SMALL:
@@ -113,6 +131,12 @@ def main():
         for key, val in res.items():
             arrays["sparse_mid/%s/%s" % ("_".join(map(str, case)), key)] = (
                 val.astype(np.float32) if val.dtype == np.float64 else val)
+    for case in LAYER_SMALL:
+        for key, val in layer_case(*case, rounded=False).items():
+            arrays["layer_small/%s/%s" % ("_".join(map(str, case)), key)] = val
+    for case in LAYER_MID:
+        for key, val in layer_case(*case, rounded=True).items():
+            arrays["layer_mid/%s/%s" % ("_".join(map(str, case)), key)] = val.astype(np.float32)
     out = HERE / "ringseq_golden.npz"
     np.savez_compressed(out, **arrays)
     print(f"wrote {out} ({out.stat().st_size} bytes, {len(arrays)} arrays)")

@@ -261,6 +261,67 @@ def test_layer_wrapper_matches_multi_head_oracle(rsa):
     assert all(t.ring_p2p_elements == 2 * (n - 1) * b * z * (seq // n) * a for t in ledger.devices)
 
 
+def _layer_inputs(b, seq, z, a, seed):
+    """As tests/golden/make_golden.py:layer_case draws them, bf16-rounded."""
+    h = z * a
+    rng = orc.make_rng(seed)
+    x, g = (orc.bf16_round(rng.standard_normal((b, seq, h))) for _ in range(2))
+    s = 1.0 / math.sqrt(h)
+    ws = [orc.bf16_round(rng.standard_normal((h, h)) * s) for _ in range(4)]
+    return x, g, ws
+
+
+# activations pass through extra bf16 roundings (projections, merged heads, dO*r) before
+# the projection GEMMs, so the layer gates are looser than the attention-core gates
+LAYER_REL = 2e-2
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_layer_backward_matches_reference_golden(rsa, golden, n):
+    """sequence_parallel_attention_backward vs the unmodified reference's multi_head_backward
+    (ringseq/reference.py:133-174) on the same bf16 inputs, for 1, 2 and 4 ring ranks."""
+    pkg, ra = rsa
+    cases = golden_cases(golden, "layer_mid")
+    assert cases
+    for case, want in cases.items():
+        b, seq, z, a, seed = (int(t) for t in case.split("_"))
+        x, g, ws = _layer_inputs(b, seq, z, a, seed)
+        cfg = pkg.AttentionConfig(batch_size=b, seq_len=seq, hidden_size=z * a, num_heads=z, head_size=a,
+                                  num_devices=n)
+        w = pkg.AttentionWeights(*ws)
+        y, _ = ra.sequence_parallel_attention(orc.chunks_of(x, n), w, cfg)
+        gx, gw, ledger = ra.sequence_parallel_attention_backward(orc.chunks_of(x, n), w, cfg, orc.chunks_of(g, n))
+        torch.cuda.synchronize()
+        got = {"y": _np(pkg.gather_sequence(y)), "grad_x": _np(pkg.gather_sequence(gx)),
+               "grad_wq": _np(gw.wq), "grad_wk": _np(gw.wk), "grad_wv": _np(gw.wv), "grad_wo": _np(gw.wo)}
+        for key, val in got.items():
+            ref = want[key].astype(np.float64)
+            rel = np.linalg.norm(val - ref) / np.linalg.norm(ref)
+            assert rel <= LAYER_REL, (key, rel)
+        c = seq // n
+        for t in ledger.devices:
+            assert t.ring_p2p_elements == 2 * (n - 1) * b * z * c * a
+        if n > 1:
+            h = z * a
+            want_ar = 2 * (n - 1) * b * z * seq * a * 2 / n + 2 * 4 * h * h * (n - 1) / n
+            assert all(float(t.allreduce_elements) == want_ar for t in ledger.devices)
+
+
+def test_layer_backward_matches_oracle_bench_like(rsa):
+    """BERT-base-like heads (A = 64) at a ragged chunk length, against the float64 oracle."""
+    pkg, ra = rsa
+    b, seq, z, a, n = 1, 384, 3, 64, 2
+    x, g, ws = _layer_inputs(b, seq, z, a, seed=90)
+    cfg = pkg.AttentionConfig(batch_size=b, seq_len=seq, hidden_size=z * a, num_heads=z, head_size=a, num_devices=n)
+    gx, gw, _ = ra.sequence_parallel_attention_backward(orc.chunks_of(x, n), pkg.AttentionWeights(*ws), cfg,
+                                                        orc.chunks_of(g, n))
+    want = orc.multi_head_backward(x, *ws, g, num_heads=z, exact=False)
+    got = [_np(pkg.gather_sequence(gx)), _np(gw.wq), _np(gw.wk), _np(gw.wv), _np(gw.wo)]
+    for name, val, ref in zip(("grad_x", "grad_wq", "grad_wk", "grad_wv", "grad_wo"), got, want):
+        rel = np.linalg.norm(val - ref) / np.linalg.norm(ref)
+        assert rel <= LAYER_REL, (name, rel)
+
+
 # Single-pass backward (rsa_bwd_fused) vs the split rsa_bwd_dkdv + rsa_bwd_dq
 # pair, both against the oracle: every geometry with <= 4 query tiles per head
 # (resident N ranks x ceil(c/128)), including ragged tails and the bench shape.

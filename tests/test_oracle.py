@@ -170,3 +170,56 @@ def test_bf16_round_is_idempotent_and_nearest():
     r = orc.bf16_round(x)
     assert np.array_equal(orc.bf16_round(r), r)
     assert np.max(np.abs(r - x) / np.abs(x)) <= 2.0 ** -8
+
+
+def layer_inputs(b, seq, z, a, seed, rounded=False):
+    """x, grad_out and the weights exactly as tests/golden/make_golden.py:layer_case draws them
+    (ringseq/reference.py:207-216: wq, wk, wv ~ N(0,1)/sqrt(H) of (H, Z*A), wo of (Z*A, H))."""
+    h = z * a
+    rng = orc.make_rng(seed)
+    x = rng.standard_normal((b, seq, h))
+    g = rng.standard_normal((b, seq, h))
+    s = 1.0 / math.sqrt(h)
+    ws = [rng.standard_normal(shape) * s for shape in ((h, h), (h, h), (h, h), (h, h))]
+    if rounded:
+        x, g = orc.bf16_round(x), orc.bf16_round(g)
+        ws = [orc.bf16_round(w) for w in ws]
+    return x, g, ws
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_layer_forward_backward_match_reference_goldens(golden, exact):
+    """multi_head_forward / multi_head_backward (ringseq/reference.py:122-174)."""
+    cases = golden_cases(golden, "layer_small")
+    assert cases
+    for case, want in cases.items():
+        b, seq, z, a, seed = _parse(case)
+        x, g, ws = layer_inputs(b, seq, z, a, seed)
+        y = orc.multi_head_forward(x, *ws, num_heads=z, exact=exact)
+        gx, gwq, gwk, gwv, gwo = orc.multi_head_backward(x, *ws, g, num_heads=z, exact=exact)
+        got = {"y": y, "grad_x": gx, "grad_wq": gwq, "grad_wk": gwk, "grad_wv": gwv, "grad_wo": gwo}
+        for key, val in got.items():
+            if exact:
+                assert np.array_equal(val, want[key]), (case, key)
+            else:
+                assert np.max(np.abs(val - want[key])) <= 1e-12, (case, key)
+
+
+def test_layer_backward_finite_differences():
+    """grad_x and grad_wq of multi_head_backward against central differences of
+    multi_head_forward (the reference's own gradient check style, tests/test_acceptance.py:99-147)."""
+    b, seq, z, a = 1, 6, 2, 3
+    x, g, ws = layer_inputs(b, seq, z, a, seed=8)
+    gx, gwq, _, _, _ = orc.multi_head_backward(x, *ws, g, num_heads=z, exact=False)
+    loss = lambda xx, wq: float(np.sum(orc.multi_head_forward(xx, wq, *ws[1:], num_heads=z, exact=False) * g))  # noqa: E731
+    eps = 1e-6
+    for idx in [(0, 0, 0), (0, 3, 5), (0, 5, 2)]:
+        d = np.zeros_like(x)
+        d[idx] = eps
+        fd = (loss(x + d, ws[0]) - loss(x - d, ws[0])) / (2 * eps)
+        assert abs(fd - gx[idx]) <= 1e-6 * max(1.0, abs(fd))
+    for idx in [(0, 0), (4, 1), (5, 5)]:
+        d = np.zeros_like(ws[0])
+        d[idx] = eps
+        fd = (loss(x, ws[0] + d) - loss(x, ws[0] - d)) / (2 * eps)
+        assert abs(fd - gwq[idx]) <= 1e-6 * max(1.0, abs(fd))
