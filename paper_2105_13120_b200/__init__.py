@@ -48,6 +48,8 @@ _LAZY = {
     "sequence_parallel_attention_backward": "ring_attention",
     "SparseRingForward": "sparse_attention",
     "sparse_ring_attention_forward": "sparse_attention",
+    "sparse_ring_attention_backward": "sparse_attention",
+    "SparseRingBackward": "sparse_attention",
     "split_projection_columns": "sparse_attention",
     "full_length_dims": "sparse_attention",
     "AttentionWeights": "weights",

@@ -35,7 +35,8 @@ from .cluster import CommLedger, resolve_executor
 from .config import SparseAttentionConfig
 from .errors import ShapeError
 
-__all__ = ["SparseRingForward", "split_projection_columns", "sparse_ring_attention_forward", "full_length_dims"]
+__all__ = ["SparseRingForward", "SparseRingBackward", "split_projection_columns", "sparse_ring_attention_forward",
+           "sparse_ring_attention_backward", "full_length_dims"]
 
 
 @dataclass
@@ -44,6 +45,18 @@ class SparseRingForward:
 
     outputs: list
     shape_logs: list
+    ledger: CommLedger
+
+
+@dataclass
+class SparseRingBackward:
+    """Per-rank (B, Z, L/N, A) gradients of q/k/v, the (K, L) projection gradients, ledger."""
+
+    grad_q: list
+    grad_k: list
+    grad_v: list
+    grad_key_proj: torch.Tensor
+    grad_value_proj: torch.Tensor
     ledger: CommLedger
 
 
@@ -72,39 +85,38 @@ def _stack(chunks, device) -> torch.Tensor:
     return out
 
 
-def sparse_ring_attention_forward(q_chunks, k_chunks, v_chunks, weights, cfg: SparseAttentionConfig, *,
-                                  executor: str | None = None) -> SparseRingForward:
-    """Projected attention on sequence-partitioned (B, Z, L/N, A) chunks (ringseq/sparse_attention.py:74-133)."""
-    resolve_executor(executor)
+def _device(chunks):
+    for x in chunks:
+        if isinstance(x, torch.Tensor) and x.is_cuda:
+            return x.device
+    return ops.default_device()
+
+
+def _check_inputs(name_chunks, weights, cfg: SparseAttentionConfig):
     base = cfg.base
     n = base.num_devices
     expect = base.chunk_shape()
-    q_chunks, k_chunks, v_chunks = list(q_chunks), list(k_chunks), list(v_chunks)
-    for name, chunks in (("q_chunks", q_chunks), ("k_chunks", k_chunks), ("v_chunks", v_chunks)):
+    out = []
+    for name, chunks in name_chunks:
+        chunks = list(chunks)
         if len(chunks) != n:
             raise ShapeError(f"{name}: got {len(chunks)} chunks for {n} devices")
         for i, c in enumerate(chunks):
             if _shape(c) != expect:
                 raise ShapeError(f"{name}[{i}] has shape {_shape(c)}, expected {expect}")
+        out.append(chunks)
     proj_shape = (cfg.proj_dim, base.seq_len)
     kp_shape, vp_shape = _shape(weights.key_proj), _shape(weights.value_proj)
     if kp_shape != proj_shape or vp_shape != proj_shape:
         raise ShapeError(f"projection shapes {kp_shape}/{vp_shape}, expected {proj_shape}")
+    return out
 
-    dev = None
-    for x in q_chunks + k_chunks + v_chunks:
-        if isinstance(x, torch.Tensor) and x.is_cuda:
-            dev = x.device
-            break
-    dev = dev or ops.default_device()
-    b, z, c, a = expect
-    kdim = cfg.proj_dim
-    q, k, v = _stack(q_chunks, dev), _stack(k_chunks, dev), _stack(v_chunks, dev)
-    e = ops.to_device(weights.key_proj, dev)  # (K, L) bf16
-    f = ops.to_device(weights.value_proj, dev)
-    # Partial projections of each rank's chunk with its own column block,
-    # accumulated over ranks in fp32 (the ring-accumulate / all-reduce).
-    k_low = torch.empty((b, z, kdim, a), dtype=torch.float32, device=dev)
+
+def _low_rank_forward(q, k, v, e, f, kdim):
+    """K' = sum_d E_d K_d, V' = sum_d F_d V_d (fp32 accumulation over ranks -- the
+    ring-accumulate / all-reduce), then P = softmax(Q K'^T / sqrt(A)) per rank."""
+    n, b, z, c, a = q.shape
+    k_low = torch.empty((b, z, kdim, a), dtype=torch.float32, device=q.device)
     v_low = torch.empty_like(k_low)
     for d in range(n):
         cols = slice(d * c, (d + 1) * c)
@@ -112,9 +124,28 @@ def sparse_ring_attention_forward(q_chunks, k_chunks, v_chunks, weights, cfg: Sp
         ops.matmul(f[:, cols], v[d], out=v_low, accumulate=d > 0)
     k_low16 = k_low.to(torch.bfloat16)
     v_low16 = v_low.to(torch.bfloat16)
-    scale = 1.0 / math.sqrt(a)
     scores = ops.matmul(q, k_low16.transpose(-1, -2))  # [N][B][Z][c][K] fp32
-    probs = ops.softmax_rows(scores, scale=scale, out_dtype=torch.bfloat16)  # NumericError on non-finite
+    probs = ops.softmax_rows(scores, scale=1.0 / math.sqrt(a), out_dtype=torch.bfloat16)  # NumericError
+    return k_low16, v_low16, probs
+
+
+def sparse_ring_attention_forward(q_chunks, k_chunks, v_chunks, weights, cfg: SparseAttentionConfig, *,
+                                  executor: str | None = None) -> SparseRingForward:
+    """Projected attention on sequence-partitioned (B, Z, L/N, A) chunks (ringseq/sparse_attention.py:74-133)."""
+    resolve_executor(executor)
+    base = cfg.base
+    n = base.num_devices
+    expect = base.chunk_shape()
+    q_chunks, k_chunks, v_chunks = _check_inputs(
+        (("q_chunks", q_chunks), ("k_chunks", k_chunks), ("v_chunks", v_chunks)), weights, cfg)
+
+    dev = _device(q_chunks + k_chunks + v_chunks)
+    b, z, c, a = expect
+    kdim = cfg.proj_dim
+    q, k, v = _stack(q_chunks, dev), _stack(k_chunks, dev), _stack(v_chunks, dev)
+    e = ops.to_device(weights.key_proj, dev)  # (K, L) bf16
+    f = ops.to_device(weights.value_proj, dev)
+    k_low16, v_low16, probs = _low_rank_forward(q, k, v, e, f, kdim)
     out = ops.matmul(probs, v_low16, out_dtype=torch.bfloat16)  # [N][B][Z][c][A]
 
     chunk, low, rows = (b, z, c, a), (b, z, kdim, a), (b, z, c, kdim)
@@ -127,6 +158,66 @@ def sparse_ring_attention_forward(q_chunks, k_chunks, v_chunks, weights, cfg: Sp
         if n > 1:
             ledger.record_ring_send(d, 2 * (n - 1) * b * z * kdim * a)
     return SparseRingForward(outputs=[out[d] for d in range(n)], shape_logs=logs, ledger=ledger)
+
+
+def sparse_ring_attention_backward(q_chunks, k_chunks, v_chunks, weights, cfg: SparseAttentionConfig,
+                                   grad_chunks, *, executor: str | None = None) -> SparseRingBackward:
+    """Gradients of ``sparse_ring_attention_forward`` (the reference
+    ships the forward only, ringseq/sparse_attention.py:74-133).
+
+    Chain rule through the forward, per rank d with its projection column blocks E_d, F_d:
+    dV' = sum_d P_d^T dO_d and dK' = sum_d dS_d^T Q_d (the two cross-rank sums -- one
+    all-reduce of [dK'; dV'] across GPUs, the same size as the forward's), then the local
+    dQ_d = dS_d K', dK_d = E_d^T dK', dV_d = F_d^T dV', and the projection gradients
+    dE[:, d-block] = sum_{b,z} dK' K_d^T, dF[:, d-block] = sum_{b,z} dV' V_d^T.
+    dS = P (dO V'^T - rowsum) / sqrt(A) is rsa_softmax_bwd.  Every product is an
+    sm_100a GEMM (tensor_ops.matmul).  The ledger charges the forward's ring-accumulate
+    convention for the two gradient sums: 2(N-1)*B*Z*K*A elements per rank.
+    """
+    resolve_executor(executor)
+    base = cfg.base
+    n = base.num_devices
+    q_chunks, k_chunks, v_chunks, grad_chunks = _check_inputs(
+        (("q_chunks", q_chunks), ("k_chunks", k_chunks), ("v_chunks", v_chunks), ("grad_chunks", grad_chunks)),
+        weights, cfg)
+    dev = _device(q_chunks + k_chunks + v_chunks + grad_chunks)
+    b, z, c, a = base.chunk_shape()
+    kdim = cfg.proj_dim
+    q, k, v, g = (_stack(x, dev) for x in (q_chunks, k_chunks, v_chunks, grad_chunks))
+    e = ops.to_device(weights.key_proj, dev)
+    f = ops.to_device(weights.value_proj, dev)
+    k_low16, v_low16, probs = _low_rank_forward(q, k, v, e, f, kdim)
+    # cross-rank sums (fp32 over ranks in ascending order)
+    d_vlow = torch.empty((b, z, kdim, a), dtype=torch.float32, device=dev)
+    for d in range(n):
+        ops.matmul(probs[d].transpose(-1, -2), g[d], out=d_vlow, accumulate=d > 0)
+    dp = ops.matmul(g, v_low16.transpose(-1, -2))  # [N][B][Z][c][K] fp32
+    ds = ops.softmax_backward(probs, dp, 1.0 / math.sqrt(a), out_dtype=torch.bfloat16)
+    dq = ops.matmul(ds, k_low16, out_dtype=torch.bfloat16)
+    d_klow = torch.empty_like(d_vlow)
+    for d in range(n):
+        ops.matmul(ds[d].transpose(-1, -2), q[d], out=d_klow, accumulate=d > 0)
+    d_klow16, d_vlow16 = d_klow.to(torch.bfloat16), d_vlow.to(torch.bfloat16)
+    dk = torch.empty_like(q)
+    dv = torch.empty_like(q)
+    grad_e = torch.empty((kdim, base.seq_len), dtype=torch.float32, device=dev)
+    grad_f = torch.empty_like(grad_e)
+    # (K, B*Z*A) views of the low-rank gradients for the shared-projection gradients
+    dk_flat = d_klow16.permute(2, 0, 1, 3).reshape(kdim, b * z * a)
+    dv_flat = d_vlow16.permute(2, 0, 1, 3).reshape(kdim, b * z * a)
+    for d in range(n):
+        cols = slice(d * c, (d + 1) * c)
+        ops.matmul(e[:, cols].transpose(0, 1), d_klow16, out=dk[d])
+        ops.matmul(f[:, cols].transpose(0, 1), d_vlow16, out=dv[d])
+        ops.matmul(dk_flat, k[d].transpose(-1, -2).reshape(b * z * a, c), out=grad_e[:, cols])
+        ops.matmul(dv_flat, v[d].transpose(-1, -2).reshape(b * z * a, c), out=grad_f[:, cols])
+    ledger = CommLedger(n)
+    if n > 1:
+        for d in range(n):
+            ledger.record_ring_send(d, 2 * (n - 1) * b * z * kdim * a)
+    return SparseRingBackward(grad_q=[dq[d] for d in range(n)], grad_k=[dk[d] for d in range(n)],
+                              grad_v=[dv[d] for d in range(n)], grad_key_proj=grad_e, grad_value_proj=grad_f,
+                              ledger=ledger)
 
 
 def full_length_dims(shape_logs, cfg: SparseAttentionConfig) -> list:

@@ -114,3 +114,26 @@ def test_errors_and_split(sp):
         spm.sparse_ring_attention_forward(chunks, bad, chunks, pkg.SparseWeights(np.zeros((3, 8)), np.zeros((3, 8))), cfg)
     logs = [[(1, 1, 10, 2), (1, 1, 40, 2)], [(4, 10)]]
     assert spm.full_length_dims(logs, _cfg(pkg, 1, 1, 40, 2, 4, 4)) == [(1, 1, 40, 2)]
+
+
+@pytest.mark.parametrize("shape", [(1, 2, 256, 64, 64, 1), (2, 2, 256, 64, 64, 2), (1, 3, 512, 64, 128, 4),
+                                   (2, 3, 40, 5, 7, 4)])
+def test_backward_matches_oracle(sp, shape):
+    """sparse_ring_attention_backward vs the oracle's chain rule (linformer_backward, pinned by
+    finite differences in tests/test_oracle.py) on the same bf16 inputs; every input's gradient."""
+    pkg, spm = sp
+    b, z, seq, a, kp, n = shape
+    q, k, v, e, f = _draw(b, z, seq, a, kp, seed=sum(shape))
+    g = orc.bf16_round(orc.make_rng(7).standard_normal((b, z, seq, a)))
+    cfg = _cfg(pkg, b, z, seq, a, kp, n)
+    ch = lambda x: orc.chunks_of(x, n)  # noqa: E731
+    res = spm.sparse_ring_attention_backward(ch(q), ch(k), ch(v), pkg.SparseWeights(e, f), cfg, ch(g))
+    torch.cuda.synchronize()
+    want = orc.linformer_backward(q, k, v, e, f, g, exact=False)
+    cat = lambda xs: np.concatenate([_np(x) for x in xs], axis=-2)  # noqa: E731
+    got = [cat(res.grad_q), cat(res.grad_k), cat(res.grad_v), _np(res.grad_key_proj), _np(res.grad_value_proj)]
+    for name, val, ref in zip(("dq", "dk", "dv", "dE", "dF"), got, want):
+        rel = np.linalg.norm(val - ref) / np.linalg.norm(ref)
+        assert rel <= 2e-2, (name, rel)
+    per_rank = 2 * (n - 1) * b * z * kp * a
+    assert all(t.ring_p2p_elements == per_rank for t in res.ledger.devices)

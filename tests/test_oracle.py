@@ -223,3 +223,29 @@ def test_layer_backward_finite_differences():
         d[idx] = eps
         fd = (loss(x, ws[0] + d) - loss(x, ws[0] - d)) / (2 * eps)
         assert abs(fd - gwq[idx]) <= 1e-6 * max(1.0, abs(fd))
+
+
+def test_linformer_backward_finite_differences():
+    """linformer_backward against central differences of linformer_forward (every input,
+    including the shared projections)."""
+    b, z, seq, a, kp = 2, 2, 12, 3, 5
+    rng = orc.make_rng(71)
+    q, k, v, g = (rng.standard_normal((b, z, seq, a)) for _ in range(4))
+    e, f = (rng.standard_normal((kp, seq)) / math.sqrt(seq) for _ in range(2))
+    grads = orc.linformer_backward(q, k, v, e, f, g, exact=False)
+    args = [q, k, v, e, f]
+
+    def loss(xs):
+        return float(np.sum(orc.linformer_forward(*xs, exact=False) * g))
+
+    eps = 1e-6
+    for which, grad in enumerate(grads):
+        x = args[which]
+        for flat in (0, x.size // 2, x.size - 1):
+            idx = np.unravel_index(flat, x.shape)
+            d = np.zeros_like(x)
+            d[idx] = eps
+            plus = [y + d if i == which else y for i, y in enumerate(args)]
+            minus = [y - d if i == which else y for i, y in enumerate(args)]
+            fd = (loss(plus) - loss(minus)) / (2 * eps)
+            assert abs(fd - grad[idx]) <= 1e-6 * max(1.0, abs(fd)), (which, idx, fd, grad[idx])
