@@ -130,7 +130,7 @@ inline bool head_map(CUtensorMap* m, const rsa_view& v, const rsa_geom* g, int n
 }
 
 // [rank][b][z][row][col], col = blk * c + key: 5-D (key, blk, row, z, b*rank).
-inline bool panel_map(CUtensorMap* m, const rsa_view& v, const rsa_geom* g, int nrank) {
+inline bool panel_map(CUtensorMap* m, const rsa_view& v, const rsa_geom* g, int nrank, uint32_t box_rows = TR) {
   if (!v.ptr || !aligned16(v.ptr)) return fail(RSA_ERR_UNSUPPORTED, "fused: panel not 16-byte aligned"), false;
   if (nrank > 1 && g->batch > 1 && v.s_rank != int64_t(g->batch) * v.s_b)
     return fail(RSA_ERR_UNSUPPORTED, "fused: panel rank stride must equal B * batch stride"), false;
@@ -141,7 +141,7 @@ inline bool panel_map(CUtensorMap* m, const rsa_view& v, const rsa_geom* g, int 
   uint64_t dims[5] = {uint64_t(g->chunk), uint64_t(nblk), uint64_t(g->chunk), uint64_t(g->heads),
                       uint64_t(g->batch) * nrank};
   uint64_t str[4] = {uint64_t(g->chunk) * 2, uint64_t(v.s_row) * 2, uint64_t(v.s_z) * 2, uint64_t(sb) * 2};
-  uint32_t box[5] = {64, 1, TR, 1, 1};
+  uint32_t box[5] = {64, 1, box_rows, 1, 1};
   return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, v.ptr, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 

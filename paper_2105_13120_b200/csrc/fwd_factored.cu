@@ -13,10 +13,8 @@
 // the reference point, so any per-row m_ref works as long as 2^(s*sl - m_ref)
 // neither overflows nor flushes the row: here m_ref is the max of the row's
 // FIRST key tile (exact, read once), and every later tile reuses it.  The row
-// sum comes from the tensor core -- the P~ V product runs with N = 80 whose
-// last 16 B-operand columns read a constant block of bf16 ones, so TMEM
-// column 64 of the O accumulator is sum_k P~[row, k] over exactly the rounded
-// values written to the panel.  A row whose true max exceeds m_ref by more
+// sum is taken over exactly the rounded bf16 values written to the panel, so
+// r * P~ sums to one.  A row whose true max exceeds m_ref by more
 // than 2^FF_HEADROOM (never for real attention logits: that is a probability
 // ratio of 2^96 between the first tile's best key and the row's best key)
 // sets bit 1 of *flag and the caller recomputes with the two-pass kernel
@@ -27,13 +25,14 @@
 // contiguous unit ranges so consecutive units mostly share the head and K
 // stays resident when a row's T <= FF_KST key tiles fit.  18 warps:
 //   warp 0        TMA producer (one lane)
-//   warp 1        tcgen05.mma issuer (elect.sync); owns the TMEM allocation
+//   warp 1        tcgen05.mma issuer of S = Q K^T (elect.sync); owns the TMEM allocation
+//   warp 18       tcgen05.mma issuer of O~ += P~ [V | 1]
 //   warps 2..17   two epilogue groups of 8 warps, group g = (w - 2) / 8 owns
 //                 query tile g of the unit; warp w reads TMEM lanes
 //                 32 * (w % 4).. (its tile rows) and column half ((w-2)/4) % 2
 // TMEM: group g owns columns [256g, 256g + 256): S at +0 (128 columns; the
 // epilogue moves it to registers at once, so one buffer suffices) and the
-// O~ accumulator at +128 (80 columns).
+// O~ accumulator at +128 (64 columns).
 #include <cstdio>
 #include <cstdlib>
 
@@ -43,7 +42,7 @@ namespace rsa {
 namespace {
 
 struct FfArgs {
-  CUtensorMap tq, tk, tv, tp, to;
+  CUtensorMap tq, tk, tv, tp, to;  // tp: 64 keys x 32 rows boxes (one per epilogue warp)
   Geo g;
   float sl;  // scale * log2(e)
   int* flag;
@@ -53,28 +52,33 @@ struct FfArgs {
 
 constexpr int FF_GROUPS = 2;
 constexpr int FF_EPI_WARPS = 8 * FF_GROUPS;
-constexpr int FF_THREADS = 64 + 32 * FF_EPI_WARPS;  // 576
-constexpr int FF_KST = 4, FF_VST = 2;
-constexpr int PV_N = HD + 16;          // O columns + 16 row-sum columns
-constexpr float FF_HEADROOM = 96.f;    // max (row max - m_ref) * sl before the two-pass fallback
+constexpr int FF_PV_WARP = 2 + FF_EPI_WARPS;            // 18: issues the P~ V products
+constexpr int FF_THREADS = 32 * (FF_PV_WARP + 1);       // 608
+#ifndef FF_ONES
+#define FF_ONES 1  // row sums from the tensor core (ones block next to V) instead of FADDs
+#endif
+#ifndef FF_EXP
+#define FF_EXP 0   // 0: one exp2 in four on the FMA pipe, 1: all MUFU, 2: ex2.approx.f16x2 pairs
+#endif
+#ifndef FF_ABSMAX
+#define FF_ABSMAX 1  // tiles after the first: max|s| only (finite check + headroom bound)
+#endif
+constexpr int FF_KST = 4, FF_VST = FF_ONES ? 2 : 3;
+constexpr int PV_N = FF_ONES ? HD + 16 : HD;  // O columns (+ 16 row-sum columns)
+constexpr float FF_HEADROOM = 96.f;
+    // max (row max - m_ref) * sl before the two-pass fallback
 constexpr uint32_t FF_OFF_Q = 0;                                  // one tile per group
 constexpr uint32_t FF_OFF_K = FF_OFF_Q + FF_GROUPS * TILE;
 constexpr uint32_t FF_OFF_V = FF_OFF_K + FF_KST * TILE;
-constexpr uint32_t FF_OFF_ONES = FF_OFF_V + FF_VST * TILE;        // 128 rows x 128 B of bf16 1.0
-constexpr uint32_t FF_OFF_P = FF_OFF_ONES + TILE;                 // one P~ tile per group
-constexpr uint32_t FF_OFF_X = FF_OFF_P + FF_GROUPS * PTILE;       // m_ref exchange [group][parity][256]
-constexpr uint32_t FF_OFF_BAR = FF_OFF_X + FF_GROUPS * 2 * 256 * 4;
+constexpr uint32_t FF_OFF_ONES = FF_OFF_V + FF_VST * TILE;        // 128 rows x 128 B of bf16 1.0 (FF_ONES)
+constexpr uint32_t FF_OFF_P = FF_OFF_ONES + (FF_ONES ? TILE : 0);  // one P~ tile per group
+constexpr uint32_t FF_OFF_X = FF_OFF_P + FF_GROUPS * PTILE;       // m_ref [group][parity][256], l [group][256]
+constexpr uint32_t FF_OFF_BAR = FF_OFF_X + FF_GROUPS * 3 * 256 * 4;
 constexpr uint32_t FF_SMEM = FF_OFF_BAR + 512 + 1024;
 static_assert(FF_SMEM <= 232448, "fwd_factored smem over the sm_100 per-CTA limit");
 
 __device__ __forceinline__ void bar_named(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
-  uint32_t r;
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
-  return __uint_as_float(r);
 }
 
 #define FF_TRACE(ev)                                                                                          \
@@ -95,6 +99,23 @@ __device__ __forceinline__ Unit unit_of(int u, int units_per_head, int nq) {
   return r;
 }
 
+// max |v| over the first `nvalid` of 32 values (NaN-propagating): one 3-input
+// FMNMX per two scores.  Finite iff every score is finite.
+__device__ __forceinline__ void absmax32(const float* v, int nvalid, float& mx_out) {
+  if (nvalid >= 32) {
+    float mx[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) mx[e] = fabsf(v[e]);
+#pragma unroll
+    for (int e = 4; e < 32; ++e) mx[e & 3] = max_nan(mx[e & 3], fabsf(v[e]));
+    mx_out = max_nan(mx_out, max_nan(max_nan(mx[0], mx[1]), max_nan(mx[2], mx[3])));
+  } else {
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if (e < nvalid) mx_out = max_nan(mx_out, fabsf(v[e]));
+  }
+}
+
 // Max and min of the first `nvalid` of 32 values (NaN-propagating).
 __device__ __forceinline__ void minmax32(const float* v, int nvalid, float& mx_out, float& mi_out) {
   if (nvalid >= 32) {
@@ -112,14 +133,28 @@ __device__ __forceinline__ void minmax32(const float* v, int nvalid, float& mx_o
   }
 }
 
-// 32 values -> 16 packed bf16 pairs of 2^(v*sl - msl) (zero past nvalid);
-// one element in four on the FMA pipe (exp2_poly) to offload MUFU.
+// 32 values -> 16 packed bf16 pairs of 2^(v*sl - msl) (zero past nvalid).  All on
+// MUFU: the epilogue is issue-bound, and the FMA-pipe polynomial costs ~9 issues.
+__device__ __forceinline__ uint32_t exp2_pair_f16(float x0, float x1) {
+  // both exponents through one MUFU op (ex2.approx.f16x2), repacked as bf16x2
+  uint32_t h, r;
+  asm("cvt.rn.f16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(x0), "f"(x1));
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(h));
+  float lo, hi;
+  asm("{.reg .f16 a, b;\n\tmov.b32 {a, b}, %2;\n\tcvt.f32.f16 %0, a;\n\tcvt.f32.f16 %1, b;}"
+      : "=f"(lo), "=f"(hi) : "r"(r));
+  return pack_bf16(lo, hi);
+}
+
 __device__ __forceinline__ void exp_pack32(const float* v, int nvalid, float sl, float msl, uint32_t* w) {
-  if (nvalid >= 32) {
+  if (nvalid >= 32 && FF_EXP == 2) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) w[e] = exp2_pair_f16(fmaf(v[2 * e], sl, -msl), fmaf(v[2 * e + 1], sl, -msl));
+  } else if (nvalid >= 32) {
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
       const float x0 = fmaf(v[2 * e], sl, -msl), x1 = fmaf(v[2 * e + 1], sl, -msl);
-      w[e] = pack_bf16(fast_exp2(x0), (e & 1) ? exp2_poly<3>(x1) : fast_exp2(x1));
+      w[e] = pack_bf16(fast_exp2(x0), (FF_EXP == 0 && (e & 1)) ? exp2_poly<3>(x1) : fast_exp2(x1));
     }
   } else {
 #pragma unroll
@@ -129,7 +164,7 @@ __device__ __forceinline__ void exp_pack32(const float* v, int nvalid, float sl,
   }
 }
 
-// 96 registers: 18 warps put 5 warps on two SM sub-partitions, each with a 16K-register file.
+// 96 registers: 19 warps put 5 warps on three SM sub-partitions, each with a 16K-register file.
 __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfArgs p) {
   uint8_t* smem = smem_base();
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FF_OFF_BAR);
@@ -152,12 +187,14 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
   const int u_end = int(int64_t(blockIdx.x + 1) * units / gridDim.x);
   const bool kres = T <= FF_KST;  // K tile t stays in slot t while the head is unchanged
 
+#if FF_ONES
   {  // constant B-operand block of ones (read by the async proxy)
     uint4* ones = reinterpret_cast<uint4*>(smem + FF_OFF_ONES);
     for (uint32_t i = threadIdx.x; i < TILE / 16; i += FF_THREADS)
       ones[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
     fence_proxy_async_smem();
   }
+#endif
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
@@ -224,9 +261,8 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
     const uint32_t idesc_s = idesc_bf16_f32(TR, TK, 0, 0);
-    const uint32_t idesc_o = idesc_bf16_f32(TR, PV_N, 0, 1);
-    Pos kq, vq;
-    uint32_t qn[2] = {0, 0}, sn[2] = {0, 0}, pn[2] = {0, 0}, on[2] = {0, 0}, kgen = 0;
+    Pos kq;
+    uint32_t qn[2] = {0, 0}, sn[2] = {0, 0}, kgen = 0;
     int prev_bz = -1;
     for (int u = u_begin; u < u_end; ++u) {
       const Unit un = unit_of(u, UH, NQ);
@@ -258,13 +294,23 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
         else if (last && k_release)
           for (int j = 0; j < T; ++j) umma_commit_ws(&k_empty[j]);
       };
-      issue_s(0);
-      for (int t = 0; t < T; ++t) {  // O~ += P~ [V | 1], one key tile behind S
-        if (t + 1 < T) issue_s(t + 1);
+      for (int t = 0; t < T; ++t) issue_s(t);
+    }
+  } else if (warp == FF_PV_WARP) {
+    // ------------------------------------------- P~ V issuer (second MMA thread)
+    // A separate issuing thread, so S(t+1) never queues behind the other group's
+    // P~ V; tcgen05.commit tracks each thread's own MMAs, so the barriers stay exact.
+    const uint32_t idesc_o = idesc_bf16_f32(TR, PV_N, 0, 1);
+    Pos vq;
+    uint32_t pn[2] = {0, 0}, on[2] = {0, 0};
+    for (int u = u_begin; u < u_end; ++u) {
+      const Unit un = unit_of(u, UH, NQ);
+      for (int t = 0; t < T; ++t) {  // O~ += P~ [V | 1]
         const uint32_t vs = vq.slot(FF_VST);
         mbar_wait(&v_full[vs], vq.phase(FF_VST));
         const uint32_t va = smem_u32(smem + FF_OFF_V + vs * TILE);
-        const uint32_t lbo = FF_OFF_ONES - (FF_OFF_V + vs * TILE);  // second 64-column atom: the ones block
+        // N = 80: the second 64-column B atom is the ones block (its offset is the LBO)
+        const uint32_t lbo = FF_ONES ? FF_OFF_ONES - (FF_OFF_V + vs * TILE) : ATOM;
         for (int gi = 0; gi < un.n; ++gi) {
           if (t == 0) mbar_wait(&o_empty[gi], (on[gi] & 1) ^ 1);
           mbar_wait(&p_full[gi], pn[gi] & 1);
@@ -283,7 +329,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
       }
       for (int gi = 0; gi < un.n; ++gi) umma_commit_ws(&o_full[gi]), ++on[gi];
     }
-  } else {
+  } else if (warp < FF_PV_WARP) {
     // ------------------------------------------------------------ epilogue
     const uint32_t gi = (warp - 2) >> 3;
     const uint32_t quad = warp & 3;
@@ -294,10 +340,10 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
     const uint32_t lane_base = (quad * 32u) << 16;
     const uint32_t t_s = tmem + lane_base + gi * 256 + half * 64;
     const uint32_t t_o = tmem + lane_base + gi * 256 + 128;
-    const uint32_t xbase = smem_u32(smem + FF_OFF_X) + gi * 2 * 256 * 4;
+    const uint32_t xbase = smem_u32(smem + FF_OFF_X) + gi * 3 * 256 * 4;
     const uint32_t ptile = smem_u32(smem + FF_OFF_P + gi * PTILE);
     uint8_t* ptile_gen = smem + FF_OFF_P + gi * PTILE + half * ATOM;
-    const uint32_t bar_half_id = 2 + gi * 2 + half, bar_rows_id = 6 + gi * 4 + quad, bar_grp_id = 14 + gi;
+    const uint32_t bar_rows_id = 6 + gi * 4 + quad, bar_grp_id = 14 + gi;
     const float sl = p.sl;
     uint32_t sn = 0, pn = 0, un_n = 0;
     bool bad = false, redo = false;
@@ -308,7 +354,12 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
       const int qi = un.qi0 + gi, d = qi / nrt, rt = qi % nrt;
       const int row = rt * TR + r;
       FF_TRACE(1);
-      float m = -INFINITY, mi = INFINITY, msl = 0.f;  // running raw max / min, reference m_ref * sl
+      // tile 0: raw max and min (the reference point); later tiles: max |s| only, which
+      // bounds the row max (headroom check) and is finite iff every score is
+      float m = -INFINITY, mi = INFINITY, am = 0.f, msl = 0.f;
+#if !FF_ONES
+      float lsum = 0.f;  // this thread's share of sum_k P~[row, k] over the bf16 values stored
+#endif
       int jo = 0, k0 = 0;
       for (int t = 0; t < T; ++t) {
         const int nvalid = min(TK, g.c - k0) - half * 64;
@@ -342,30 +393,40 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
             float v[32];
             tmem_ld32(t_s + cc * 32, v);
             tmem_ld_wait();
+            FF_TRACE(40 + cc);
             if (cc == 1) {  // both chunks are in registers: free S for the next key tile
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(&s_empty[gi]);
             }
-            minmax32(v, nvalid - cc * 32, m, mi);
+            if (FF_ABSMAX) absmax32(v, nvalid - cc * 32, am);
+            else minmax32(v, nvalid - cc * 32, m, mi);
             exp_pack32(v, nvalid - cc * 32, sl, msl, w + cc * 16);
           }
         }
         ++sn;
+#if !FF_ONES
+#pragma unroll
+        for (int e = 0; e < 32; ++e) lsum += __uint_as_float(w[e] << 16) + __uint_as_float(w[e] & 0xFFFF0000u);
+#endif
         FF_TRACE(4);
         mbar_wait(&p_empty[gi], (pn & 1) ^ 1);  // the previous P~ V product has read the tile
-        if (storer) tma_store_wait_read<0>();    // and the previous TMA store has read it
-        bar_named(bar_half_id, 128);
+        FF_TRACE(5);
+        // Each warp stores its own 32 rows x 64 keys (4 KB, 1024-byte aligned, so the
+        // 128-byte swizzle pattern is the tile's): no cross-warp barrier on this path.
+        if (lane == 0) tma_store_wait_read<0>();  // this warp's previous store has read its rows
+        __syncwarp();
 #pragma unroll
         for (int q4 = 0; q4 < 8; ++q4)
           st_shared_v4(ptile + half * ATOM + sw128_offset(r, q4), w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2],
                        w[4 * q4 + 3]);
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[gi]);
-        bar_named(bar_half_id, 128);
-        if (storer) {
-          if (nvalid > 0) tma_store_5d(&p.tp, ptile_gen, k0 + half * 64, g.org_lo + jo, rt * TR, z, d * g.B + b);
+        if (lane == 0) {
+          mbar_arrive(&p_full[gi]);
+          if (nvalid > 0)
+            tma_store_5d(&p.tp, ptile_gen + quad * 4096, k0 + half * 64, g.org_lo + jo, rt * TR + quad * 32, z,
+                         d * g.B + b);
           tma_store_commit();
         }
         FF_TRACE(6);
@@ -373,9 +434,10 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
         if (k0 + TK >= g.c) k0 = 0, ++jo;
         else k0 += TK;
       }
-      if (!(m == -INFINITY && mi == INFINITY))  // this thread saw at least one valid key
+      if (!(m == -INFINITY && mi == INFINITY))  // this thread saw at least one valid key in tile 0
         bad |= !(fabsf(m) <= 3.402823466e38f) || !(fabsf(mi) <= 3.402823466e38f);
-      redo |= m * sl - msl > FF_HEADROOM;
+      bad |= !(am <= 3.402823466e38f);
+      redo |= (FF_ABSMAX ? am : m) * sl - msl > FF_HEADROOM;  // |s| >= s: conservative
       // ---- O = O~ / l, r = 1 / l (l >= 1 unless the row needs the fallback)
       mbar_wait(&o_full[gi], un_n & 1);
       FF_TRACE(7);
@@ -383,16 +445,32 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
       float o[32];
       __syncwarp();
       tmem_ld32(t_o + half * 32, o);
-      const float l = tmem_ld1(t_o + HD);
+#if FF_ONES
+      uint32_t lraw;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(lraw) : "r"(t_o + HD));
+#endif
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[gi]);
+      float l;
+#if FF_ONES
+      l = __uint_as_float(lraw);
+#else
+      {  // the row sum: this half's share plus the other half's
+        const uint32_t slot = xbase + 2 * 256 * 4;
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(slot + et * 4), "f"(lsum) : "memory");
+        bar_named(bar_rows_id, 64);
+        float o2;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o2) : "r"(slot + ((et + 128) & 255) * 4) : "memory");
+        l = lsum + o2;
+      }
+#endif
       ++un_n;
       const float rinv = 1.f / l;
       redo |= !(l >= 1.f && l <= 3.402823466e38f);
       // O -> the group's P~ buffer (atom 0, swizzled like a TMA tile) -> one TMA store
-      if (storer) tma_store_wait_read<0>();  // the unit's last P~ stores have left the buffer
+      if (lane == 0) tma_store_wait_read<0>();  // every warp's last P~ store has left the buffer
       bar_named(bar_grp_id, 256);
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4)
@@ -405,12 +483,14 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
       if (storer && half == 0) {
         tma_store_4d(&p.to, smem + FF_OFF_P + gi * PTILE, 0, rt * TR, z, d * g.B + b);
         tma_store_commit();
+        tma_store_wait_read<0>();  // other warps' next P~ rows go into this atom
       }
+      bar_named(bar_grp_id, 256);
       if (row < g.c && half == 0) p.rowscale[(int64_t(d * g.B + b) * g.Z + z) * g.c + row] = rinv;
       FF_TRACE(21);
     }
     if (p.flag && (bad || redo)) atomicOr(p.flag, (bad ? 1 : 0) | (redo ? 2 : 0));
-    if (storer) tma_store_wait_all<0>();
+    if (lane == 0) tma_store_wait_all<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -432,7 +512,7 @@ int rsa_fwd_factored(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_
     return fail(RSA_ERR_UNSUPPORTED, "rsa_fwd_factored: output / row-scale / flag buffers missing or misaligned");
   FfArgs a{};
   if (!head_map(&a.tq, q, g, g->n_rank) || !head_map(&a.tk, k, g, g->n_org) || !head_map(&a.tv, v, g, g->n_org) ||
-      !panel_map(&a.tp, panel, g, g->n_rank) || !head_map(&a.to, o_out, g, g->n_rank))
+      !panel_map(&a.tp, panel, g, g->n_rank, 32) || !head_map(&a.to, o_out, g, g->n_rank))
     return RSA_ERR_UNSUPPORTED;
   a.g = to_geo(g);
   a.sl = g->scale * LOG2E;
@@ -441,8 +521,8 @@ int rsa_fwd_factored(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_
   static long long* trace_buf = nullptr;
   const char* trace_path = getenv("RSA_FF_TRACE");
   if (trace_path) {
-    if (!trace_buf) cudaMalloc(&trace_buf, 18 * 4096 * sizeof(long long));
-    cudaMemset(trace_buf, 0, 18 * 4096 * sizeof(long long));
+    if (!trace_buf) cudaMalloc(&trace_buf, (FF_THREADS / 32) * 4096 * sizeof(long long));
+    cudaMemset(trace_buf, 0, (FF_THREADS / 32) * 4096 * sizeof(long long));
     a.trace = trace_buf;
   }
   const int nq = g->n_rank * ((g->chunk + TR - 1) / TR);
@@ -456,7 +536,7 @@ int rsa_fwd_factored(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_
   const int grid = units < num_sms() ? units : num_sms();
   fwd_factored_kernel<<<grid, FF_THREADS, FF_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(a);
   if (trace_path) {
-    static long long host[18 * 4096];
+    static long long host[(FF_THREADS / 32) * 4096];
     cudaMemcpy(host, trace_buf, sizeof(host), cudaMemcpyDeviceToHost);
     if (FILE* f = fopen(trace_path, "wb")) fwrite(host, sizeof(host), 1, f), fclose(f);
   }
