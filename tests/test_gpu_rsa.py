@@ -461,3 +461,21 @@ def test_backward_does_not_materialise_saved_panels(rsa):
     _, fwd, _ = _run(pkg, ra, q, k, v, g, n, "fused")
     assert all(list.__getitem__(fwd.probs, d) is None for d in range(n))
     assert fwd.probs[1].dtype == torch.float32 and list.__getitem__(fwd.probs, 1) is not None
+
+
+@pytest.mark.parametrize("key", [50, 300])
+def test_negative_overflow_score_raises_numeric_error(rsa, key):
+    """A score that overflows the fp32 range to -inf while every other score of its row
+    stays finite -- the case a max-only check misses -- raises NumericError
+    (ringseq/tensor_ops.py:80-81), whether it sits in the first key tile (key 50) or a
+    later one (key 300, where the factored kernel checks max |s|).  (The float64
+    reference would not overflow here: scores beyond the fp32 range are the one
+    documented behavioural difference.)"""
+    pkg, ra = rsa
+    q, k, v, _ = _inputs(1, 1, 512, 64, seed=12)
+    q[0, 0, 7, 0] = -3.0e38
+    k[0, 0, :, 0] = 0.0
+    k[0, 0, key, 0] = 3.0e38
+    cfg = _cfg(pkg, 1, 1, 512, 64, 1)
+    with pytest.raises(pkg.NumericError):
+        ra.ring_attention_forward([q], [k], [v], cfg, path="fused")
