@@ -1,0 +1,93 @@
+"""One-GPU measurements of BASELINE.json's configs (besides bench.py's headline config 2).
+
+  config 1  single RSA layer fwd+bwd, H=768 Z=12 L=512 B=4, sequence over 4 logical ranks
+  config 4  BERT-large attention (Z=16, A=64) single layer fwd+bwd at L=16384, B=4, the
+            sequence over 8 logical ranks (the per-box work of the paper's 8-GPU run)
+  config 5  Linformer sequence-parallel fwd+bwd at L=114688 (8 x 14336), B=4, Z=12, Kp=256,
+            8 logical ranks
+
+Device-resident synthetic inputs, CUDA events, median of `--iters` after warm-up.
+(Config 3's sweep and max length: tools/seq_sweep.py.)
+usage: python tools/configs.py [--out gpurun_out/configs.json]
+"""
+import argparse
+import json
+import statistics
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2105_13120_b200 import AttentionConfig, SparseAttentionConfig, SparseWeights, engine  # noqa: E402
+from paper_2105_13120_b200.sparse_attention import (sparse_ring_attention_backward,  # noqa: E402
+                                                    sparse_ring_attention_forward)
+
+
+def timed(fn, iters, warmup=2):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts)
+
+
+def rsa_layer(n, b, z, seq, a, iters, dev):
+    c = seq // n
+    gen = torch.Generator(device=dev).manual_seed(seq)
+    q, k, v, g = (torch.randn((n, b, z, c, a), generator=gen, device=dev).to(torch.bfloat16) for _ in range(4))
+
+    def step():
+        fwd = engine.forward(q, k, v, path="fused")
+        engine.backward(q, k, v, fwd.panel, g, outputs=fwd.out, rowscale=fwd.rowscale, path="fused")
+
+    ms = timed(step, iters)
+    return {"ms_per_layer_fwd_bwd": ms, "tokens_per_s": b * seq / (ms / 1e3),
+            "fused_backward": "rsa_bwd_fused" if engine.single_pass_supported(n, b, z, c, a) else
+            "rsa_bwd_dkdv + rsa_bwd_dq"}
+
+
+def linformer(n, b, z, seq, a, kp, iters, dev):
+    c = seq // n
+    gen = torch.Generator(device=dev).manual_seed(5)
+    ch = [[torch.randn((b, z, c, a), generator=gen, device=dev).to(torch.bfloat16) for _ in range(n)]
+          for _ in range(4)]
+    s = seq ** -0.5
+    w = SparseWeights((torch.randn((kp, seq), generator=gen, device=dev) * s).to(torch.bfloat16),
+                      (torch.randn((kp, seq), generator=gen, device=dev) * s).to(torch.bfloat16))
+    base = AttentionConfig(batch_size=b, seq_len=seq, hidden_size=z * a, num_heads=z, head_size=a, num_devices=n)
+    cfg = SparseAttentionConfig(base=base, proj_dim=kp)
+    fwd_ms = timed(lambda: sparse_ring_attention_forward(ch[0], ch[1], ch[2], w, cfg), iters)
+    bwd_ms = timed(lambda: sparse_ring_attention_backward(ch[0], ch[1], ch[2], w, cfg, ch[3]), iters)
+    return {"ms_fwd": fwd_ms, "ms_bwd_incl_recompute": bwd_ms, "tokens_per_s_fwd": b * seq / (fwd_ms / 1e3),
+            "tokens_per_s_fwd_bwd": b * seq / ((fwd_ms + bwd_ms) / 1e3)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--out", default="gpurun_out/configs.json")
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    res = {}
+    res["config1"] = {"shape": "B4 Z12 A64 L512, N=4 logical ranks", **rsa_layer(4, 4, 12, 512, 64, args.iters, dev)}
+    print(json.dumps(res["config1"]), flush=True)
+    res["config4"] = {"shape": "BERT-large attention Z16 A64 L16384 B4, N=8 logical ranks (c=2048)",
+                      **rsa_layer(8, 4, 16, 16384, 64, args.iters, dev)}
+    print(json.dumps(res["config4"]), flush=True)
+    res["config5"] = {"shape": "Linformer B4 Z12 A64 L114688 Kp256, N=8 logical ranks",
+                      **linformer(8, 4, 12, 114688, 64, 256, args.iters, dev)}
+    print(json.dumps(res["config5"]), flush=True)
+    Path(args.out).parent.mkdir(parents=True, exist_ok=True)
+    Path(args.out).write_text(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
