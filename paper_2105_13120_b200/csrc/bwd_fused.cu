@@ -342,10 +342,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
     };
     for (int item = blockIdx.x; item < items; item += gridDim.x, ++head_it) {
       const int b = item / g.Z, z = item % g.Z;
+      // D of this thread's row in each query tile of the head: loaded once per head
+      // (every key tile revisits the same rows), so no global load sits in a step
+      float dh[MAX_QT];
+#pragma unroll
+      for (int j = 0; j < MAX_QT; ++j) {
+        const int rj = (j % nrt) * TR + r;
+        dh[j] = (j < NQ && rj < g.c) ? __ldg(p.dvec + (int64_t((j / nrt) * g.B + b) * g.Z + z) * g.c + rj) : 0.f;
+      }
       for (int t = 0; t < T; ++t) {
         const int kk = t / NQ, qt = t % NQ;
         const int d = qt / nrt, row = (qt % nrt) * TR + r;
-        const float dval = row < g.c ? p.dvec[(int64_t(d * g.B + b) * g.Z + z) * g.c + row] : 0.f;
+        const float dval = qt == 0 ? dh[0] : qt == 1 ? dh[1] : qt == 2 ? dh[2] : dh[3];
         const uint32_t ps = pq.slot(BF_P);
         const uint32_t pt = smem_u32(smem + BF_OFF_P + ps * PTILE);
         BF_TRACE(20);
