@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
+      const uint64_t pol = l2_evict_first();
       Pos dq_, qq, kq, vq, pq;
       // one 16 KB head tile (rows r0.. of rank/origin `blk`) into ring slot
       auto load_tile = [&](const Ring& r, Pos& pos, int depth, uint32_t off, const CUtensorMap* map, int r0, int z,
@@ -147,8 +148,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
             mbar_wait(&rp.empty[s], pq.phase(BF_P) ^ 1);
             mbar_arrive_expect_tx(&rp.full[s], PTILE);
             uint8_t* pt = smem + BF_OFF_P + s * PTILE;
-            tma_load_5d(pt, &p.tp, &rp.full[s], k0, g.org_lo + jo, r0, z, d * g.B + b);
-            tma_load_5d(pt + ATOM, &p.tp, &rp.full[s], k0 + 64, g.org_lo + jo, r0, z, d * g.B + b);
+            // the panel streams through once: evict it first, keep dO / Q / K / V tiles in L2
+            tma_load_5d_hint(pt, &p.tp, &rp.full[s], k0, g.org_lo + jo, r0, z, d * g.B + b, pol);
+            tma_load_5d_hint(pt + ATOM, &p.tp, &rp.full[s], k0 + 64, g.org_lo + jo, r0, z, d * g.B + b, pol);
             BF_TRACE(1);
             ++pq.i;
             load_tile(rq, qq, BF_Q, BF_OFF_Q, &p.tq, r0, z, d * g.B + b);

@@ -347,6 +347,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
     const float sl = p.sl;
     uint32_t sn = 0, pn = 0, un_n = 0;
     bool bad = false, redo = false;
+    const uint64_t pol = l2_evict_first();
     for (int u = u_begin; u < u_end; ++u) {
       const Unit un = unit_of(u, UH, NQ);
       if (int(gi) >= un.n) continue;
@@ -424,9 +425,9 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&p_full[gi]);
-          if (nvalid > 0)
-            tma_store_5d(&p.tp, ptile_gen + quad * 4096, k0 + half * 64, g.org_lo + jo, rt * TR + quad * 32, z,
-                         d * g.B + b);
+          if (nvalid > 0)  // the panel is read back only by the backward: evict-first in L2
+            tma_store_5d_hint(&p.tp, ptile_gen + quad * 4096, k0 + half * 64, g.org_lo + jo, rt * TR + quad * 32, z,
+                              d * g.B + b, pol);
           tma_store_commit();
         }
         FF_TRACE(6);
