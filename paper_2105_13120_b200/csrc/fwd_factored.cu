@@ -63,12 +63,18 @@ constexpr int FF_THREADS = 32 * (FF_PV_WARP + 1);       // 608
 #ifndef FF_ABSMAX
 #define FF_ABSMAX 1  // tiles after the first: max|s| only (finite check + headroom bound)
 #endif
-constexpr int FF_KST = 4, FF_VST = FF_ONES ? 2 : 3;
+#ifndef FF_QST
+#define FF_QST 1  // Q tiles per group (2: the next unit's Q loads during this unit)
+#endif
+#ifndef FF_KSTAGES
+#define FF_KSTAGES 4
+#endif
+constexpr int FF_KST = FF_KSTAGES, FF_VST = FF_ONES ? 2 : 3;
 constexpr int PV_N = FF_ONES ? HD + 16 : HD;  // O columns (+ 16 row-sum columns)
 constexpr float FF_HEADROOM = 96.f;
     // max (row max - m_ref) * sl before the two-pass fallback
 constexpr uint32_t FF_OFF_Q = 0;                                  // one tile per group
-constexpr uint32_t FF_OFF_K = FF_OFF_Q + FF_GROUPS * TILE;
+constexpr uint32_t FF_OFF_K = FF_OFF_Q + FF_GROUPS * FF_QST * TILE;
 constexpr uint32_t FF_OFF_V = FF_OFF_K + FF_KST * TILE;
 constexpr uint32_t FF_OFF_ONES = FF_OFF_V + FF_VST * TILE;        // 128 rows x 128 B of bf16 1.0 (FF_ONES)
 constexpr uint32_t FF_OFF_P = FF_OFF_ONES + (FF_ONES ? TILE : 0);  // one P~ tile per group
@@ -168,8 +174,8 @@ __device__ __forceinline__ void exp_pack32(const float* v, int nvalid, float sl,
 __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfArgs p) {
   uint8_t* smem = smem_base();
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FF_OFF_BAR);
-  uint64_t *q_full = bar, *q_empty = q_full + 2;
-  uint64_t *k_full = q_empty + 2, *k_empty = k_full + FF_KST;
+  uint64_t *q_full = bar, *q_empty = q_full + 2 * FF_QST;  // [group][stage]
+  uint64_t *k_full = q_empty + 2 * FF_QST, *k_empty = k_full + FF_KST;
   uint64_t *v_full = k_empty + FF_KST, *v_empty = v_full + FF_VST;
   uint64_t *s_full = v_empty + FF_VST, *s_empty = s_full + 2;
   uint64_t *p_full = s_empty + 2, *p_empty = p_full + 2;
@@ -198,7 +204,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&q_full[s], 1), mbar_init(&q_empty[s], 1);
+      for (int q = 0; q < FF_QST; ++q) mbar_init(&q_full[s * FF_QST + q], 1), mbar_init(&q_empty[s * FF_QST + q], 1);
       mbar_init(&s_full[s], 1), mbar_init(&s_empty[s], 8);
       mbar_init(&p_full[s], 8), mbar_init(&p_empty[s], 1);
       mbar_init(&o_full[s], 1), mbar_init(&o_empty[s], 8);
@@ -226,9 +232,10 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
         const int b = un.bz / g.Z, z = un.bz % g.Z;
         for (int gi = 0; gi < un.n; ++gi) {
           const int qi = un.qi0 + gi, d = qi / nrt, rt = qi % nrt;
-          mbar_wait(&q_empty[gi], (qn[gi] & 1) ^ 1);
-          mbar_arrive_expect_tx(&q_full[gi], TILE);
-          tma_load_4d(smem + FF_OFF_Q + gi * TILE, &p.tq, &q_full[gi], 0, rt * TR, z, d * g.B + b);
+          const int qx = gi * FF_QST + int(qn[gi] % FF_QST);
+          mbar_wait(&q_empty[qx], ((qn[gi] / FF_QST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&q_full[qx], TILE);
+          tma_load_4d(smem + FF_OFF_Q + qx * TILE, &p.tq, &q_full[qx], 0, rt * TR, z, d * g.B + b);
           ++qn[gi];
         }
         if (kres && un.bz != prev_bz) {
@@ -270,7 +277,8 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
       prev_bz = un.bz;
       // resident K: release the slots after the unit's last S unless the next unit reuses them
       const bool k_release = kres && u + 1 < u_end && unit_of(u + 1, UH, NQ).bz != un.bz;
-      for (int gi = 0; gi < un.n; ++gi) mbar_wait(&q_full[gi], qn[gi] & 1);
+      for (int gi = 0; gi < un.n; ++gi)
+        mbar_wait(&q_full[gi * FF_QST + qn[gi] % FF_QST], (qn[gi] / FF_QST) & 1);
       // S(g) = Q_g K_t^T for both query tiles of the unit from one K tile
       auto issue_s = [&](int t) {
         const bool last = t + 1 == T;
@@ -280,14 +288,14 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
         for (int gi = 0; gi < un.n; ++gi) {
           mbar_wait(&s_empty[gi], (sn[gi] & 1) ^ 1);
           tc_fence_after();
-          const uint32_t qa = smem_u32(smem + FF_OFF_Q + gi * TILE);
+          const uint32_t qa = smem_u32(smem + FF_OFF_Q + (gi * FF_QST + qn[gi] % FF_QST) * TILE);
 #pragma unroll
           for (int k = 0; k < HD / 16; ++k)
             umma_bf16_ws(tmem + gi * 256, smem_desc_sw128(qa + k * 32, 0, 1024), smem_desc_sw128(ka + k * 32, 0, 1024),
                          idesc_s, k > 0);
           umma_commit_ws(&s_full[gi]);
           FF_TRACE(10 + gi);
-          if (last) umma_commit_ws(&q_empty[gi]), ++qn[gi];
+          if (last) umma_commit_ws(&q_empty[gi * FF_QST + qn[gi] % FF_QST]), ++qn[gi];
           ++sn[gi];
         }
         if (!kres) umma_commit_ws(&k_empty[ks]), ++kq.i;
