@@ -126,6 +126,15 @@ int rsa_rowdot_scale(const void* a, int64_t lda, const void* b, int64_t ldb, con
 int rsa_panel_normalize(const void* p, int64_t ld_p, const float* scale, int64_t rows, int64_t cols, void* y,
                         int y_dtype, int64_t ld_y, void* stream);
 
+/*
+ * Exact GELU y = x * Phi(x) (ringseq/tensor_ops.py:87-90, the reference's mlp_forward
+ * activation, ringseq/reference.py:177-185) and its backward dx = dy * (Phi(x) + x phi(x)),
+ * elementwise over n values; fp32 / bf16 per dtype argument.
+ */
+int rsa_gelu(const void* x, int x_dtype, int64_t n, void* y, int y_dtype, void* stream);
+int rsa_gelu_bwd(const void* x, int x_dtype, const void* dy, int dy_dtype, int64_t n, void* dx, int dx_dtype,
+                 void* stream);
+
 /* --------------------------------------------------- fused RSA kernels */
 
 /*

@@ -46,6 +46,9 @@ _LAZY = {
     "ring_attention_backward": "ring_attention",
     "sequence_parallel_attention": "ring_attention",
     "sequence_parallel_attention_backward": "ring_attention",
+    "sequence_parallel_mlp": "ring_attention",
+    "sequence_parallel_mlp_backward": "ring_attention",
+    "MlpWeights": "weights",
     "SparseRingForward": "sparse_attention",
     "sparse_ring_attention_forward": "sparse_attention",
     "sparse_ring_attention_backward": "sparse_attention",

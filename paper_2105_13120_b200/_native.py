@@ -86,6 +86,8 @@ EXPORTS = {
         c_int,
         [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_int64, c_void_p],
     ),
+    "rsa_gelu": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int, c_void_p]),
+    "rsa_gelu_bwd": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int64, c_void_p, c_int, c_void_p]),
     "rsa_panel_normalize": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_int, c_int64, c_void_p]),
     "rsa_fwd_stats": (c_int, [_GEOM, _V, _V, c_void_p, c_int, c_void_p, c_void_p]),
     "rsa_fwd_probs_pv": (c_int, [_GEOM, _V, _V, _V, c_void_p, c_int, _V, _V, c_int, _V, c_void_p]),

@@ -279,6 +279,87 @@ __global__ void __launch_bounds__(256) panel_normalize_kernel(const __nv_bfloat1
   for (int64_t c = lane; c < cols; c += 32) y[row * ldy + c] = TO(__bfloat162float(p[row * ldp + c]) * sc);
 }
 
+
+// Exact GELU (ringseq/tensor_ops.py:87-90): y = x * Phi(x), Phi(x) = (1 + erf(x / sqrt 2)) / 2,
+// and its backward dx = dy * (Phi(x) + x * phi(x)).  Grid-stride, 4 elements per thread
+// per iteration when the pointers allow it.
+constexpr float INV_SQRT2 = 0.7071067811865476f;
+constexpr float INV_SQRT_2PI = 0.3989422804014327f;
+
+__device__ __forceinline__ float gelu_f(float x) { return 0.5f * x * (1.f + erff(x * INV_SQRT2)); }
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  return 0.5f * (1.f + erff(x * INV_SQRT2)) + x * INV_SQRT_2PI * __expf(-0.5f * x * x);
+}
+
+template <typename TI, typename TO, bool VEC>
+__global__ void __launch_bounds__(256) gelu_kernel(const TI* __restrict__ x, int64_t n, TO* __restrict__ y) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  if (VEC) {
+    for (int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < n; i += stride * 4) {
+      float v[4];
+      ld4<TI>(x + i, v);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = gelu_f(v[e]);
+      st4<TO>(y + i, v);
+    }
+  } else {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) st1<TO>(y, i, gelu_f(ld1<TI>(x, i)));
+  }
+}
+
+template <typename TI, typename TG, typename TO, bool VEC>
+__global__ void __launch_bounds__(256) gelu_bwd_kernel(const TI* __restrict__ x, const TG* __restrict__ dy, int64_t n,
+                                                       TO* __restrict__ dx) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  if (VEC) {
+    for (int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < n; i += stride * 4) {
+      float v[4], g[4];
+      ld4<TI>(x + i, v);
+      ld4<TG>(dy + i, g);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = g[e] * gelu_grad_f(v[e]);
+      st4<TO>(dx + i, v);
+    }
+  } else {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+      st1<TO>(dx, i, ld1<TG>(dy, i) * gelu_grad_f(ld1<TI>(x, i)));
+  }
+}
+
+template <typename T>
+bool aligned_vec(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) % (4 * sizeof(T))) == 0;
+}
+
+int elementwise_grid(int64_t n) {
+  const int64_t blocks = (n / 4 + 255) / 256;
+  const int64_t cap = int64_t(num_sms()) * 8;
+  return int(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
+}
+
+template <typename TI, typename TO>
+int gelu_launch(const void* x, int64_t n, void* y, cudaStream_t st) {
+  const auto* xi = static_cast<const TI*>(x);
+  auto* yo = static_cast<TO*>(y);
+  if (n % 4 == 0 && aligned_vec<TI>(x) && aligned_vec<TO>(y))
+    gelu_kernel<TI, TO, true><<<elementwise_grid(n), 256, 0, st>>>(xi, n, yo);
+  else
+    gelu_kernel<TI, TO, false><<<elementwise_grid(n), 256, 0, st>>>(xi, n, yo);
+  return check_launch("gelu_kernel");
+}
+
+template <typename TI, typename TG, typename TO>
+int gelu_bwd_launch(const void* x, const void* dy, int64_t n, void* dx, cudaStream_t st) {
+  const auto* xi = static_cast<const TI*>(x);
+  const auto* gi = static_cast<const TG*>(dy);
+  auto* o = static_cast<TO*>(dx);
+  if (n % 4 == 0 && aligned_vec<TI>(x) && aligned_vec<TG>(dy) && aligned_vec<TO>(dx))
+    gelu_bwd_kernel<TI, TG, TO, true><<<elementwise_grid(n), 256, 0, st>>>(xi, gi, n, o);
+  else
+    gelu_bwd_kernel<TI, TG, TO, false><<<elementwise_grid(n), 256, 0, st>>>(xi, gi, n, o);
+  return check_launch("gelu_bwd_kernel");
+}
+
 template <typename T>
 bool vec_ok(const void* ptr, int64_t ld, int64_t cols) {
   const int64_t esz = sizeof(T);
@@ -396,6 +477,37 @@ int rsa_panel_normalize(const void* p, int64_t ld_p, const float* scale, int64_t
   else
     return fail(RSA_ERR_INVALID, "panel_normalize: bad output dtype");
   return check_launch("panel_normalize_kernel");
+}
+
+int rsa_gelu(const void* x, int x_dtype, int64_t n, void* y, int y_dtype, void* stream) {
+  using namespace rsa;
+  if (n < 0 || !x || !y) return fail(RSA_ERR_INVALID, "gelu: bad arguments");
+  if (n == 0) return RSA_OK;
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  if (x_dtype == RSA_F32 && y_dtype == RSA_F32) return gelu_launch<float, float>(x, n, y, st);
+  if (x_dtype == RSA_F32 && y_dtype == RSA_BF16) return gelu_launch<float, __nv_bfloat16>(x, n, y, st);
+  if (x_dtype == RSA_BF16 && y_dtype == RSA_F32) return gelu_launch<__nv_bfloat16, float>(x, n, y, st);
+  if (x_dtype == RSA_BF16 && y_dtype == RSA_BF16) return gelu_launch<__nv_bfloat16, __nv_bfloat16>(x, n, y, st);
+  return fail(RSA_ERR_INVALID, "gelu: bad dtype");
+}
+
+int rsa_gelu_bwd(const void* x, int x_dtype, const void* dy, int dy_dtype, int64_t n, void* dx, int dx_dtype,
+                 void* stream) {
+  using namespace rsa;
+  if (n < 0 || !x || !dy || !dx) return fail(RSA_ERR_INVALID, "gelu_bwd: bad arguments");
+  if (n == 0) return RSA_OK;
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  if (x_dtype == RSA_F32 && dy_dtype == RSA_F32 && dx_dtype == RSA_F32)
+    return gelu_bwd_launch<float, float, float>(x, dy, n, dx, st);
+  if (x_dtype == RSA_F32 && dy_dtype == RSA_F32 && dx_dtype == RSA_BF16)
+    return gelu_bwd_launch<float, float, __nv_bfloat16>(x, dy, n, dx, st);
+  if (x_dtype == RSA_BF16 && dy_dtype == RSA_BF16 && dx_dtype == RSA_BF16)
+    return gelu_bwd_launch<__nv_bfloat16, __nv_bfloat16, __nv_bfloat16>(x, dy, n, dx, st);
+  if (x_dtype == RSA_BF16 && dy_dtype == RSA_F32 && dx_dtype == RSA_BF16)
+    return gelu_bwd_launch<__nv_bfloat16, float, __nv_bfloat16>(x, dy, n, dx, st);
+  if (x_dtype == RSA_F32 && dy_dtype == RSA_BF16 && dx_dtype == RSA_BF16)
+    return gelu_bwd_launch<float, __nv_bfloat16, __nv_bfloat16>(x, dy, n, dx, st);
+  return fail(RSA_ERR_INVALID, "gelu_bwd: unsupported dtype combination");
 }
 
 }  // extern "C"

@@ -43,6 +43,8 @@ __all__ = [
     "ring_attention_backward",
     "sequence_parallel_attention",
     "sequence_parallel_attention_backward",
+    "sequence_parallel_mlp",
+    "sequence_parallel_mlp_backward",
     "ProbPanels",
 ]
 
@@ -377,3 +379,75 @@ def sequence_parallel_attention_backward(x_chunks, weights, cfg: AttentionConfig
         for d in range(n):
             ledger.record_allreduce(d, 2 * h * za + za * h + h * za)  # wq, wk, wv, wo gradients
     return [gx[d] for d in range(n)], AttentionWeights(grad_wq, grad_wk, grad_wv, grad_wo), ledger
+
+
+def _mlp_weights(weights, h: int, dev):
+    up_s, down_s = _shape_of(weights.up), _shape_of(weights.down)
+    if len(up_s) != 2 or up_s[0] != h or down_s != (up_s[1], h):
+        raise ShapeError(f"mlp weights {up_s} / {down_s} do not match input feature size {h}")
+    return ops.to_device(weights.up, dev), ops.to_device(weights.down, dev)
+
+
+def _chunks_of_rows(x_chunks):
+    x_chunks = x_chunks if isinstance(x_chunks, list) else list(x_chunks)
+    if not x_chunks:
+        raise ShapeError("x_chunks: need at least one chunk")
+    shape = _shape_of(x_chunks[0])
+    for i, c in enumerate(x_chunks):
+        if _shape_of(c) != shape:
+            raise ShapeError(f"x_chunks[{i}] has shape {_shape_of(c)}, expected {shape}")
+    return x_chunks, shape
+
+
+def sequence_parallel_mlp(x_chunks, weights, *, executor: str | None = None):
+    """Feed-forward block on sequence-partitioned inputs (ringseq/ring_attention.py:244-256).
+
+    gelu(x @ up) @ down per rank (ringseq/reference.py:177-185); token rows never
+    interact, so nothing is communicated and the ledger stays at zero.  The GEMMs are
+    rsa_gemm (tcgen05), the activation rsa_gelu (exact erf form).  Returns
+    (per-rank outputs (B, L/N, H) bf16, ledger).
+    """
+    resolve_executor(executor)
+    x_chunks, shape = _chunks_of_rows(x_chunks)
+    dev = _device_of(x_chunks)
+    up, down = _mlp_weights(weights, shape[-1], dev)
+    x = _stack(x_chunks, dev)
+    a = ops.gelu(ops.matmul(x, up), out_dtype=torch.bfloat16)
+    y = ops.matmul(a, down, out_dtype=torch.bfloat16)
+    return [y[d] for d in range(len(x_chunks))], CommLedger(len(x_chunks))
+
+
+def sequence_parallel_mlp_backward(x_chunks, weights, grad_chunks, *, executor: str | None = None):
+    """Gradients of ``sequence_parallel_mlp`` (the reference ships the forward only).
+
+    Chain rule through gelu(x @ up) @ down with the pre-activation recomputed:
+    grad_down = a^T dy, dh = (dy down^T) * gelu'(h), grad_up = x^T dh, grad_x = dh up^T.
+    Weight gradients sum every rank's rows (one all-reduce of the replicated weights on N
+    devices, charged with the reference's all-reduce convention, ringseq/cluster.py:320-359).
+    Returns (grad_x chunks bf16, MlpWeights(grad_up, grad_down) fp32, ledger).
+    """
+    from .weights import MlpWeights
+
+    resolve_executor(executor)
+    x_chunks, shape = _chunks_of_rows(x_chunks)
+    grad_chunks, gshape = _chunks_of_rows(grad_chunks)
+    if gshape != shape or len(grad_chunks) != len(x_chunks):
+        raise ShapeError(f"grad_chunks shape {gshape} x {len(grad_chunks)} does not match x_chunks {shape}")
+    n, h = len(x_chunks), shape[-1]
+    dev = _device_of(x_chunks, grad_chunks)
+    up, down = _mlp_weights(weights, h, dev)
+    inner = up.shape[1]
+    x = _stack(x_chunks, dev)
+    g = _stack(grad_chunks, dev)
+    hpre = ops.matmul(x, up)  # fp32 pre-activation
+    a = ops.gelu(hpre, out_dtype=torch.bfloat16)
+    grad_down = ops.matmul(a.reshape(-1, inner).transpose(0, 1), g.reshape(-1, h))
+    da = ops.matmul(g, down.transpose(0, 1))  # fp32
+    dh = ops.gelu_backward(hpre, da, out_dtype=torch.bfloat16)
+    grad_up = ops.matmul(x.reshape(-1, h).transpose(0, 1), dh.reshape(-1, inner))
+    gx = ops.matmul(dh, up.transpose(0, 1), out_dtype=torch.bfloat16)
+    ledger = CommLedger(n)
+    if n > 1:
+        for d in range(n):
+            ledger.record_allreduce(d, 2 * h * inner)
+    return [gx[d] for d in range(n)], MlpWeights(grad_up, grad_down), ledger

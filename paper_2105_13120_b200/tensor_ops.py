@@ -29,6 +29,8 @@ __all__ = [
     "softmax_backward",
     "rowdot",
     "rowdot_scale",
+    "gelu",
+    "gelu_backward",
     "panel_normalize",
     "split_heads",
     "merge_heads",
@@ -251,6 +253,28 @@ def panel_normalize(panel: torch.Tensor, scale: torch.Tensor, out_dtype=torch.fl
     check(lib().rsa_panel_normalize(panel.data_ptr(), cols, scale.data_ptr(), rows, cols, out.data_ptr(),
                                     _DT[out_dtype], cols, _stream(panel)), "rsa_panel_normalize")
     return out
+
+
+def gelu(x: torch.Tensor, out_dtype=torch.bfloat16) -> torch.Tensor:
+    """Exact GELU x * Phi(x) (ringseq/tensor_ops.py:87-90), fp32 arithmetic (rsa_gelu)."""
+    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype in _DT):
+        x = to_device(x, dtype=torch.float32)
+    x = x.contiguous()
+    y = torch.empty(x.shape, dtype=out_dtype, device=x.device)
+    check(lib().rsa_gelu(x.data_ptr(), _DT[x.dtype], x.numel(), y.data_ptr(), _DT[out_dtype], _stream(x)),
+          "rsa_gelu")
+    return y
+
+
+def gelu_backward(x: torch.Tensor, dy: torch.Tensor, out_dtype=torch.bfloat16) -> torch.Tensor:
+    """dx = dy * (Phi(x) + x phi(x)) for y = gelu(x) (rsa_gelu_bwd)."""
+    if x.shape != dy.shape:
+        raise ShapeError(f"gelu_backward shapes {tuple(x.shape)} vs {tuple(dy.shape)}")
+    x, dy = x.contiguous(), dy.contiguous()
+    dx = torch.empty(x.shape, dtype=out_dtype, device=x.device)
+    check(lib().rsa_gelu_bwd(x.data_ptr(), _DT[x.dtype], dy.data_ptr(), _DT[dy.dtype], x.numel(), dx.data_ptr(),
+                             _DT[out_dtype], _stream(x)), "rsa_gelu_bwd")
+    return dx
 
 
 def split_heads(t, num_heads: int):

@@ -9,7 +9,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-__all__ = ["AttentionWeights", "SparseWeights"]
+__all__ = ["AttentionWeights", "SparseWeights", "MlpWeights"]
 
 
 @dataclass(frozen=True)
@@ -29,3 +29,11 @@ class SparseWeights:
 
     key_proj: object
     value_proj: object
+
+
+@dataclass(frozen=True)
+class MlpWeights:
+    """Feed-forward weights: up is (H, 4H), down is (4H, H) (ringseq/reference.py:46-51)."""
+
+    up: object
+    down: object

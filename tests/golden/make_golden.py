@@ -48,6 +48,8 @@ SPARSE_SMALL = [  # (B, Z, L, A, K, N, seed)
 SPARSE_MID = [(1, 2, 256, 64, 64, 2, 61)]
 LAYER_SMALL = [(2, 12, 3, 4, 31)]      # (B, L, Z, A, seed): multi_head_forward / _backward, float64
 LAYER_MID = [(2, 256, 2, 64, 32)]      # bf16-rounded inputs at tensor-core shapes, float32 results
+MLP_SMALL = [(2, 6, 4, 33)]             # (B, L, H, seed): mlp_forward, float64
+MLP_MID = [(2, 128, 128, 34)]           # bf16-rounded inputs, float32 results
 
 
 def draw(shape, seed, n_tensors, rounded):
@@ -109,6 +111,17 @@ def layer_case(b, seq, z, a, seed, rounded):
     return {"y": y, "grad_x": gx, "grad_wq": gw.wq, "grad_wk": gw.wk, "grad_wv": gw.wv, "grad_wo": gw.wo}
 
 
+def mlp_case(b, seq, h, seed, rounded):
+    """The reference's feed-forward block (ringseq/reference.py:177-185, weights :219-224)."""
+    rng = ringseq.make_rng(seed)
+    x = rng.standard_normal((b, seq, h))
+    w = ringseq.random_mlp_weights(h, rng)
+    if rounded:
+        x = bf16_round(x)
+        w = ringseq.MlpWeights(bf16_round(w.up), bf16_round(w.down))
+    return {"y": ringseq.mlp_forward(x, w)}
+
+
 def main():
     arrays = {}
     for case in RSA_SMALL:
@@ -137,6 +150,12 @@ def main():
     for case in LAYER_MID:
         for key, val in layer_case(*case, rounded=True).items():
             arrays["layer_mid/%s/%s" % ("_".join(map(str, case)), key)] = val.astype(np.float32)
+    for case in MLP_SMALL:
+        for key, val in mlp_case(*case, rounded=False).items():
+            arrays["mlp_small/%s/%s" % ("_".join(map(str, case)), key)] = val
+    for case in MLP_MID:
+        for key, val in mlp_case(*case, rounded=True).items():
+            arrays["mlp_mid/%s/%s" % ("_".join(map(str, case)), key)] = val.astype(np.float32)
     out = HERE / "ringseq_golden.npz"
     np.savez_compressed(out, **arrays)
     print(f"wrote {out} ({out.stat().st_size} bytes, {len(arrays)} arrays)")

@@ -479,3 +479,50 @@ def test_negative_overflow_score_raises_numeric_error(rsa, key):
     cfg = _cfg(pkg, 1, 1, 512, 64, 1)
     with pytest.raises(pkg.NumericError):
         ra.ring_attention_forward([q], [k], [v], cfg, path="fused")
+
+
+def test_gelu_kernels_match_torch_fp32(rsa):
+    """rsa_gelu / rsa_gelu_bwd against a plain PyTorch fp32 reference of the same op."""
+    from paper_2105_13120_b200 import tensor_ops as ops
+
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev).manual_seed(3)
+    for n in (4096, 1001):
+        x = 3 * torch.randn(n, generator=gen, device=dev)
+        dy = torch.randn(n, generator=gen, device=dev)
+        want = torch.nn.functional.gelu(x)  # exact (erf) form
+        assert torch.allclose(ops.gelu(x, out_dtype=torch.float32), want, rtol=1e-5, atol=1e-6)
+        xr = x.detach().requires_grad_(True)
+        torch.nn.functional.gelu(xr).backward(dy)
+        got = ops.gelu_backward(x, dy, out_dtype=torch.float32)
+        assert torch.allclose(got, xr.grad, rtol=1e-4, atol=1e-5)
+        xb = x.to(torch.bfloat16)
+        assert torch.allclose(ops.gelu(xb).float(), torch.nn.functional.gelu(xb.float()), rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_mlp_forward_backward(rsa, golden, n):
+    """sequence_parallel_mlp vs the unmodified reference's mlp_forward (golden) and
+    sequence_parallel_mlp_backward vs the oracle's chain rule, on the same bf16 inputs."""
+    pkg, ra = rsa
+    for case, want in golden_cases(golden, "mlp_mid").items():
+        b, seq, h, seed = (int(t) for t in case.split("_"))
+        rng = orc.make_rng(seed)
+        x = orc.bf16_round(rng.standard_normal((b, seq, h)))
+        s = 1.0 / math.sqrt(h)
+        up = orc.bf16_round(rng.standard_normal((h, 4 * h)) * s)
+        down = orc.bf16_round(rng.standard_normal((4 * h, h)) * (s / 2.0))
+        w = pkg.MlpWeights(up, down)
+        y, ledger = ra.sequence_parallel_mlp(orc.chunks_of(x, n), w)
+        got = _np(pkg.gather_sequence(y))
+        assert np.linalg.norm(got - want["y"]) / np.linalg.norm(want["y"]) <= 2e-2
+        assert all(t.total_elements() == 0 for t in ledger.devices)
+        g = orc.bf16_round(orc.make_rng(seed + 1).standard_normal((b, seq, h)))
+        gx, gw, led = ra.sequence_parallel_mlp_backward(orc.chunks_of(x, n), w, orc.chunks_of(g, n))
+        ref = orc.mlp_backward(x, up, down, g, exact=False)
+        for name, val, r in zip(("grad_x", "grad_up", "grad_down"),
+                                (_np(pkg.gather_sequence(gx)), _np(gw.up), _np(gw.down)), ref):
+            rel = np.linalg.norm(val - r) / np.linalg.norm(r)
+            assert rel <= 2e-2, (name, rel)
+        if n > 1:
+            assert all(float(t.allreduce_elements) == 2 * 2 * h * 4 * h * (n - 1) / n for t in led.devices)

@@ -249,3 +249,53 @@ def test_linformer_backward_finite_differences():
             minus = [y - d if i == which else y for i, y in enumerate(args)]
             fd = (loss(plus) - loss(minus)) / (2 * eps)
             assert abs(fd - grad[idx]) <= 1e-6 * max(1.0, abs(fd)), (which, idx, fd, grad[idx])
+
+
+def mlp_inputs(b, seq, h, seed, rounded=False):
+    """x and MlpWeights as tests/golden/make_golden.py:mlp_case draws them
+    (ringseq/reference.py:219-224: up ~ N(0,1)/sqrt(H) of (H, 4H), down ~ N(0,1)/(2 sqrt(H)))."""
+    rng = orc.make_rng(seed)
+    x = rng.standard_normal((b, seq, h))
+    s = 1.0 / math.sqrt(h)
+    up = rng.standard_normal((h, 4 * h)) * s
+    down = rng.standard_normal((4 * h, h)) * (s / 2.0)
+    if rounded:
+        x, up, down = orc.bf16_round(x), orc.bf16_round(up), orc.bf16_round(down)
+    return x, up, down
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_mlp_forward_matches_reference_goldens(golden, exact):
+    cases = golden_cases(golden, "mlp_small")
+    assert cases
+    for case, want in cases.items():
+        b, seq, h, seed = _parse(case)
+        x, up, down = mlp_inputs(b, seq, h, seed)
+        y = orc.mlp_forward(x, up, down, exact=exact)
+        if exact:
+            assert np.array_equal(y, want["y"]), case
+        else:
+            assert np.max(np.abs(y - want["y"])) <= 1e-12
+
+
+def test_mlp_backward_finite_differences():
+    b, seq, h = 1, 5, 3
+    x, up, down = mlp_inputs(b, seq, h, seed=35)
+    g = orc.make_rng(36).standard_normal((b, seq, h))
+    grads = orc.mlp_backward(x, up, down, g, exact=False)
+    args = [x, up, down]
+
+    def loss(xs):
+        return float(np.sum(orc.mlp_forward(*xs, exact=False) * g))
+
+    eps = 1e-6
+    for which, grad in enumerate(grads):
+        arr = args[which]
+        for flat in (0, arr.size // 2, arr.size - 1):
+            idx = np.unravel_index(flat, arr.shape)
+            d = np.zeros_like(arr)
+            d[idx] = eps
+            plus = [y + d if i == which else y for i, y in enumerate(args)]
+            minus = [y - d if i == which else y for i, y in enumerate(args)]
+            fd = (loss(plus) - loss(minus)) / (2 * eps)
+            assert abs(fd - grad[idx]) <= 1e-6 * max(1.0, abs(fd)), (which, idx)
