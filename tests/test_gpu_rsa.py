@@ -526,3 +526,42 @@ def test_mlp_forward_backward(rsa, golden, n):
             assert rel <= 2e-2, (name, rel)
         if n > 1:
             assert all(float(t.allreduce_elements) == 2 * 2 * h * 4 * h * (n - 1) / n for t in led.devices)
+
+
+@pytest.mark.parametrize("n", [1, 2])
+def test_encoder_layer_matches_oracle(rsa, n):
+    """EncoderLayer (x1 = x + MHA(x), y = x1 + MLP(x1)) forward and backward against the
+    oracle composition of multi_head_forward/_backward and mlp_forward/_backward
+    (ringseq/reference.py:122-185) on the same bf16 weights and inputs."""
+    from paper_2105_13120_b200.encoder import EncoderLayer, EncoderWeights
+
+    pkg, _ = rsa
+    b, seq, z, a = 1, 256, 2, 64
+    h = z * a
+    cfg = pkg.AttentionConfig(batch_size=b, seq_len=seq, hidden_size=h, num_heads=z, head_size=a, num_devices=n)
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev).manual_seed(17)
+    w = EncoderWeights.random(cfg, dev, gen)
+    x = torch.randn((b, seq, h), generator=gen, device=dev).to(torch.bfloat16)
+    gy = torch.randn((b, seq, h), generator=gen, device=dev).to(torch.bfloat16)
+    stack = lambda t: torch.stack(torch.chunk(t, n, dim=-2))  # noqa: E731
+    layer = EncoderLayer(cfg, w)
+    y = layer.forward(stack(x))
+    dx, gw = layer.backward(stack(gy))
+    torch.cuda.synchronize()
+    unstack = lambda t: _np(torch.cat(list(t), dim=-2))  # noqa: E731
+    xn, gn = _np(x), _np(gy)
+    wn = {k: _np(getattr(w, k)) for k in ("wq", "wk", "wv", "wo", "up", "down")}
+    x1 = xn + orc.multi_head_forward(xn, wn["wq"], wn["wk"], wn["wv"], wn["wo"], num_heads=z, exact=False)
+    want_y = x1 + orc.mlp_forward(x1, wn["up"], wn["down"], exact=False)
+    gx1_m, g_up, g_down = orc.mlp_backward(x1, wn["up"], wn["down"], gn, exact=False)
+    gx1 = gn + gx1_m
+    gx_a, g_wq, g_wk, g_wv, g_wo = orc.multi_head_backward(xn, wn["wq"], wn["wk"], wn["wv"], wn["wo"], gx1,
+                                                           num_heads=z, exact=False)
+    want = {"y": want_y, "dx": gx1 + gx_a, "wq": g_wq, "wk": g_wk, "wv": g_wv, "wo": g_wo, "up": g_up,
+            "down": g_down}
+    got = {"y": unstack(y), "dx": unstack(dx), **{k: _np(getattr(gw, k)) for k in ("wq", "wk", "wv", "wo", "up",
+                                                                                   "down")}}
+    for key in want:
+        rel = np.linalg.norm(got[key] - want[key]) / np.linalg.norm(want[key])
+        assert rel <= 3e-2, (key, rel)
