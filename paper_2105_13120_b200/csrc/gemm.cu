@@ -32,7 +32,11 @@ struct GemmArgs {
   int a_mn, b_mn;
   int nb2;
   int a_bc1, a_bc2, b_bc1, b_bc2;
-  int n_tiles;
+  int n_tiles;   // N tiles
+  int mn_tiles;  // M tiles * N tiles
+  int batches;
+  int splits;    // split-K slices (1: none); slices of a tile add into C in slice order
+  int* flags;    // per (batch, tile) count of finished slices (split-K only)
   void* C;
   int c_bf16;
   int vec_ok;
@@ -48,36 +52,53 @@ struct GemmSmem {
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr uint32_t TOTAL = BAR_OFF + 256 + 1024;  // barriers + alignment slack
+  static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
 };
 
+struct Work {  // item -> (slice, batch, tile); slice-major, so every slice waits only on earlier items
+  int ks, b1, b2, m0, n0, kb0, kb1, flag;
+};
+
+__device__ __forceinline__ Work work_of(const GemmArgs& p, int item, int kblocks, int bn) {
+  Work w;
+  const int per_split = p.batches * p.mn_tiles;
+  w.ks = item / per_split;
+  const int rem = item % per_split;
+  const int bidx = rem / p.mn_tiles, tile = rem % p.mn_tiles;
+  w.b1 = bidx / p.nb2, w.b2 = bidx % p.nb2;
+  w.m0 = (tile / p.n_tiles) * BM;
+  w.n0 = (tile % p.n_tiles) * bn;
+  const int ksz = (kblocks + p.splits - 1) / p.splits;
+  w.kb0 = w.ks * ksz;
+  w.kb1 = min(kblocks, w.kb0 + ksz);
+  w.flag = rem;
+  return w;
+}
+
+// Persistent, warp-specialised tcgen05 GEMM: warp 0 streams A/B k-blocks through a
+// 4-stage TMA ring, warp 1 issues tcgen05.mma into one of two TMEM accumulators, warps
+// 2..5 drain the other accumulator (warp w owns TMEM lanes 32 * (w % 4) = tile rows),
+// so a tile's epilogue overlaps the next tile's MMAs.
 template <int BN>
-__global__ void __launch_bounds__(128, 1) gemm_tc_kernel(const __grid_constant__ GemmArgs p) {
+__global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__ GemmArgs p) {
   using S = GemmSmem<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
   uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* acc_full = empty + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int tile = blockIdx.x;
-  const int m0 = (tile / p.n_tiles) * BM;
-  const int n0 = (tile % p.n_tiles) * BN;
-  const int bidx = blockIdx.y;
-  const int b1 = bidx / p.nb2, b2 = bidx % p.nb2;
   const int kblocks = (p.K + BK - 1) / BK;
+  const int items = p.splits * p.batches * p.mn_tiles;
 
-  if (warp == 0) tmem_alloc(tmem_slot, BN);
-  if (threadIdx.x == 32) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(done, 1);
+  if (warp == 1) tmem_alloc(tmem_slot, S::TMEM_COLS);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    for (int s = 0; s < 2; ++s) mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], 4);
     fence_barrier_init();
-  }
-  if (threadIdx.x == 64) {
     tma_prefetch(&p.ta);
     tma_prefetch(&p.tb);
   }
@@ -86,99 +107,140 @@ __global__ void __launch_bounds__(128, 1) gemm_tc_kernel(const __grid_constant__
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    const int ab1 = p.a_bc1 ? 0 : b1, ab2 = p.a_bc2 ? 0 : b2;
-    const int bb1 = p.b_bc1 ? 0 : b1, bb2 = p.b_bc2 ? 0 : b2;
-    for (int kb = 0; kb < kblocks; ++kb) {
-      const int s = kb % STAGES;
-      if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
-      mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
-      uint8_t* sa = smem + s * S::STAGE_BYTES;
-      uint8_t* sb = sa + S::A_BYTES;
-      const int k0 = kb * BK;
-      if (!p.a_mn) {
-        tma_load_4d(sa, &p.ta, &full[s], k0, m0, ab2, ab1);
-      } else {
-        tma_load_4d(sa, &p.ta, &full[s], m0, k0, ab2, ab1);
-        tma_load_4d(sa + 8192, &p.ta, &full[s], m0 + 64, k0, ab2, ab1);
-      }
-      if (!p.b_mn) {
-        tma_load_4d(sb, &p.tb, &full[s], k0, n0, bb2, bb1);
-      } else {
-#pragma unroll
-        for (int i = 0; i < BN / 64; ++i) tma_load_4d(sb + i * 8192, &p.tb, &full[s], n0 + 64 * i, k0, bb2, bb1);
-      }
-    }
-  } else if (warp == 1 && lane == 0) {
-    const uint32_t idesc = idesc_bf16_f32(BM, BN, p.a_mn, p.b_mn);
-    for (int kb = 0; kb < kblocks; ++kb) {
-      const int s = kb % STAGES;
-      mbar_wait(&full[s], (kb / STAGES) & 1);
-      tc_fence_after();
-      const uint32_t sa = smem_u32(smem + s * S::STAGE_BYTES);
-      const uint32_t sb = sa + S::A_BYTES;
-#pragma unroll
-      for (int k = 0; k < BK / 16; ++k) {
-        const uint64_t ad = p.a_mn ? smem_desc_sw128(sa + k * 2048, 8192, 1024) : smem_desc_sw128(sa + k * 32, 0, 1024);
-        const uint64_t bd = p.b_mn ? smem_desc_sw128(sb + k * 2048, 8192, 1024) : smem_desc_sw128(sb + k * 32, 0, 1024);
-        umma_bf16(tmem, ad, bd, idesc, (kb | k) != 0);
-      }
-      umma_commit(&empty[s]);
-    }
-    umma_commit(done);
-  }
-  __syncwarp();
-  mbar_wait(done, 0);
-  tc_fence_after();
-
-  const int row = m0 + warp * 32 + lane;
-  const int64_t cbase = int64_t(b1) * p.c_s1 + int64_t(b2) * p.c_s2 + int64_t(row) * p.ldc;
-#pragma unroll 1
-  for (int cc = 0; cc < BN / 32; ++cc) {
-    float v[32];
-    __syncwarp();
-    tmem_ld32(tmem + ((warp * 32u) << 16) + cc * 32, v);
-    tmem_ld_wait();
-    const int col0 = n0 + cc * 32;
-    if (row >= p.M || col0 >= p.N) continue;
-    const bool full_chunk = p.vec_ok && (col0 + 32 <= p.N);
-    if (!p.c_bf16) {
-      float* c = reinterpret_cast<float*>(p.C) + cbase + col0;
-      if (full_chunk) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          float4 o = make_float4(p.alpha * v[i], p.alpha * v[i + 1], p.alpha * v[i + 2], p.alpha * v[i + 3]);
-          if (p.accumulate) {
-            const float4 old = *reinterpret_cast<const float4*>(c + i);
-            o.x += old.x, o.y += old.y, o.z += old.z, o.w += old.w;
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const Work w = work_of(p, item, kblocks, BN);
+        const int ab1 = p.a_bc1 ? 0 : w.b1, ab2 = p.a_bc2 ? 0 : w.b2;
+        const int bb1 = p.b_bc1 ? 0 : w.b1, bb2 = p.b_bc2 ? 0 : w.b2;
+        for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
+          const uint32_t s = it % STAGES;
+          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
+          uint8_t* sa = smem + s * S::STAGE_BYTES;
+          uint8_t* sb = sa + S::A_BYTES;
+          const int k0 = kb * BK;
+          if (!p.a_mn) {
+            tma_load_4d(sa, &p.ta, &full[s], k0, w.m0, ab2, ab1);
+          } else {
+            tma_load_4d(sa, &p.ta, &full[s], w.m0, k0, ab2, ab1);
+            tma_load_4d(sa + 8192, &p.ta, &full[s], w.m0 + 64, k0, ab2, ab1);
           }
-          *reinterpret_cast<float4*>(c + i) = o;
-        }
-      } else {
-        for (int i = 0; i < 32 && col0 + i < p.N; ++i) c[i] = p.alpha * v[i] + (p.accumulate ? c[i] : 0.f);
-      }
-    } else {
-      __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(p.C) + cbase + col0;
-      if (p.accumulate) {
-        for (int i = 0; i < 32; ++i) v[i] = p.alpha * v[i] + ((col0 + i < p.N) ? __bfloat162float(c[i]) : 0.f);
-      } else {
-        for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
-      }
-      if (full_chunk) {
+          if (!p.b_mn) {
+            tma_load_4d(sb, &p.tb, &full[s], k0, w.n0, bb2, bb1);
+          } else {
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint4 o = make_uint4(pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]), pack_bf16(v[i + 4], v[i + 5]),
-                               pack_bf16(v[i + 6], v[i + 7]));
-          *reinterpret_cast<uint4*>(c + i) = o;
+            for (int i = 0; i < BN / 64; ++i) tma_load_4d(sb + i * 8192, &p.tb, &full[s], w.n0 + 64 * i, k0, bb2, bb1);
+          }
         }
-      } else {
-        for (int i = 0; i < 32 && col0 + i < p.N; ++i) c[i] = __float2bfloat16_rn(v[i]);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_bf16_f32(BM, BN, p.a_mn, p.b_mn);
+    uint32_t it = 0, tn = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++tn) {
+      const Work w = work_of(p, item, kblocks, BN);
+      const uint32_t ab = tn & 1;
+      mbar_wait(&acc_empty[ab], ((tn >> 1) & 1) ^ 1);
+      tc_fence_after();
+      for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
+        const uint32_t s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * S::STAGE_BYTES);
+        const uint32_t sb = sa + S::A_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          const uint64_t ad = p.a_mn ? smem_desc_sw128(sa + k * 2048, 8192, 1024) : smem_desc_sw128(sa + k * 32, 0, 1024);
+          const uint64_t bd = p.b_mn ? smem_desc_sw128(sb + k * 2048, 8192, 1024) : smem_desc_sw128(sb + k * 32, 0, 1024);
+          umma_bf16_ws(tmem + ab * BN, ad, bd, idesc, (kb > w.kb0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit_ws(&empty[s]);
+      }
+      umma_commit_ws(&acc_full[ab]);
+    }
+  } else {
+    const uint32_t quad = warp & 3;
+    uint32_t tn = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++tn) {
+      const Work w = work_of(p, item, kblocks, BN);
+      const uint32_t ab = tn & 1;
+      if (p.splits > 1 && w.ks > 0) {  // add into C only after the previous slice has
+        if (threadIdx.x == 64) {
+          volatile int* f = p.flags + w.flag;
+          while (*f < w.ks) __nanosleep(64);
+          __threadfence();
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+      mbar_wait(&acc_full[ab], (tn >> 1) & 1);
+      tc_fence_after();
+      const int row = w.m0 + quad * 32 + lane;
+      const int64_t cbase = int64_t(w.b1) * p.c_s1 + int64_t(w.b2) * p.c_s2 + int64_t(row) * p.ldc;
+      const bool acc = p.accumulate || w.ks > 0;
+#pragma unroll 1
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        float v[32];
+        __syncwarp();
+        tmem_ld32(tmem + ((quad * 32u) << 16) + ab * BN + cc * 32, v);
+        tmem_ld_wait();
+        const int col0 = w.n0 + cc * 32;
+        if (row >= p.M || col0 >= p.N) continue;
+        const bool full_chunk = p.vec_ok && (col0 + 32 <= p.N);
+        if (!p.c_bf16) {
+          float* c = reinterpret_cast<float*>(p.C) + cbase + col0;
+          if (full_chunk) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              float4 o = make_float4(p.alpha * v[i], p.alpha * v[i + 1], p.alpha * v[i + 2], p.alpha * v[i + 3]);
+              if (acc) {
+                const float4 old = *reinterpret_cast<const float4*>(c + i);
+                o.x += old.x, o.y += old.y, o.z += old.z, o.w += old.w;
+              }
+              *reinterpret_cast<float4*>(c + i) = o;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < p.N) c[i] = p.alpha * v[i] + (acc ? c[i] : 0.f);
+          }
+        } else {
+          __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(p.C) + cbase + col0;
+          if (acc) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = p.alpha * v[i] + ((col0 + i < p.N) ? __bfloat162float(c[i]) : 0.f);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
+          }
+          if (full_chunk) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              uint4 o = make_uint4(pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]),
+                                   pack_bf16(v[i + 4], v[i + 5]), pack_bf16(v[i + 6], v[i + 7]));
+              *reinterpret_cast<uint4*>(c + i) = o;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < p.N) c[i] = __float2bfloat16_rn(v[i]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[ab]);
+      if (p.splits > 1 && w.ks + 1 < p.splits) {  // publish this slice to the next one
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 64) atomicAdd(p.flags + w.flag, 1);
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, BN);
+  if (warp == 1) tmem_dealloc(tmem, S::TMEM_COLS);
 }
 
 // ----------------------------------------------------------- SIMT path
@@ -262,6 +324,18 @@ bool operand_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t out
   return encode_tmap(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, ptr, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+int* split_flags(int n, cudaStream_t st) {  // library scratch: per-tile slice counters
+  static int* buf = nullptr;
+  static int cap = 0;
+  if (n > cap) {
+    if (buf) cudaFree(buf);
+    cap = n < 4096 ? 4096 : n;
+    if (cudaMalloc(&buf, sizeof(int) * cap) != cudaSuccess) return buf = nullptr, cap = 0, nullptr;
+  }
+  cudaMemsetAsync(buf, 0, sizeof(int) * n, st);
+  return buf;
+}
+
 template <int BN>
 int launch_tc(GemmArgs& a, int batches, cudaStream_t st) {
   using S = GemmSmem<BN>;
@@ -272,8 +346,19 @@ int launch_tc(GemmArgs& a, int batches, cudaStream_t st) {
   }
   const int mt = (a.M + BM - 1) / BM;
   a.n_tiles = (a.N + BN - 1) / BN;
-  dim3 grid(mt * a.n_tiles, batches);
-  gemm_tc_kernel<BN><<<grid, 128, S::TOTAL, st>>>(a);
+  a.mn_tiles = mt * a.n_tiles;
+  a.batches = batches;
+  const int tiles = a.mn_tiles * batches, sms = num_sms();
+  const int kblocks = (a.K + BK - 1) / BK;
+  a.splits = 1;
+  // split K when the tiles leave most SMs idle and each slice keeps >= 8 k-blocks;
+  // only for fp32 C, where the slices add into C in a fixed order (deterministic)
+  if (!a.c_bf16 && tiles * 2 <= sms && kblocks >= 16) {
+    a.splits = std::min({(sms + tiles - 1) / tiles, kblocks / 8, 8});
+    if (a.splits > 1 && !(a.flags = split_flags(tiles, st))) a.splits = 1;
+  }
+  const int items = tiles * a.splits;
+  gemm_tc_kernel<BN><<<std::min(items, sms), 192, S::TOTAL, st>>>(a);
   return check_launch("gemm_tc_kernel");
 }
 
@@ -283,7 +368,8 @@ int gemm_tc(int M, int N, int K, const void* A, int64_t lda, int ta, int64_t a_s
   if (!aligned16(A) || !aligned16(B) || !stride_ok(lda * 2) || !stride_ok(ldb * 2) || !stride_ok(a_s1 * 2) ||
       !stride_ok(a_s2 * 2) || !stride_ok(b_s1 * 2) || !stride_ok(b_s2 * 2))
     return fail(RSA_ERR_UNSUPPORTED, "gemm: operands not 16-byte aligned for TMA");
-  if (int64_t(nb1) * nb2 > 65535) return fail(RSA_ERR_UNSUPPORTED, "gemm: batch too large");
+  if (int64_t(nb1) * nb2 * ((int64_t(M) + 127) / 128) * ((int64_t(N) + 63) / 64) > (int64_t(1) << 30))
+    return fail(RSA_ERR_UNSUPPORTED, "gemm: too many tiles");
   GemmArgs a{};
   const int BN = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
   a.M = M, a.N = N, a.K = K;
@@ -318,7 +404,8 @@ int gemm_simt(int M, int N, int K, const void* A, int a_dtype, int64_t lda, int 
               const void* B, int b_dtype, int64_t ldb, int tb, int64_t b_s1, int64_t b_s2, void* C, int c_dtype,
               int64_t ldc, int64_t c_s1, int64_t c_s2, int nb1, int nb2, float alpha, int accumulate,
               cudaStream_t st) {
-  if (int64_t(nb1) * nb2 > 65535) return fail(RSA_ERR_UNSUPPORTED, "gemm: batch too large");
+  if (int64_t(nb1) * nb2 * ((int64_t(M) + 127) / 128) * ((int64_t(N) + 63) / 64) > (int64_t(1) << 30))
+    return fail(RSA_ERR_UNSUPPORTED, "gemm: too many tiles");
   SimtArgs p{M, N, K, A, lda, a_s1, a_s2, ta, B, ldb, b_s1, b_s2, tb, C, c_dtype == RSA_BF16, ldc, c_s1, c_s2,
              nb2, alpha, accumulate};
   dim3 grid((N + 15) / 16, (M + 15) / 16, nb1 * nb2);
