@@ -49,6 +49,11 @@ _LAZY = {
     "sequence_parallel_mlp": "ring_attention",
     "sequence_parallel_mlp_backward": "ring_attention",
     "MlpWeights": "weights",
+    "tensor_parallel_attention": "tensor_parallel",
+    "tensor_parallel_mlp": "tensor_parallel",
+    "split_attention_heads": "tensor_parallel",
+    "split_mlp_weights": "tensor_parallel",
+    "ColumnRowSplitWeights": "tensor_parallel",
     "SparseRingForward": "sparse_attention",
     "sparse_ring_attention_forward": "sparse_attention",
     "sparse_ring_attention_backward": "sparse_attention",

@@ -50,6 +50,7 @@ LAYER_SMALL = [(2, 12, 3, 4, 31)]      # (B, L, Z, A, seed): multi_head_forward 
 LAYER_MID = [(2, 256, 2, 64, 32)]      # bf16-rounded inputs at tensor-core shapes, float32 results
 MLP_SMALL = [(2, 6, 4, 33)]             # (B, L, H, seed): mlp_forward, float64
 MLP_MID = [(2, 128, 128, 34)]           # bf16-rounded inputs, float32 results
+TP_MID = [(1, 256, 4, 64, 2, 37), (1, 256, 4, 64, 4, 38)]  # (B, L, Z, A, N, seed): tensor-parallel comparator
 
 
 def draw(shape, seed, n_tensors, rounded):
@@ -122,6 +123,22 @@ def mlp_case(b, seq, h, seed, rounded):
     return {"y": ringseq.mlp_forward(x, w)}
 
 
+def tp_case(b, seq, z, a, n, seed):
+    """The reference's tensor-parallel attention and MLP (ringseq/tensor_parallel.py:79-122), bf16 inputs."""
+    cfg = ringseq.AttentionConfig(batch_size=b, seq_len=seq, hidden_size=z * a, num_heads=z, head_size=a,
+                                  num_devices=n)
+    rng = ringseq.make_rng(seed)
+    x = bf16_round(rng.standard_normal((b, seq, z * a)))
+    w = ringseq.random_attention_weights(cfg, rng)
+    w = ringseq.AttentionWeights(*(bf16_round(m) for m in (w.wq, w.wk, w.wv, w.wo)))
+    mw = ringseq.random_mlp_weights(z * a, rng)
+    mw = ringseq.MlpWeights(bf16_round(mw.up), bf16_round(mw.down))
+    y_att, led = ringseq.tensor_parallel_attention(x, w, cfg)
+    y_mlp, _ = ringseq.tensor_parallel_mlp(x, mw, cfg)
+    return {"y_attention": y_att, "y_mlp": y_mlp,
+            "ledger_ar": np.array([float(t.allreduce_elements) for t in led.devices])}
+
+
 def main():
     arrays = {}
     for case in RSA_SMALL:
@@ -156,6 +173,10 @@ def main():
     for case in MLP_MID:
         for key, val in mlp_case(*case, rounded=True).items():
             arrays["mlp_mid/%s/%s" % ("_".join(map(str, case)), key)] = val.astype(np.float32)
+    for case in TP_MID:
+        for key, val in tp_case(*case).items():
+            arrays["tp_mid/%s/%s" % ("_".join(map(str, case)), key)] = (
+                val.astype(np.float32) if key != "ledger_ar" else val)
     out = HERE / "ringseq_golden.npz"
     np.savez_compressed(out, **arrays)
     print(f"wrote {out} ({out.stat().st_size} bytes, {len(arrays)} arrays)")

@@ -565,3 +565,34 @@ def test_encoder_layer_matches_oracle(rsa, n):
     for key in want:
         rel = np.linalg.norm(got[key] - want[key]) / np.linalg.norm(want[key])
         assert rel <= 3e-2, (key, rel)
+
+
+def test_tensor_parallel_comparator_matches_reference_goldens(rsa, golden):
+    """tensor_parallel_attention / tensor_parallel_mlp (ringseq/tensor_parallel.py:79-122) against
+    the unmodified reference on the same bf16 inputs, with the all-reduce ledger exact."""
+    from paper_2105_13120_b200 import tensor_parallel as tp
+
+    pkg, _ = rsa
+    cases = golden_cases(golden, "tp_mid")
+    assert len(cases) == 2
+    for case, want in cases.items():
+        b, seq, z, a, n, seed = (int(t) for t in case.split("_"))
+        h = z * a
+        cfg = pkg.AttentionConfig(batch_size=b, seq_len=seq, hidden_size=h, num_heads=z, head_size=a, num_devices=n)
+        rng = orc.make_rng(seed)
+        x = orc.bf16_round(rng.standard_normal((b, seq, h)))
+        s = 1.0 / math.sqrt(h)
+        ws = [orc.bf16_round(rng.standard_normal((h, h)) * s) for _ in range(4)]
+        up = orc.bf16_round(rng.standard_normal((h, 4 * h)) * s)
+        down = orc.bf16_round(rng.standard_normal((4 * h, h)) * (s / 2.0))
+        y, led = tp.tensor_parallel_attention(x, pkg.AttentionWeights(*ws), cfg)
+        rel = np.linalg.norm(_np(y) - want["y_attention"]) / np.linalg.norm(want["y_attention"])
+        assert rel <= 2e-2, rel
+        assert [float(t.allreduce_elements) for t in led.devices] == list(want["ledger_ar"])
+        ym, _ = tp.tensor_parallel_mlp(x, pkg.MlpWeights(up, down), cfg)
+        rel = np.linalg.norm(_np(ym) - want["y_mlp"]) / np.linalg.norm(want["y_mlp"])
+        assert rel <= 2e-2, rel
+    with pytest.raises(pkg.ConfigError):
+        tp.tensor_parallel_attention(x, pkg.AttentionWeights(*ws),
+                                     pkg.AttentionConfig(batch_size=b, seq_len=seq, hidden_size=h, num_heads=z,
+                                                         head_size=a, num_devices=3))
