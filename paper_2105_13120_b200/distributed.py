@@ -134,9 +134,16 @@ class RingContext:
 class SpmdRing:
     """One rank's view of the RSA ring over a torch.distributed process group."""
 
-    def __init__(self, group=None, kernels=None, mode: str = "reduce_scatter", overlap: bool = True):
+    def __init__(self, group=None, kernels=None, mode: str = "reduce_scatter", overlap: bool = True,
+                 transport: str = "device"):
+        """``transport="host"`` stages every hop and reduction through host memory, for
+        process groups whose backend cannot move device tensors point to point (gloo);
+        the default sends the device buffers themselves (NCCL over NVLink)."""
         if mode not in ("reduce_scatter", "paper"):
             raise ValueError(f"unknown mode {mode!r}")
+        if transport not in ("device", "host"):
+            raise ValueError(f"unknown transport {transport!r}")
+        self.host_staged = transport == "host"
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
@@ -152,14 +159,23 @@ class SpmdRing:
         n = self.world
         nxt = dist.get_global_rank(self.group, (self.rank + 1) % n) if self.group else (self.rank + 1) % n
         prv = dist.get_global_rank(self.group, (self.rank - 1) % n) if self.group else (self.rank - 1) % n
-        ops = [dist.P2POp(dist.isend, send, nxt, self.group), dist.P2POp(dist.irecv, recv, prv, self.group)]
         self.ledger.record_ring_send(self.rank, send.numel(), send.numel() * send.element_size())
-        return dist.batch_isend_irecv(ops)
+        if self.host_staged and send.is_cuda:
+            s_h, r_h = send.cpu(), torch.empty(recv.shape, dtype=recv.dtype)
+            ops = [dist.P2POp(dist.isend, s_h, nxt, self.group), dist.P2POp(dist.irecv, r_h, prv, self.group)]
+            return (dist.batch_isend_irecv(ops), recv, r_h, s_h)
+        ops = [dist.P2POp(dist.isend, send, nxt, self.group), dist.P2POp(dist.irecv, recv, prv, self.group)]
+        return (dist.batch_isend_irecv(ops), None, None, None)
 
     @staticmethod
-    def _wait(works):
-        for w in works or ():
+    def _wait(pending):
+        if not pending:
+            return
+        works, recv, r_h, _ = pending
+        for w in works:
             w.wait()
+        if recv is not None:
+            recv.copy_(r_h)
 
     def _circulate(self, slots: torch.Tensor, on_arrival):
         """Run the ring over per-origin ``slots`` ([N][...]); slot d must hold
@@ -248,7 +264,11 @@ class SpmdRing:
         kdim = e_cols.shape[0]
         low = kern.project_pair(e_cols, k[0], f_cols, v[0])  # [2][B][Z][K][A] accumulator dtype
         self.ledger.record_ring_send(d, 2 * (n - 1) * b * z * kdim * a)
-        if n > 1:
+        if n > 1 and self.host_staged and low.is_cuda:
+            host = low.cpu()
+            dist.all_reduce(host, group=self.group)
+            low.copy_(host)
+        elif n > 1:
             dist.all_reduce(low, group=self.group)
             self.ledger.devices[d].wire_bytes += 2 * low.numel() * low.element_size() * (n - 1) // n
         return kern.low_rank_attention(q, low[0], low[1])
@@ -265,7 +285,12 @@ class SpmdRing:
             dist.reduce_scatter_tensor(out, part, group=self.group)
             self.ledger.devices[d].wire_bytes += part.numel() * part.element_size() * (n - 1) // n
             return out
-        dist.all_reduce(part, group=self.group)
+        if self.host_staged and part.is_cuda:
+            host = part.cpu()
+            dist.all_reduce(host, group=self.group)
+            part.copy_(host)
+        else:
+            dist.all_reduce(part, group=self.group)
         self.ledger.devices[d].wire_bytes += 2 * part.numel() * part.element_size() * (n - 1) // n
         return part[d:d + 1].clone()
 

@@ -1,0 +1,103 @@
+"""The SPMD ring (distributed.SpmdRing) with its real sm_100a per-hop kernels.
+
+Two or three processes share cuda:0 and talk over gloo with host-staged hops
+(``transport="host"``), so the CUDA hop kernels -- rsa_fwd_stats / rsa_fwd_probs_pv per
+arriving origin, rsa_bwd_dkdv / rsa_bwd_dq per hop with fp32 cross-hop accumulation, the
+dK/dV partial all-reduce, and the Linformer projection all-reduce -- run exactly as on N
+GPUs, against the float64 oracle (tests/test_distributed_gloo.py checks the same schedule
+with a float64 double of the kernels).  Tolerances as in test_gpu_rsa.py.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import ringseq_np as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _inputs(b, z, seq, a, seed):
+    rng = orc.make_rng(seed)
+    return [orc.bf16_round(rng.standard_normal((b, z, seq, a))) for _ in range(4)]
+
+
+def _worker(rank, world, port, shape, seed, mode, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from paper_2105_13120_b200.distributed import SpmdRing
+
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        b, z, seq, a = shape
+        q, k, v, g = _inputs(b, z, seq, a, seed)
+        ch = lambda x: torch.from_numpy(orc.chunks_of(x, world)[rank][None].copy()).to(dev, torch.bfloat16)  # noqa
+        ring = SpmdRing(mode=mode, transport="host")
+        out, ctx = ring.forward(ch(q), ch(k), ch(v))
+        dq, dk, dv = ring.backward(ctx, ch(g))
+        # Linformer: this rank's column blocks of E / F
+        kp = 32
+        rng = orc.make_rng(seed + 5)
+        e = orc.bf16_round(rng.standard_normal((kp, seq)) / math.sqrt(seq))
+        f = orc.bf16_round(rng.standard_normal((kp, seq)) / math.sqrt(seq))
+        c = seq // world
+        cols = lambda m: torch.from_numpy(m[:, rank * c:(rank + 1) * c].copy()).to(dev, torch.bfloat16)  # noqa
+        lin = ring.linformer_forward(ch(q), ch(k), ch(v), cols(e), cols(f))
+        torch.cuda.synchronize()
+        f64 = lambda t: t.float().cpu().numpy().astype(np.float64)  # noqa: E731
+        results[rank] = {"out": f64(out[0]), "panel": f64(ctx.panel[0]), "dq": f64(dq[0]), "dk": f64(dk[0]),
+                         "dv": f64(dv[0]), "lin": f64(lin[0] if lin.dim() == 5 else lin),
+                         "ring": ring.ledger.devices[rank].ring_p2p_elements,
+                         "flag": int(ctx.extra["flag"].item())}
+    finally:
+        dist.destroy_process_group()
+
+
+def _rel(x, y):
+    return np.linalg.norm(x - y) / np.linalg.norm(y)
+
+
+@pytest.mark.parametrize("world,mode,shape", [(2, "reduce_scatter", (1, 2, 256, 64)), (3, "paper", (1, 2, 384, 64)),
+                                              (2, "paper", (2, 1, 400, 64))])
+def test_spmd_ring_cuda_kernels_match_oracle(world, mode, shape):
+    seed = 40 + world
+    mgr = mp.get_context("spawn").Manager()
+    results = mgr.dict()
+    mp.start_processes(_worker, args=(world, _free_port(), shape, seed, mode, results), nprocs=world, join=True,
+                       start_method="spawn")
+    b, z, seq, a = shape
+    q, k, v, g = _inputs(b, z, seq, a, seed)
+    ch = lambda x: orc.chunks_of(x, world)  # noqa: E731
+    outs, probs, _ = orc.ring_forward(ch(q), ch(k), ch(v), exact=False)
+    dq, dk, dv, _ = orc.ring_backward(ch(q), ch(k), ch(v), probs, ch(g), exact=False)
+    rng = orc.make_rng(seed + 5)
+    e = orc.bf16_round(rng.standard_normal((32, seq)) / math.sqrt(seq))
+    f = orc.bf16_round(rng.standard_normal((32, seq)) / math.sqrt(seq))
+    lin, _ = orc.sparse_ring_forward(ch(q), ch(k), ch(v), e, f, exact=False)
+    for d in range(world):
+        r = results[d]
+        assert r["flag"] == 0
+        assert _rel(r["out"], outs[d]) <= 1e-2
+        assert np.max(np.abs(r["panel"] - probs[d])) <= 4e-3
+        for name, want in (("dq", dq[d]), ("dk", dk[d]), ("dv", dv[d]), ("lin", lin[d])):
+            assert _rel(r[name], want) <= 1e-2, (d, name, _rel(r[name], want))
+        assert r["ring"] == 4 * (world - 1) * b * z * (seq // world) * a + 2 * (world - 1) * b * z * 32 * a
