@@ -223,6 +223,30 @@ int rsa_bwd_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_vie
                   int dkv_dtype, int accumulate_dkv, void* stream);
 int rsa_bwd_fused_supported(const rsa_geom* g);
 
+/* --------------------------------------------- peer-resident origins (NVLink) */
+
+#define RSA_MAX_PEERS 8
+
+/*
+ * One rank's whole RSA forward / backward with every origin's K and V chunk read
+ * in place from the rank that owns it -- device pointers opened through CUDA IPC
+ * (CUDA IPC), so on an NVSwitch box the tiles stream over NVLink inside the
+ * kernel's TMA pipeline instead of travelling a ring of NCCL hops (the K/V rings of
+ * ringseq/ring_attention.py:124-217).  g: n_rank = 1 (this rank's query chunk),
+ * org_lo = 0, n_org = N <= RSA_MAX_PEERS; k_origin[j] / v_origin[j] view origin j's
+ * [1][B][Z][c][A] chunk (the Python host opens peers' buffers with torch's CUDA IPC,
+ * paper_2105_13120_b200/distributed.py:PeerRing).  The forward is rsa_fwd_factored's single pass (factored
+ * panel, row scale); the backward is rsa_bwd_fused's single pass with fp32 dK / dV
+ * partials for every origin ([N][B][Z][c][A], dk_part / dv_part) left for the
+ * caller's reduce-scatter (the reference's all-reduce + slice, :206-209).
+ */
+int rsa_fwd_factored_peer(const rsa_geom* g, rsa_view q, const rsa_view* k_origin, const rsa_view* v_origin,
+                          rsa_view panel, rsa_view o_out, float* rowscale, int* flag, void* stream);
+int rsa_bwd_fused_peer(const rsa_geom* g, rsa_view q, const rsa_view* k_origin, const rsa_view* v_origin,
+                       rsa_view dout, rsa_view panel, const float* dvec, rsa_view dq_out, rsa_view dk_part,
+                       rsa_view dv_part, void* stream);
+
+
 #ifdef __cplusplus
 }
 #endif

@@ -93,6 +93,8 @@ EXPORTS = {
     "rsa_fwd_probs_pv": (c_int, [_GEOM, _V, _V, _V, c_void_p, c_int, _V, _V, c_int, _V, c_void_p]),
     "rsa_fwd_resident": (c_int, [_GEOM, _V, _V, _V, _V, _V, c_void_p, c_void_p]),
     "rsa_fwd_factored": (c_int, [_GEOM, _V, _V, _V, _V, _V, c_void_p, c_void_p, c_void_p]),
+    "rsa_fwd_factored_peer": (c_int, [_GEOM, _V, _P(RsaView), _P(RsaView), _V, _V, c_void_p, c_void_p, c_void_p]),
+    "rsa_bwd_fused_peer": (c_int, [_GEOM, _V, _P(RsaView), _P(RsaView), _V, _V, c_void_p, _V, _V, _V, c_void_p]),
     "rsa_bwd_dkdv": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, _V, _V, c_int, c_int, c_void_p]),
     "rsa_bwd_dq": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, _V, c_int, _V, c_void_p]),
     "rsa_fused_supported": (c_int, [_GEOM]),

@@ -27,6 +27,7 @@
 // tiles 3 deep (the only HBM stream that matters; dO/Q re-reads are L2 hits).  dS overwrites P in place once P^T dO has consumed it.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "fused_common.cuh"
 
@@ -38,6 +39,8 @@ constexpr int MAX_QT = 4;  // query tiles per head that fit the dQ columns of TM
 struct BwdArgs {
   CUtensorMap tq, tk, tv, tdo, tp, tdk, tdv;
   int kv_tma;  // bf16, non-accumulating dK/dV: staged in the retiring P slot and TMA-stored
+  int peer;    // K / V of origin j from pm.k[j] / pm.v[j] (rsa_bwd_fused_peer)
+  PeerMaps pm;
   Geo g;
   const float* dvec;
   OutView dq_acc, dq_out, dk, dv;
@@ -133,8 +136,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
       auto load_vk = [&](int item, int kk) {
         const int b = item / g.Z, z = item % g.Z;
         const int jo = kk / ntk, k0 = (kk % ntk) * TK;
-        load_tile(rv, vq, BF_V, BF_OFF_V, &p.tv, k0, z, jo * g.B + b);
-        load_tile(rk, kq, BF_K, BF_OFF_K, &p.tk, k0, z, jo * g.B + b);
+        load_tile(rv, vq, BF_V, BF_OFF_V, p.peer ? &p.pm.v[jo] : &p.tv, k0, z, p.peer ? b : jo * g.B + b);
+        load_tile(rk, kq, BF_K, BF_OFF_K, p.peer ? &p.pm.k[jo] : &p.tk, k0, z, p.peer ? b : jo * g.B + b);
       };
       if (blockIdx.x < items) load_vk(blockIdx.x, 0);
       for (int item = blockIdx.x; item < items; item += gridDim.x) {
@@ -476,6 +479,30 @@ int rsa_bwd_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_vie
     if (FILE* f = fopen(trace_path, "wb")) fwrite(host, sizeof(host), 1, f), fclose(f);
   }
   return rc;
+}
+
+int rsa_bwd_fused_peer(const rsa_geom* g, rsa_view q, const rsa_view* k_origin, const rsa_view* v_origin,
+                       rsa_view dout, rsa_view panel, const float* dvec, rsa_view dq_out, rsa_view dk_part,
+                       rsa_view dv_part, void* stream) {
+  using namespace rsa;
+  if (!bwd_fused_geom_ok(g) || !dvec || !k_origin || !v_origin)
+    return fail(RSA_ERR_INVALID, "rsa_bwd_fused_peer: unsupported geometry (need A=64, c%%8==0, ceil(c/128)<=4)");
+  if (g->n_rank != 1 || g->org_lo != 0 || g->n_org != g->seq_len / g->chunk)
+    return fail(RSA_ERR_INVALID, "rsa_bwd_fused_peer: need n_rank = 1, org_lo = 0, n_org = L / c");
+  if (!dk_part.ptr || !dv_part.ptr || !out_ok(dk_part, 4) || !out_ok(dv_part, 4) || !dq_out.ptr || !out_ok(dq_out, 2))
+    return fail(RSA_ERR_UNSUPPORTED, "rsa_bwd_fused_peer: output views missing or misaligned");
+  BwdArgs a{};
+  a.peer = 1;
+  if (!peer_maps(&a.pm, k_origin, v_origin, g) || !head_map(&a.tq, q, g, 1) || !head_map(&a.tdo, dout, g, 1) ||
+      !panel_map(&a.tp, panel, g, 1))
+    return RSA_ERR_UNSUPPORTED;
+  a.g = to_geo(g);
+  a.dvec = dvec;
+  a.dq_out = to_out(dq_out);
+  a.dk = to_out(dk_part);
+  a.dv = to_out(dv_part);
+  a.dkv_bf16 = 0;  // fp32 partials of every origin, reduce-scattered by the caller
+  return launch(bwd_fused_kernel, g->batch * g->heads, BF_SMEM, a, stream, "bwd_fused_kernel");
 }
 
 }  // extern "C"

@@ -145,6 +145,20 @@ inline bool panel_map(CUtensorMap* m, const rsa_view& v, const rsa_geom* g, int 
   return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, v.ptr, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+// Per-origin K / V maps for peer-resident origins (one rank's chunk each, possibly in
+// another GPU's memory through CUDA IPC / UVA): origin j's tile (k0, z, b) is
+// map[j] at coordinates (0, k0, z, b).
+struct PeerMaps {
+  CUtensorMap k[RSA_MAX_PEERS], v[RSA_MAX_PEERS];
+};
+
+inline bool peer_maps(PeerMaps* pm, const rsa_view* k, const rsa_view* v, const rsa_geom* g) {
+  if (g->n_org > RSA_MAX_PEERS) return fail(RSA_ERR_UNSUPPORTED, "peer kernels: at most %d origins", RSA_MAX_PEERS), false;
+  for (int j = 0; j < g->n_org; ++j)
+    if (!head_map(&pm->k[j], k[j], g, 1) || !head_map(&pm->v[j], v[j], g, 1)) return false;
+  return true;
+}
+
 inline OutView to_out(const rsa_view& v) { return OutView{v.ptr, v.s_rank, v.s_b, v.s_z, v.s_row}; }
 
 inline bool out_ok(const rsa_view& v, int esz) {

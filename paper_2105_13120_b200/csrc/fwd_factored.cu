@@ -48,6 +48,8 @@ struct FfArgs {
   int* flag;
   float* rowscale;   // [rank][b][z][c]
   long long* trace;  // RSA_FF_TRACE: per-warp (event, clock) log of CTA 0 (timeline experiments)
+  int peer;          // K / V of origin j from pm.k[j] / pm.v[j] (rsa_fwd_factored_peer)
+  PeerMaps pm;
 };
 
 constexpr int FF_GROUPS = 2;
@@ -243,7 +245,8 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
             const int jo = t / ntk, k0 = (t % ntk) * TK;
             mbar_wait(&k_empty[t], (kgen & 1) ^ 1);
             mbar_arrive_expect_tx(&k_full[t], TILE);
-            tma_load_4d(smem + FF_OFF_K + t * TILE, &p.tk, &k_full[t], 0, k0, z, (g.org_lo + jo) * g.B + b);
+            tma_load_4d(smem + FF_OFF_K + t * TILE, p.peer ? &p.pm.k[jo] : &p.tk, &k_full[t], 0, k0, z,
+                        p.peer ? b : (g.org_lo + jo) * g.B + b);
           }
           ++kgen;
         }
@@ -254,13 +257,15 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
             const uint32_t ks = kq.slot(FF_KST);
             mbar_wait(&k_empty[ks], kq.phase(FF_KST) ^ 1);
             mbar_arrive_expect_tx(&k_full[ks], TILE);
-            tma_load_4d(smem + FF_OFF_K + ks * TILE, &p.tk, &k_full[ks], 0, k0, z, (g.org_lo + jo) * g.B + b);
+            tma_load_4d(smem + FF_OFF_K + ks * TILE, p.peer ? &p.pm.k[jo] : &p.tk, &k_full[ks], 0, k0, z,
+                        p.peer ? b : (g.org_lo + jo) * g.B + b);
             ++kq.i;
           }
           const uint32_t vs = vq.slot(FF_VST);
           mbar_wait(&v_empty[vs], vq.phase(FF_VST) ^ 1);
           mbar_arrive_expect_tx(&v_full[vs], TILE);
-          tma_load_4d(smem + FF_OFF_V + vs * TILE, &p.tv, &v_full[vs], 0, k0, z, (g.org_lo + jo) * g.B + b);
+          tma_load_4d(smem + FF_OFF_V + vs * TILE, p.peer ? &p.pm.v[jo] : &p.tv, &v_full[vs], 0, k0, z,
+                      p.peer ? b : (g.org_lo + jo) * g.B + b);
           ++vq.i;
         }
       }
@@ -509,19 +514,15 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
 }  // namespace
 }  // namespace rsa
 
-extern "C" {
+namespace rsa {
+namespace {
 
-int rsa_fwd_factored(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view panel, rsa_view o_out,
-                     float* rowscale, int* flag, void* stream) {
-  using namespace rsa;
-  if (!geom_ok(g)) return fail(RSA_ERR_INVALID, "rsa_fwd_factored: unsupported geometry");
-  if (g->org_lo != 0 || g->n_org != g->seq_len / g->chunk)
-    return fail(RSA_ERR_INVALID, "rsa_fwd_factored: every origin must be resident (org_lo = 0, n_org = L / c)");
+int ff_launch(FfArgs& a, const rsa_geom* g, rsa_view q, rsa_view panel, rsa_view o_out, float* rowscale, int* flag,
+              void* stream) {
   if (!rowscale || !flag || !o_out.ptr || !out_ok(o_out, 2))
     return fail(RSA_ERR_UNSUPPORTED, "rsa_fwd_factored: output / row-scale / flag buffers missing or misaligned");
-  FfArgs a{};
-  if (!head_map(&a.tq, q, g, g->n_rank) || !head_map(&a.tk, k, g, g->n_org) || !head_map(&a.tv, v, g, g->n_org) ||
-      !panel_map(&a.tp, panel, g, g->n_rank, 32) || !head_map(&a.to, o_out, g, g->n_rank))
+  if (!head_map(&a.tq, q, g, g->n_rank) || !panel_map(&a.tp, panel, g, g->n_rank, 32) ||
+      !head_map(&a.to, o_out, g, g->n_rank))
     return RSA_ERR_UNSUPPORTED;
   a.g = to_geo(g);
   a.sl = g->scale * LOG2E;
@@ -550,6 +551,34 @@ int rsa_fwd_factored(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_
     if (FILE* f = fopen(trace_path, "wb")) fwrite(host, sizeof(host), 1, f), fclose(f);
   }
   return check_launch("fwd_factored_kernel");
+}
+
+}  // namespace
+}  // namespace rsa
+
+extern "C" {
+
+int rsa_fwd_factored(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view panel, rsa_view o_out,
+                     float* rowscale, int* flag, void* stream) {
+  using namespace rsa;
+  if (!geom_ok(g)) return fail(RSA_ERR_INVALID, "rsa_fwd_factored: unsupported geometry");
+  if (g->org_lo != 0 || g->n_org != g->seq_len / g->chunk)
+    return fail(RSA_ERR_INVALID, "rsa_fwd_factored: every origin must be resident (org_lo = 0, n_org = L / c)");
+  FfArgs a{};
+  if (!head_map(&a.tk, k, g, g->n_org) || !head_map(&a.tv, v, g, g->n_org)) return RSA_ERR_UNSUPPORTED;
+  return ff_launch(a, g, q, panel, o_out, rowscale, flag, stream);
+}
+
+int rsa_fwd_factored_peer(const rsa_geom* g, rsa_view q, const rsa_view* k_origin, const rsa_view* v_origin,
+                          rsa_view panel, rsa_view o_out, float* rowscale, int* flag, void* stream) {
+  using namespace rsa;
+  if (!geom_ok(g) || !k_origin || !v_origin) return fail(RSA_ERR_INVALID, "rsa_fwd_factored_peer: bad arguments");
+  if (g->n_rank != 1 || g->org_lo != 0 || g->n_org != g->seq_len / g->chunk)
+    return fail(RSA_ERR_INVALID, "rsa_fwd_factored_peer: need n_rank = 1, org_lo = 0, n_org = L / c");
+  FfArgs a{};
+  a.peer = 1;
+  if (!peer_maps(&a.pm, k_origin, v_origin, g)) return RSA_ERR_UNSUPPORTED;
+  return ff_launch(a, g, q, panel, o_out, rowscale, flag, stream);
 }
 
 }  // extern "C"

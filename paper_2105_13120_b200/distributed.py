@@ -42,7 +42,7 @@ import torch.distributed as dist
 
 from .cluster import CommLedger
 
-__all__ = ["SpmdRing", "CudaHopKernels", "RingContext", "bench_main"]
+__all__ = ["SpmdRing", "PeerRing", "CudaHopKernels", "RingContext", "bench_main"]
 
 
 def _acc_dtype(t: torch.Tensor) -> torch.dtype:
@@ -147,7 +147,7 @@ class SpmdRing:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        self.kernels = kernels or CudaHopKernels()
+        self.kernels = CudaHopKernels() if kernels is None else kernels  # False: communication only
         self.mode = mode
         self.overlap = overlap
         self.ledger = CommLedger(self.world)
@@ -293,6 +293,135 @@ class SpmdRing:
             dist.all_reduce(part, group=self.group)
         self.ledger.devices[d].wire_bytes += 2 * part.numel() * part.element_size() * (n - 1) // n
         return part[d:d + 1].clone()
+
+
+class _PeerSlot:
+    """One registered K/V buffer: this rank's [2][B][Z][c][A] chunk pair and every peer's,
+    opened through torch's CUDA IPC (the device pointers a peer kernel reads over NVLink)."""
+
+    def __init__(self, local: torch.Tensor, peers: list):
+        self.local, self.peers = local, peers
+
+
+class PeerRing:
+    """Ring-free RSA across the ranks of one NVLink/NVSwitch box.
+
+    Every rank stages its K/V chunk in a registered buffer that all ranks have opened
+    through CUDA IPC; one ``rsa_fwd_factored_peer`` launch then reads every origin's
+    K/V tiles in place -- TMA loads from the owner's HBM over NVLink inside the kernel's
+    pipeline, overlapped with the tensor-core work -- instead of N-1 ring hops with one
+    kernel launch each.  The backward is one ``rsa_bwd_fused_peer`` launch (dQ complete,
+    fp32 dK/dV partials for every origin) and a reduce-scatter of the partials, as in
+    ``SpmdRing``.  The panel is the factored one.  The ledger
+    charges the reference's ring convention (ringseq/ring_attention.py:124-217) for the
+    same K/V bytes.
+
+    This is the correctness-first form: staging is fenced by host barriers (buffer free
+    on every rank, then staged on every rank).  Cross-process CUDA IPC events would
+    replace them.
+    """
+
+    def __init__(self, group=None, mode: str = "reduce_scatter", transport: str = "device"):
+        self.ring = SpmdRing(group, mode=mode, transport=transport, kernels=False)
+        self.group, self.rank, self.world = group, self.ring.rank, self.ring.world
+        self.ledger = self.ring.ledger
+        self._free: dict = {}
+
+    def _barrier(self):
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+
+    def _slot(self, shape, dtype, dev) -> _PeerSlot:
+        key = (tuple(shape), dtype)
+        pool = self._free.setdefault(key, [])
+        if pool:
+            return pool.pop()
+        local = torch.empty((2,) + tuple(shape), dtype=dtype, device=dev)
+        share = local.untyped_storage()._share_cuda_()
+        shares = [None] * self.world
+        dist.all_gather_object(shares, share, group=self.group)
+        peers = []
+        for j, sh in enumerate(shares):
+            if j == self.rank:
+                peers.append(local)
+                continue
+            st = torch.UntypedStorage._new_shared_cuda(*sh)
+            t = torch.empty(0, dtype=dtype, device=dev)
+            t.set_(st, 0, local.shape, local.stride())
+            peers.append(t)
+        return _PeerSlot(local, peers)
+
+    def _views(self, slot: _PeerSlot, which: int):
+        from .engine import _view
+
+        views = (self.ring_view_type * self.world)()
+        for j, t in enumerate(slot.peers):
+            views[j] = _view(t[which].unsqueeze(0))
+        return views
+
+    @property
+    def ring_view_type(self):
+        from ._native import RsaView
+
+        return RsaView
+
+    def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, flag: torch.Tensor | None = None):
+        """q/k/v: this rank's [1][B][Z][c][A] bf16 chunks.  Returns (out, ctx)."""
+        from . import engine
+        from ._native import check, lib
+
+        n, d = self.world, self.rank
+        _, b, z, c, a = q.shape
+        seq = n * c
+        dev = q.device
+        if flag is None:
+            flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        slot = self._slot((b, z, c, a), k.dtype, dev)
+        self._barrier()  # no rank still reads this buffer (a released slot of an earlier layer)
+        slot.local[0].copy_(k[0])
+        slot.local[1].copy_(v[0])
+        self._barrier()  # every origin is staged
+        panel = torch.empty((1, b, z, c, seq), dtype=torch.bfloat16, device=dev)
+        out = torch.empty((1, b, z, c, a), dtype=torch.bfloat16, device=dev)
+        rowscale = torch.empty((1, b, z, c), dtype=torch.float32, device=dev)
+        g = engine._geom(1, b, z, c, a, seq, 0, n)
+        check(lib().rsa_fwd_factored_peer(ctypes.byref(g), engine._view(q), self._views(slot, 0), self._views(slot, 1),
+                                          engine._view(panel), engine._view(out), rowscale.data_ptr(),
+                                          flag.data_ptr(), torch.cuda.current_stream(dev).cuda_stream),
+              "rsa_fwd_factored_peer")
+        elements = b * z * c * a
+        self.ledger.record_ring_send(d, 2 * (n - 1) * elements, 2 * (n - 1) * elements * q.element_size())
+        return out, RingContext(q=q, k_slots=None, panel=panel, out=out, v_local=v,
+                                extra={"flag": flag, "rowscale": rowscale, "slot": slot})
+
+    def backward(self, ctx: RingContext, grad: torch.Tensor):
+        """grad: this rank's [1][B][Z][c][A] dO.  Returns (dq, dk, dv) chunks."""
+        from . import engine
+        from . import tensor_ops as ops
+        from ._native import check, lib
+
+        n, d = self.world, self.rank
+        _, b, z, c, a = grad.shape
+        seq = n * c
+        dev = grad.device
+        slot = ctx.extra["slot"]
+        dvec, grad_r = ops.rowdot_scale(grad, ctx.out, ctx.extra["rowscale"])  # D*r and dO*r (factored panel)
+        dq = torch.empty((1, b, z, c, a), dtype=torch.bfloat16, device=dev)
+        dk_part = torch.empty((n, b, z, c, a), dtype=torch.float32, device=dev)
+        dv_part = torch.empty_like(dk_part)
+        g = engine._geom(1, b, z, c, a, seq, 0, n)
+        if not lib().rsa_bwd_fused_supported(ctypes.byref(g)):
+            raise ValueError(f"PeerRing backward needs <= 4 query tiles per rank (c = {c})")
+        check(lib().rsa_bwd_fused_peer(ctypes.byref(g), engine._view(ctx.q), self._views(slot, 0),
+                                       self._views(slot, 1), engine._view(grad_r), engine._view(ctx.panel),
+                                       dvec.data_ptr(), engine._view(dq), engine._view(dk_part),
+                                       engine._view(dv_part), torch.cuda.current_stream(dev).cuda_stream),
+              "rsa_bwd_fused_peer")
+        self.ledger.record_ring_send(d, 2 * (n - 1) * b * z * c * a, 2 * (n - 1) * b * z * c * a * 2)
+        dk = self.ring._reduce(dk_part)
+        dv = self.ring._reduce(dv_part)
+        self._free.setdefault((tuple(slot.local.shape[1:]), slot.local.dtype), []).append(slot)
+        return dq, dk.to(grad.dtype), dv.to(grad.dtype)
 
 
 # ------------------------------------------------------------------ bench

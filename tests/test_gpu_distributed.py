@@ -101,3 +101,63 @@ def test_spmd_ring_cuda_kernels_match_oracle(world, mode, shape):
         for name, want in (("dq", dq[d]), ("dk", dk[d]), ("dv", dv[d]), ("lin", lin[d])):
             assert _rel(r[name], want) <= 1e-2, (d, name, _rel(r[name], want))
         assert r["ring"] == 4 * (world - 1) * b * z * (seq // world) * a + 2 * (world - 1) * b * z * 32 * a
+
+
+def _peer_worker(rank, world, port, shape, seed, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from paper_2105_13120_b200 import engine
+        from paper_2105_13120_b200.distributed import PeerRing
+
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        b, z, seq, a = shape
+        q, k, v, g = _inputs(b, z, seq, a, seed)
+        ch = lambda x: torch.from_numpy(orc.chunks_of(x, world)[rank][None].copy()).to(dev, torch.bfloat16)  # noqa
+        ring = PeerRing(transport="host")
+        outs = []
+        for layer in range(2):  # two layers in flight: two registered slots, then reuse
+            out, ctx = ring.forward(ch(q), ch(k), ch(v))
+            outs.append((out, ctx))
+        dq, dk, dv = ring.backward(outs[1][1], ch(g))
+        dq0, dk0, dv0 = ring.backward(outs[0][1], ch(g))
+        out, ctx = ring.forward(ch(q), ch(k), ch(v))  # reuses a released slot
+        torch.cuda.synchronize()
+        f64 = lambda t: t.float().cpu().numpy().astype(np.float64)  # noqa: E731
+        probs = engine.normalized_panel(ctx.panel[0], ctx.extra["rowscale"][0])
+        results[rank] = {"out": f64(out[0]), "probs": f64(probs), "dq": f64(dq[0]), "dk": f64(dk[0]),
+                         "dv": f64(dv[0]), "same": bool(torch.equal(dq, dq0) and torch.equal(dk, dk0)
+                                                        and torch.equal(dv, dv0)),
+                         "flag": int(ctx.extra["flag"].item()), "ring": ring.ledger.devices[rank].ring_p2p_elements}
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,shape", [(2, (1, 2, 256, 64)), (3, (2, 2, 384, 64)), (4, (1, 3, 512, 64))])
+def test_peer_ring_matches_oracle(world, shape):
+    """PeerRing: one fwd_factored_peer / bwd_fused_peer launch per rank reading every origin's
+    K/V through CUDA IPC (here: processes sharing one B200), against the oracle."""
+    seed = 60 + world
+    mgr = mp.get_context("spawn").Manager()
+    results = mgr.dict()
+    mp.start_processes(_peer_worker, args=(world, _free_port(), shape, seed, results), nprocs=world, join=True,
+                       start_method="spawn")
+    b, z, seq, a = shape
+    q, k, v, g = _inputs(b, z, seq, a, seed)
+    ch = lambda x: orc.chunks_of(x, world)  # noqa: E731
+    outs, probs, _ = orc.ring_forward(ch(q), ch(k), ch(v), exact=False)
+    dq, dk, dv, _ = orc.ring_backward(ch(q), ch(k), ch(v), probs, ch(g), exact=False)
+    for d in range(world):
+        r = results[d]
+        assert r["flag"] == 0 and r["same"]
+        assert _rel(r["out"], outs[d]) <= 1e-2
+        assert np.max(np.abs(r["probs"] - probs[d])) <= 4e-3
+        for name, want in (("dq", dq[d]), ("dk", dk[d]), ("dv", dv[d])):
+            assert _rel(r[name], want) <= 1e-2, (d, name, _rel(r[name], want))
+        c = seq // world
+        assert r["ring"] == 3 * 2 * (world - 1) * b * z * c * a + 2 * 2 * (world - 1) * b * z * c * a
