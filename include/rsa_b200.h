@@ -234,8 +234,8 @@ int rsa_bwd_fused_supported(const rsa_geom* g);
  * kernel's TMA pipeline instead of travelling a ring of NCCL hops (the K/V rings of
  * ringseq/ring_attention.py:124-217).  g: n_rank = 1 (this rank's query chunk),
  * org_lo = 0, n_org = N <= RSA_MAX_PEERS; k_origin[j] / v_origin[j] view origin j's
- * [1][B][Z][c][A] chunk (the Python host opens peers' buffers with torch's CUDA IPC,
- * paper_2105_13120_b200/distributed.py:PeerRing).  The forward is rsa_fwd_factored's single pass (factored
+ * [1][B][Z][c][A] chunk (peers' buffers come from rsa_ipc_alloc / rsa_ipc_open below,
+ * driven by paper_2105_13120_b200/distributed.py:PeerRing).  The forward is rsa_fwd_factored's single pass (factored
  * panel, row scale); the backward is rsa_bwd_fused's single pass with fp32 dK / dV
  * partials for every origin ([N][B][Z][c][A], dk_part / dv_part) left for the
  * caller's reduce-scatter (the reference's all-reduce + slice, :206-209).
@@ -245,6 +245,19 @@ int rsa_fwd_factored_peer(const rsa_geom* g, rsa_view q, const rsa_view* k_origi
 int rsa_bwd_fused_peer(const rsa_geom* g, rsa_view q, const rsa_view* k_origin, const rsa_view* v_origin,
                        rsa_view dout, rsa_view panel, const float* dvec, rsa_view dq_out, rsa_view dk_part,
                        rsa_view dv_part, void* stream);
+
+/*
+ * The registered K/V buffers those kernels read: rsa_ipc_alloc cudaMallocs `bytes`
+ * and writes its 64-byte CUDA IPC handle to `handle`; every other rank maps it with
+ * rsa_ipc_open (cudaIpcOpenMemHandle, lazy peer access).  Tear down in the order
+ * rsa_ipc_close on every mapping, then rsa_ipc_free by the owner.  Stands in for the
+ * ring's per-hop send/recv buffers (ringseq/ring_attention.py:124-217).
+ */
+#define RSA_IPC_HANDLE_BYTES 64
+int rsa_ipc_alloc(size_t bytes, void** ptr, void* handle);
+int rsa_ipc_open(const void* handle, void** ptr);
+int rsa_ipc_close(void* ptr);
+int rsa_ipc_free(void* ptr);
 
 
 #ifdef __cplusplus

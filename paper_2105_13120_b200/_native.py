@@ -95,6 +95,10 @@ EXPORTS = {
     "rsa_fwd_factored": (c_int, [_GEOM, _V, _V, _V, _V, _V, c_void_p, c_void_p, c_void_p]),
     "rsa_fwd_factored_peer": (c_int, [_GEOM, _V, _P(RsaView), _P(RsaView), _V, _V, c_void_p, c_void_p, c_void_p]),
     "rsa_bwd_fused_peer": (c_int, [_GEOM, _V, _P(RsaView), _P(RsaView), _V, _V, c_void_p, _V, _V, _V, c_void_p]),
+    "rsa_ipc_alloc": (c_int, [ctypes.c_size_t, _P(c_void_p), c_void_p]),
+    "rsa_ipc_open": (c_int, [c_void_p, _P(c_void_p)]),
+    "rsa_ipc_close": (c_int, [c_void_p]),
+    "rsa_ipc_free": (c_int, [c_void_p]),
     "rsa_bwd_dkdv": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, _V, _V, c_int, c_int, c_void_p]),
     "rsa_bwd_dq": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, _V, c_int, _V, c_void_p]),
     "rsa_fused_supported": (c_int, [_GEOM]),

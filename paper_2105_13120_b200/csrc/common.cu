@@ -3,6 +3,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstring>
 #include <mutex>
 
 #include "common.h"
@@ -83,5 +84,35 @@ extern "C" {
 int rsa_abi_version(void) { return RSA_ABI_VERSION; }
 const char* rsa_last_error(void) { return rsa::g_err; }
 int rsa_num_sms(void) { return rsa::num_sms(); }
+
+int rsa_ipc_alloc(size_t bytes, void** ptr, void* handle) {
+  if (!ptr || !handle || !bytes) return rsa::fail(RSA_ERR_INVALID, "rsa_ipc_alloc: null argument or zero size");
+  *ptr = nullptr;
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle), *ptr);
+  if (e != cudaSuccess) {
+    if (*ptr) cudaFree(*ptr), *ptr = nullptr;
+    return rsa::fail(RSA_ERR_CUDA, "rsa_ipc_alloc: %s", cudaGetErrorString(e));
+  }
+  return RSA_OK;
+}
+
+int rsa_ipc_open(const void* handle, void** ptr) {
+  if (!ptr || !handle) return rsa::fail(RSA_ERR_INVALID, "rsa_ipc_open: null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  const cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? RSA_OK : rsa::fail(RSA_ERR_CUDA, "rsa_ipc_open: %s", cudaGetErrorString(e));
+}
+
+int rsa_ipc_close(void* ptr) {
+  const cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  return e == cudaSuccess ? RSA_OK : rsa::fail(RSA_ERR_CUDA, "rsa_ipc_close: %s", cudaGetErrorString(e));
+}
+
+int rsa_ipc_free(void* ptr) {
+  const cudaError_t e = cudaFree(ptr);
+  return e == cudaSuccess ? RSA_OK : rsa::fail(RSA_ERR_CUDA, "rsa_ipc_free: %s", cudaGetErrorString(e));
+}
 
 }  // extern "C"

@@ -168,11 +168,12 @@ inline bool out_ok(const rsa_view& v, int esz) {
 }
 
 template <typename K, typename A>
-int launch(K kernel, int items, uint32_t smem, const A& args, void* stream, const char* name) {
+int launch(K kernel, int items, uint32_t smem, const A& args, void* stream, const char* name,
+           int threads = NTHREADS) {
   if (items <= 0) return RSA_OK;
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int grid = items < num_sms() ? items : num_sms();
-  kernel<<<grid, NTHREADS, smem, reinterpret_cast<cudaStream_t>(stream)>>>(args);
+  kernel<<<grid, threads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(args);
   return check_launch(name);
 }
 

@@ -295,12 +295,22 @@ class SpmdRing:
         return part[d:d + 1].clone()
 
 
-class _PeerSlot:
-    """One registered K/V buffer: this rank's [2][B][Z][c][A] chunk pair and every peer's,
-    opened through torch's CUDA IPC (the device pointers a peer kernel reads over NVLink)."""
+class _CudaBuffer:
+    """A raw device allocation seen by torch through ``__cuda_array_interface__``
+    (int16 words; viewed as bf16).  The tensor does not own the memory."""
 
-    def __init__(self, local: torch.Tensor, peers: list):
-        self.local, self.peers = local, peers
+    def __init__(self, ptr: int, shape: tuple):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<i2", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class _PeerSlot:
+    """One registered K/V buffer: this rank's [2][B][Z][c][A] chunk pair (``rsa_ipc_alloc``)
+    and every peer's, mapped with ``rsa_ipc_open`` -- the device pointers a peer kernel
+    reads over NVLink."""
+
+    def __init__(self, ptr: int, peer_ptrs: list, local: torch.Tensor, peers: list):
+        self.ptr, self.peer_ptrs, self.local, self.peers = ptr, peer_ptrs, local, peers
 
 
 class PeerRing:
@@ -318,7 +328,9 @@ class PeerRing:
 
     This is the correctness-first form: staging is fenced by host barriers (buffer free
     on every rank, then staged on every rank).  Cross-process CUDA IPC events would
-    replace them.
+    replace them.  The buffers are plain cudaMalloc allocations exported with
+    cudaIpcGetMemHandle (``rsa_ipc_*``), outside torch's allocator, so their lifetime is
+    exactly ``close()``.
     """
 
     def __init__(self, group=None, mode: str = "reduce_scatter", transport: str = "device"):
@@ -326,30 +338,57 @@ class PeerRing:
         self.group, self.rank, self.world = group, self.ring.rank, self.ring.world
         self.ledger = self.ring.ledger
         self._free: dict = {}
+        self._all: list = []
 
     def _barrier(self):
         torch.cuda.synchronize()
         dist.barrier(group=self.group)
 
     def _slot(self, shape, dtype, dev) -> _PeerSlot:
+        from ._native import check, lib
+
+        if dtype != torch.bfloat16:
+            raise ValueError(f"PeerRing stages bf16 K/V, got {dtype}")
         key = (tuple(shape), dtype)
         pool = self._free.setdefault(key, [])
         if pool:
             return pool.pop()
-        local = torch.empty((2,) + tuple(shape), dtype=dtype, device=dev)
-        share = local.untyped_storage()._share_cuda_()
-        shares = [None] * self.world
-        dist.all_gather_object(shares, share, group=self.group)
-        peers = []
-        for j, sh in enumerate(shares):
+        full = (2,) + tuple(shape)
+        nbytes = 2 * math.prod(full)
+        ptr, handle = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+        check(lib().rsa_ipc_alloc(nbytes, ctypes.byref(ptr), handle), "rsa_ipc_alloc")
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle.raw, group=self.group)
+        ptrs, tensors = [], []
+        for j, h in enumerate(handles):
             if j == self.rank:
-                peers.append(local)
-                continue
-            st = torch.UntypedStorage._new_shared_cuda(*sh)
-            t = torch.empty(0, dtype=dtype, device=dev)
-            t.set_(st, 0, local.shape, local.stride())
-            peers.append(t)
-        return _PeerSlot(local, peers)
+                p = ptr.value
+            else:
+                pj = ctypes.c_void_p()
+                check(lib().rsa_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(pj)), "rsa_ipc_open")
+                p = pj.value
+            ptrs.append(p)
+            tensors.append(torch.as_tensor(_CudaBuffer(p, full), device=dev).view(torch.bfloat16))
+        slot = _PeerSlot(ptr.value, ptrs, tensors[self.rank], tensors)
+        self._all.append(slot)
+        return slot
+
+    def close(self):
+        """Unmap every peer's buffer, then free this rank's own -- in that order on every
+        rank, so no process frees memory a peer still maps or reads.  Call it before
+        ``destroy_process_group``; the ring is unusable afterwards."""
+        from ._native import check, lib
+
+        self._barrier()  # every rank's kernels on the shared buffers have finished
+        for s in self._all:
+            s.local, s.peers = None, []
+            for j, p in enumerate(s.peer_ptrs):
+                if j != self.rank:
+                    check(lib().rsa_ipc_close(ctypes.c_void_p(p)), "rsa_ipc_close")
+        self._barrier()  # every mapping is closed
+        for s in self._all:
+            check(lib().rsa_ipc_free(ctypes.c_void_p(s.ptr)), "rsa_ipc_free")
+        self._all, self._free = [], {}
 
     def _views(self, slot: _PeerSlot, which: int):
         from .engine import _view

@@ -134,6 +134,8 @@ def _peer_worker(rank, world, port, shape, seed, results):
                          "dv": f64(dv[0]), "same": bool(torch.equal(dq, dq0) and torch.equal(dk, dk0)
                                                         and torch.equal(dv, dv0)),
                          "flag": int(ctx.extra["flag"].item()), "ring": ring.ledger.devices[rank].ring_p2p_elements}
+        ring.backward(ctx, ch(g))  # hand the last slot back, then unmap everything before teardown
+        ring.close()
     finally:
         dist.destroy_process_group()
 
