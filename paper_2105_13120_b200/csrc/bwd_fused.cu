@@ -71,6 +71,20 @@ static_assert(BF_SMEM <= 232448, "bwd_fused smem over the sm_100 per-CTA limit")
 
 constexpr uint32_t COL_DP = 0, COL_DV = 128, COL_DK = 192, COL_DQ = 256;
 
+// dS of two adjacent keys: P * (dP - D) with packed fp32x2 arithmetic (FADD2 / FMUL2;
+// the same roundings as the scalar form), packed to bf16x2.  pw: the bf16 pair of P;
+// nd: (-D, -D).
+__device__ __forceinline__ uint32_t ds_pair(uint32_t pw, float dp0, float dp1, uint64_t nd) {
+  uint64_t x, pp;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(dp0), "f"(dp1));
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(nd));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pp) : "f"(__uint_as_float(pw << 16)), "f"(__uint_as_float(pw & 0xFFFF0000u)));
+  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(pp));
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x));
+  return pack_bf16(a, b);
+}
+
 struct Ring {  // full/empty barrier pair array of one operand ring
   uint64_t *full, *empty;
 };
@@ -383,13 +397,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
         ++dpq.i;
         // dS' = P (dP - D) as packed bf16 (the 1/sqrt(A) scale is applied to dQ / dK at the end)
         uint32_t dsw[32];
+        uint64_t nd;
+        asm("mov.b64 %0, {%1, %1};" : "=l"(nd) : "f"(-dval));
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
-          float pv[32];
-          ld_row32_sw128(pt, r, half * 64 + cc * 32, pv);
+          const uint32_t atom = (half * 64 + cc * 32) >> 6, chunk0 = ((half * 64 + cc * 32) & 63) >> 3;
 #pragma unroll
-          for (int e = 0; e < 32; e += 2)
-            dsw[cc * 16 + e / 2] = pack_bf16(pv[e] * (dp[cc * 32 + e] - dval), pv[e + 1] * (dp[cc * 32 + e + 1] - dval));
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t w[4];
+            ld_shared_v4(pt + atom * ATOM + sw128_offset(r, chunk0 + q4), w[0], w[1], w[2], w[3]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              dsw[cc * 16 + q4 * 4 + e] = ds_pair(w[e], dp[cc * 32 + q4 * 8 + 2 * e], dp[cc * 32 + q4 * 8 + 2 * e + 1], nd);
+          }
         }
         BF_TRACE(23);
         mbar_wait(&p_read[ps], pq.phase(BF_P));
