@@ -71,20 +71,6 @@ static_assert(BF_SMEM <= 232448, "bwd_fused smem over the sm_100 per-CTA limit")
 
 constexpr uint32_t COL_DP = 0, COL_DV = 128, COL_DK = 192, COL_DQ = 256;
 
-// dS of two adjacent keys: P * (dP - D) with packed fp32x2 arithmetic (FADD2 / FMUL2;
-// the same roundings as the scalar form), packed to bf16x2.  pw: the bf16 pair of P;
-// nd: (-D, -D).
-__device__ __forceinline__ uint32_t ds_pair(uint32_t pw, float dp0, float dp1, uint64_t nd) {
-  uint64_t x, pp;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(dp0), "f"(dp1));
-  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(nd));
-  asm("mov.b64 %0, {%1, %2};" : "=l"(pp) : "f"(__uint_as_float(pw << 16)), "f"(__uint_as_float(pw & 0xFFFF0000u)));
-  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(pp));
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x));
-  return pack_bf16(a, b);
-}
-
 struct Ring {  // full/empty barrier pair array of one operand ring
   uint64_t *full, *empty;
 };

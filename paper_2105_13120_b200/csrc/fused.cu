@@ -398,6 +398,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dkdv_kernel(const __grid_cons
     if (lane == 0) {
       Pos lq;
       uint32_t it = 0;
+      const uint64_t pol = l2_evict_first();  // the panel streams through once
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
         const int kt = item % ntk, bz = (item / ntk) % BZ, jo = item / (ntk * BZ);
         const int b = bz / g.Z, z = bz % g.Z, k0 = kt * TK, jg = g.org_lo + jo;
@@ -412,8 +413,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dkdv_kernel(const __grid_cons
           uint8_t* st = smem + BK_OFF_ST + s * BK_STAGE;
           tma_load_4d(st, &p.tdo, &ld_full[s], 0, r0, z, d * g.B + b);
           tma_load_4d(st + TILE, &p.tq, &ld_full[s], 0, r0, z, d * g.B + b);
-          tma_load_5d(st + 2 * TILE, &p.tp, &ld_full[s], k0, jg, r0, z, d * g.B + b);
-          tma_load_5d(st + 2 * TILE + ATOM, &p.tp, &ld_full[s], k0 + 64, jg, r0, z, d * g.B + b);
+          tma_load_5d_hint(st + 2 * TILE, &p.tp, &ld_full[s], k0, jg, r0, z, d * g.B + b, pol);
+          tma_load_5d_hint(st + 2 * TILE + ATOM, &p.tp, &ld_full[s], k0 + 64, jg, r0, z, d * g.B + b, pol);
           ++lq.i;
         }
       }
@@ -483,29 +484,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dkdv_kernel(const __grid_cons
       const int kt = item % ntk, bz = (item / ntk) % BZ, jo = item / (ntk * BZ);
       const int b = bz / g.Z, z = bz % g.Z, k0 = kt * TK;
       int d = 0, r0 = 0;
+      float dnext = r < g.c ? p.dvec[(int64_t(b) * g.Z + z) * g.c + r] : 0.f;
       for (int t = 0; t < T; ++t) {
-        const int row = r0 + r;
         const uint32_t s = lq.slot(BK_ST), db = dq_.slot(2);
-        const float dval = row < g.c ? p.dvec[(int64_t(d * g.B + b) * g.Z + z) * g.c + row] : 0.f;
+        const float dval = dnext;
         if (r0 + TR >= g.c) r0 = 0, ++d;
         else r0 += TR;
+        if (t + 1 < T) {  // next step's D now: its load latency hides behind this step
+          const int nrow = r0 + r;
+          dnext = nrow < g.c ? p.dvec[(int64_t(d * g.B + b) * g.Z + z) * g.c + nrow] : 0.f;
+        }
         const uint32_t pt = smem_u32(smem + BK_OFF_ST + s * BK_STAGE + 2 * TILE);
         const uint32_t dst = pt;  // dS overwrites P in place
         mbar_wait(&ld_full[s], lq.phase(BK_ST));
         mbar_wait(&dp_full[db], dq_.phase(2));
         tc_fence_after();
+        const uint64_t nd = neg_pair(dval);
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
-          float v[32], pv[32];
+          float v[32];
           const int col = half * 64 + cc * 32;
           __syncwarp();
           tmem_ld32(tmem + lane_base + db * TK + col, v);
-          ld_row32_sw128(pt, r, col, pv);
           tmem_ld_wait();
-          // dS' = P (dP - D); the 1/sqrt(A) scale is applied to dK once, at the end
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = pv[e] * (v[e] - dval);
-          st_row32_sw128(dst, r, col, v);
+          // dS' = P (dP - D) in place; the 1/sqrt(A) scale is applied to dK once, at the end
+          ds_row32_inplace(dst, r, col, v, nd);
         }
         tc_fence_before();
         fence_proxy_async_smem();
@@ -601,6 +604,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dq_kernel(const __grid_consta
     if (lane == 0) {
       Pos lq;
       uint32_t it = 0;
+      const uint64_t pol = l2_evict_first();  // the panel streams through once
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
         const int rt = item % nrt, bz = (item / nrt) % BZ, d = item / (nrt * BZ);
         const int b = bz / g.Z, z = bz % g.Z, r0 = rt * TR;
@@ -616,8 +620,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dq_kernel(const __grid_consta
           uint8_t* st = smem + DQ_OFF_ST + s * DQ_STAGE;
           tma_load_4d(st, &p.tv, &ld_full[s], 0, k0, z, jo * g.B + b);
           tma_load_4d(st + TILE, &p.tk, &ld_full[s], 0, k0, z, jo * g.B + b);
-          tma_load_5d(st + 2 * TILE, &p.tp, &ld_full[s], k0, g.org_lo + jo, r0, z, d * g.B + b);
-          tma_load_5d(st + 2 * TILE + ATOM, &p.tp, &ld_full[s], k0 + 64, g.org_lo + jo, r0, z, d * g.B + b);
+          tma_load_5d_hint(st + 2 * TILE, &p.tp, &ld_full[s], k0, g.org_lo + jo, r0, z, d * g.B + b, pol);
+          tma_load_5d_hint(st + 2 * TILE + ATOM, &p.tp, &ld_full[s], k0 + 64, g.org_lo + jo, r0, z, d * g.B + b, pol);
           ++lq.i;
         }
       }
@@ -683,17 +687,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dq_kernel(const __grid_consta
         mbar_wait(&ld_full[s], lq.phase(DQ_ST));
         mbar_wait(&dp_full[db], dq_.phase(2));
         tc_fence_after();
+        const uint64_t nd = neg_pair(dval);
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
-          float v[32], pv[32];
+          float v[32];
           const int col = half * 64 + cc * 32;
           __syncwarp();
           tmem_ld32(tmem + lane_base + db * TK + col, v);
-          ld_row32_sw128(pt, r, col, pv);
           tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = pv[e] * (v[e] - dval);  // dS' = P (dP - D); scale applied to dQ
-          st_row32_sw128(dst, r, col, v);
+          ds_row32_inplace(dst, r, col, v, nd);  // dS' = P (dP - D); scale applied to dQ
         }
         tc_fence_before();
         fence_proxy_async_smem();

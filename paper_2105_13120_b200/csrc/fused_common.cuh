@@ -58,6 +58,42 @@ __device__ __forceinline__ void ld_row32_sw128(uint32_t tile, uint32_t r, int co
   }
 }
 
+// dS of two adjacent keys: P * (dP - D) with packed fp32x2 arithmetic (FADD2 / FMUL2;
+// the same roundings as the scalar form), packed to bf16x2.  pw: the bf16 pair of P;
+// nd: (-D, -D).
+__device__ __forceinline__ uint32_t ds_pair(uint32_t pw, float dp0, float dp1, uint64_t nd) {
+  uint64_t x, pp;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(dp0), "f"(dp1));
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(nd));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pp) : "f"(__uint_as_float(pw << 16)), "f"(__uint_as_float(pw & 0xFFFF0000u)));
+  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(pp));
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x));
+  return pack_bf16(a, b);
+}
+
+// dS = P * (dP - D) for 32 keys of row r in place over the bf16 P tile (columns
+// col0..col0+31 of a SWIZZLE_128B [64-col atom][128 rows] tile); dp: the fp32 dP row
+// chunk, nd: (-D, -D).
+__device__ __forceinline__ void ds_row32_inplace(uint32_t tile, uint32_t r, int col0, const float* dp, uint64_t nd) {
+  const uint32_t atom = col0 >> 6, chunk0 = (col0 & 63) >> 3;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t addr = tile + atom * ATOM + sw128_offset(r, chunk0 + q);
+    uint32_t w[4];
+    ld_shared_v4(addr, w[0], w[1], w[2], w[3]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) w[e] = ds_pair(w[e], dp[8 * q + 2 * e], dp[8 * q + 2 * e + 1], nd);
+    st_shared_v4(addr, w[0], w[1], w[2], w[3]);
+  }
+}
+
+__device__ __forceinline__ uint64_t neg_pair(float d) {
+  uint64_t nd;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(nd) : "f"(-d));
+  return nd;
+}
+
 struct OutView {  // strided output [rank][b][z][row][a]
   void* ptr;
   int64_t s_rank, s_b, s_z, s_row;
