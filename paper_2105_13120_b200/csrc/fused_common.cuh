@@ -77,15 +77,15 @@ __device__ __forceinline__ uint32_t ds_pair(uint32_t pw, float dp0, float dp1, u
 // chunk, nd: (-D, -D).
 __device__ __forceinline__ void ds_row32_inplace(uint32_t tile, uint32_t r, int col0, const float* dp, uint64_t nd) {
   const uint32_t atom = col0 >> 6, chunk0 = (col0 & 63) >> 3;
+  uint32_t w[16];  // every load before the first store (the compiler cannot reorder them)
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const uint32_t addr = tile + atom * ATOM + sw128_offset(r, chunk0 + q);
-    uint32_t w[4];
-    ld_shared_v4(addr, w[0], w[1], w[2], w[3]);
+  for (int q = 0; q < 4; ++q)
+    ld_shared_v4(tile + atom * ATOM + sw128_offset(r, chunk0 + q), w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) w[e] = ds_pair(w[e], dp[8 * q + 2 * e], dp[8 * q + 2 * e + 1], nd);
-    st_shared_v4(addr, w[0], w[1], w[2], w[3]);
-  }
+  for (int e = 0; e < 16; ++e) w[e] = ds_pair(w[e], dp[2 * e], dp[2 * e + 1], nd);
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    st_shared_v4(tile + atom * ATOM + sw128_offset(r, chunk0 + q), w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
 }
 
 __device__ __forceinline__ uint64_t neg_pair(float d) {
