@@ -142,10 +142,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
       if (blockIdx.x < items) load_vk(blockIdx.x, 0);
       for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const int b = item / g.Z, z = item % g.Z;
-        for (int kk = 0; kk < NK; ++kk) {
-          const int jo = kk / ntk, k0 = (kk % ntk) * TK;
-          for (int qt = 0; qt < NQ; ++qt) {
-            const int d = qt / nrt, r0 = (qt % nrt) * TR;
+        // (origin, key offset) and (rank, row offset) advance by counters: no integer
+        // division by a runtime count in any per-step path
+        for (int kk = 0, jo = 0, k0 = 0; kk < NK; ++kk, k0 = k0 + TK >= ntk * TK ? (++jo, 0) : k0 + TK) {
+          for (int qt = 0, d = 0, r0 = 0; qt < NQ; ++qt, r0 = r0 + TR >= nrt * TR ? (++d, 0) : r0 + TR) {
             load_tile(rdo, dq_, BF_DO, BF_OFF_DO, &p.tdo, r0, z, d * g.B + b);
             const uint32_t s = pq.slot(BF_P);
             mbar_wait(&rp.empty[s], pq.phase(BF_P) ^ 1);
@@ -179,8 +179,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
       uint32_t head_it = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++head_it) {
         // dP(t) = dO V^T into the single dP buffer (after the epilogue has read dP(t-1))
-        auto issue_dp = [&](int t) {
-          const int qt = t % NQ;
+        auto issue_dp = [&](int qt) {
           const uint32_t vs = v_a.slot(BF_V), ds = do_a.slot(BF_DO);
           if (qt == 0) mbar_wait(&rv.full[vs], v_a.phase(BF_V));
           mbar_wait(&rdo.full[ds], do_a.phase(BF_DO));
@@ -200,8 +199,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
           ++dpq.i;
         };
         // dV += P^T dO; p_read certifies P has been consumed, so dS may overwrite it
-        auto issue_dv = [&](int t) {
-          const int qt = t % NQ;
+        auto issue_dv = [&](int qt) {
           const uint32_t ds = do_a.slot(BF_DO), ps = p_a.slot(BF_P);
           if (qt == 0) mbar_wait(acc_empty, accq.phase(1) ^ 1);
           mbar_wait(&rp.full[ps], p_a.phase(BF_P));
@@ -218,8 +216,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
           if (qt == NQ - 1) ++accq.i;
         };
         // dK += dS^T Q and dQ(qt) += dS K once the epilogue has written dS(t)
-        auto issue_b = [&](int t) {
-          const int kk = t / NQ, qt = t % NQ;
+        auto issue_b = [&](int kk, int qt) {
           const uint32_t ks = k_b.slot(BF_K), qs = q_b.slot(BF_Q), ps = p_b.slot(BF_P);
           if (qt == 0) mbar_wait(&rk.full[ks], k_b.phase(BF_K));
           mbar_wait(&rq.full[qs], q_b.phase(BF_Q));
@@ -254,14 +251,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
         };
         issue_dp(0);
         issue_dv(0);
-        for (int t = 0; t < T; ++t) {
+        for (int t = 0, kk = 0, qt = 0; t < T; ++t) {
           const bool next = t + 1 < T;
-          const bool new_kt = next && (t + 1) % NQ == 0;
-          if (next && !new_kt) issue_dp(t + 1), issue_dv(t + 1);
-          issue_b(t);
+          const int nqt = qt + 1 == NQ ? 0 : qt + 1;
+          const bool new_kt = next && nqt == 0;
+          if (next && !new_kt) issue_dp(nqt), issue_dv(nqt);
+          issue_b(kk, qt);
           // key-tile boundary: the finished tile's dK products go first, so the epilogue's
           // dK/dV readout (which frees the accumulators for the next dV) waits the least
-          if (new_kt) issue_dp(t + 1), issue_dv(t + 1);
+          if (new_kt) issue_dp(nqt), issue_dv(nqt);
+          kk += nqt == 0, qt = nqt;
         }
       }
     }
@@ -355,9 +354,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
         const int rj = (j % nrt) * TR + r;
         dh[j] = (j < NQ && rj < g.c) ? __ldg(p.dvec + (int64_t((j / nrt) * g.B + b) * g.Z + z) * g.c + rj) : 0.f;
       }
-      for (int t = 0; t < T; ++t) {
-        const int kk = t / NQ, qt = t % NQ;
-        const int d = qt / nrt, row = (qt % nrt) * TR + r;
+      for (int t = 0, kk = 0, qt = 0, d = 0, r0 = 0, jo = 0, k0 = 0; t < T; ++t) {
+        const int row = r0 + r;
         const float dval = qt == 0 ? dh[0] : qt == 1 ? dh[1] : qt == 2 ? dh[2] : dh[3];
         const uint32_t ps = pq.slot(BF_P);
         const uint32_t pt = smem_u32(smem + BF_OFF_P + ps * PTILE);
@@ -418,8 +416,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
           rel_pending = false;
         }
         if (q_on) flush_q();
-        if (qt == NQ - 1) kv_on = true, kjo = kk / ntk, kk0 = (kk % ntk) * TK, kb = b, kz = z, kslot = ps;
+        if (qt == NQ - 1) kv_on = true, kjo = jo, kk0 = k0, kb = b, kz = z, kslot = ps;
         if (kk == NK - 1) q_on = true, qqt = qt, qd = d, qrow = row, qb = b, qz = z, qphase = head_it & 1;
+        if (++qt == NQ) {  // advance (query tile, rank, row) and, after the last query tile, the key tile
+          qt = 0, d = 0, r0 = 0, ++kk;
+          if (k0 + TK >= ntk * TK) k0 = 0, ++jo;
+          else k0 += TK;
+        } else if (r0 + TR >= nrt * TR) {
+          r0 = 0, ++d;
+        } else {
+          r0 += TR;
+        }
       }
     }
     if (kv_on) {
