@@ -107,8 +107,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fwd_kernel(const __grid_constant_
         tma_load_4d(smem + F_OFF_Q + qb * TILE, &p.tq, &q_full[qb], 0, rt * TR, z, d * g.B + b);
         for (int pass = 0; pass < 2; ++pass) {
           if ((pass == 0 && !pass_a) || (pass == 1 && !pass_b)) continue;
-          for (int t = 0; t < T; ++t) {
-            const int jo = t / ntk, k0 = (t % ntk) * TK;
+          for (int t = 0, jo = 0, k0 = 0; t < T; ++t, k0 = k0 + TK >= ntk * TK ? (++jo, 0) : k0 + TK) {
             const uint32_t ks = kq.slot(FK_ST);
             mbar_wait(&k_empty[ks], kq.phase(FK_ST) ^ 1);
             mbar_arrive_expect_tx(&k_full[ks], TILE);
@@ -405,8 +404,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dkdv_kernel(const __grid_cons
         mbar_wait(v_empty, (it & 1) ^ 1);
         mbar_arrive_expect_tx(v_full, TILE);
         tma_load_4d(smem + BK_OFF_V, &p.tv, v_full, 0, k0, z, jo * g.B + b);
-        for (int t = 0; t < T; ++t) {
-          const int d = t / nrt, r0 = (t % nrt) * TR;
+        for (int t = 0, d = 0, r0 = 0; t < T; ++t, r0 = r0 + TR >= nrt * TR ? (++d, 0) : r0 + TR) {
           const uint32_t s = lq.slot(BK_ST);
           mbar_wait(&ld_empty[s], lq.phase(BK_ST) ^ 1);
           mbar_arrive_expect_tx(&ld_full[s], BK_STAGE);
@@ -612,8 +610,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dq_kernel(const __grid_consta
         mbar_wait(&do_empty[ob], ((it >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&do_full[ob], TILE);
         tma_load_4d(smem + DQ_OFF_DO + ob * TILE, &p.tdo, &do_full[ob], 0, r0, z, d * g.B + b);
-        for (int t = 0; t < T; ++t) {
-          const int jo = t / ntk, k0 = (t % ntk) * TK;
+        for (int t = 0, jo = 0, k0 = 0; t < T; ++t, k0 = k0 + TK >= ntk * TK ? (++jo, 0) : k0 + TK) {
           const uint32_t s = lq.slot(DQ_ST);
           mbar_wait(&ld_empty[s], lq.phase(DQ_ST) ^ 1);
           mbar_arrive_expect_tx(&ld_full[s], DQ_STAGE);

@@ -241,8 +241,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
           ++qn[gi];
         }
         if (kres && un.bz != prev_bz) {
-          for (int t = 0; t < T; ++t) {
-            const int jo = t / ntk, k0 = (t % ntk) * TK;
+          for (int t = 0, jo = 0, k0 = 0; t < T; ++t, k0 = k0 + TK >= ntk * TK ? (++jo, 0) : k0 + TK) {
             mbar_wait(&k_empty[t], (kgen & 1) ^ 1);
             mbar_arrive_expect_tx(&k_full[t], TILE);
             tma_load_4d(smem + FF_OFF_K + t * TILE, p.peer ? &p.pm.k[jo] : &p.tk, &k_full[t], 0, k0, z,
@@ -251,8 +250,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
           ++kgen;
         }
         prev_bz = un.bz;
-        for (int t = 0; t < T; ++t) {
-          const int jo = t / ntk, k0 = (t % ntk) * TK;
+        for (int t = 0, jo = 0, k0 = 0; t < T; ++t, k0 = k0 + TK >= ntk * TK ? (++jo, 0) : k0 + TK) {
           if (!kres) {
             const uint32_t ks = kq.slot(FF_KST);
             mbar_wait(&k_empty[ks], kq.phase(FF_KST) ^ 1);
