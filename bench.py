@@ -241,7 +241,8 @@ def ours(args):
     if world > 1:
         from paper_2105_13120_b200 import distributed
 
-        return distributed.bench_main(args, METRIC, UNIT, config_obj(args, world))
+        return distributed.bench_main(args, METRIC, UNIT, config_obj(args, world), clock_sampler=ClockSampler,
+                                      peaks=peaks())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     B, Z, L, A, LAYERS = args.batch, args.heads, args.seq, args.head_size, args.layers

@@ -465,21 +465,33 @@ class PeerRing:
 
 # ------------------------------------------------------------------ bench
 
-def bench_main(args, metric, unit, config):
-    """Multi-GPU arm of bench.py (launched under torchrun, one rank per GPU)."""
+def bench_main(args, metric, unit, config, clock_sampler=None, peaks=None):
+    """Multi-GPU arm of bench.py (launched under torchrun, one rank per GPU).
+
+    Each rank holds B = batch * N sequences' c = L / N chunk (the paper's weak-scaling
+    batch rule) and runs the 12-layer stack through ``SpmdRing``: K/V rings and dK/dV
+    reduce-scatters over NCCL.  ``value`` is the whole job's tokens/s with the step time
+    taken as the max over ranks; ``e2e`` repeats the step with every rank's chunks
+    uploaded from pinned host memory and its outputs copied back.  RSA_BENCH_BACKEND=gloo
+    runs the same code with host-staged transfers (several ranks on one GPU; test only).
+    """
     import json
     import os
 
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("RSA_BENCH_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n, rank = dist.get_world_size(), dist.get_rank()
     dev = torch.device("cuda", local)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+    n, rank = dist.get_world_size(), dist.get_rank()
     B, Z, L, A, LAYERS = args.batch * n, args.heads, args.seq, args.head_size, args.layers
     if L % n:
         raise SystemExit(f"seq {L} not divisible by {n} ranks")
     c = L // n
-    ring = SpmdRing()
+    ring = SpmdRing(transport="device" if backend == "nccl" else "host")
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
 
     def rnd():
@@ -496,29 +508,77 @@ def bench_main(args, metric, unit, config):
         for ly, ctx in zip(reversed(layers), reversed(ctxs)):
             ring.backward(ctx, ly["g"])
 
+    def timed(fn, steps):
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = torch.tensor([e0.elapsed_time(e1) / steps], device=dev)
+        if backend != "nccl":
+            t = t.cpu()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(args.steps):
-        step()
-    e1.record()
-    torch.cuda.synchronize()
-    dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
+    if clock_sampler is not None:
+        with clock_sampler(local) as clk:
+            ms = timed(step, args.steps)
+        clocks = clk.result()
+    else:
+        ms, clocks = timed(step, args.steps), None
+
+    # end to end: this rank's q, k, v, dO chunks from pinned host memory, O and dQ/dK/dV back
+    hg = torch.Generator().manual_seed(2000 + rank)
+    host = [[torch.randn((1, B, Z, c, A), generator=hg).to(torch.bfloat16).pin_memory() for _ in range(4)]
+            for _ in range(LAYERS)]
+    outs = [[torch.empty((1, B, Z, c, A), dtype=torch.bfloat16).pin_memory() for _ in range(4)]
+            for _ in range(LAYERS)]
+
+    def e2e_step():
+        ctxs = []
+        for (q, k, v, _), o in zip(host, outs):
+            out, ctx = ring.forward(q.to(dev, non_blocking=True), k.to(dev, non_blocking=True),
+                                    v.to(dev, non_blocking=True), flag)
+            o[0].copy_(out, non_blocking=True)
+            ctxs.append(ctx)
+        for i in reversed(range(LAYERS)):
+            dq, dk, dv = ring.backward(ctxs[i], host[i][3].to(dev, non_blocking=True))
+            for j, t in enumerate((dq, dk, dv)):
+                outs[i][j + 1].copy_(t, non_blocking=True)
+
+    e2e_step()
+    e2e_steps = max(1, min(args.steps, getattr(args, "e2e_steps", 2)))
+    e2e_ms = timed(e2e_step, e2e_steps)
+    chunk_bytes = B * Z * c * A * 2
+
+    if int(flag.item()):
+        raise RuntimeError("non-finite scores in the benchmark inputs")
     if rank == 0:
         value = B * L / (ms / 1e3)
+        # whole-step roofline per GPU: algorithmic HBM bytes of the fused path (panel written
+        # once and read once, per-kernel chunk traffic) over the step time
+        p_e, c_e = B * Z * c * L, B * Z * c * A
+        step_bytes = LAYERS * ((2 * p_e + 8 * c_e) + (6 * c_e + 8 * B * Z * c) + (2 * p_e + 14 * c_e))
+        hbm = (peaks or {}).get("hbm_gbs", 6650.0)
+        achieved = step_bytes / (ms / 1e3) / 1e9
         print(json.dumps({
             "metric": metric, "value": value, "unit": unit, "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic N(0,1) bf16 inputs, per-layer q/k/v/dO", "config": config,
+            "clocks": clocks,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "kernel": "whole step per GPU (ring hops overlapped with the kernels)", "traffic": None},
             "gpu_launches": (LAYERS * (2 * n + 2 * n + 1)) * args.steps,
-            "comm": {"mode": ring.mode, "wire_bytes_per_rank_per_step":
-                     ring.ledger.devices[rank].wire_bytes // max(1, args.steps + args.warmup)},
+            "e2e": {"value": B * L / (e2e_ms / 1e3), "unit": unit, "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": LAYERS * 4 * chunk_bytes, "d2h_bytes_per_step": LAYERS * 4 * chunk_bytes,
+                    "path": "SpmdRing.forward/backward per rank, pinned host chunks in, O/dQ/dK/dV out"},
+            "comm": {"mode": ring.mode, "backend": backend, "wire_bytes_per_rank_per_step":
+                     ring.ledger.devices[rank].wire_bytes // max(1, args.steps + args.warmup + e2e_steps + 1)},
         }), flush=True)
     dist.destroy_process_group()

@@ -163,3 +163,28 @@ def test_peer_ring_matches_oracle(world, shape):
             assert _rel(r[name], want) <= 1e-2, (d, name, _rel(r[name], want))
         c = seq // world
         assert r["ring"] == 3 * 2 * (world - 1) * b * z * c * a + 2 * 2 * (world - 1) * b * z * c * a
+
+
+def test_bench_multi_rank_arm_runs_under_torchrun():
+    """bench.py's N > 1 arm (distributed.bench_main) end to end under torchrun with 2 ranks on
+    this one GPU (gloo, host-staged hops: the only multi-rank transport one GPU supports):
+    one JSON line from rank 0 with the contract's keys, the step time the max over ranks."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RSA_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+           "--steps", "1", "--warmup", "1", "--layers", "2", "--batch", "4", "--e2e-steps", "1"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["config"]["global_batch"] == 8 and d["config"]["ring_ranks"] == 2
+    for key in ("clocks", "roofline", "e2e", "gpu_launches"):
+        assert key in d
+    assert d["e2e"]["h2d_bytes_per_step"] == 2 * 4 * (8 * 12 * 256 * 64 * 2)
