@@ -34,3 +34,13 @@ for L in (512, 8192):
     print(f"TMA stores, 4 KB per-warp boxes, L={L}:", " ".join(
         f"depth{d}={(4 << 30) / lib.tma_store_stream(buf.data_ptr(), rows, L, 3, d) / 1e6:.0f}" for d in (1, 2)),
         "GB/s", flush=True)
+us = here / "umma_rate.so"
+if not us.exists():
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-shared", "-Xcompiler", "-fPIC",
+                    "-o", str(us), str(here / "umma_rate.cu")], check=True)
+ul = ctypes.CDLL(str(us))
+ul.umma_rate.restype = ctypes.c_double
+ul.umma_rate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
+for mn in (0, 1):
+    print(f"tcgen05.mma SS M=128 K=16 ({'MN' if mn else 'K'}-major operands), clk per instruction, all 148 SMs:",
+          " ".join(f"N={n}: {ul.umma_rate(4096, n, mn):.1f}" for n in (64, 128, 256)), flush=True)
