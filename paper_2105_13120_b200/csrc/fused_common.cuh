@@ -122,10 +122,23 @@ __device__ __forceinline__ void store_row32(const OutView& acc, const OutView& f
   }
   if (fin.ptr) {
     __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(fin.ptr) + out_off(fin, rank, b, z, row) + col0;
+    if ((reinterpret_cast<uintptr_t>(p) & 31) == 0) {
+      // whole 32-byte sectors per instruction (256-bit stores): a warp's stores touch 32
+      // rows, and half-sector writes cost the L2 a merge each
 #pragma unroll
-    for (int i = 0; i < 32; i += 8)
-      *reinterpret_cast<uint4*>(p + i) = make_uint4(pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]),
-                                                    pack_bf16(v[i + 4], v[i + 5]), pack_bf16(v[i + 6], v[i + 7]));
+      for (int i = 0; i < 32; i += 16)
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p + i),
+                     "r"(pack_bf16(v[i], v[i + 1])), "r"(pack_bf16(v[i + 2], v[i + 3])),
+                     "r"(pack_bf16(v[i + 4], v[i + 5])), "r"(pack_bf16(v[i + 6], v[i + 7])),
+                     "r"(pack_bf16(v[i + 8], v[i + 9])), "r"(pack_bf16(v[i + 10], v[i + 11])),
+                     "r"(pack_bf16(v[i + 12], v[i + 13])), "r"(pack_bf16(v[i + 14], v[i + 15]))
+                     : "memory");
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; i += 8)
+        *reinterpret_cast<uint4*>(p + i) = make_uint4(pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]),
+                                                      pack_bf16(v[i + 4], v[i + 5]), pack_bf16(v[i + 6], v[i + 7]));
+    }
   }
 }
 
