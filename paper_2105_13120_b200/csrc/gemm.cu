@@ -190,7 +190,27 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
         const bool full_chunk = p.vec_ok && (col0 + 32 <= p.N);
         if (!p.c_bf16) {
           float* c = reinterpret_cast<float*>(p.C) + cbase + col0;
-          if (full_chunk) {
+          if (full_chunk && (reinterpret_cast<uintptr_t>(c) & 31) == 0) {
+            // 256-bit loads / stores: whole 32-byte sectors (each warp instruction touches 32 rows)
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              float o[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) o[e] = p.alpha * v[i + e];
+              if (acc) {
+                float q[8];
+                asm volatile("ld.global.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                             : "=f"(q[0]), "=f"(q[1]), "=f"(q[2]), "=f"(q[3]), "=f"(q[4]), "=f"(q[5]), "=f"(q[6]),
+                               "=f"(q[7])
+                             : "l"(c + i));
+#pragma unroll
+                for (int e = 0; e < 8; ++e) o[e] += q[e];
+              }
+              asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(c + i), "f"(o[0]),
+                           "f"(o[1]), "f"(o[2]), "f"(o[3]), "f"(o[4]), "f"(o[5]), "f"(o[6]), "f"(o[7])
+                           : "memory");
+            }
+          } else if (full_chunk) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
               float4 o = make_float4(p.alpha * v[i], p.alpha * v[i + 1], p.alpha * v[i + 2], p.alpha * v[i + 3]);
@@ -214,7 +234,16 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
           }
-          if (full_chunk) {
+          if (full_chunk && (reinterpret_cast<uintptr_t>(c) & 31) == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 16)
+              asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(c + i),
+                           "r"(pack_bf16(v[i], v[i + 1])), "r"(pack_bf16(v[i + 2], v[i + 3])),
+                           "r"(pack_bf16(v[i + 4], v[i + 5])), "r"(pack_bf16(v[i + 6], v[i + 7])),
+                           "r"(pack_bf16(v[i + 8], v[i + 9])), "r"(pack_bf16(v[i + 10], v[i + 11])),
+                           "r"(pack_bf16(v[i + 12], v[i + 13])), "r"(pack_bf16(v[i + 14], v[i + 15]))
+                           : "memory");
+          } else if (full_chunk) {
 #pragma unroll
             for (int i = 0; i < 32; i += 8) {
               uint4 o = make_uint4(pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]),
