@@ -344,16 +344,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
       if (qrow < g.c) store_row32(p.dq_acc, p.dq_out, p.accumulate_dq, qd, qb, qz, qrow, half * 32, o);
       q_on = false;
     };
-    for (int item = blockIdx.x; item < items; item += gridDim.x, ++head_it) {
-      const int b = item / g.Z, z = item % g.Z;
-      // D of this thread's row in each query tile of the head: loaded once per head
-      // (every key tile revisits the same rows), so no global load sits in a step
-      float dh[MAX_QT];
+    auto load_d = [&](int it, float* out) {  // D of this thread's rows of head `it`
+      const int hb = it / g.Z, hz = it % g.Z;
 #pragma unroll
       for (int j = 0; j < MAX_QT; ++j) {
         const int rj = (j % nrt) * TR + r;
-        dh[j] = (j < NQ && rj < g.c) ? __ldg(p.dvec + (int64_t((j / nrt) * g.B + b) * g.Z + z) * g.c + rj) : 0.f;
+        out[j] = (it < items && j < NQ && rj < g.c)
+                     ? __ldg(p.dvec + (int64_t((j / nrt) * g.B + hb) * g.Z + hz) * g.c + rj)
+                     : 0.f;
       }
+    };
+    float dn[MAX_QT];
+    load_d(blockIdx.x, dn);
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++head_it) {
+      const int b = item / g.Z, z = item % g.Z;
+      // D of this thread's row in each query tile of the head: loaded once per head (every
+      // key tile revisits the same rows), and a whole head ahead, so its load latency never
+      // sits at a head boundary
+      float dh[MAX_QT];
+#pragma unroll
+      for (int j = 0; j < MAX_QT; ++j) dh[j] = dn[j];
+      load_d(item + int(gridDim.x), dn);
       for (int t = 0, kk = 0, qt = 0, d = 0, r0 = 0, jo = 0, k0 = 0; t < T; ++t) {
         const int row = r0 + r;
         const float dval = qt == 0 ? dh[0] : qt == 1 ? dh[1] : qt == 2 ? dh[2] : dh[3];
