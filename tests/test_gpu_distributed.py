@@ -140,7 +140,8 @@ def _peer_worker(rank, world, port, shape, seed, results):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,shape", [(2, (1, 2, 256, 64)), (3, (2, 2, 384, 64)), (4, (1, 3, 512, 64))])
+@pytest.mark.parametrize("world,shape", [(2, (1, 2, 256, 64)), (3, (2, 2, 384, 64)), (4, (1, 3, 512, 64)),
+                                         (2, (2, 2, 400, 64))])  # c = 200: ragged tiles
 def test_peer_ring_matches_oracle(world, shape):
     """PeerRing: one fwd_factored_peer / bwd_fused_peer launch per rank reading every origin's
     K/V through CUDA IPC (here: processes sharing one B200), against the oracle."""
