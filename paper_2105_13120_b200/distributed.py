@@ -326,8 +326,9 @@ class PeerRing:
     charges the reference's ring convention (ringseq/ring_attention.py:124-217) for the
     same K/V bytes.
 
-    This is the correctness-first form: staging is fenced by host barriers (buffer free
-    on every rank, then staged on every rank).  Cross-process CUDA IPC events would
+    ``forward`` does not read its status flag back; call ``PeerRing.check(ctx)`` (one device
+    sync) before trusting a layer's outputs.  This is the correctness-first form: staging
+    is fenced by host barriers (buffer free on every rank, then staged on every rank).  Cross-process CUDA IPC events would
     replace them.  The buffers are plain cudaMalloc allocations exported with
     cudaIpcGetMemHandle (``rsa_ipc_*``), outside torch's allocator, so their lifetime is
     exactly ``close()``.
@@ -432,6 +433,21 @@ class PeerRing:
         self.ledger.record_ring_send(d, 2 * (n - 1) * elements, 2 * (n - 1) * elements * q.element_size())
         return out, RingContext(q=q, k_slots=None, panel=panel, out=out, v_local=v,
                                 extra={"flag": flag, "rowscale": rowscale, "slot": slot})
+
+    @staticmethod
+    def check(ctx: RingContext) -> None:
+        """Host read of the forward's status flag (a device sync).  Bit 0: a non-finite score
+        (``NumericError``, as ringseq/tensor_ops.py:80-81).  Bit 1: a row whose scores exceed
+        the single-pass panel's headroom above its first key tile's max.
+        The resident engine reruns those layers two-pass; this ring has no two-pass peer
+        kernel, so it raises and ``SpmdRing`` is the path for such inputs."""
+        from .errors import NumericError
+
+        status = int(ctx.extra["flag"].item())
+        if status & 1:
+            raise NumericError("softmax_rows requires finite inputs")
+        if status & 2:
+            raise NumericError("score range exceeds the single-pass panel's headroom; use SpmdRing")
 
     def backward(self, ctx: RingContext, grad: torch.Tensor):
         """grad: this rank's [1][B][Z][c][A] dO.  Returns (dq, dk, dv) chunks."""

@@ -127,6 +127,7 @@ def _peer_worker(rank, world, port, shape, seed, results):
         dq, dk, dv = ring.backward(outs[1][1], ch(g))
         dq0, dk0, dv0 = ring.backward(outs[0][1], ch(g))
         out, ctx = ring.forward(ch(q), ch(k), ch(v))  # reuses a released slot
+        PeerRing.check(ctx)
         torch.cuda.synchronize()
         f64 = lambda t: t.float().cpu().numpy().astype(np.float64)  # noqa: E731
         probs = engine.normalized_panel(ctx.panel[0], ctx.extra["rowscale"][0])
