@@ -549,28 +549,59 @@ def bench_main(args, metric, unit, config, clock_sampler=None, peaks=None):
     else:
         ms, clocks = timed(step, args.steps), None
 
-    # end to end: this rank's q, k, v, dO chunks from pinned host memory, O and dQ/dK/dV back
+    # end to end: this rank's q, k, v, dO chunks from pinned host memory, O and dQ/dK/dV back;
+    # step s + 1's uploads run on a copy stream into the other buffer set while step s
+    # computes and copies down (the same pipelining as bench.py's single-GPU e2e)
     hg = torch.Generator().manual_seed(2000 + rank)
     host = [[torch.randn((1, B, Z, c, A), generator=hg).to(torch.bfloat16).pin_memory() for _ in range(4)]
             for _ in range(LAYERS)]
     outs = [[torch.empty((1, B, Z, c, A), dtype=torch.bfloat16).pin_memory() for _ in range(4)]
             for _ in range(LAYERS)]
+    copy = torch.cuda.Stream(dev)
+    cur = torch.cuda.current_stream(dev)
+    bufs = [[[torch.empty((1, B, Z, c, A), dtype=torch.bfloat16, device=dev) for _ in range(4)]
+             for _ in range(LAYERS)] for _ in range(2)]
+    up, free = [None, None], [None, None]
 
-    def e2e_step():
+    def upload(si):
+        with torch.cuda.stream(copy):
+            if free[si] is not None:
+                copy.wait_event(free[si])
+            for hb, db in zip(host, bufs[si]):
+                for dst, src in zip(db, hb):
+                    dst.copy_(src, non_blocking=True)
+            up[si] = torch.cuda.Event()
+            up[si].record(copy)
+
+    def e2e_step(si, prefetch):
+        cur.wait_event(up[si])
         ctxs = []
-        for (q, k, v, _), o in zip(host, outs):
-            out, ctx = ring.forward(q.to(dev, non_blocking=True), k.to(dev, non_blocking=True),
-                                    v.to(dev, non_blocking=True), flag)
+        for (q, k, v, _), o in zip(bufs[si], outs):
+            out, ctx = ring.forward(q, k, v, flag)
             o[0].copy_(out, non_blocking=True)
             ctxs.append(ctx)
+        if prefetch:
+            upload(1 - si)
         for i in reversed(range(LAYERS)):
-            dq, dk, dv = ring.backward(ctxs[i], host[i][3].to(dev, non_blocking=True))
+            dq, dk, dv = ring.backward(ctxs[i], bufs[si][i][3])
             for j, t in enumerate((dq, dk, dv)):
                 outs[i][j + 1].copy_(t, non_blocking=True)
+        free[si] = torch.cuda.Event()
+        free[si].record(cur)
 
-    e2e_step()
-    e2e_steps = max(1, min(args.steps, getattr(args, "e2e_steps", 2)))
-    e2e_ms = timed(e2e_step, e2e_steps)
+    upload(0)
+    e2e_step(0, False)
+    e2e_steps = max(1, getattr(args, "e2e_steps", 8))
+    state = {"i": 0}
+
+    def timed_e2e():
+        i = state["i"]
+        if i == 0:
+            upload(0)
+        e2e_step(i % 2, i + 1 < e2e_steps)
+        state["i"] = i + 1
+
+    e2e_ms = timed(timed_e2e, e2e_steps)
     chunk_bytes = B * Z * c * A * 2
 
     if int(flag.item()):
