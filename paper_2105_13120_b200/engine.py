@@ -47,9 +47,12 @@ class KernelTimer:
     launch; ``totals()`` returns {name: (launches, total_ms)} after a sync.
     """
 
-    def __init__(self):
+    def __init__(self, external: bool = False):
         self.events: dict[str, list] = {}
         self.enabled = True
+        # external: events that keep their timestamps when recorded inside a CUDA-graph
+        # capture (cudaEventRecordExternal), so a replayed step can be timed per kernel
+        self.external = external
 
     def __call__(self, name: str):
         return _Span(self, name)
@@ -70,12 +73,12 @@ class _Span:
 
     def __enter__(self):
         if self.t.enabled:
-            self.a = torch.cuda.Event(enable_timing=True)
+            self.a = torch.cuda.Event(enable_timing=True, external=self.t.external)
             self.a.record()
 
     def __exit__(self, *exc):
         if self.t.enabled:
-            b = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True, external=self.t.external)
             b.record()
             self.t.events.setdefault(self.name, []).append((self.a, b))
 
