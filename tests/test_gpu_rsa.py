@@ -596,3 +596,45 @@ def test_tensor_parallel_comparator_matches_reference_goldens(rsa, golden):
         tp.tensor_parallel_attention(x, pkg.AttentionWeights(*ws),
                                      pkg.AttentionConfig(batch_size=b, seq_len=seq, hidden_size=h, num_heads=z,
                                                          head_size=a, num_devices=3))
+
+
+def _random_geometries(count, seed):
+    """Seeded (B, Z, L, A=64, N) draws: every chunk a multiple of 8 rows, some with more
+    than 4 query tiles per head (the two-kernel backward), ragged last tiles included."""
+    rng = np.random.default_rng(seed)
+    shapes = []
+    while len(shapes) < count:
+        n = int(rng.integers(1, 5))
+        c = 8 * int(rng.integers(1, 97))  # 8 .. 768 rows per rank
+        b, z = int(rng.integers(1, 3)), int(rng.integers(1, 4))
+        if b * z * (n * c) ** 2 > 3_000_000:  # keep the float64 oracle quick
+            continue
+        shapes.append((b, z, n * c, 64, n))
+    return shapes
+
+
+@pytest.mark.parametrize("shape", _random_geometries(10, seed=2105))
+def test_fused_paths_match_oracle_random_geometry(rsa, shape):
+    """Seeded geometry sweep of the fused forward (factored panel) and whichever backward
+    the engine picks (single pass when <= 4 query tiles per head, else rsa_bwd_dkdv +
+    rsa_bwd_dq), against the float64 oracle with the same gates as the fixed shapes."""
+    from paper_2105_13120_b200 import engine
+
+    b, z, seq, a, n = shape
+    q, k, v, g = _inputs(b, z, seq, a, seed=7 + seq + 13 * n)
+    dev = torch.device("cuda", 0)
+    stack = lambda x: torch.from_numpy(np.stack(orc.chunks_of(x, n))).to(dev, torch.bfloat16)  # noqa: E731
+    tq, tk, tv, tg = (stack(x) for x in (q, k, v, g))
+    out, panel, rowscale, flag = engine.forward(tq, tk, tv, path="auto")
+    assert int(flag.item()) == 0
+    dq, dk, dv = engine.backward(tq, tk, tv, panel, tg, outputs=out, rowscale=rowscale, path="auto")
+    torch.cuda.synchronize()
+    wout, wprobs, wdq, wdk, wdv = _oracle(q, k, v, g, n)
+    cat = lambda t: np.concatenate([_np(t[d]) for d in range(n)], axis=-2)  # noqa: E731
+    _gate("out", cat(out), wout)
+    for d in range(n):
+        got = _np(engine.normalized_panel(panel[d], None if rowscale is None else rowscale[d]))
+        assert np.max(np.abs(got - wprobs[d])) <= PROB_ABS
+    _gate("dq", cat(dq), wdq)
+    _gate("dk", cat(dk), wdk)
+    _gate("dv", cat(dv), wdv)
