@@ -137,54 +137,104 @@ class ClockSampler:
 
 # ------------------------------------------------------------- CPU oracle
 
-def cpu_oracle_sample(args, threads):
-    """Time the reference algorithm (oracle port) on one layer of a B=1 slice.
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    Uses N_sim = threads simulated ranks on a thread pool (the reference's
-    concurrent executor); returns tokens/s for the 12-layer stack.
-    """
+
+def host_threads() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def _oracle_layer(args, n_sim, workers, rng):
+    """One RSA layer fwd+bwd of ONE sequence (B=1, Z, L, A) through the oracle port of the
+    reference algorithm (oracle/ringseq_np.py, exact=True: float64 rank-1-update matmul as
+    ringseq/tensor_ops.py:44-72) with n_sim simulated ring ranks on `workers` threads."""
     from oracle import ringseq_np as orc
 
-    seq, z, a = args.seq, args.heads, args.head_size
-    n_sim = max(1, min(threads, 8))
-    while seq % n_sim:
-        n_sim -= 1
-    rng = orc.make_rng(0)
-    q, k, v, g = (rng.standard_normal((1, z, seq, a)) for _ in range(4))
+    q, k, v, g = (rng.standard_normal((1, args.heads, args.seq, args.head_size)) for _ in range(4))
     ch = lambda x: orc.chunks_of(x, n_sim)  # noqa: E731
-    best = math.inf
-    for _ in range(2):
-        t0 = time.perf_counter()
-        _, probs, _ = orc.ring_forward(ch(q), ch(k), ch(v), exact=True, workers=n_sim)
-        orc.ring_backward(ch(q), ch(k), ch(v), probs, ch(g), exact=True, workers=n_sim)
-        best = min(best, time.perf_counter() - t0)
-    tokens_per_s = seq / (best * args.layers)
-    sample = (f"1 RSA layer fwd+bwd, B=1 Z={z} L={seq} A={a}, {n_sim} simulated ranks on {n_sim} threads, "
-              f"float64 rank-1-update matmul (oracle/ringseq_np.py exact=True); best of 2 = {best:.3f} s; "
-              f"scaled to the {args.layers}-layer step")
+    t0 = time.perf_counter()
+    _, probs, _ = orc.ring_forward(ch(q), ch(k), ch(v), exact=True, workers=workers)
+    orc.ring_backward(ch(q), ch(k), ch(v), probs, ch(g), exact=True, workers=workers)
+    return time.perf_counter() - t0
+
+
+def _sim_ranks(args, threads):
+    n_sim = max(1, min(threads, 8))
+    while args.seq % n_sim:
+        n_sim -= 1
+    return n_sim
+
+
+def cpu_oracle_sample(args, threads):
+    """cpu_baseline of our arm: one layer of one sequence (bounded, ~0.3 s on 8 cores),
+    best of 2, as tokens/s of the layer stack (per-token work is batch-independent)."""
+    from oracle import ringseq_np as orc
+
+    n_sim = _sim_ranks(args, threads)
+    rng = orc.make_rng(0)
+    best = min(_oracle_layer(args, n_sim, n_sim, rng) for _ in range(2))
+    tokens_per_s = args.seq / (best * args.layers)
+    sample = (f"1 RSA layer fwd+bwd of 1 sequence (B=1 Z={args.heads} L={args.seq} A={args.head_size}), "
+              f"{n_sim} simulated ranks on {n_sim} threads, float64 rank-1-update matmul (oracle/ringseq_np.py "
+              f"exact=True); best of 2 = {best:.3f} s per layer; tokens/s = L / ({args.layers} x layer time)")
     return tokens_per_s, n_sim, sample
 
 
 def reference_arm(args):
+    """--impl reference: the reference's CPU algorithm on the host cores, timed per step.
+
+    /root/reference does not travel to the GPU box, so the oracle port (pinned bitwise to
+    goldens generated from the unmodified reference) is what runs.  One step is a bounded
+    sample of the workload: ONE of the B sequences through all `layers` RSA layers fwd+bwd
+    (the same work per token as the GPU step), with the sequence split over simulated ring
+    ranks run on all host threads (the reference's concurrent executor).  `ms_per_step` and
+    `steps` are what actually ran; `value` = tokens of the sample / step time.
+    """
     world, rank, _ = dist_env()
     n = max(args.gpus, world)
     if rank != 0:
         return
-    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    vals = []
-    for _ in range(max(1, args.steps)):
-        v, cores, sample = cpu_oracle_sample(args, threads)
-        vals.append(v)
-    value = statistics.median(vals)
+    from oracle import ringseq_np as orc
+
+    threads = host_threads()
+    n_sim = _sim_ranks(args, threads)
+    rng = orc.make_rng(0)
+
+    def one_step():
+        return sum(_oracle_layer(args, n_sim, n_sim, rng) for _ in range(args.layers))
+
+    warm = min(args.warmup, 1)
+    for _ in range(warm):
+        one_step()
+    times = [one_step() for _ in range(max(1, args.steps))]
+    ms = 1e3 * sum(times) / len(times)
+    value = args.seq / (ms / 1e3)
+    seq_one = _oracle_layer(args, n_sim, 1, rng)  # the sequential executor: one core
+    sample = (f"per step: 1 of the {args.batch * n} sequences (B=1 Z={args.heads} L={args.seq} A={args.head_size}) "
+              f"through all {args.layers} layers fwd+bwd, {n_sim} simulated ring ranks on {n_sim} threads, float64 "
+              f"rank-1-update matmul (oracle/ringseq_np.py exact=True)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": args.batch * n * args.seq / value * 1e3,
+        "steps": len(times), "warmup": warm, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_obj(args, n),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "data": "synthetic N(0,1) float64 (make_rng(0))", "config": config_obj(args, n),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": n_sim, "kind": "port", "sample": sample,
+                         "cpu_model": cpu_model(), "cpu_count": os.cpu_count(), "affinity": threads,
+                         "sequential_executor": {"value": args.seq / (seq_one * args.layers), "unit": UNIT,
+                                                 "cores": 1, "layer_s": seq_one}},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_sample": {"sequences_per_step": 1, "of_global_batch": args.batch * n, "layers": args.layers,
+                        "step_times_s": [round(t, 4) for t in times]},
         "note": "reference is a float64 NumPy simulator; /root/reference is absent on the GPU box, so the "
-                "oracle port of its algorithm (pinned bitwise to reference goldens) is timed",
+                "oracle port of its algorithm (pinned bitwise to reference goldens) is timed; warm-up capped at "
+                "1 step (no device state to warm)",
     }
     print(json.dumps(line), flush=True)
 
@@ -262,7 +312,6 @@ def ours(args):
     dvec = torch.empty((1, B, Z, c), dtype=torch.float32, device=dev)
     g_scaled = torch.empty((1, B, Z, c, A), dtype=torch.bfloat16, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    timer = engine.KernelTimer()
 
     def step(tm=None):
         for ly in layers:
@@ -310,41 +359,58 @@ def ours(args):
     value = B * L / (ms / 1e3)
     clocks = clk.result()
 
-    # per-kernel timing pass: event pairs around each launch on its stream -- inside the
-    # replayed graph when the step is timed as one (external events keep their timestamps
-    # in a capture), else around the eager launches
-    reps = max(1, min(args.steps, 3))
-    tot = None
-    if graph_used:
-        try:
-            gt = engine.KernelTimer(external=True)
-            tgraph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(tgraph):
-                step(gt)
-            acc = {}
-            for _ in range(reps):
-                tgraph.replay()
-                for k, (n_, ms_) in gt.totals().items():
-                    c0, t0 = acc.get(k, (0, 0.0))
-                    acc[k] = (c0 + n_, t0 + ms_)
-            tot = acc
-            timing_mode = "event pairs inside the replayed step graph"
-        except Exception as exc:
-            print(f"graph-captured kernel timing failed ({exc}); timing eager launches", file=sys.stderr)
-            torch.cuda.synchronize()
-    if tot is None:
-        timer.reset()
+    # Per-kernel timing: one CUDA graph per kernel type holding only that type's launches
+    # of the step (the step's own arguments, in step order), replayed and timed with an
+    # event pair on the capture/replay stream.  No timing node sits inside a measured graph,
+    # so the per-type times add up to the step time (up to launch-gap noise) and the
+    # dominant kernel's per-launch time is its own.
+    from paper_2105_13120_b200 import tensor_ops as ops
+
+    def launches(kind):
+        def run():
+            if kind == "fwd_factored":
+                for ly in layers:
+                    engine.forward(ly["q"], ly["k"], ly["v"], path="fused", flag=flag, out=ly["o"], panel=ly["p"],
+                                   rowscale=ly["r"])
+            elif kind == "rowdot":
+                for ly in reversed(layers):
+                    ops.rowdot_scale(ly["g"], ly["o"], ly["r"], out=dvec, a_scaled=g_scaled)
+            else:
+                for ly in reversed(layers):
+                    engine.backward(ly["q"], ly["k"], ly["v"], ly["p"], ly["g"], outputs=ly["o"], path="fused",
+                                    grads=ly["grads"], dvec=dvec, rowscale=ly["r"], grad_scaled=g_scaled,
+                                    prologue=False)
+        return run
+
+    reps = max(3, min(args.steps, 10))
+    kinds = ["fwd_factored", "rowdot", "bwd_fused"]
+    type_ms = {}
+    for kind in kinds:
+        fn = launches(kind)
+        fn()
+        torch.cuda.synchronize()
+        replay = fn
+        if graph_used:
+            kg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(kg):
+                fn()
+            replay = kg.replay
+            replay()
+        torch.cuda.synchronize()
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record()
         for _ in range(reps):
-            step(timer)
-        tot = timer.totals()
-        timing_mode = "event pairs around eager launches"
+            replay()
+        k1.record()
+        torch.cuda.synchronize()
+        type_ms[kind] = k0.elapsed_time(k1) / reps
+    timing_mode = (f"per kernel type: a CUDA graph of that type's {LAYERS} launches of the step, replayed {reps}x, "
+                   f"event pair on the replay stream")
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)
     tc = pk.get("bf16_tflops_sustained", 1400.0)
-    shares = {k: v[1] for k, v in tot.items()}
-    dom = max(shares, key=shares.get)
-    launches, dom_ms = tot[dom]
-    per_launch_s = dom_ms / launches / 1e3
+    dom = max(type_ms, key=type_ms.get)
+    per_launch_s = type_ms[dom] / LAYERS / 1e3
     byts, flops = kernel_model(dom, 1, B, Z, c, L, A)
     t_hbm, t_tc = byts / (hbm * 1e9), flops / (tc * 1e12)
     if t_hbm >= t_tc:
@@ -353,17 +419,33 @@ def ours(args):
         roof = {"bound": "tensor", "achieved": flops / per_launch_s / 1e12, "peak": tc, "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["kernel"] = dom
+    roof["us_per_launch"] = per_launch_s * 1e6
+    roof["algorithmic_bytes_per_launch"] = byts
     roof["traffic"] = traffic_of(dom)
+    roof["traffic_source"] = "profiles/traffic.json (ncu --set full capture of this kernel at this shape)"
     roof["peak_source"] = "MEASURED_PEAKS.json" if pk else "fallback (B200_PROFILING.md)"
     roof["timing"] = timing_mode
+    # whole step against SURVEY.md section 8(d): 4*P_e + 16*C_e algorithmic HBM bytes per layer
+    p_e, c_e = B * Z * c * L, B * Z * c * A
+    step_bytes = LAYERS * (4 * p_e + 16 * c_e)
+    roof["step"] = {"bytes": step_bytes, "achieved": step_bytes / (ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                    "frac": step_bytes / (ms / 1e3) / 1e9 / hbm,
+                    "definition": "SURVEY.md 8(d): per layer 4*P_e (bf16 panel written + read) + 16*C_e "
+                                  "(q, k, v, o, dO, dQ, dK, dV bf16)"}
     kernels = {}
-    step_kernel_ms = sum(shares.values()) / max(1, min(args.steps, 3))
-    for k, (cnt, tms) in tot.items():
+    for k, tms in type_ms.items():
         b_, f_ = kernel_model(k, 1, B, Z, c, L, A)
-        per = tms / cnt / 1e3
-        kernels[k] = {"launches_per_step": cnt // max(1, min(args.steps, 3)), "us_per_launch": per * 1e6,
-                      "share": tms / sum(shares.values()), "GB/s": b_ / per / 1e9, "TFLOP/s": f_ / per / 1e12}
-    launches_per_step = sum(v["launches_per_step"] for v in kernels.values())
+        per = tms / LAYERS / 1e3
+        kernels[k] = {"launches_per_step": LAYERS, "us_per_launch": per * 1e6, "ms_per_step": tms,
+                      "share_of_step": tms / ms, "GB/s": b_ / per / 1e9, "TFLOP/s": f_ / per / 1e12}
+    kernel_sum = sum(type_ms.values())
+    launches_per_step = LAYERS * len(kinds)
+
+    # parity of the timed path: re-run one step, then check sampled heads of the first and
+    # last layer against the float64 oracle (ringseq/reference.py:66-103 per head)
+    run()
+    torch.cuda.synchronize()
+    parity = sampled_parity(layers, B, Z, seed=11)
 
     # end to end through the public API, pinned host buffers
     e2e = e2e_public_api(args, dev)
@@ -373,14 +455,48 @@ def ours(args):
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic N(0,1) bf16 inputs, per-layer q/k/v/dO", "config": config_obj(args, 1),
         "launch": "cuda graph of the whole step, replayed" if graph_used else "eager launches",
-        "clocks": clocks, "roofline": roof, "kernels": kernels, "kernel_ms_per_step": step_kernel_ms,
-        "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
+        "clocks": clocks, "roofline": roof, "kernels": kernels, "kernel_ms_sum": kernel_sum,
+        "kernel_sum_over_step": kernel_sum / ms, "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
+        "parity": parity,
     }
     if not args.no_cpu_baseline:
-        threads = len(os.sched_getaffinity(0))
-        v, cores, sample = cpu_oracle_sample(args, threads)
+        v, cores, sample = cpu_oracle_sample(args, host_threads())
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
     print(json.dumps(line), flush=True)
+
+
+def sampled_parity(layers, B, Z, seed, heads_per_layer=8):
+    """Max errors of sampled heads of the first and last layer of the timed step vs the
+    oracle (oracle.attention_head_sampled, float64), with the parity tests' gates."""
+    import numpy as np
+    import torch
+
+    from oracle import ringseq_np as orc
+    from paper_2105_13120_b200 import engine
+
+    rng = np.random.default_rng(seed)
+    worst = {"out": 0.0, "probs_abs": 0.0, "dq": 0.0, "dk": 0.0, "dv": 0.0}
+    checked = 0
+    for li in (0, len(layers) - 1):
+        ly = layers[li]
+        for item in sorted(set(rng.integers(0, B * Z, heads_per_layer).tolist()) | {B * Z - 1}):
+            b, z = divmod(int(item), Z)
+            f = lambda t: t[0, b, z].double().cpu().numpy()  # noqa: E731
+            q, k, v, g = (f(ly[x]) for x in ("q", "k", "v", "g"))
+            seq = q.shape[0]
+            want = orc.attention_head_sampled(q, k, v, g, np.arange(seq), np.arange(seq))
+            got = {"out": f(ly["o"]), "dq": f(ly["grads"][0]), "dk": f(ly["grads"][1]), "dv": f(ly["grads"][2])}
+            for key, val in got.items():
+                ref = want[key]
+                worst[key] = max(worst[key], float(np.linalg.norm(val - ref) / np.linalg.norm(ref)))
+            p = engine.normalized_panel(ly["p"][0, b, z], ly["r"][0, b, z]).double().cpu().numpy()
+            worst["probs_abs"] = max(worst["probs_abs"], float(np.max(np.abs(p - want["probs"]))))
+            checked += 1
+    ok = all(worst[k] <= 1e-2 for k in ("out", "dq", "dk", "dv")) and worst["probs_abs"] <= 4e-3
+    return {"heads_checked": checked, "layers": [0, len(layers) - 1], "max_error": worst, "pass": ok,
+            "gates": "out, dq, dk, dv: relative Frobenius error <= 1e-2; probs_abs: max |diff| of the "
+                     "materialised probability rows <= 4e-3",
+            "oracle": "oracle/ringseq_np.py attention_head_sampled (float64), same bf16 inputs"}
 
 
 def e2e_public_api(args, dev):

@@ -69,6 +69,11 @@ int rsa_abi_version(void);
 const char* rsa_last_error(void);
 int rsa_num_sms(void);
 
+/* Test hook: cap the grid of every persistent kernel at max_ctas CTAs (0 = one per SM,
+ * the default), so small shapes exercise the multi-unit-per-CTA paths (resident K tiles,
+ * next-head prefetch, phase flips) that large launches take.  Returns the previous cap. */
+int rsa_set_max_ctas(int max_ctas);
+
 /* ------------------------------------------------------------ primitives */
 
 /*

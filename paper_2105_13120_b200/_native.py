@@ -64,6 +64,7 @@ EXPORTS = {
     "rsa_abi_version": (c_int, []),
     "rsa_last_error": (ctypes.c_char_p, []),
     "rsa_num_sms": (c_int, []),
+    "rsa_set_max_ctas": (c_int, [c_int]),
     "rsa_gemm": (
         c_int,
         [c_int, c_int, c_int,

@@ -77,6 +77,14 @@ int num_sms() {
   return cached;
 }
 
+static int g_max_ctas = 0;  // 0: one CTA per SM (rsa_set_max_ctas)
+
+int persistent_grid(int64_t items) {
+  int64_t grid = num_sms();
+  if (g_max_ctas > 0 && g_max_ctas < grid) grid = g_max_ctas;
+  return int(items < grid ? items : grid);
+}
+
 }  // namespace rsa
 
 extern "C" {
@@ -84,6 +92,12 @@ extern "C" {
 int rsa_abi_version(void) { return RSA_ABI_VERSION; }
 const char* rsa_last_error(void) { return rsa::g_err; }
 int rsa_num_sms(void) { return rsa::num_sms(); }
+
+int rsa_set_max_ctas(int max_ctas) {
+  const int prev = rsa::g_max_ctas;
+  rsa::g_max_ctas = max_ctas > 0 ? max_ctas : 0;
+  return prev;
+}
 
 int rsa_ipc_alloc(size_t bytes, void** ptr, void* handle) {
   if (!ptr || !handle || !bytes) return rsa::fail(RSA_ERR_INVALID, "rsa_ipc_alloc: null argument or zero size");

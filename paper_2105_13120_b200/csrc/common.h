@@ -31,4 +31,7 @@ inline bool stride_ok(int64_t bytes) { return bytes >= 0 && (bytes % 16) == 0 &&
 
 int num_sms();
 
+// Grid of a persistent kernel: min(items, SMs, the rsa_set_max_ctas cap).
+int persistent_grid(int64_t items);
+
 }  // namespace rsa

@@ -221,7 +221,7 @@ int launch(K kernel, int items, uint32_t smem, const A& args, void* stream, cons
            int threads = NTHREADS) {
   if (items <= 0) return RSA_OK;
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const int grid = items < num_sms() ? items : num_sms();
+  const int grid = persistent_grid(items);
   kernel<<<grid, threads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(args);
   return check_launch(name);
 }

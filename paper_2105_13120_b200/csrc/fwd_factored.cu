@@ -541,7 +541,7 @@ int ff_launch(FfArgs& a, const rsa_geom* g, rsa_view q, rsa_view panel, rsa_view
   if (cudaFuncGetAttributes(&fa, fwd_factored_kernel) == cudaSuccess && fa.maxThreadsPerBlock < FF_THREADS)
     return fail(RSA_ERR_CUDA, "rsa_fwd_factored: %d registers/thread allow only %d threads per CTA (need %d)",
                 fa.numRegs, fa.maxThreadsPerBlock, FF_THREADS);
-  const int grid = units < num_sms() ? units : num_sms();
+  const int grid = persistent_grid(units);
   fwd_factored_kernel<<<grid, FF_THREADS, FF_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(a);
   if (trace_path) {
     static long long host[(FF_THREADS / 32) * 4096];

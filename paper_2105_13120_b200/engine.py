@@ -255,7 +255,8 @@ def single_pass_supported(n: int, b: int, z: int, c: int, a: int) -> bool:
 
 def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path: str = "auto",
              grads: tuple | None = None, dvec: torch.Tensor | None = None, rowscale: torch.Tensor | None = None,
-             grad_scaled: torch.Tensor | None = None, timer=None, single_pass: bool | None = None):
+             grad_scaled: torch.Tensor | None = None, timer=None, single_pass: bool | None = None,
+             prologue: bool = True):
     """RSA backward on stacked chunks; returns (dq, dk, dv) as [N][B][Z][c][A] bf16.
 
     ``grads`` / ``dvec`` optionally supply preallocated output and D buffers
@@ -266,7 +267,9 @@ def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path:
     ``rowscale`` marks ``panel`` as factored (P = rowscale * panel, see
     ``forward``): rsa_rowdot_scale then forms D*r and dO*r (``grad_scaled``
     optionally preallocates the latter) and the same kernels consume the
-    factored panel unchanged."""
+    factored panel unchanged.  ``prologue=False`` skips that row pass: ``dvec`` (and
+    ``grad_scaled`` for a factored panel) must already hold its results (bench.py times
+    the two launches separately)."""
     n, b, z, c, a = q.shape
     seq = n * c
     dev = q.device
@@ -279,11 +282,18 @@ def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path:
     which = _pick(path, n, b, z, c, a)
     if which == "fused":
         tm = timer or _NO_TIMER
-        if outputs is None:
+        if outputs is None and prologue:
             outputs = recompute_outputs(normalized_panel(panel, rowscale, torch.bfloat16), v)
         if dvec is None:
+            if not prologue:
+                raise ValueError("prologue=False needs the precomputed dvec")
             dvec = torch.empty((n, b, z, c), dtype=torch.float32, device=dev)
-        if rowscale is None:
+        if not prologue:
+            if rowscale is not None:
+                if grad_scaled is None:
+                    raise ValueError("prologue=False with a factored panel needs grad_scaled")
+                grad = grad_scaled
+        elif rowscale is None:
             with tm("rowdot"):
                 ops.rowdot(grad, outputs, out=dvec)  # D = rowsum(dO * O) = rowsum(dP * P)
         else:  # factored panel: D*r and dO*r, so P (dP - D) = P~ (dO*r V^T - D*r) and P^T dO = P~^T (dO*r)

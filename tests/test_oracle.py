@@ -299,3 +299,19 @@ def test_mlp_backward_finite_differences():
             minus = [y - d if i == which else y for i, y in enumerate(args)]
             fd = (loss(plus) - loss(minus)) / (2 * eps)
             assert abs(fd - grad[idx]) <= 1e-6 * max(1.0, abs(fd)), (which, idx)
+
+
+def test_attention_head_sampled_matches_dense_oracle():
+    """The blockwise sampled-head oracle (used by the large-geometry GPU tests and by
+    bench.py's parity field) against the dense attention oracle."""
+    rng = orc.make_rng(5)
+    seq, a = 300, 16
+    q, k, v, g = (rng.standard_normal((seq, a)) for _ in range(4))
+    rows, keys = [0, 7, 128, 299], [1, 64, 250]
+    got = orc.attention_head_sampled(q, k, v, g, rows, keys, block=64)
+    out = orc.attention_forward(q, k, v, exact=False)
+    dq, dk, dv = orc.attention_backward(q, k, v, g, exact=False)
+    probs = orc.softmax_rows(orc.matmul(q, k.T, exact=False) / np.sqrt(a))
+    for name, want in (("out", out[rows]), ("probs", probs[rows]), ("dq", dq[rows]), ("dk", dk[keys]),
+                       ("dv", dv[keys])):
+        assert np.max(np.abs(got[name] - want)) <= 1e-12, name
