@@ -455,11 +455,16 @@ class PeerRing:
         from . import tensor_ops as ops
         from ._native import check, lib
 
+        from .errors import StateError
+
         n, d = self.world, self.rank
         _, b, z, c, a = grad.shape
         seq = n * c
         dev = grad.device
-        slot = ctx.extra["slot"]
+        if "slot" not in ctx.extra:
+            raise StateError("PeerRing.backward: this context's K/V slot was already released by a backward")
+        self.check(ctx)  # the forward's status flag, read at this first synchronising use
+        slot = ctx.extra.pop("slot")  # released exactly once: a second backward must not re-pool it
         dvec, grad_r = ops.rowdot_scale(grad, ctx.out, ctx.extra["rowscale"])  # D*r and dO*r (factored panel)
         dq = torch.empty((1, b, z, c, a), dtype=torch.bfloat16, device=dev)
         dk_part = torch.empty((n, b, z, c, a), dtype=torch.float32, device=dev)

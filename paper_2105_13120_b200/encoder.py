@@ -101,6 +101,7 @@ class EncoderLayer:
         y = ops.matmul(act, w.down)
         y += x1
         self.flag = res.flag
+        self.unchecked = not check
         self.saved = (x, q, k, v, res, merged, x1b, hpre, act)
         return y.to(torch.bfloat16)
 
@@ -108,6 +109,15 @@ class EncoderLayer:
         """gy: dL/dy [N][B][c][H] -> (dL/dx bf16, EncoderWeights of fp32 gradients)."""
         c, w = self.cfg, self.w
         x, q, k, v, res, merged, x1b, hpre, act = self.saved
+        if getattr(self, "unchecked", False):
+            # an unchecked forward is checked here, at its first synchronising use: its
+            # outputs already flowed on, so a flagged layer cannot be recomputed silently
+            status = int(res.flag.item())
+            if status & 1:
+                raise NumericError("softmax_rows requires finite inputs")
+            if status & 2:
+                raise NumericError("a row exceeded the single-pass panel's headroom in an unchecked forward; "
+                                   "rerun the layer with forward(check=True)")
         h, inner, za = c.hidden_size, w.up.shape[1], c.num_heads * c.head_size
         gy = gy.to(torch.bfloat16)
         # MLP

@@ -93,6 +93,13 @@ class ProbPanels(list):
         # in-place version) of the caller's torch chunks: a backward called with the same,
         # unmodified tensors reuses them instead of uploading again
         self.inputs = inputs or []
+        # a caller that replaces a panel (probs[d] = X) gets reference semantics: the
+        # backward then uses the given panels, not the saved stack
+        self.dirty = False
+
+    def __setitem__(self, i, value):
+        list.__setitem__(self, i, value)
+        self.dirty = True
 
     def _get(self, d: int):
         item = list.__getitem__(self, d)
@@ -121,7 +128,7 @@ def _check_chunks(name: str, chunks, cfg: AttentionConfig, expect: tuple) -> lis
     chunks = chunks if isinstance(chunks, list) else list(chunks)  # keep ProbPanels intact
     if len(chunks) != cfg.num_devices:
         raise ShapeError(f"{name}: got {len(chunks)} chunks for {cfg.num_devices} devices")
-    if isinstance(chunks, ProbPanels):  # shape check without materialising the panels
+    if isinstance(chunks, ProbPanels) and not chunks.dirty:  # shape check without materialising the panels
         if chunks.panel_shape != expect:
             raise ShapeError(f"{name}[0] has shape {chunks.panel_shape}, expected {expect}")
         return chunks
@@ -149,7 +156,7 @@ def _stack(chunks: list, device) -> torch.Tensor:
     bf16 torch chunks in pinned host memory are copied asynchronously on the
     current stream; a single device chunk that is already bf16 and contiguous
     is used in place (a view, no copy)."""
-    if isinstance(chunks, ProbPanels) and chunks.stacked.device == device:
+    if isinstance(chunks, ProbPanels) and not chunks.dirty and chunks.stacked.device == device:
         return chunks.stacked
     first = chunks[0]
     if (len(chunks) == 1 and isinstance(first, torch.Tensor) and first.device == device
@@ -265,17 +272,24 @@ def ring_attention_backward(q_chunks, k_chunks, v_chunks, probs, grad_chunks, cf
     dev = _device_of(q_chunks, k_chunks, v_chunks, grad_chunks, probs)
     saved = probs.inputs if isinstance(probs, ProbPanels) else []
 
-    def stack_or_saved(chunks):
-        for key, t in saved:
+    def stack_or_saved(chunks, i):
+        if i < len(saved):
+            key, t = saved[i]
             if t.device == dev and _same_chunks(key, chunks):
-                return t
-        return _stack(chunks, dev)
+                return t, True
+            if key is None and t.device == dev:  # NumPy chunks: identity unknown, compare values
+                up = _stack(chunks, dev)
+                return (t, True) if torch.equal(up, t) else (up, False)
+        return _stack(chunks, dev), False
 
-    q, k, v = (stack_or_saved(x) for x in (q_chunks, k_chunks, v_chunks))
+    (q, _), (k, _), (v, v_saved) = (stack_or_saved(x, i) for i, x in enumerate((q_chunks, k_chunks, v_chunks)))
     g = _stack(grad_chunks, dev)
     panel = _stack(probs, dev)
     own = isinstance(probs, ProbPanels) and panel is probs.stacked
-    outputs = probs.outputs if own else None
+    # the forward's O = P V is reused for D = rowsum(dP * P) = rowsum(dO * O) only when the
+    # caller passes the forward's own, unmodified panels AND values; otherwise D follows the
+    # given arguments (O recomputed from them), as the reference computes it
+    outputs = probs.outputs if own and v_saved else None
     rowscale = probs.rowscale if own else None
     if outputs is not None and (outputs.shape != q.shape or outputs.device != dev):
         outputs = None

@@ -463,6 +463,42 @@ def test_backward_does_not_materialise_saved_panels(rsa):
     assert fwd.probs[1].dtype == torch.float32 and list.__getitem__(fwd.probs, 1) is not None
 
 
+@pytest.mark.parametrize("as_torch", [False, True])
+def test_backward_follows_given_values_and_panels(rsa, as_torch):
+    """The backward uses the values and panels it is GIVEN (ringseq/ring_attention.py:150-209):
+    D = rowsum(dP * P) with dP = dO V_given^T.  The forward's saved O is reused only for
+    the forward's own values and unmodified panels; a different V, or a replaced panel
+    (probs[d] = X), must change the gradients exactly as the oracle's do."""
+    pkg, ra = rsa
+    b, z, seq, a, n = 1, 2, 256, 64, 2
+    q, k, v, g = _inputs(b, z, seq, a, seed=41)
+    v2 = orc.bf16_round(orc.make_rng(42).standard_normal(v.shape))
+    q2 = orc.bf16_round(orc.make_rng(43).standard_normal(q.shape))
+    cfg = _cfg(pkg, b, z, seq, a, n)
+    dev = torch.device("cuda", 0)
+    conv = (lambda x: torch.from_numpy(x).to(dev, torch.bfloat16)) if as_torch else (lambda x: x)  # noqa: E731
+    ch = lambda x: [conv(c) for c in orc.chunks_of(x, n)]  # noqa: E731
+    qc, kc, vc, gc = ch(q), ch(k), ch(v), ch(g)
+    fwd = ra.ring_attention_forward(qc, kc, vc, cfg)
+    # (1) other values than the forward's
+    bwd = ra.ring_attention_backward(qc, kc, ch(v2), fwd.probs, gc, cfg)
+    _, probs, _ = orc.ring_forward(orc.chunks_of(q, n), orc.chunks_of(k, n), orc.chunks_of(v, n), exact=False)
+    want = orc.ring_backward(orc.chunks_of(q, n), orc.chunks_of(k, n), orc.chunks_of(v2, n), probs,
+                             orc.chunks_of(g, n), exact=False)
+    for name, got, ref in zip(("dq", "dk", "dv"), (bwd.grad_q, bwd.grad_k, bwd.grad_v), want[:3]):
+        _gate(name, _np(pkg.gather_sequence(got)), np.concatenate(ref, -2))
+    # (2) a replaced panel: rank 0's probabilities of other queries
+    other = ra.ring_attention_forward(ch(q2), kc, vc, cfg)
+    probs_mixed = fwd.probs
+    probs_mixed[0] = other.probs[0]
+    bwd = ra.ring_attention_backward(qc, kc, vc, probs_mixed, gc, cfg)
+    given = [orc.bf16_round(_np(other.probs[0])), orc.bf16_round(_np(fwd.probs[1]))]
+    want = orc.ring_backward(orc.chunks_of(q, n), orc.chunks_of(k, n), orc.chunks_of(v, n), given,
+                             orc.chunks_of(g, n), exact=False)
+    for name, got, ref in zip(("dq", "dk", "dv"), (bwd.grad_q, bwd.grad_k, bwd.grad_v), want[:3]):
+        _gate(name, _np(pkg.gather_sequence(got)), np.concatenate(ref, -2))
+
+
 @pytest.mark.parametrize("key", [50, 300])
 def test_negative_overflow_score_raises_numeric_error(rsa, key):
     """A score that overflows the fp32 range to -inf while every other score of its row
