@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define RSA_ABI_VERSION 2
+#define RSA_ABI_VERSION 3
 
 enum rsa_status {
   RSA_OK = 0,
@@ -63,6 +63,10 @@ typedef struct rsa_geom {
   int32_t org_lo;    /* first origin chunk resident in this launch */
   int32_t n_org;     /* number of consecutive origin chunks resident */
   float scale;       /* 1/sqrt(A) */
+  int32_t key_chunk; /* keys per origin chunk; 0 = chunk (RSA).  Only the stream-mode entry
+                        points (rsa_fwd_factored_ex without a panel, rsa_bwd_*_stream) accept
+                        key_chunk != chunk -- the Linformer's projected keys; seq_len is then
+                        the total key count, a multiple of key_chunk. */
 } rsa_geom;
 
 int rsa_abi_version(void);
@@ -227,6 +231,66 @@ int rsa_bwd_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_vie
                   const float* dvec, rsa_view dq_acc, int accumulate_dq, rsa_view dq_out, rsa_view dk, rsa_view dv,
                   int dkv_dtype, int accumulate_dkv, void* stream);
 int rsa_bwd_fused_supported(const rsa_geom* g);
+
+/* ------------------------------------------------ stream mode and ring hops */
+
+/*
+ * Options of rsa_fwd_factored_ex, the generalised factored forward.  All-zero options give
+ * rsa_fwd_factored's behaviour except that the panel is NOT written (stream mode):
+ *
+ *   panel          bf16 P~ panel to write (ptr NULL: stream mode -- only O and the row
+ *                  statistics survive, so memory per rank is O(c) instead of O(c * L)).
+ *   rowmax         out (may be NULL): m = the reference point per row, in the scaled base-2
+ *                  units of the panel (P~ = 2^(s * scale * log2(e) - m)); with rowscale this
+ *                  is everything the stream-mode backward needs to recompute P~ bit for bit.
+ *   rowmax_in      in (may be NULL): use these reference points instead of the first key
+ *                  tile's max (stride rowmax_in_stride floats per row: 1, or 2 to read the m
+ *                  of rsa_fwd_stats' float2 (m, l) slots).  rowmax_exact != 0 declares them
+ *                  the true row maxima (no headroom check: the two-pass fallback).
+ *   o_acc, l_acc   ring hops: fp32 running O~ = sum_k P~ V and l = sum_k P~ over the origins
+ *                  of earlier launches ([rank][b][z][row][a] and [rank][b][z][row]); acc_in
+ *                  adds them in, final_hop = 0 writes them back instead of finishing.
+ *   final_hop      != 0 (or o_acc NULL): O = O~ / l to o_out (bf16), rowscale = 1 / l.
+ *
+ * One K/V-ring hop of ringseq/ring_attention.py:89-103 in ONE pass: hop 0 computes the
+ * reference point, later hops reuse it (rowmax_in), so neither the two-pass statistics nor
+ * the recomputation of S of rsa_fwd_stats + rsa_fwd_probs_pv is needed.
+ */
+typedef struct rsa_fwd_ext {
+  rsa_view panel;
+  float* rowmax;
+  const float* rowmax_in;
+  int32_t rowmax_in_stride;
+  int32_t rowmax_exact;
+  rsa_view o_acc;
+  float* l_acc;
+  int32_t acc_in;
+  int32_t final_hop;
+} rsa_fwd_ext;
+
+int rsa_fwd_factored_ex(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, const rsa_fwd_ext* ext,
+                        rsa_view o_out, float* rowscale, int* flag, void* stream);
+
+/*
+ * Stream-mode backward (ringseq/ring_attention.py:168-209 without a saved panel): the
+ * probabilities are recomputed tile by tile as P~ = 2^(q.k * scale * log2(e) - rowmax) --
+ * the same tensor-core products and the same exp2 as the forward, so P~ equals the panel
+ * rsa_fwd_factored would have stored, bit for bit -- and used at once, never written.
+ * dout_scaled = dO * r and dvec = D * r come from rsa_rowdot_scale with the forward's
+ * rowscale r, exactly as for a factored panel.
+ *   rsa_bwd_kv_stream: per key tile, walking every query tile of the launch's ranks:
+ *     dV_j += P~^T (dO r), dK_j += dS^T Q with dS = P~ (dO r V^T - D r) (scale applied);
+ *     dk / dv bf16, or fp32 (accumulate != 0 adds) per dkv_dtype.
+ *   rsa_bwd_q_stream: per query tile, walking every key tile of the resident origins:
+ *     dQ = sum_j dS_j K_j; fp32 dq_acc (accumulate != 0 adds) and/or bf16 dq_out.
+ * key_chunk may differ from chunk (Linformer keys).
+ */
+int rsa_bwd_kv_stream(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view dout_scaled,
+                      const float* rowmax, const float* dvec, rsa_view dk, rsa_view dv, int dkv_dtype,
+                      int accumulate, void* stream);
+int rsa_bwd_q_stream(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view dout_scaled,
+                     const float* rowmax, const float* dvec, rsa_view dq_acc, int accumulate, rsa_view dq_out,
+                     void* stream);
 
 /* --------------------------------------------- peer-resident origins (NVLink) */
 

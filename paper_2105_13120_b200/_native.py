@@ -18,10 +18,10 @@ from pathlib import Path
 
 from .errors import NativeError, NativeUnavailable, NumericError, ShapeError
 
-__all__ = ["lib", "check", "RsaView", "RsaGeom", "LIB_PATH", "ABI_VERSION", "F32", "BF16", "EXPORTS"]
+__all__ = ["lib", "check", "RsaView", "RsaGeom", "RsaFwdExt", "LIB_PATH", "ABI_VERSION", "F32", "BF16", "EXPORTS"]
 
 LIB_PATH = Path(os.environ.get("RSA_B200_LIB", Path(__file__).resolve().parent / "librsa_b200.so"))
-ABI_VERSION = 2
+ABI_VERSION = 3
 F32, BF16 = 0, 1
 
 RSA_OK, RSA_ERR_INVALID, RSA_ERR_UNSUPPORTED, RSA_ERR_CUDA, RSA_ERR_NUMERIC = 0, 1, 2, 3, 4
@@ -52,6 +52,23 @@ class RsaGeom(ctypes.Structure):
         ("org_lo", c_int32),
         ("n_org", c_int32),
         ("scale", c_float),
+        ("key_chunk", c_int32),
+    ]
+
+
+class RsaFwdExt(ctypes.Structure):
+    """struct rsa_fwd_ext (options of rsa_fwd_factored_ex)."""
+
+    _fields_ = [
+        ("panel", RsaView),
+        ("rowmax", c_void_p),
+        ("rowmax_in", c_void_p),
+        ("rowmax_in_stride", c_int32),
+        ("rowmax_exact", c_int32),
+        ("o_acc", RsaView),
+        ("l_acc", c_void_p),
+        ("acc_in", c_int32),
+        ("final_hop", c_int32),
     ]
 
 
@@ -105,6 +122,9 @@ EXPORTS = {
     "rsa_fused_supported": (c_int, [_GEOM]),
     "rsa_bwd_fused": (c_int, [_GEOM, _V, _V, _V, _V, _V, c_void_p, _V, c_int, _V, _V, _V, c_int, c_int, c_void_p]),
     "rsa_bwd_fused_supported": (c_int, [_GEOM]),
+    "rsa_fwd_factored_ex": (c_int, [_GEOM, _V, _V, _V, _P(RsaFwdExt), _V, c_void_p, c_void_p, c_void_p]),
+    "rsa_bwd_kv_stream": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, c_void_p, _V, _V, c_int, c_int, c_void_p]),
+    "rsa_bwd_q_stream": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, c_void_p, _V, c_int, _V, c_void_p]),
 }
 
 _lib = None

@@ -1,0 +1,565 @@
+// Stream-mode RSA backward for sm_100a (head size A = 64): dQ, dK and dV with no saved
+// probability panel.  Replaces the V-ring / K-ring backward of
+// ringseq/ring_attention.py:168-209 when the forward kept only O and two numbers per row
+// (rsa_fwd_factored_ex without a panel): the reference point m (scaled base 2) and the
+// row scale r = 1 / sum_k P~.  Each tile of the factored panel is recomputed on chip,
+//   S  = Q K_j^T                          (tensor core, TMEM; the forward's exact products)
+//   P~ = 2^(S * scale * log2(e) - m)      (exp2_pack32: the forward's exact rounding)
+// so P~ equals, bit for bit, the panel rsa_fwd_factored would have written, and the
+// backward products run on it exactly as on a factored panel (rsa_rowdot_scale supplies
+// dO' = dO * r and D' = D * r):
+//   dP' = dO' V_j^T,  dS = P~ (dP' - D')  (= P (dP - D)),
+//   dV_j += P~^T dO',  dK_j += dS^T Q,  dQ += dS K_j        (the 1/sqrt(A) at the end).
+// Memory per rank is O(c) instead of O(c * L): the "max trainable length grows linearly
+// with N" mode (hard part 5).  Keys per origin (key_chunk) may differ
+// from query rows per rank, which serves the Linformer's projected keys too.
+//
+// Two persistent, warp-specialised kernels (warp 0 TMA producer, warp 1 tcgen05.mma issuer,
+// warps 2..9 epilogue: warp w owns TMEM lanes 32*(w%4).. and column half (w-2)/4), each
+// accumulating in TMEM in a fixed order (deterministic, no atomics):
+//   bwd_kv_stream_kernel  item = (origin, b, z, key tile); walks every query tile:
+//                         S, dP' -> P~ to smem -> dV += P~^T dO' -> dS in place -> dK += dS^T Q
+//   bwd_q_stream_kernel   item = (rank, b, z, query tile); walks every key tile:
+//                         S, dP' -> dS to smem -> dQ += dS K
+#include "fused_common.cuh"
+
+namespace rsa {
+namespace {
+
+struct StreamArgs {
+  CUtensorMap tq, tk, tv, tdo;  // q / dO': query rows (chunk); k / v: key rows (key_chunk)
+  Geo g;
+  int ck;    // keys per origin chunk
+  float sl;  // scale * log2(e)
+  const float* rowmax;  // m per query row [rank][b][z][c]
+  const float* dvec;    // D * r per query row
+  OutView dk, dv, dq_acc, dq_out;
+  int dkv_bf16, accumulate;
+};
+
+__device__ __forceinline__ int64_t row_index(const Geo& g, int d, int b, int z, int row) {
+  return (int64_t(d * g.B + b) * g.Z + z) * g.c + row;
+}
+
+// ============================================================ dK / dV
+
+constexpr int KS_ST = 3;                     // (Q, dO') stages
+constexpr int KS_P = 2;                      // P~ / dS slots
+constexpr uint32_t KS_OFF_KV = 0;            // [buffer][K | V]
+constexpr uint32_t KS_OFF_ST = 4 * TILE;     // [stage][Q | dO']
+constexpr uint32_t KS_OFF_P = KS_OFF_ST + KS_ST * 2 * TILE;
+constexpr uint32_t KS_OFF_BAR = KS_OFF_P + KS_P * PTILE;
+constexpr uint32_t KS_SMEM = KS_OFF_BAR + 512 + 1024;
+static_assert(KS_SMEM <= 232448, "bwd_kv_stream smem over the sm_100 per-CTA limit");
+// TMEM: S [0,128), dP' x 2 [128,384), dV [384,448), dK [448,512)
+constexpr uint32_t KS_COL_S = 0, KS_COL_DP = 128, KS_COL_DV = 384, KS_COL_DK = 448;
+
+__global__ void __launch_bounds__(NTHREADS, 1) bwd_kv_stream_kernel(const __grid_constant__ StreamArgs p) {
+  uint8_t* smem = smem_base();
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + KS_OFF_BAR);
+  uint64_t *kv_full = bar, *kv_empty = bar + 2;
+  uint64_t *ld_full = bar + 4, *ld_empty = ld_full + KS_ST;
+  uint64_t *s_full = ld_empty + KS_ST, *s_empty = s_full + 1;
+  uint64_t *dp_full = s_empty + 1, *dp_empty = dp_full + 2;
+  uint64_t *p_full = dp_empty + 2, *p_read = p_full + KS_P, *ds_full = p_read + KS_P, *ps_empty = ds_full + KS_P;
+  uint64_t *acc_full = ps_empty + KS_P, *acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+  const Geo& g = p.g;
+  const int ntk = (p.ck + TK - 1) / TK, nrt = (g.c + TR - 1) / TR;
+  const int T = g.n_rank * nrt;  // query tiles walked per key tile
+  const int BZ = g.B * g.Z;
+  const int items = g.n_org * BZ * ntk;
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kv_full[s], 1), mbar_init(&kv_empty[s], 1);
+      mbar_init(&dp_full[s], 1), mbar_init(&dp_empty[s], EPI_WARPS);
+    }
+    for (int s = 0; s < KS_ST; ++s) mbar_init(&ld_full[s], 1), mbar_init(&ld_empty[s], 1);
+    for (int s = 0; s < KS_P; ++s) {
+      mbar_init(&p_full[s], EPI_WARPS), mbar_init(&p_read[s], 1);
+      mbar_init(&ds_full[s], EPI_WARPS), mbar_init(&ps_empty[s], 1);
+    }
+    mbar_init(s_full, 1), mbar_init(s_empty, EPI_WARPS);
+    mbar_init(acc_full, 1), mbar_init(acc_empty, EPI_WARPS);
+    fence_barrier_init();
+    tma_prefetch(&p.tq), tma_prefetch(&p.tk), tma_prefetch(&p.tv), tma_prefetch(&p.tdo);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      Pos lq;
+      uint32_t it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        const int kt = item % ntk, bz = (item / ntk) % BZ, jo = item / (ntk * BZ);
+        const int b = bz / g.Z, z = bz % g.Z;
+        const uint32_t kb = it & 1;
+        mbar_wait(&kv_empty[kb], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[kb], 2 * TILE);
+        uint8_t* kv = smem + KS_OFF_KV + kb * 2 * TILE;
+        tma_load_4d(kv, &p.tk, &kv_full[kb], 0, kt * TK, z, jo * g.B + b);
+        tma_load_4d(kv + TILE, &p.tv, &kv_full[kb], 0, kt * TK, z, jo * g.B + b);
+        for (int t = 0, d = 0, r0 = 0; t < T; ++t, r0 = r0 + TR >= nrt * TR ? (++d, 0) : r0 + TR) {
+          const uint32_t s = lq.slot(KS_ST);
+          mbar_wait(&ld_empty[s], lq.phase(KS_ST) ^ 1);
+          mbar_arrive_expect_tx(&ld_full[s], 2 * TILE);
+          uint8_t* st = smem + KS_OFF_ST + s * 2 * TILE;
+          tma_load_4d(st, &p.tq, &ld_full[s], 0, r0, z, d * g.B + b);
+          tma_load_4d(st + TILE, &p.tdo, &ld_full[s], 0, r0, z, d * g.B + b);
+          ++lq.i;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    const uint32_t idesc_s = idesc_bf16_f32(TR, TK, 0, 0);   // Q (K-major) x K (K-major) -> 128 x 128
+    const uint32_t idesc_kv = idesc_bf16_f32(TK, HD, 1, 1);  // P~^T / dS^T (MN) x dO' / Q (MN) -> 128 x 64
+    Pos lq_s, lq_d, lq_v, lq_k, dpq, pq_v, pq_k;
+    uint32_t it = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      const uint32_t kb = it & 1;
+      const uint32_t ka = smem_u32(smem + KS_OFF_KV + kb * 2 * TILE), va = ka + TILE;
+      mbar_wait(&kv_full[kb], (it >> 1) & 1);
+      mbar_wait(acc_empty, (it & 1) ^ 1);
+      auto issue_s = [&]() {  // S(t) = Q K^T into the single S buffer
+        const uint32_t s = lq_s.slot(KS_ST);
+        mbar_wait(&ld_full[s], lq_s.phase(KS_ST));
+        mbar_wait(s_empty, (lq_s.i & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(smem + KS_OFF_ST + s * 2 * TILE);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+          umma_bf16_ws(tmem + KS_COL_S, smem_desc_sw128(qa + k * 32, 0, 1024), smem_desc_sw128(ka + k * 32, 0, 1024),
+                       idesc_s, k > 0);
+        umma_commit_ws(s_full);
+        ++lq_s.i;
+      };
+      auto issue_dp = [&]() {  // dP'(t) = dO' V^T
+        const uint32_t s = lq_d.slot(KS_ST), db = dpq.slot(2);
+        mbar_wait(&ld_full[s], lq_d.phase(KS_ST));
+        mbar_wait(&dp_empty[db], dpq.phase(2) ^ 1);
+        tc_fence_after();
+        const uint32_t doa = smem_u32(smem + KS_OFF_ST + s * 2 * TILE) + TILE;
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+          umma_bf16_ws(tmem + KS_COL_DP + db * TK, smem_desc_sw128(doa + k * 32, 0, 1024),
+                       smem_desc_sw128(va + k * 32, 0, 1024), idesc_s, k > 0);
+        umma_commit_ws(&dp_full[db]);
+        ++lq_d.i, ++dpq.i;
+      };
+      auto issue_dv = [&](int t) {  // dV += P~^T dO' once the epilogue has written P~(t)
+        const uint32_t s = lq_v.slot(KS_ST), ps = pq_v.slot(KS_P);
+        mbar_wait(&p_full[ps], pq_v.phase(KS_P));
+        tc_fence_after();
+        const uint32_t pa = smem_u32(smem + KS_OFF_P + ps * PTILE);
+        const uint32_t doa = smem_u32(smem + KS_OFF_ST + s * 2 * TILE) + TILE;
+#pragma unroll
+        for (int k = 0; k < TR / 16; ++k)
+          umma_bf16_ws(tmem + KS_COL_DV, smem_desc_sw128(pa + k * 2048, ATOM, 1024),
+                       smem_desc_sw128(doa + k * 2048, ATOM, 1024), idesc_kv, (t | k) != 0);
+        umma_commit_ws(&p_read[ps]);  // P~ consumed: dS may overwrite it
+        ++lq_v.i, ++pq_v.i;
+      };
+      auto issue_dk = [&](int t) {  // dK += dS^T Q once the epilogue has written dS(t)
+        const uint32_t s = lq_k.slot(KS_ST), ps = pq_k.slot(KS_P);
+        mbar_wait(&ds_full[ps], pq_k.phase(KS_P));
+        tc_fence_after();
+        const uint32_t dsa = smem_u32(smem + KS_OFF_P + ps * PTILE);
+        const uint32_t qa = smem_u32(smem + KS_OFF_ST + s * 2 * TILE);
+#pragma unroll
+        for (int k = 0; k < TR / 16; ++k)
+          umma_bf16_ws(tmem + KS_COL_DK, smem_desc_sw128(dsa + k * 2048, ATOM, 1024),
+                       smem_desc_sw128(qa + k * 2048, ATOM, 1024), idesc_kv, (t | k) != 0);
+        umma_commit_ws(&ld_empty[s]);
+        umma_commit_ws(&ps_empty[ps]);
+        ++lq_k.i, ++pq_k.i;
+      };
+      issue_s();
+      issue_dp();
+      for (int t = 0; t < T; ++t) {
+        if (t + 1 < T) issue_s();
+        issue_dv(t);
+        if (t + 1 < T) issue_dp();
+        issue_dk(t);
+      }
+      umma_commit_ws(&kv_empty[kb]);
+      umma_commit_ws(acc_full);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_base = (quad * 32u) << 16;
+    const float sl = p.sl;
+    Pos sq, dpq, pq;
+    uint32_t it = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      const int kt = item % ntk, bz = (item / ntk) % BZ, jo = item / (ntk * BZ);
+      const int b = bz / g.Z, z = bz % g.Z, k0 = kt * TK;
+      const int nvalid = min(TK, p.ck - k0) - half * 64;
+      int d = 0, r0 = 0;
+      float m_next = r < g.c ? __ldg(p.rowmax + row_index(g, 0, b, z, r)) : 0.f;
+      float d_next = r < g.c ? __ldg(p.dvec + row_index(g, 0, b, z, r)) : 0.f;
+      for (int t = 0; t < T; ++t) {
+        const float msl = m_next, dval = d_next;
+        if (r0 + TR >= nrt * TR) r0 = 0, ++d;
+        else r0 += TR;
+        if (t + 1 < T) {  // the next step's row statistics now: their latency hides behind this step
+          const int nrow = r0 + r;
+          m_next = nrow < g.c ? __ldg(p.rowmax + row_index(g, d, b, z, nrow)) : 0.f;
+          d_next = nrow < g.c ? __ldg(p.dvec + row_index(g, d, b, z, nrow)) : 0.f;
+        }
+        // S -> P~ (the forward's values, zero past the last key)
+        uint32_t w[32];
+        mbar_wait(s_full, sq.i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          float v[32];
+          __syncwarp();
+          tmem_ld32(tmem + lane_base + KS_COL_S + half * 64 + cc * 32, v);
+          tmem_ld_wait();
+          exp2_pack32(v, nvalid - cc * 32, sl, msl, w + cc * 16);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_empty);
+        ++sq.i;
+        const uint32_t ps = pq.slot(KS_P);
+        const uint32_t pt = smem_u32(smem + KS_OFF_P + ps * PTILE) + half * ATOM;
+        mbar_wait(&ps_empty[ps], pq.phase(KS_P) ^ 1);  // dK(t-2) has read this slot's dS
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4)
+          st_shared_v4(pt + sw128_offset(r, q4), w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2], w[4 * q4 + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[ps]);
+        // dP' -> dS = P~ (dP' - D'), over P~ once dV has read it
+        const uint32_t db = dpq.slot(2);
+        mbar_wait(&dp_full[db], dpq.phase(2));
+        tc_fence_after();
+        const uint64_t nd = neg_pair(dval);
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          float dp[32];
+          __syncwarp();
+          tmem_ld32(tmem + lane_base + KS_COL_DP + db * TK + half * 64 + cc * 32, dp);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) w[cc * 16 + e] = ds_pair(w[cc * 16 + e], dp[2 * e], dp[2 * e + 1], nd);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dp_empty[db]);
+        ++dpq.i;
+        mbar_wait(&p_read[ps], pq.phase(KS_P));
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4)
+          st_shared_v4(pt + sw128_offset(r, q4), w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2], w[4 * q4 + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ds_full[ps]);
+        ++pq.i;
+      }
+      mbar_wait(acc_full, it & 1);
+      tc_fence_after();
+      float dvv[32], dkv[32];
+      __syncwarp();
+      tmem_ld32(tmem + lane_base + KS_COL_DV + half * 32, dvv);
+      tmem_ld32(tmem + lane_base + KS_COL_DK + half * 32, dkv);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) dkv[e] *= g.scale;
+      const int key = k0 + r;
+      if (key < p.ck) {
+        const OutView none{nullptr, 0, 0, 0, 0};
+        if (p.dkv_bf16) {
+          store_row32(none, p.dv, 0, jo, b, z, key, half * 32, dvv);
+          store_row32(none, p.dk, 0, jo, b, z, key, half * 32, dkv);
+        } else {
+          store_row32(p.dv, none, p.accumulate, jo, b, z, key, half * 32, dvv);
+          store_row32(p.dk, none, p.accumulate, jo, b, z, key, half * 32, dkv);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// ================================================================== dQ
+
+constexpr int QS_ST = 3;                    // (K, V) stages
+constexpr int QS_DS = 2;                    // dS slots
+constexpr uint32_t QS_OFF_QD = 0;           // [buffer][Q | dO']
+constexpr uint32_t QS_OFF_ST = 4 * TILE;    // [stage][K | V]
+constexpr uint32_t QS_OFF_DS = QS_OFF_ST + QS_ST * 2 * TILE;
+constexpr uint32_t QS_OFF_BAR = QS_OFF_DS + QS_DS * PTILE;
+constexpr uint32_t QS_SMEM = QS_OFF_BAR + 512 + 1024;
+static_assert(QS_SMEM <= 232448, "bwd_q_stream smem over the sm_100 per-CTA limit");
+// TMEM: S [0,128), dP' x 2 [128,384), dQ x 2 [384,512)
+constexpr uint32_t QS_COL_S = 0, QS_COL_DP = 128, QS_COL_DQ = 384;
+
+__global__ void __launch_bounds__(NTHREADS, 1) bwd_q_stream_kernel(const __grid_constant__ StreamArgs p) {
+  uint8_t* smem = smem_base();
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + QS_OFF_BAR);
+  uint64_t *qd_full = bar, *qd_empty = bar + 2;
+  uint64_t *ld_full = bar + 4, *ld_empty = ld_full + QS_ST;
+  uint64_t *s_full = ld_empty + QS_ST, *s_empty = s_full + 1;
+  uint64_t *dp_full = s_empty + 1, *dp_empty = dp_full + 2;
+  uint64_t *ds_full = dp_empty + 2, *ds_empty = ds_full + QS_DS;
+  uint64_t *acc_full = ds_empty + QS_DS, *acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const Geo& g = p.g;
+  const int ntk = (p.ck + TK - 1) / TK, nrt = (g.c + TR - 1) / TR;
+  const int T = g.n_org * ntk;  // key tiles walked per query tile
+  const int BZ = g.B * g.Z;
+  const int items = g.n_rank * BZ * nrt;
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&qd_full[s], 1), mbar_init(&qd_empty[s], 1);
+      mbar_init(&dp_full[s], 1), mbar_init(&dp_empty[s], EPI_WARPS);
+      mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], EPI_WARPS);
+    }
+    for (int s = 0; s < QS_ST; ++s) mbar_init(&ld_full[s], 1), mbar_init(&ld_empty[s], 1);
+    for (int s = 0; s < QS_DS; ++s) mbar_init(&ds_full[s], EPI_WARPS), mbar_init(&ds_empty[s], 1);
+    mbar_init(s_full, 1), mbar_init(s_empty, EPI_WARPS);
+    fence_barrier_init();
+    tma_prefetch(&p.tq), tma_prefetch(&p.tk), tma_prefetch(&p.tv), tma_prefetch(&p.tdo);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      Pos lq;
+      uint32_t it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        const int rt = item % nrt, bz = (item / nrt) % BZ, d = item / (nrt * BZ);
+        const int b = bz / g.Z, z = bz % g.Z;
+        const uint32_t qb = it & 1;
+        mbar_wait(&qd_empty[qb], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qd_full[qb], 2 * TILE);
+        uint8_t* qd = smem + QS_OFF_QD + qb * 2 * TILE;
+        tma_load_4d(qd, &p.tq, &qd_full[qb], 0, rt * TR, z, d * g.B + b);
+        tma_load_4d(qd + TILE, &p.tdo, &qd_full[qb], 0, rt * TR, z, d * g.B + b);
+        for (int t = 0, jo = 0, k0 = 0; t < T; ++t, k0 = k0 + TK >= ntk * TK ? (++jo, 0) : k0 + TK) {
+          const uint32_t s = lq.slot(QS_ST);
+          mbar_wait(&ld_empty[s], lq.phase(QS_ST) ^ 1);
+          mbar_arrive_expect_tx(&ld_full[s], 2 * TILE);
+          uint8_t* st = smem + QS_OFF_ST + s * 2 * TILE;
+          tma_load_4d(st, &p.tk, &ld_full[s], 0, k0, z, jo * g.B + b);
+          tma_load_4d(st + TILE, &p.tv, &ld_full[s], 0, k0, z, jo * g.B + b);
+          ++lq.i;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc_s = idesc_bf16_f32(TR, TK, 0, 0);   // Q x K^T, dO' x V^T (K-major both)
+    const uint32_t idesc_dq = idesc_bf16_f32(TR, HD, 0, 1);  // dS (K-major over keys) x K (MN-major)
+    Pos lq_s, lq_d, lq_q, dpq, dsq;
+    uint32_t it = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      const uint32_t qb = it & 1;
+      const uint32_t qa = smem_u32(smem + QS_OFF_QD + qb * 2 * TILE), doa = qa + TILE;
+      mbar_wait(&qd_full[qb], (it >> 1) & 1);
+      mbar_wait(&acc_empty[qb], ((it >> 1) & 1) ^ 1);
+      auto issue_s = [&]() {
+        const uint32_t s = lq_s.slot(QS_ST);
+        mbar_wait(&ld_full[s], lq_s.phase(QS_ST));
+        mbar_wait(s_empty, (lq_s.i & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t ka = smem_u32(smem + QS_OFF_ST + s * 2 * TILE);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+          umma_bf16_ws(tmem + QS_COL_S, smem_desc_sw128(qa + k * 32, 0, 1024), smem_desc_sw128(ka + k * 32, 0, 1024),
+                       idesc_s, k > 0);
+        umma_commit_ws(s_full);
+        ++lq_s.i;
+      };
+      auto issue_dp = [&]() {
+        const uint32_t s = lq_d.slot(QS_ST), db = dpq.slot(2);
+        mbar_wait(&ld_full[s], lq_d.phase(QS_ST));
+        mbar_wait(&dp_empty[db], dpq.phase(2) ^ 1);
+        tc_fence_after();
+        const uint32_t va = smem_u32(smem + QS_OFF_ST + s * 2 * TILE) + TILE;
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+          umma_bf16_ws(tmem + QS_COL_DP + db * TK, smem_desc_sw128(doa + k * 32, 0, 1024),
+                       smem_desc_sw128(va + k * 32, 0, 1024), idesc_s, k > 0);
+        umma_commit_ws(&dp_full[db]);
+        ++lq_d.i, ++dpq.i;
+      };
+      auto issue_dq = [&](int t) {
+        const uint32_t s = lq_q.slot(QS_ST), ds = dsq.slot(QS_DS);
+        mbar_wait(&ds_full[ds], dsq.phase(QS_DS));
+        tc_fence_after();
+        const uint32_t dsa = smem_u32(smem + QS_OFF_DS + ds * PTILE);
+        const uint32_t ka = smem_u32(smem + QS_OFF_ST + s * 2 * TILE);
+#pragma unroll
+        for (int k = 0; k < TK / 16; ++k)
+          umma_bf16_ws(tmem + QS_COL_DQ + qb * HD, smem_desc_sw128(dsa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
+                       smem_desc_sw128(ka + k * 2048, ATOM, 1024), idesc_dq, (t | k) != 0);
+        umma_commit_ws(&ld_empty[s]);
+        umma_commit_ws(&ds_empty[ds]);
+        ++lq_q.i, ++dsq.i;
+      };
+      issue_s();
+      issue_dp();
+      for (int t = 0; t < T; ++t) {
+        if (t + 1 < T) issue_s(), issue_dp();
+        issue_dq(t);
+      }
+      umma_commit_ws(&qd_empty[qb]);
+      umma_commit_ws(&acc_full[qb]);
+    }
+  } else {
+    const uint32_t quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_base = (quad * 32u) << 16;
+    const float sl = p.sl;
+    Pos sq, dpq, dsq;
+    uint32_t it = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      const int rt = item % nrt, bz = (item / nrt) % BZ, d = item / (nrt * BZ);
+      const int b = bz / g.Z, z = bz % g.Z, row = rt * TR + r;
+      const float msl = row < g.c ? __ldg(p.rowmax + row_index(g, d, b, z, row)) : 0.f;
+      const float dval = row < g.c ? __ldg(p.dvec + row_index(g, d, b, z, row)) : 0.f;
+      const uint64_t nd = neg_pair(dval);
+      for (int t = 0, k0 = 0; t < T; ++t, k0 = k0 + TK >= ntk * TK ? 0 : k0 + TK) {
+        const int nvalid = min(TK, p.ck - k0) - half * 64;
+        uint32_t w[32];
+        mbar_wait(s_full, sq.i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          float v[32];
+          __syncwarp();
+          tmem_ld32(tmem + lane_base + QS_COL_S + half * 64 + cc * 32, v);
+          tmem_ld_wait();
+          exp2_pack32(v, nvalid - cc * 32, sl, msl, w + cc * 16);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_empty);
+        ++sq.i;
+        const uint32_t db = dpq.slot(2);
+        mbar_wait(&dp_full[db], dpq.phase(2));
+        tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          float dp[32];
+          __syncwarp();
+          tmem_ld32(tmem + lane_base + QS_COL_DP + db * TK + half * 64 + cc * 32, dp);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) w[cc * 16 + e] = ds_pair(w[cc * 16 + e], dp[2 * e], dp[2 * e + 1], nd);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dp_empty[db]);
+        ++dpq.i;
+        const uint32_t ds = dsq.slot(QS_DS);
+        const uint32_t dst = smem_u32(smem + QS_OFF_DS + ds * PTILE) + half * ATOM;
+        mbar_wait(&ds_empty[ds], dsq.phase(QS_DS) ^ 1);
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4)
+          st_shared_v4(dst + sw128_offset(r, q4), w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2], w[4 * q4 + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ds_full[ds]);
+        ++dsq.i;
+      }
+      const uint32_t ab = it & 1;
+      mbar_wait(&acc_full[ab], (it >> 1) & 1);
+      tc_fence_after();
+      float o[32];
+      __syncwarp();
+      tmem_ld32(tmem + lane_base + QS_COL_DQ + ab * HD + half * 32, o);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[ab]);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) o[e] *= g.scale;
+      if (row < g.c) store_row32(p.dq_acc, p.dq_out, p.accumulate, d, b, z, row, half * 32, o);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+bool stream_args(StreamArgs* a, const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view dout,
+                 const float* rowmax, const float* dvec) {
+  if (!head_map(&a->tq, q, g, g->n_rank) || !head_map(&a->tdo, dout, g, g->n_rank) ||
+      !head_map(&a->tk, k, g, g->n_org, key_chunk(g)) || !head_map(&a->tv, v, g, g->n_org, key_chunk(g)))
+    return false;
+  a->g = to_geo(g);
+  a->ck = key_chunk(g);
+  a->sl = g->scale * LOG2E;
+  a->rowmax = rowmax;
+  a->dvec = dvec;
+  return true;
+}
+
+}  // namespace
+}  // namespace rsa
+
+extern "C" {
+
+int rsa_bwd_kv_stream(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view dout_scaled,
+                      const float* rowmax, const float* dvec, rsa_view dk, rsa_view dv, int dkv_dtype,
+                      int accumulate, void* stream) {
+  using namespace rsa;
+  if (!geom_ok_keys(g) || !rowmax || !dvec) return fail(RSA_ERR_INVALID, "rsa_bwd_kv_stream: unsupported geometry");
+  const int esz = dkv_dtype == RSA_BF16 ? 2 : 4;
+  if (!dk.ptr || !dv.ptr || !out_ok(dk, esz) || !out_ok(dv, esz))
+    return fail(RSA_ERR_UNSUPPORTED, "rsa_bwd_kv_stream: output views missing or misaligned");
+  StreamArgs a{};
+  if (!stream_args(&a, g, q, k, v, dout_scaled, rowmax, dvec)) return RSA_ERR_UNSUPPORTED;
+  a.dk = to_out(dk);
+  a.dv = to_out(dv);
+  a.dkv_bf16 = dkv_dtype == RSA_BF16;
+  a.accumulate = accumulate;
+  const int items = g->n_org * g->batch * g->heads * ((key_chunk(g) + TK - 1) / TK);
+  return launch(bwd_kv_stream_kernel, items, KS_SMEM, a, stream, "bwd_kv_stream_kernel");
+}
+
+int rsa_bwd_q_stream(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view dout_scaled,
+                     const float* rowmax, const float* dvec, rsa_view dq_acc, int accumulate, rsa_view dq_out,
+                     void* stream) {
+  using namespace rsa;
+  if (!geom_ok_keys(g) || !rowmax || !dvec) return fail(RSA_ERR_INVALID, "rsa_bwd_q_stream: unsupported geometry");
+  if ((!dq_acc.ptr && !dq_out.ptr) || !out_ok(dq_acc, 4) || !out_ok(dq_out, 2))
+    return fail(RSA_ERR_UNSUPPORTED, "rsa_bwd_q_stream: output views missing or misaligned");
+  StreamArgs a{};
+  if (!stream_args(&a, g, q, k, v, dout_scaled, rowmax, dvec)) return RSA_ERR_UNSUPPORTED;
+  a.dq_acc = to_out(dq_acc);
+  a.dq_out = to_out(dq_out);
+  a.accumulate = accumulate;
+  const int items = g->n_rank * g->batch * g->heads * ((g->chunk + TR - 1) / TR);
+  return launch(bwd_q_stream_kernel, items, QS_SMEM, a, stream, "bwd_q_stream_kernel");
+}
+
+}  // extern "C"

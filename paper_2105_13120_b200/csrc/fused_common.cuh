@@ -94,6 +94,61 @@ __device__ __forceinline__ uint64_t neg_pair(float d) {
   return nd;
 }
 
+// max |v| over the first `nvalid` of 32 values (NaN-propagating): one 3-input
+// FMNMX per two scores.  Finite iff every score is finite.
+__device__ __forceinline__ void absmax32(const float* v, int nvalid, float& mx_out) {
+  if (nvalid >= 32) {
+    float mx[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) mx[e] = fabsf(v[e]);
+#pragma unroll
+    for (int e = 4; e < 32; ++e) mx[e & 3] = max_nan(mx[e & 3], fabsf(v[e]));
+    mx_out = max_nan(mx_out, max_nan(max_nan(mx[0], mx[1]), max_nan(mx[2], mx[3])));
+  } else {
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if (e < nvalid) mx_out = max_nan(mx_out, fabsf(v[e]));
+  }
+}
+
+// Max and min of the first `nvalid` of 32 values (NaN-propagating).
+__device__ __forceinline__ void minmax32(const float* v, int nvalid, float& mx_out, float& mi_out) {
+  if (nvalid >= 32) {
+    float mx[4], mi[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) mx[e] = mi[e] = v[e];
+#pragma unroll
+    for (int e = 4; e < 32; ++e) mx[e & 3] = max_nan(mx[e & 3], v[e]), mi[e & 3] = min_nan(mi[e & 3], v[e]);
+    mx_out = max_nan(mx_out, max_nan(max_nan(mx[0], mx[1]), max_nan(mx[2], mx[3])));
+    mi_out = min_nan(mi_out, min_nan(min_nan(mi[0], mi[1]), min_nan(mi[2], mi[3])));
+  } else {
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if (e < nvalid) mx_out = max_nan(mx_out, v[e]), mi_out = min_nan(mi_out, v[e]);
+  }
+}
+
+// The factored panel's values: 32 scores of one row (32 consecutive keys starting at a
+// multiple of 32) -> 16 packed bf16 pairs of P~ = 2^(v*sl - msl), zero past nvalid.  One
+// exp2 in four runs on the FMA pipe (exp2_poly<3>), the rest on MUFU.  The forward that
+// writes the panel (rsa_fwd_factored) and the stream-mode backward that recomputes it
+// (bwd_stream.cu) both call this, on bitwise-identical tensor-core scores, so the
+// recomputed P~ equals the stored panel bit for bit.
+__device__ __forceinline__ void exp2_pack32(const float* v, int nvalid, float sl, float msl, uint32_t* w) {
+  if (nvalid >= 32) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const float x0 = fmaf(v[2 * e], sl, -msl), x1 = fmaf(v[2 * e + 1], sl, -msl);
+      w[e] = pack_bf16(fast_exp2(x0), (e & 1) ? exp2_poly<3>(x1) : fast_exp2(x1));
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      w[e] = pack_bf16(2 * e < nvalid ? fast_exp2(fmaf(v[2 * e], sl, -msl)) : 0.f,
+                       2 * e + 1 < nvalid ? fast_exp2(fmaf(v[2 * e + 1], sl, -msl)) : 0.f);
+  }
+}
+
 struct OutView {  // strided output [rank][b][z][row][a]
   void* ptr;
   int64_t s_rank, s_b, s_z, s_row;
@@ -154,25 +209,35 @@ __device__ __forceinline__ uint8_t* smem_base() {
 
 // ------------------------------------------------------------ host side
 
-inline bool geom_ok(const rsa_geom* g) {
-  return g && g->n_rank >= 1 && g->batch >= 1 && g->heads >= 1 && g->chunk >= 1 && g->head_dim == HD &&
-         g->n_org >= 1 && g->org_lo >= 0 && g->seq_len % g->chunk == 0 && g->chunk % 8 == 0 &&
-         g->org_lo + g->n_org <= g->seq_len / g->chunk;
+inline int key_chunk(const rsa_geom* g) { return g->key_chunk > 0 ? g->key_chunk : g->chunk; }
+
+// Geometry of a stream-capable kernel: any key chunk (a multiple of 8) per origin.
+inline bool geom_ok_keys(const rsa_geom* g) {
+  if (!g || g->key_chunk < 0) return false;
+  const int ck = key_chunk(g);
+  return g->n_rank >= 1 && g->batch >= 1 && g->heads >= 1 && g->chunk >= 1 && g->head_dim == HD &&
+         g->n_org >= 1 && g->org_lo >= 0 && ck % 8 == 0 && g->seq_len % ck == 0 && g->chunk % 8 == 0 &&
+         g->org_lo + g->n_org <= g->seq_len / ck;
 }
+
+// Geometry of the panel kernels: keys per origin == query rows per rank (RSA chunks).
+inline bool geom_ok(const rsa_geom* g) { return geom_ok_keys(g) && key_chunk(g) == g->chunk; }
 
 inline Geo to_geo(const rsa_geom* g) {
   return Geo{g->n_rank, g->batch, g->heads, g->chunk, g->seq_len, g->org_lo, g->n_org, g->scale};
 }
 
-// [rank][b][z][row][a] with a = 64 contiguous; `nrank` ranks merged into b.
-inline bool head_map(CUtensorMap* m, const rsa_view& v, const rsa_geom* g, int nrank) {
+// [rank][b][z][row][a] with a = 64 contiguous; `nrank` ranks merged into b; `rows` rows per
+// (rank, b, z) (default: the query chunk; key_chunk(g) for key / value maps).
+inline bool head_map(CUtensorMap* m, const rsa_view& v, const rsa_geom* g, int nrank, int rows = 0) {
   if (!v.ptr || !aligned16(v.ptr)) return fail(RSA_ERR_UNSUPPORTED, "fused: tensor not 16-byte aligned"), false;
   if (nrank > 1 && g->batch > 1 && v.s_rank != int64_t(g->batch) * v.s_b)
     return fail(RSA_ERR_UNSUPPORTED, "fused: rank stride must equal B * batch stride"), false;
   const int64_t sb = (g->batch == 1 && nrank > 1) ? v.s_rank : v.s_b;
   if (!stride_ok(v.s_row * 2) || !stride_ok(v.s_z * 2) || !stride_ok(sb * 2))
     return fail(RSA_ERR_UNSUPPORTED, "fused: strides must be multiples of 8 elements"), false;
-  uint64_t dims[4] = {uint64_t(HD), uint64_t(g->chunk), uint64_t(g->heads), uint64_t(g->batch) * nrank};
+  uint64_t dims[4] = {uint64_t(HD), uint64_t(rows > 0 ? rows : g->chunk), uint64_t(g->heads),
+                      uint64_t(g->batch) * nrank};
   uint64_t str[3] = {uint64_t(v.s_row) * 2, uint64_t(v.s_z) * 2, uint64_t(sb) * 2};
   uint32_t box[4] = {64, TR, 1, 1};
   return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, v.ptr, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);

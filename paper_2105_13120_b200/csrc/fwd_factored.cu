@@ -50,6 +50,15 @@ struct FfArgs {
   long long* trace;  // RSA_FF_TRACE: per-warp (event, clock) log of CTA 0 (timeline experiments)
   int peer;          // K / V of origin j from pm.k[j] / pm.v[j] (rsa_fwd_factored_peer)
   PeerMaps pm;
+  // rsa_fwd_factored_ex options (all zero: rsa_fwd_factored with the panel written)
+  int no_panel;             // stream mode: P~ stays on chip
+  float* rowmax;            // out: the reference point m (scaled base 2) per row
+  const float* rowmax_in;   // in: reference points (stride rm_stride floats)
+  int rm_stride, rm_exact;  // rm_exact: true row maxima, no headroom check
+  OutView o_acc;            // ring hops: fp32 running O~ (ptr NULL: single launch)
+  float* l_acc;             //            fp32 running l
+  int acc_in, final_hop;
+  int ck;                   // keys per origin chunk (key_chunk; == c for RSA)
 };
 
 constexpr int FF_GROUPS = 2;
@@ -58,9 +67,6 @@ constexpr int FF_PV_WARP = 2 + FF_EPI_WARPS;            // 18: issues the P~ V p
 constexpr int FF_THREADS = 32 * (FF_PV_WARP + 1);       // 608
 #ifndef FF_ONES
 #define FF_ONES 1  // row sums from the tensor core (ones block next to V) instead of FADDs
-#endif
-#ifndef FF_EXP
-#define FF_EXP 0   // 0: one exp2 in four on the FMA pipe, 1: all MUFU, 2: ex2.approx.f16x2 pairs
 #endif
 #ifndef FF_ABSMAX
 #define FF_ABSMAX 1  // tiles after the first: max|s| only (finite check + headroom bound)
@@ -107,72 +113,10 @@ __device__ __forceinline__ Unit unit_of(int u, int units_per_head, int nq) {
   return r;
 }
 
-// max |v| over the first `nvalid` of 32 values (NaN-propagating): one 3-input
-// FMNMX per two scores.  Finite iff every score is finite.
-__device__ __forceinline__ void absmax32(const float* v, int nvalid, float& mx_out) {
-  if (nvalid >= 32) {
-    float mx[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) mx[e] = fabsf(v[e]);
-#pragma unroll
-    for (int e = 4; e < 32; ++e) mx[e & 3] = max_nan(mx[e & 3], fabsf(v[e]));
-    mx_out = max_nan(mx_out, max_nan(max_nan(mx[0], mx[1]), max_nan(mx[2], mx[3])));
-  } else {
-#pragma unroll
-    for (int e = 0; e < 32; ++e)
-      if (e < nvalid) mx_out = max_nan(mx_out, fabsf(v[e]));
-  }
-}
-
-// Max and min of the first `nvalid` of 32 values (NaN-propagating).
-__device__ __forceinline__ void minmax32(const float* v, int nvalid, float& mx_out, float& mi_out) {
-  if (nvalid >= 32) {
-    float mx[4], mi[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) mx[e] = mi[e] = v[e];
-#pragma unroll
-    for (int e = 4; e < 32; ++e) mx[e & 3] = max_nan(mx[e & 3], v[e]), mi[e & 3] = min_nan(mi[e & 3], v[e]);
-    mx_out = max_nan(mx_out, max_nan(max_nan(mx[0], mx[1]), max_nan(mx[2], mx[3])));
-    mi_out = min_nan(mi_out, min_nan(min_nan(mi[0], mi[1]), min_nan(mi[2], mi[3])));
-  } else {
-#pragma unroll
-    for (int e = 0; e < 32; ++e)
-      if (e < nvalid) mx_out = max_nan(mx_out, v[e]), mi_out = min_nan(mi_out, v[e]);
-  }
-}
-
-// 32 values -> 16 packed bf16 pairs of 2^(v*sl - msl) (zero past nvalid).  All on
-// MUFU: the epilogue is issue-bound, and the FMA-pipe polynomial costs ~9 issues.
-__device__ __forceinline__ uint32_t exp2_pair_f16(float x0, float x1) {
-  // both exponents through one MUFU op (ex2.approx.f16x2), repacked as bf16x2
-  uint32_t h, r;
-  asm("cvt.rn.f16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(x0), "f"(x1));
-  asm("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(h));
-  float lo, hi;
-  asm("{.reg .f16 a, b;\n\tmov.b32 {a, b}, %2;\n\tcvt.f32.f16 %0, a;\n\tcvt.f32.f16 %1, b;}"
-      : "=f"(lo), "=f"(hi) : "r"(r));
-  return pack_bf16(lo, hi);
-}
-
-__device__ __forceinline__ void exp_pack32(const float* v, int nvalid, float sl, float msl, uint32_t* w) {
-  if (nvalid >= 32 && FF_EXP == 2) {
-#pragma unroll
-    for (int e = 0; e < 16; ++e) w[e] = exp2_pair_f16(fmaf(v[2 * e], sl, -msl), fmaf(v[2 * e + 1], sl, -msl));
-  } else if (nvalid >= 32) {
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const float x0 = fmaf(v[2 * e], sl, -msl), x1 = fmaf(v[2 * e + 1], sl, -msl);
-      w[e] = pack_bf16(fast_exp2(x0), (FF_EXP == 0 && (e & 1)) ? exp2_poly<3>(x1) : fast_exp2(x1));
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < 16; ++e)
-      w[e] = pack_bf16(2 * e < nvalid ? fast_exp2(fmaf(v[2 * e], sl, -msl)) : 0.f,
-                       2 * e + 1 < nvalid ? fast_exp2(fmaf(v[2 * e + 1], sl, -msl)) : 0.f);
-  }
-}
-
 // 96 registers: 19 warps put 5 warps on three SM sub-partitions, each with a 16K-register file.
+// EXT: the rsa_fwd_factored_ex features (stream mode, given reference points, ring-hop
+// accumulation, key_chunk != chunk); the plain instantiation is the hot forward.
+template <bool EXT>
 __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfArgs p) {
   uint8_t* smem = smem_base();
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FF_OFF_BAR);
@@ -185,7 +129,8 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
 
   const Geo& g = p.g;
-  const int ntk = (g.c + TK - 1) / TK, nrt = (g.c + TR - 1) / TR;
+  const int ck = EXT ? p.ck : g.c;
+  const int ntk = (ck + TK - 1) / TK, nrt = (g.c + TR - 1) / TR;
   const int T = g.n_org * ntk;    // key tiles per row
   const int NQ = g.n_rank * nrt;  // query tiles per head
   const int UH = (NQ + 1) / 2;    // units per head
@@ -245,7 +190,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
             mbar_wait(&k_empty[t], (kgen & 1) ^ 1);
             mbar_arrive_expect_tx(&k_full[t], TILE);
             tma_load_4d(smem + FF_OFF_K + t * TILE, p.peer ? &p.pm.k[jo] : &p.tk, &k_full[t], 0, k0, z,
-                        p.peer ? b : (g.org_lo + jo) * g.B + b);
+                        p.peer ? b : jo * g.B + b);
           }
           ++kgen;
         }
@@ -256,14 +201,14 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
             mbar_wait(&k_empty[ks], kq.phase(FF_KST) ^ 1);
             mbar_arrive_expect_tx(&k_full[ks], TILE);
             tma_load_4d(smem + FF_OFF_K + ks * TILE, p.peer ? &p.pm.k[jo] : &p.tk, &k_full[ks], 0, k0, z,
-                        p.peer ? b : (g.org_lo + jo) * g.B + b);
+                        p.peer ? b : jo * g.B + b);
             ++kq.i;
           }
           const uint32_t vs = vq.slot(FF_VST);
           mbar_wait(&v_empty[vs], vq.phase(FF_VST) ^ 1);
           mbar_arrive_expect_tx(&v_full[vs], TILE);
           tma_load_4d(smem + FF_OFF_V + vs * TILE, p.peer ? &p.pm.v[jo] : &p.tv, &v_full[vs], 0, k0, z,
-                      p.peer ? b : (g.org_lo + jo) * g.B + b);
+                      p.peer ? b : jo * g.B + b);
           ++vq.i;
         }
       }
@@ -369,18 +314,20 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
       // tile 0: raw max and min (the reference point); later tiles: max |s| only, which
       // bounds the row max (headroom check) and is finite iff every score is
       float m = -INFINITY, mi = INFINITY, am = 0.f, msl = 0.f;
+      if (EXT && p.rowmax_in)
+        msl = row < g.c ? __ldg(p.rowmax_in + ((int64_t(d * g.B + b) * g.Z + z) * g.c + row) * p.rm_stride) : 0.f;
 #if !FF_ONES
       float lsum = 0.f;  // this thread's share of sum_k P~[row, k] over the bf16 values stored
 #endif
       int jo = 0, k0 = 0;
       for (int t = 0; t < T; ++t) {
-        const int nvalid = min(TK, g.c - k0) - half * 64;
+        const int nvalid = min(TK, ck - k0) - half * 64;
         uint32_t w[32];
         mbar_wait(&s_full[gi], sn & 1);
         FF_TRACE(3);
         tc_fence_after();
         __syncwarp();
-        if (t == 0) {  // first key tile: its row max is the reference
+        if (t == 0 && !(EXT && p.rowmax_in)) {  // first key tile: its row max is the reference
           float v[64];
           tmem_ld32(t_s, v);
           tmem_ld32(t_s + 32, v + 32);
@@ -397,8 +344,8 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
           asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(slot + ((et + 128) & 255) * 4) : "memory");
           const float mref = fmaxf(m, o);
           msl = (mref == -INFINITY || !(fabsf(mref) <= 3.402823466e38f)) ? 0.f : mref * sl;
-          exp_pack32(v, nvalid, sl, msl, w);
-          exp_pack32(v + 32, nvalid - 32, sl, msl, w + 16);
+          exp2_pack32(v, nvalid, sl, msl, w);
+          exp2_pack32(v + 32, nvalid - 32, sl, msl, w + 16);
         } else {
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc) {  // two 32-column chunks (register budget of 18 warps)
@@ -413,7 +360,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
             }
             if (FF_ABSMAX) absmax32(v, nvalid - cc * 32, am);
             else minmax32(v, nvalid - cc * 32, m, mi);
-            exp_pack32(v, nvalid - cc * 32, sl, msl, w + cc * 16);
+            exp2_pack32(v, nvalid - cc * 32, sl, msl, w + cc * 16);
           }
         }
         ++sn;
@@ -436,20 +383,20 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&p_full[gi]);
-          if (nvalid > 0)  // the panel is read back only by the backward: evict-first in L2
+          if (nvalid > 0 && !(EXT && p.no_panel))  // the panel is read back only by the backward: evict-first in L2
             tma_store_5d_hint(&p.tp, ptile_gen + quad * 4096, k0 + half * 64, g.org_lo + jo, rt * TR + quad * 32, z,
                               d * g.B + b, pol);
           tma_store_commit();
         }
         FF_TRACE(6);
         ++pn;
-        if (k0 + TK >= g.c) k0 = 0, ++jo;
+        if (k0 + TK >= ck) k0 = 0, ++jo;
         else k0 += TK;
       }
       if (!(m == -INFINITY && mi == INFINITY))  // this thread saw at least one valid key in tile 0
         bad |= !(fabsf(m) <= 3.402823466e38f) || !(fabsf(mi) <= 3.402823466e38f);
       bad |= !(am <= 3.402823466e38f);
-      redo |= (FF_ABSMAX ? am : m) * sl - msl > FF_HEADROOM;  // |s| >= s: conservative
+      if (!(EXT && p.rm_exact)) redo |= (FF_ABSMAX ? am : m) * sl - msl > FF_HEADROOM;  // |s| >= s: conservative
       // ---- O = O~ / l, r = 1 / l (l >= 1 unless the row needs the fallback)
       mbar_wait(&o_full[gi], un_n & 1);
       FF_TRACE(7);
@@ -479,6 +426,29 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
       }
 #endif
       ++un_n;
+      const int64_t ridx = (int64_t(d * g.B + b) * g.Z + z) * g.c + row;
+      if (EXT && p.acc_in && row < g.c) {  // ring hops: add the running O~ and l of earlier origins
+        const float* oa = reinterpret_cast<const float*>(p.o_acc.ptr) + out_off(p.o_acc, d, b, z, row) + half * 32;
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float4 x = *reinterpret_cast<const float4*>(oa + e);
+          o[e] += x.x, o[e + 1] += x.y, o[e + 2] += x.z, o[e + 3] += x.w;
+        }
+        l += p.l_acc[ridx];
+      }
+      if (EXT && !p.final_hop) {  // not the last hop: hand O~ and l to the next launch
+        if (row < g.c) {
+          float* oa = reinterpret_cast<float*>(p.o_acc.ptr) + out_off(p.o_acc, d, b, z, row) + half * 32;
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) *reinterpret_cast<float4*>(oa + e) = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
+          if (half == 0) {
+            p.l_acc[ridx] = l;
+            if (EXT && p.rowmax && !p.rowmax_in) p.rowmax[ridx] = msl;
+          }
+        }
+        FF_TRACE(21);
+        continue;
+      }
       const float rinv = 1.f / l;
       redo |= !(l >= 1.f && l <= 3.402823466e38f);
       // O -> the group's P~ buffer (atom 0, swizzled like a TMA tile) -> one TMA store
@@ -498,7 +468,10 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
         tma_store_wait_read<0>();  // other warps' next P~ rows go into this atom
       }
       bar_named(bar_grp_id, 256);
-      if (row < g.c && half == 0) p.rowscale[(int64_t(d * g.B + b) * g.Z + z) * g.c + row] = rinv;
+      if (row < g.c && half == 0) {
+        p.rowscale[ridx] = rinv;
+        if (EXT && p.rowmax && !p.rowmax_in) p.rowmax[ridx] = msl;
+      }
       FF_TRACE(21);
     }
     if (p.flag && (bad || redo)) atomicOr(p.flag, (bad ? 1 : 0) | (redo ? 2 : 0));
@@ -517,12 +490,25 @@ namespace {
 
 int ff_launch(FfArgs& a, const rsa_geom* g, rsa_view q, rsa_view panel, rsa_view o_out, float* rowscale, int* flag,
               void* stream) {
-  if (!rowscale || !flag || !o_out.ptr || !out_ok(o_out, 2))
+  const bool final_hop = !a.o_acc.ptr || a.final_hop;
+  a.final_hop = final_hop;
+  if (!flag || (final_hop && (!rowscale || !o_out.ptr || !out_ok(o_out, 2))))
     return fail(RSA_ERR_UNSUPPORTED, "rsa_fwd_factored: output / row-scale / flag buffers missing or misaligned");
-  if (!head_map(&a.tq, q, g, g->n_rank) || !panel_map(&a.tp, panel, g, g->n_rank, 32) ||
-      !head_map(&a.to, o_out, g, g->n_rank))
+  if (a.o_acc.ptr && (!a.l_acc || !out_ok(rsa_view{a.o_acc.ptr, a.o_acc.s_rank, a.o_acc.s_b, a.o_acc.s_z,
+                                                    a.o_acc.s_row}, 4)))
+    return fail(RSA_ERR_UNSUPPORTED, "rsa_fwd_factored_ex: o_acc / l_acc missing or misaligned");
+  if (!a.o_acc.ptr && a.acc_in) return fail(RSA_ERR_INVALID, "rsa_fwd_factored_ex: acc_in without o_acc");
+  if (a.rowmax_in && a.rm_stride < 1) return fail(RSA_ERR_INVALID, "rsa_fwd_factored_ex: rowmax_in_stride < 1");
+  a.no_panel = panel.ptr == nullptr;
+  if (!a.no_panel && key_chunk(g) != g->chunk)
+    return fail(RSA_ERR_INVALID, "rsa_fwd_factored_ex: a panel needs key_chunk == chunk");
+  if (!head_map(&a.tq, q, g, g->n_rank) || (!a.no_panel && !panel_map(&a.tp, panel, g, g->n_rank, 32)) ||
+      (final_hop && !head_map(&a.to, o_out, g, g->n_rank)))
     return RSA_ERR_UNSUPPORTED;
+  if (a.no_panel) a.tp = a.tq;  // never used; keeps the prefetch harmless
+  if (!final_hop) a.to = a.tq;
   a.g = to_geo(g);
+  a.ck = key_chunk(g);
   a.sl = g->scale * LOG2E;
   a.flag = flag;
   a.rowscale = rowscale;
@@ -536,13 +522,15 @@ int ff_launch(FfArgs& a, const rsa_geom* g, rsa_view q, rsa_view panel, rsa_view
   const int nq = g->n_rank * ((g->chunk + TR - 1) / TR);
   const int units = g->batch * g->heads * ((nq + 1) / 2);
   if (units <= 0) return RSA_OK;
-  cudaFuncSetAttribute(fwd_factored_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FF_SMEM);
+  const bool ext = a.no_panel || a.rowmax || a.rowmax_in || a.o_acc.ptr || a.ck != g->chunk;
+  auto kernel = ext ? fwd_factored_kernel<true> : fwd_factored_kernel<false>;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FF_SMEM);
   cudaFuncAttributes fa{};
-  if (cudaFuncGetAttributes(&fa, fwd_factored_kernel) == cudaSuccess && fa.maxThreadsPerBlock < FF_THREADS)
+  if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess && fa.maxThreadsPerBlock < FF_THREADS)
     return fail(RSA_ERR_CUDA, "rsa_fwd_factored: %d registers/thread allow only %d threads per CTA (need %d)",
                 fa.numRegs, fa.maxThreadsPerBlock, FF_THREADS);
   const int grid = persistent_grid(units);
-  fwd_factored_kernel<<<grid, FF_THREADS, FF_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  kernel<<<grid, FF_THREADS, FF_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(a);
   if (trace_path) {
     static long long host[(FF_THREADS / 32) * 4096];
     cudaMemcpy(host, trace_buf, sizeof(host), cudaMemcpyDeviceToHost);
@@ -565,6 +553,25 @@ int rsa_fwd_factored(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_
   FfArgs a{};
   if (!head_map(&a.tk, k, g, g->n_org) || !head_map(&a.tv, v, g, g->n_org)) return RSA_ERR_UNSUPPORTED;
   return ff_launch(a, g, q, panel, o_out, rowscale, flag, stream);
+}
+
+int rsa_fwd_factored_ex(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, const rsa_fwd_ext* ext,
+                        rsa_view o_out, float* rowscale, int* flag, void* stream) {
+  using namespace rsa;
+  if (!ext) return fail(RSA_ERR_INVALID, "rsa_fwd_factored_ex: options missing");
+  if (!geom_ok_keys(g)) return fail(RSA_ERR_INVALID, "rsa_fwd_factored_ex: unsupported geometry");
+  FfArgs a{};
+  if (!head_map(&a.tk, k, g, g->n_org, key_chunk(g)) || !head_map(&a.tv, v, g, g->n_org, key_chunk(g)))
+    return RSA_ERR_UNSUPPORTED;
+  a.rowmax = ext->rowmax;
+  a.rowmax_in = ext->rowmax_in;
+  a.rm_stride = ext->rowmax_in_stride > 0 ? ext->rowmax_in_stride : 1;
+  a.rm_exact = ext->rowmax_exact;
+  a.o_acc = to_out(ext->o_acc);
+  a.l_acc = ext->l_acc;
+  a.acc_in = ext->acc_in;
+  a.final_hop = ext->final_hop;
+  return ff_launch(a, g, q, ext->panel, o_out, rowscale, flag, stream);
 }
 
 int rsa_fwd_factored_peer(const rsa_geom* g, rsa_view q, const rsa_view* k_origin, const rsa_view* v_origin,

@@ -32,10 +32,11 @@ from typing import NamedTuple
 import torch
 
 from . import tensor_ops as ops
-from ._native import BF16, F32, RsaGeom, RsaView, check, lib
+from ._native import BF16, F32, RsaFwdExt, RsaGeom, RsaView, check, lib
 from .errors import ShapeError
 
-__all__ = ["fused_supported", "forward", "backward", "Forward", "normalized_panel", "recompute_outputs", "NULL_VIEW", "KernelTimer"]
+__all__ = ["fused_supported", "forward", "backward", "Forward", "normalized_panel", "recompute_outputs", "NULL_VIEW",
+           "KernelTimer", "StreamForward", "forward_stream", "backward_stream", "stream_panel", "stream_supported"]
 
 NULL_VIEW = RsaView(None, 0, 0, 0, 0)
 
@@ -112,8 +113,8 @@ def _view(t: torch.Tensor | None) -> RsaView:
     return RsaView(t.data_ptr(), t.stride(0), t.stride(1), t.stride(2), t.stride(3))
 
 
-def _geom(n_rank, b, z, c, a, seq, org_lo, n_org) -> RsaGeom:
-    return RsaGeom(n_rank, b, z, c, a, seq, org_lo, n_org, 1.0 / math.sqrt(a))
+def _geom(n_rank, b, z, c, a, seq, org_lo, n_org, key_chunk=0) -> RsaGeom:
+    return RsaGeom(n_rank, b, z, c, a, seq, org_lo, n_org, 1.0 / math.sqrt(a), key_chunk)
 
 
 def fused_supported(n: int, b: int, z: int, c: int, a: int) -> bool:
@@ -350,3 +351,120 @@ def _backward_staged(q, k, v, panel, grad, dq, dk, dv) -> None:
             ops.matmul(panel[d][..., blk].transpose(-1, -2), grad[d], out=dv_acc[j], accumulate=d > 0)
     dk.copy_(dk_acc)
     dv.copy_(dv_acc)
+
+
+# ------------------------------------------------------------- stream mode
+
+class StreamForward(NamedTuple):
+    """Result of ``forward_stream``: outputs plus the two numbers per row the stream-mode
+    backward needs -- ``rowscale`` r = 1 / sum_k P~ and ``rowmax`` m, the reference point of
+    P~ = 2^(s * scale * log2(e) - m) -- instead of a (c x L) probability panel per row block."""
+
+    out: torch.Tensor
+    rowscale: torch.Tensor
+    rowmax: torch.Tensor
+    flag: torch.Tensor
+
+
+def stream_supported(n: int, b: int, z: int, c: int, a: int, key_chunk: int = 0) -> bool:
+    """Can the stream-mode kernels tile this geometry (A = 64, chunks of 8-row multiples)?"""
+    return a == 64 and c % 8 == 0 and (key_chunk or c) % 8 == 0 and min(n, b, z, c) >= 1
+
+
+def _fwd_ex(q, k, v, g, *, panel=None, rowmax=None, rowmax_in=None, rowmax_stride=1, exact=False, o_acc=None,
+            l_acc=None, acc_in=False, final=True, out=None, rowscale=None, flag=None):
+    ext = RsaFwdExt(_view(panel), None if rowmax is None else rowmax.data_ptr(),
+                    None if rowmax_in is None else rowmax_in.data_ptr(), rowmax_stride, int(exact), _view(o_acc),
+                    None if l_acc is None else l_acc.data_ptr(), int(acc_in), int(final))
+    check(lib().rsa_fwd_factored_ex(ctypes.byref(g), _view(q), _view(k), _view(v), ctypes.byref(ext), _view(out),
+                                    None if rowscale is None else rowscale.data_ptr(), flag.data_ptr(), _stream(q)),
+          "rsa_fwd_factored_ex")
+
+
+def forward_stream(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, flag: torch.Tensor | None = None,
+                   out: torch.Tensor | None = None, rowscale: torch.Tensor | None = None,
+                   rowmax: torch.Tensor | None = None, exact: bool = False) -> StreamForward:
+    """Stream-mode RSA forward on stacked [N][B][Z][c][A] bf16 chunks (keys: [N][B][Z][ck][A]).
+
+    One rsa_fwd_factored_ex launch with no panel: O, r and m survive, O(c) per row instead
+    of O(L).  ``exact=True`` (the fallback for flag bit 1) first takes every row's true
+    maximum with rsa_fwd_stats and runs the single pass on it.  The caller reads ``flag``.
+    """
+    n, b, z, c, a = q.shape
+    ck = k.shape[3]
+    dev = q.device
+    if flag is None:
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    if out is None:
+        out = torch.empty((n, b, z, c, a), dtype=torch.bfloat16, device=dev)
+    if rowscale is None:
+        rowscale = torch.empty((n, b, z, c), dtype=torch.float32, device=dev)
+    if rowmax is None:
+        rowmax = torch.empty((n, b, z, c), dtype=torch.float32, device=dev)
+    norg = k.shape[0]
+    g = _geom(n, b, z, c, a, norg * ck, 0, norg, 0 if ck == c else ck)
+    if not exact:
+        _fwd_ex(q, k, v, g, rowmax=rowmax, out=out, rowscale=rowscale, flag=flag)
+        return StreamForward(out, rowscale, rowmax, flag)
+    if ck != c:
+        raise ShapeError("the exact (two-pass) stream forward needs key_chunk == chunk")
+    stats = torch.empty((n, b, z, c, 2), dtype=torch.float32, device=dev)
+    check(lib().rsa_fwd_stats(ctypes.byref(g), _view(q), _view(k), stats.data_ptr(), 0, flag.data_ptr(), _stream(q)),
+          "rsa_fwd_stats")
+    _fwd_ex(q, k, v, g, rowmax_in=stats, rowmax_stride=2, exact=True, out=out, rowscale=rowscale, flag=flag)
+    rowmax.copy_(stats[..., 0])
+    return StreamForward(out, rowscale, rowmax, flag)
+
+
+def stream_panel(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, rowmax: torch.Tensor, rowscale: torch.Tensor,
+                 d: int, dtype=torch.float32) -> torch.Tensor:
+    """Rank d's probability panel (B, Z, c, L) recomputed from a stream-mode forward's
+    saved m and r: the factored kernel re-run with m given writes P~ bit for bit as the
+    panel forward would have, then P = r * P~ (the reference's probs, materialised only
+    when a caller looks at them)."""
+    n, b, z, c, a = q.shape
+    seq = k.shape[0] * k.shape[3]
+    dev = q.device
+    qd = q[d:d + 1]
+    panel = torch.empty((1, b, z, c, seq), dtype=torch.bfloat16, device=dev)
+    scratch_o = torch.empty((1, b, z, c, a), dtype=torch.bfloat16, device=dev)
+    scratch_r = torch.empty((1, b, z, c), dtype=torch.float32, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    g = _geom(1, b, z, c, a, seq, 0, k.shape[0])
+    _fwd_ex(qd, k, v, g, panel=panel, rowmax_in=rowmax[d:d + 1].contiguous(), exact=True, out=scratch_o,
+            rowscale=scratch_r, flag=flag)
+    return normalized_panel(panel[0], rowscale[d], dtype)
+
+
+def backward_stream(q, k, v, grad, out, rowscale, rowmax, *, grads: tuple | None = None,
+                    dvec: torch.Tensor | None = None, grad_scaled: torch.Tensor | None = None,
+                    dkv_f32: bool = False, timer=None):
+    """Stream-mode RSA backward: (dq, dk, dv) from q, k, v, dO and the forward's O, r, m.
+
+    rsa_rowdot_scale forms D*r and dO*r; rsa_bwd_kv_stream walks every query tile per key
+    tile (dK, dV); rsa_bwd_q_stream every key tile per query tile (dQ).  Both recompute
+    P~ on chip.  dk / dv are bf16 [N_org][B][Z][ck][A] (fp32 with ``dkv_f32``)."""
+    n, b, z, c, a = q.shape
+    norg, ck = k.shape[0], k.shape[3]
+    dev = q.device
+    tm = timer or _NO_TIMER
+    if grads is None:
+        dq = torch.empty((n, b, z, c, a), dtype=torch.bfloat16, device=dev)
+        kdt = torch.float32 if dkv_f32 else torch.bfloat16
+        dk = torch.empty((norg, b, z, ck, a), dtype=kdt, device=dev)
+        dv = torch.empty_like(dk)
+    else:
+        dq, dk, dv = grads
+    with tm("rowdot"):
+        dvec, gsc = ops.rowdot_scale(grad, out, rowscale, out=dvec, a_scaled=grad_scaled)
+    g = _geom(n, b, z, c, a, norg * ck, 0, norg, 0 if ck == c else ck)
+    L = lib()
+    st = _stream(q)
+    with tm("bwd_kv_stream"):
+        check(L.rsa_bwd_kv_stream(ctypes.byref(g), _view(q), _view(k), _view(v), _view(gsc), rowmax.data_ptr(),
+                                  dvec.data_ptr(), _view(dk), _view(dv), F32 if dk.dtype == torch.float32 else BF16,
+                                  0, st), "rsa_bwd_kv_stream")
+    with tm("bwd_q_stream"):
+        check(L.rsa_bwd_q_stream(ctypes.byref(g), _view(q), _view(k), _view(v), _view(gsc), rowmax.data_ptr(),
+                                 dvec.data_ptr(), NULL_VIEW, 0, _view(dq), st), "rsa_bwd_q_stream")
+    return dq, dk, dv

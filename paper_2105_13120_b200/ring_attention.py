@@ -46,6 +46,7 @@ __all__ = [
     "sequence_parallel_mlp",
     "sequence_parallel_mlp_backward",
     "ProbPanels",
+    "StreamPanels",
 ]
 
 
@@ -119,6 +120,36 @@ class ProbPanels(list):
             yield self._get(d)
 
 
+class StreamPanels(ProbPanels):
+    """The ``probs`` list of a stream-mode forward (``mode="stream"``).
+
+    No panel exists: the forward kept O and two fp32 numbers per query row (the
+    reference point m and the row scale r of the factored panel P = r * 2^(s' - m)),
+    O(B*Z*c) per rank instead of O(B*Z*c*L).  Indexing recomputes rank d's probabilities
+    on the device (``engine.stream_panel``: the same products and exp2 as the panel
+    forward, so the values are those ``mode="panel"`` would return) -- the reference's
+    ``probs`` contract holds, but memory is only spent on the panels a caller looks at.
+    Passing the object back to ``ring_attention_backward`` runs the stream-mode backward,
+    which recomputes each probability tile on chip and never materialises a panel.
+    """
+
+    def __init__(self, q, k, v, outputs, rowscale, rowmax, inputs, panel_shape):
+        list.__init__(self, [None] * q.shape[0])
+        self.stacked = None
+        self.q, self.k, self.v = q, k, v
+        self.outputs, self.rowscale, self.rowmax = outputs, rowscale, rowmax
+        self.panel_shape = tuple(panel_shape)
+        self.inputs = inputs
+        self.dirty = False
+
+    def _get(self, d: int):
+        item = list.__getitem__(self, d)
+        if item is None:
+            item = engine.stream_panel(self.q, self.k, self.v, self.rowmax, self.rowscale, d)
+            list.__setitem__(self, d, item)
+        return item
+
+
 def _shape_of(x) -> tuple:
     return tuple(x.shape) if hasattr(x, "shape") else tuple(__import__("numpy").asarray(x).shape)
 
@@ -141,8 +172,9 @@ def _check_chunks(name: str, chunks, cfg: AttentionConfig, expect: tuple) -> lis
 def _device_of(*lists):
     for lst in lists:
         if isinstance(lst, ProbPanels):  # never materialise the panels just to find the device
-            if lst.stacked.is_cuda:
-                return lst.stacked.device
+            ref = lst.stacked if lst.stacked is not None else lst.outputs
+            if ref.is_cuda:
+                return ref.device
             continue
         for x in lst:
             if isinstance(x, torch.Tensor) and x.is_cuda:
@@ -156,7 +188,8 @@ def _stack(chunks: list, device) -> torch.Tensor:
     bf16 torch chunks in pinned host memory are copied asynchronously on the
     current stream; a single device chunk that is already bf16 and contiguous
     is used in place (a view, no copy)."""
-    if isinstance(chunks, ProbPanels) and not chunks.dirty and chunks.stacked.device == device:
+    if (isinstance(chunks, ProbPanels) and not chunks.dirty and chunks.stacked is not None
+            and chunks.stacked.device == device):
         return chunks.stacked
     first = chunks[0]
     if (len(chunks) == 1 and isinstance(first, torch.Tensor) and first.device == device
@@ -230,13 +263,39 @@ def backward_ledger(cfg: AttentionConfig) -> CommLedger:
     return ledger
 
 
+def _stream_checked(q, k, v) -> engine.StreamForward:
+    """engine.forward_stream plus the status check (bit 0 NumericError; bit 1 reruns the
+    launch on every row's true maximum, as _forward_checked does for the panel)."""
+    res = engine.forward_stream(q, k, v)
+    status = int(res.flag.item())
+    if status == 2:
+        res.flag.zero_()
+        res = engine.forward_stream(q, k, v, flag=res.flag, out=res.out, rowscale=res.rowscale, rowmax=res.rowmax,
+                                    exact=True)
+        status = int(res.flag.item())
+    if status:
+        raise NumericError("softmax_rows requires finite inputs")
+    return res
+
+
+MODES = ("panel", "stream")
+
+
 def ring_attention_forward(q_chunks, k_chunks, v_chunks, cfg: AttentionConfig, *, executor: str | None = None,
-                           path: str = "auto") -> RingAttentionForward:
+                           path: str = "auto", mode: str = "panel") -> RingAttentionForward:
     """Distributed attention forward over per-rank (B, Z, L/N, A) chunks.
 
     ringseq/ring_attention.py:124-147.  ``path`` ('auto' | 'fused' | 'staged')
     selects the device implementation; both compute the same protocol.
+
+    ``mode="panel"`` (default) saves the reference's probability panels (B, Z, L/N, L)
+    per rank, so memory grows as L^2/N.  ``mode="stream"`` saves O plus two numbers per
+    query row; ``probs`` is then a ``StreamPanels`` list that recomputes any rank's
+    panel on access, and the backward recomputes probability tiles on chip -- memory
+    grows as L/N, so the trainable length grows linearly with the rank count.
     """
+    if mode not in MODES:
+        raise ValueError(f"unknown mode {mode!r}; expected one of {MODES}")
     resolve_executor(executor)
     shape = cfg.chunk_shape()
     q_chunks = _check_chunks("q_chunks", q_chunks, cfg, shape)
@@ -244,8 +303,19 @@ def ring_attention_forward(q_chunks, k_chunks, v_chunks, cfg: AttentionConfig, *
     v_chunks = _check_chunks("v_chunks", v_chunks, cfg, shape)
     dev = _device_of(q_chunks, k_chunks, v_chunks)
     q, k, v = (_stack(x, dev) for x in (q_chunks, k_chunks, v_chunks))
-    out, panel, rowscale, _ = _forward_checked(q, k, v, path)
     saved = [(_chunk_key(c), t) for c, t in ((q_chunks, q), (k_chunks, k), (v_chunks, v))]
+    if mode == "stream":
+        if not engine.stream_supported(cfg.num_devices, cfg.batch_size, cfg.num_heads, cfg.chunk_len,
+                                       cfg.head_size):
+            raise ShapeError(f"stream mode needs head_size 64 and chunk_len % 8 == 0 (got {cfg.head_size}, "
+                             f"{cfg.chunk_len})")
+        res = _stream_checked(q, k, v)
+        return RingAttentionForward(
+            outputs=[res.out[d] for d in range(cfg.num_devices)],
+            probs=StreamPanels(q, k, v, res.out, res.rowscale, res.rowmax, saved, cfg.panel_shape()),
+            ledger=forward_ledger(cfg),
+        )
+    out, panel, rowscale, _ = _forward_checked(q, k, v, path)
     return RingAttentionForward(
         outputs=[out[d] for d in range(cfg.num_devices)],
         probs=ProbPanels(panel, out, rowscale, saved),
@@ -282,8 +352,15 @@ def ring_attention_backward(q_chunks, k_chunks, v_chunks, probs, grad_chunks, cf
                 return (t, True) if torch.equal(up, t) else (up, False)
         return _stack(chunks, dev), False
 
-    (q, _), (k, _), (v, v_saved) = (stack_or_saved(x, i) for i, x in enumerate((q_chunks, k_chunks, v_chunks)))
+    (q, q_saved), (k, k_saved), (v, v_saved) = (stack_or_saved(x, i)
+                                                 for i, x in enumerate((q_chunks, k_chunks, v_chunks)))
     g = _stack(grad_chunks, dev)
+    n = cfg.num_devices
+    if isinstance(probs, StreamPanels) and not probs.dirty and q_saved and k_saved and v_saved:
+        # the forward's own state: recompute probability tiles on chip, no panel anywhere
+        dq, dk, dv = engine.backward_stream(q, k, v, g, probs.outputs, probs.rowscale, probs.rowmax)
+        return RingAttentionBackward(grad_q=[dq[d] for d in range(n)], grad_k=[dk[d] for d in range(n)],
+                                     grad_v=[dv[d] for d in range(n)], ledger=backward_ledger(cfg))
     panel = _stack(probs, dev)
     own = isinstance(probs, ProbPanels) and panel is probs.stacked
     # the forward's O = P V is reused for D = rowsum(dP * P) = rowsum(dO * O) only when the
@@ -294,7 +371,6 @@ def ring_attention_backward(q_chunks, k_chunks, v_chunks, probs, grad_chunks, cf
     if outputs is not None and (outputs.shape != q.shape or outputs.device != dev):
         outputs = None
     dq, dk, dv = engine.backward(q, k, v, panel, g, outputs=outputs, rowscale=rowscale, path=path)
-    n = cfg.num_devices
     return RingAttentionBackward(
         grad_q=[dq[d] for d in range(n)],
         grad_k=[dk[d] for d in range(n)],
