@@ -211,9 +211,18 @@ def _chunk_key(chunks):
     return tuple((c, c._version) for c in chunks)
 
 
+def _same_tensor(k: torch.Tensor, ver: int, c) -> bool:
+    """c is k, or a view of the same memory with the same layout, unmodified since
+    (views share the version counter of their base, so an in-place write shows)."""
+    if c is k:
+        return c._version == ver
+    return (isinstance(c, torch.Tensor) and c.device == k.device and c.dtype == k.dtype and c.shape == k.shape
+            and c.stride() == k.stride() and c.data_ptr() == k.data_ptr() and c._version == ver)
+
+
 def _same_chunks(key, chunks) -> bool:
     return key is not None and len(key) == len(chunks) and all(
-        c is k and c._version == ver for (k, ver), c in zip(key, chunks))
+        _same_tensor(k, ver, c) for (k, ver), c in zip(key, chunks))
 
 
 def _chunk_elements(cfg: AttentionConfig) -> int:
