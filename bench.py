@@ -403,17 +403,19 @@ def ours(args):
     # affects every figure alike and the per-type times add up to the step
     rounds = 3
     acc = {k: 0.0 for k in replays}
-    for _ in range(rounds):
-        for kind, replay in replays.items():
-            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            k0.record()
-            for _ in range(reps):
-                replay()
-            k1.record()
-            torch.cuda.synchronize()
-            acc[kind] += k0.elapsed_time(k1)
+    with ClockSampler(local) as kclk:
+        for _ in range(rounds):
+            for kind, replay in replays.items():
+                k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                k0.record()
+                for _ in range(reps):
+                    replay()
+                k1.record()
+                torch.cuda.synchronize()
+                acc[kind] += k0.elapsed_time(k1)
     type_ms = {k: acc[k] / (rounds * reps) for k in kinds}
     step_ref_ms = acc["step"] / (rounds * reps)
+    kernel_clocks = kclk.result()
     timing_mode = (f"per kernel type: a CUDA graph of that type's {LAYERS} launches of the step, replayed {reps}x back "
                    f"to back per round, {rounds} rounds interleaved with the step graph; event pair on the replay "
                    f"stream")
@@ -467,7 +469,8 @@ def ours(args):
         "data": "synthetic N(0,1) bf16 inputs, per-layer q/k/v/dO", "config": config_obj(args, 1),
         "launch": "cuda graph of the whole step, replayed" if graph_used else "eager launches",
         "clocks": clocks, "roofline": roof, "kernels": kernels, "kernel_ms_sum": kernel_sum,
-        "kernel_sum_over_step": kernel_sum / step_ref_ms, "step_ms_interleaved": step_ref_ms, "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
+        "kernel_sum_over_step": kernel_sum / step_ref_ms, "step_ms_interleaved": step_ref_ms,
+        "kernel_timing_clocks": kernel_clocks, "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
         "parity": parity,
     }
     if not args.no_cpu_baseline:
