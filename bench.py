@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the captured step")
+    ap.add_argument("--attn", default="panel", choices=["panel", "stream"],
+                    help="panel: the reference's saved probability panels; stream: O(L) state, P recomputed")
     return ap.parse_args()
 
 
@@ -67,7 +69,11 @@ def dist_env():
 
 def config_obj(args, n):
     return {
-        "workload": "BERT-base RSA stack: 12 layers x ring self-attention fwd+bwd (probs panels saved)",
+        "workload": ("BERT-base RSA stack: 12 layers x ring self-attention fwd+bwd (probs panels saved)"
+                     if args.attn == "panel" else
+                     "BERT-base RSA stack: 12 layers x ring self-attention fwd+bwd, stream mode (row statistics "
+                     "saved, probabilities recomputed in the backward)"),
+        "attn": args.attn,
         "model": "bert-base attention (Z=12, A=64, H=768)",
         "layers": args.layers,
         "global_batch": args.batch * n,
@@ -278,6 +284,10 @@ def kernel_model(name, n, b, z, c, seq, a):
         return 2 * pe + 2 * 4 * ce, 4 * pe * a        # read P; dO,K,V in, dQ out; dO V^T, dS K
     if name == "rowdot":
         return 2 * 3 * ce + 8 * rows, 3 * ce            # read dO, O, r; write D*r, dO*r
+    if name == "fwd_stream":
+        return 2 * 4 * ce + 8 * rows, 4 * pe * a        # Q,K,V in, O out, r and m out; QK^T, PV (algorithmic)
+    if name == "bwd_stream":
+        return 2 * 7 * ce + 8 * rows, 8 * pe * a        # Q,K,V,dO' in, dQ,dK,dV out, m, D' in; the 4 bwd products
     return 0, 0
 
 
@@ -304,22 +314,41 @@ def ours(args):
         return torch.randn((1, B, Z, c, A), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
 
     layers = [dict(q=rnd(), k=rnd(), v=rnd(), g=rnd()) for _ in range(LAYERS)]
+    stream = args.attn == "stream"
     for ly in layers:
         ly["o"] = torch.empty_like(ly["q"])
-        ly["p"] = torch.empty((1, B, Z, c, L), dtype=torch.bfloat16, device=dev)
+        if stream:  # the stream mode saves two fp32 numbers per row instead of the (c x L) panel
+            ly["m"] = torch.empty((1, B, Z, c), dtype=torch.float32, device=dev)
+        else:
+            ly["p"] = torch.empty((1, B, Z, c, L), dtype=torch.bfloat16, device=dev)
         ly["r"] = torch.empty((1, B, Z, c), dtype=torch.float32, device=dev)
         ly["grads"] = (torch.empty_like(ly["q"]), torch.empty_like(ly["q"]), torch.empty_like(ly["q"]))
     dvec = torch.empty((1, B, Z, c), dtype=torch.float32, device=dev)
     g_scaled = torch.empty((1, B, Z, c, A), dtype=torch.bfloat16, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
 
-    def step(tm=None):
-        for ly in layers:
+    def fwd_layer(ly):
+        if stream:
+            engine.forward_stream(ly["q"], ly["k"], ly["v"], flag=flag, out=ly["o"], rowscale=ly["r"], rowmax=ly["m"])
+        else:
             engine.forward(ly["q"], ly["k"], ly["v"], path="fused", flag=flag, out=ly["o"], panel=ly["p"],
-                           rowscale=ly["r"], timer=tm)
+                           rowscale=ly["r"])
+
+    def bwd_layer(ly, prologue=True):
+        if stream:
+            from paper_2105_13120_b200 import tensor_ops as ops_
+
+            if prologue:
+                ops_.rowdot_scale(ly["g"], ly["o"], ly["r"], out=dvec, a_scaled=g_scaled)
+            return engine.stream_backward_kernels(ly["q"], ly["k"], ly["v"], g_scaled, ly["m"], dvec, ly["grads"])
+        engine.backward(ly["q"], ly["k"], ly["v"], ly["p"], ly["g"], outputs=ly["o"], path="fused",
+                        grads=ly["grads"], dvec=dvec, rowscale=ly["r"], grad_scaled=g_scaled, prologue=prologue)
+
+    def step():
+        for ly in layers:
+            fwd_layer(ly)
         for ly in reversed(layers):
-            engine.backward(ly["q"], ly["k"], ly["v"], ly["p"], ly["g"], outputs=ly["o"], path="fused",
-                            grads=ly["grads"], dvec=dvec, rowscale=ly["r"], grad_scaled=g_scaled, timer=tm)
+            bwd_layer(ly)
 
     for _ in range(args.warmup):
         step()
@@ -367,23 +396,20 @@ def ours(args):
     from paper_2105_13120_b200 import tensor_ops as ops
 
     def launches(kind):
-        def run():
-            if kind == "fwd_factored":
+        def run_kind():
+            if kind in ("fwd_factored", "fwd_stream"):
                 for ly in layers:
-                    engine.forward(ly["q"], ly["k"], ly["v"], path="fused", flag=flag, out=ly["o"], panel=ly["p"],
-                                   rowscale=ly["r"])
+                    fwd_layer(ly)
             elif kind == "rowdot":
                 for ly in reversed(layers):
                     ops.rowdot_scale(ly["g"], ly["o"], ly["r"], out=dvec, a_scaled=g_scaled)
             else:
                 for ly in reversed(layers):
-                    engine.backward(ly["q"], ly["k"], ly["v"], ly["p"], ly["g"], outputs=ly["o"], path="fused",
-                                    grads=ly["grads"], dvec=dvec, rowscale=ly["r"], grad_scaled=g_scaled,
-                                    prologue=False)
-        return run
+                    bwd_layer(ly, prologue=False)
+        return run_kind
 
     reps = max(3, min(args.steps, 10))
-    kinds = ["fwd_factored", "rowdot", "bwd_fused"]
+    kinds = ["fwd_stream", "rowdot", "bwd_stream"] if stream else ["fwd_factored", "rowdot", "bwd_fused"]
     replays = {}
     for kind in kinds:
         fn = launches(kind)
@@ -503,7 +529,12 @@ def sampled_parity(layers, B, Z, seed, heads_per_layer=8):
             for key, val in got.items():
                 ref = want[key]
                 worst[key] = max(worst[key], float(np.linalg.norm(val - ref) / np.linalg.norm(ref)))
-            p = engine.normalized_panel(ly["p"][0, b, z], ly["r"][0, b, z]).double().cpu().numpy()
+            if "p" in ly:
+                p = engine.normalized_panel(ly["p"][0, b, z], ly["r"][0, b, z]).double().cpu().numpy()
+            else:  # stream mode: the head's panel recomputed from its saved row statistics
+                hd = lambda t: t[:, b:b + 1, z:z + 1]  # noqa: E731
+                p = engine.stream_panel(hd(ly["q"]), hd(ly["k"]), hd(ly["v"]), hd(ly["m"]).contiguous(),
+                                        hd(ly["r"]).contiguous(), 0)[0, 0].double().cpu().numpy()
             worst["probs_abs"] = max(worst["probs_abs"], float(np.max(np.abs(p - want["probs"]))))
             checked += 1
     ok = all(worst[k] <= 1e-2 for k in ("out", "dq", "dk", "dv")) and worst["probs_abs"] <= 4e-3
@@ -562,7 +593,7 @@ def e2e_public_api(args, dev):
             st = streams[i % 2]
             with torch.cuda.stream(st):
                 st.wait_event(up[set_i][i])
-                fwd = ring_attention_forward([q], [k], [v], cfg)
+                fwd = ring_attention_forward([q], [k], [v], cfg, mode=args.attn)
                 outs[0].copy_(fwd.outputs[0], non_blocking=True)
             saved.append(fwd)
         if prefetch_next:

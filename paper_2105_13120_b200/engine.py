@@ -36,7 +36,8 @@ from ._native import BF16, F32, RsaFwdExt, RsaGeom, RsaView, check, lib
 from .errors import ShapeError
 
 __all__ = ["fused_supported", "forward", "backward", "Forward", "normalized_panel", "recompute_outputs", "NULL_VIEW",
-           "KernelTimer", "StreamForward", "forward_stream", "backward_stream", "stream_panel", "stream_supported"]
+           "KernelTimer", "StreamForward", "forward_stream", "backward_stream", "stream_backward_kernels", "stream_panel",
+           "stream_supported"]
 
 NULL_VIEW = RsaView(None, 0, 0, 0, 0)
 
@@ -457,14 +458,24 @@ def backward_stream(q, k, v, grad, out, rowscale, rowmax, *, grads: tuple | None
         dq, dk, dv = grads
     with tm("rowdot"):
         dvec, gsc = ops.rowdot_scale(grad, out, rowscale, out=dvec, a_scaled=grad_scaled)
+    return stream_backward_kernels(q, k, v, gsc, rowmax, dvec, (dq, dk, dv), timer=timer)
+
+
+def stream_backward_kernels(q, k, v, grad_scaled, rowmax, dvec, grads, timer=None):
+    """The two stream-mode backward launches on prepared dO*r (``grad_scaled``) and D*r
+    (``dvec``): rsa_bwd_kv_stream into grads[1:] (bf16 or fp32), rsa_bwd_q_stream into grads[0]."""
+    n, b, z, c, a = q.shape
+    norg, ck = k.shape[0], k.shape[3]
+    dq, dk, dv = grads
+    tm = timer or _NO_TIMER
     g = _geom(n, b, z, c, a, norg * ck, 0, norg, 0 if ck == c else ck)
     L = lib()
     st = _stream(q)
     with tm("bwd_kv_stream"):
-        check(L.rsa_bwd_kv_stream(ctypes.byref(g), _view(q), _view(k), _view(v), _view(gsc), rowmax.data_ptr(),
-                                  dvec.data_ptr(), _view(dk), _view(dv), F32 if dk.dtype == torch.float32 else BF16,
-                                  0, st), "rsa_bwd_kv_stream")
+        check(L.rsa_bwd_kv_stream(ctypes.byref(g), _view(q), _view(k), _view(v), _view(grad_scaled),
+                                  rowmax.data_ptr(), dvec.data_ptr(), _view(dk), _view(dv),
+                                  F32 if dk.dtype == torch.float32 else BF16, 0, st), "rsa_bwd_kv_stream")
     with tm("bwd_q_stream"):
-        check(L.rsa_bwd_q_stream(ctypes.byref(g), _view(q), _view(k), _view(v), _view(gsc), rowmax.data_ptr(),
-                                 dvec.data_ptr(), NULL_VIEW, 0, _view(dq), st), "rsa_bwd_q_stream")
+        check(L.rsa_bwd_q_stream(ctypes.byref(g), _view(q), _view(k), _view(v), _view(grad_scaled),
+                                 rowmax.data_ptr(), dvec.data_ptr(), NULL_VIEW, 0, _view(dq), st), "rsa_bwd_q_stream")
     return dq, dk, dv

@@ -12,7 +12,12 @@ K'_d = E[:, d-block] K_d and V'_d = F[:, d-block] V_d (tcgen05 GEMMs with the
 projection shared across the B*Z heads through a stride-0 batch), the
 partials summed across ranks (the reference's N-1 ring-accumulate hops,
 :59-71, i.e. an all-reduce), then local low-rank attention softmax(Q_d K'^T /
-sqrt(A)) V'.  With every rank resident on one GPU the sum is one fp32
+sqrt(A)) V' -- for A = 64 and K, c multiples of 8 ONE stream-mode launch
+(rsa_fwd_factored_ex with key_chunk = K: scores in TMEM, probabilities in
+registers and shared memory, neither in HBM), and its backward the two
+stream kernels (rsa_bwd_kv_stream gives the cross-rank sums dK', dV' directly,
+rsa_bwd_q_stream gives dQ); other shapes take the primitive kernels (fp32 scores,
+rsa_softmax_rows).  With every rank resident on one GPU the sum is one fp32
 accumulation over the ranks' partial GEMMs (every rank gets the same total;
 the reference's totals differ only in addition grouping); across GPUs it is
 one NCCL all-reduce of the concatenated [K'; V'] buffer
@@ -30,13 +35,14 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import engine
 from . import tensor_ops as ops
 from .cluster import CommLedger, resolve_executor
 from .config import SparseAttentionConfig
-from .errors import ShapeError
+from .errors import NumericError, ShapeError
 
 __all__ = ["SparseRingForward", "SparseRingBackward", "split_projection_columns", "sparse_ring_attention_forward",
-           "sparse_ring_attention_backward", "full_length_dims"]
+           "sparse_ring_attention_backward", "full_length_dims", "low_rank_attention"]
 
 
 @dataclass
@@ -112,9 +118,10 @@ def _check_inputs(name_chunks, weights, cfg: SparseAttentionConfig):
     return out
 
 
-def _low_rank_forward(q, k, v, e, f, kdim):
-    """K' = sum_d E_d K_d, V' = sum_d F_d V_d (fp32 accumulation over ranks -- the
-    ring-accumulate / all-reduce), then P = softmax(Q K'^T / sqrt(A)) per rank."""
+def _project(q, k, v, e, f, kdim):
+    """K' = sum_d E_d K_d, V' = sum_d F_d V_d as bf16 [B][Z][K][A]: rsa_gemm with the projection
+    block shared by the B*Z heads (stride-0 batch), accumulated in fp32 over the ranks in
+    ascending order -- the reference's ring-accumulate (:59-71) when every rank is resident."""
     n, b, z, c, a = q.shape
     k_low = torch.empty((b, z, kdim, a), dtype=torch.float32, device=q.device)
     v_low = torch.empty_like(k_low)
@@ -122,11 +129,42 @@ def _low_rank_forward(q, k, v, e, f, kdim):
         cols = slice(d * c, (d + 1) * c)
         ops.matmul(e[:, cols], k[d], out=k_low, accumulate=d > 0)
         ops.matmul(f[:, cols], v[d], out=v_low, accumulate=d > 0)
-    k_low16 = k_low.to(torch.bfloat16)
-    v_low16 = v_low.to(torch.bfloat16)
+    return k_low.to(torch.bfloat16), v_low.to(torch.bfloat16)
+
+
+def _fused_ok(a: int, c: int, kdim: int) -> bool:
+    return engine.stream_supported(1, 1, 1, c, a, kdim)
+
+
+def _low_rank_stream(q, k_low16, v_low16):
+    """softmax(Q K'^T / sqrt(A)) V' as ONE stream-mode launch (rsa_fwd_factored_ex with
+    key_chunk = K, no panel): scores and probabilities never reach HBM.  Returns the
+    engine.StreamForward, or None when a row needs the two-pass treatment (flag bit 1)."""
+    res = engine.forward_stream(q, k_low16.unsqueeze(0), v_low16.unsqueeze(0))
+    status = int(res.flag.item())
+    if status & 1:
+        raise NumericError("softmax_rows requires finite inputs")
+    return None if status else res
+
+
+def _low_rank_staged(q, k_low16, v_low16):
+    """The same product through the primitive kernels (fp32 scores, rsa_softmax_rows, bf16 P):
+    shapes the fused kernels cannot tile (A != 64, K or c not a multiple of 8) and flag-bit-1 rows."""
+    a = q.shape[-1]
     scores = ops.matmul(q, k_low16.transpose(-1, -2))  # [N][B][Z][c][K] fp32
     probs = ops.softmax_rows(scores, scale=1.0 / math.sqrt(a), out_dtype=torch.bfloat16)  # NumericError
-    return k_low16, v_low16, probs
+    return probs, ops.matmul(probs, v_low16, out_dtype=torch.bfloat16)
+
+
+def low_rank_attention(q, k_low, v_low) -> torch.Tensor:
+    """Local attention of [N][B][Z][c][A] queries against the projected (B, Z, K, A) keys and
+    values (ringseq/sparse_attention.py:124-125); every row is local to its rank."""
+    k_low16, v_low16 = k_low.to(torch.bfloat16), v_low.to(torch.bfloat16)
+    if _fused_ok(q.shape[-1], q.shape[-2], k_low.shape[-2]):
+        res = _low_rank_stream(q, k_low16, v_low16)
+        if res is not None:
+            return res.out
+    return _low_rank_staged(q, k_low16, v_low16)[1]
 
 
 def sparse_ring_attention_forward(q_chunks, k_chunks, v_chunks, weights, cfg: SparseAttentionConfig, *,
@@ -145,8 +183,8 @@ def sparse_ring_attention_forward(q_chunks, k_chunks, v_chunks, weights, cfg: Sp
     q, k, v = _stack(q_chunks, dev), _stack(k_chunks, dev), _stack(v_chunks, dev)
     e = ops.to_device(weights.key_proj, dev)  # (K, L) bf16
     f = ops.to_device(weights.value_proj, dev)
-    k_low16, v_low16, probs = _low_rank_forward(q, k, v, e, f, kdim)
-    out = ops.matmul(probs, v_low16, out_dtype=torch.bfloat16)  # [N][B][Z][c][A]
+    k_low16, v_low16 = _project(q, k, v, e, f, kdim)
+    out = low_rank_attention(q, k_low16, v_low16)  # [N][B][Z][c][A]
 
     chunk, low, rows = (b, z, c, a), (b, z, kdim, a), (b, z, c, kdim)
     logs = []
@@ -186,17 +224,26 @@ def sparse_ring_attention_backward(q_chunks, k_chunks, v_chunks, weights, cfg: S
     q, k, v, g = (_stack(x, dev) for x in (q_chunks, k_chunks, v_chunks, grad_chunks))
     e = ops.to_device(weights.key_proj, dev)
     f = ops.to_device(weights.value_proj, dev)
-    k_low16, v_low16, probs = _low_rank_forward(q, k, v, e, f, kdim)
-    # cross-rank sums (fp32 over ranks in ascending order)
-    d_vlow = torch.empty((b, z, kdim, a), dtype=torch.float32, device=dev)
-    for d in range(n):
-        ops.matmul(probs[d].transpose(-1, -2), g[d], out=d_vlow, accumulate=d > 0)
-    dp = ops.matmul(g, v_low16.transpose(-1, -2))  # [N][B][Z][c][K] fp32
-    ds = ops.softmax_backward(probs, dp, 1.0 / math.sqrt(a), out_dtype=torch.bfloat16)
-    dq = ops.matmul(ds, k_low16, out_dtype=torch.bfloat16)
-    d_klow = torch.empty_like(d_vlow)
-    for d in range(n):
-        ops.matmul(ds[d].transpose(-1, -2), q[d], out=d_klow, accumulate=d > 0)
+    k_low16, v_low16 = _project(q, k, v, e, f, kdim)
+    res = _low_rank_stream(q, k_low16, v_low16) if _fused_ok(a, c, kdim) else None
+    if res is not None:
+        # fused: P recomputed on chip; the kv kernel walks every rank's query rows, so its
+        # fp32 dK' / dV' are already the cross-rank sums
+        dq, d_klow, d_vlow = engine.backward_stream(q, k_low16.unsqueeze(0), v_low16.unsqueeze(0), g, res.out,
+                                                    res.rowscale, res.rowmax, dkv_f32=True)
+        d_klow, d_vlow = d_klow[0], d_vlow[0]
+    else:
+        probs, _ = _low_rank_staged(q, k_low16, v_low16)
+        # cross-rank sums (fp32 over ranks in ascending order)
+        d_vlow = torch.empty((b, z, kdim, a), dtype=torch.float32, device=dev)
+        for d in range(n):
+            ops.matmul(probs[d].transpose(-1, -2), g[d], out=d_vlow, accumulate=d > 0)
+        dp = ops.matmul(g, v_low16.transpose(-1, -2))  # [N][B][Z][c][K] fp32
+        ds = ops.softmax_backward(probs, dp, 1.0 / math.sqrt(a), out_dtype=torch.bfloat16)
+        dq = ops.matmul(ds, k_low16, out_dtype=torch.bfloat16)
+        d_klow = torch.empty_like(d_vlow)
+        for d in range(n):
+            ops.matmul(ds[d].transpose(-1, -2), q[d], out=d_klow, accumulate=d > 0)
     d_klow16, d_vlow16 = d_klow.to(torch.bfloat16), d_vlow.to(torch.bfloat16)
     dk = torch.empty_like(q)
     dv = torch.empty_like(q)

@@ -24,49 +24,68 @@ from oracle import ringseq_np as orc
 
 
 class CpuHopKernels:
-    """float64 restatement of the per-hop kernel contracts (test double)."""
+    """float64 restatement of the per-hop kernel contracts (test double).
 
-    def new_stats(self, q, n):
-        _, b, z, c, _ = q.shape
-        return torch.empty((n, b, z, c, 2), dtype=torch.float64)
+    Same factored convention as the device kernels: the panel block of origin j holds
+    P~ = exp(s - m) with m the row's reference point (taken at hop 0, reused later), the
+    running O~ = sum P~ V and l = sum P~ finish as O = O~ / l and r = 1 / l."""
 
-    def stats(self, q, k_j, origin, seq, stats, flag):
-        s = q[0] @ k_j[0].transpose(-1, -2) / math.sqrt(q.shape[-1])
-        m = s.max(-1).values
-        stats[origin, ..., 0] = m
-        stats[origin, ..., 1] = torch.exp(s - m[..., None]).sum(-1)
-
-    def probs_pv(self, q, k_j, v_j, origin, seq, stats, n_slots, panel, o_acc, accumulate, o_out):
-        m_all = stats[:n_slots, ..., 0]
-        mx = m_all.max(0).values
-        lsum = (stats[:n_slots, ..., 1] * torch.exp(m_all - mx)).sum(0)
-        s = q[0] @ k_j[0].transpose(-1, -2) / math.sqrt(q.shape[-1])
-        p = torch.exp(s - mx[..., None]) / lsum[..., None]
-        c = q.shape[-2]
-        panel[0][..., origin * c:(origin + 1) * c] = p
-        o = p @ v_j[0]
-        o_acc[0] = o_acc[0] + o if accumulate else o
-        if o_out is not None:
-            o_out.copy_(o_acc)
-
-    def rowdot(self, grad, out):
-        return (grad * out).sum(-1)
+    def new_state(self, q):
+        _, b, z, c, a = q.shape
+        rows = (1, b, z, c)
+        return {"o_acc": torch.zeros((1, b, z, c, a), dtype=torch.float64),
+                "l_acc": torch.zeros(rows, dtype=torch.float64), "rowmax": torch.zeros(rows, dtype=torch.float64),
+                "rowscale": torch.zeros(rows, dtype=torch.float64),
+                "out": torch.zeros((1, b, z, c, a), dtype=torch.float64), "flag": torch.zeros(1, dtype=torch.int32)}
 
     @staticmethod
-    def _ds(grad, v_j, panel, dvec, origin):
-        c = v_j.shape[-2]
-        p = panel[0][..., origin * c:(origin + 1) * c]
-        dp = grad[0] @ v_j[0].transpose(-1, -2)
-        return p, p * (dp - dvec[0][..., None]) / math.sqrt(grad.shape[-1])
+    def _s(q, k_j):
+        return q[0] @ k_j[0].transpose(-1, -2) / math.sqrt(q.shape[-1])
 
-    def dkdv(self, q, v_j, grad, panel, dvec, origin, seq, dk_j, dv_j):
-        p, dsb = self._ds(grad, v_j, panel, dvec, origin)
-        dk_j[0] = dsb.transpose(-1, -2) @ q[0]
-        dv_j[0] = p.transpose(-1, -2) @ grad[0]
+    def hop_forward(self, q, k_j, v_j, origin, seq, st, first, last, panel, exact=False):
+        s = self._s(q, k_j)
+        if first and not exact:
+            st["rowmax"][0] = s.max(-1).values
+        pt = torch.exp(s - st["rowmax"][0][..., None])
+        c = q.shape[-2]
+        if panel is not None:
+            panel[0][..., origin * c:(origin + 1) * c] = pt
+        o, lsum = pt @ v_j[0], pt.sum(-1)
+        if not first:
+            o, lsum = o + st["o_acc"][0], lsum + st["l_acc"][0]
+        if last:
+            st["out"][0] = o / lsum[..., None]
+            st["rowscale"][0] = 1.0 / lsum
+        else:
+            st["o_acc"][0], st["l_acc"][0] = o, lsum
 
-    def dq(self, grad, k_j, v_j, panel, dvec, origin, seq, dq_acc, accumulate, dq_out):
-        _, dsb = self._ds(grad, v_j, panel, dvec, origin)
-        t = dsb @ k_j[0]
+    def rowdot_scale(self, grad, out, rowscale):
+        return rowscale * (grad * out).sum(-1), grad * rowscale[..., None]
+
+    def _ds(self, pt, grad_r, v_j, dvec):
+        dp = grad_r[0] @ v_j[0].transpose(-1, -2)
+        return pt * (dp - dvec[0][..., None]) / math.sqrt(grad_r.shape[-1])
+
+    def bwd_resident(self, q, k_slots, v_slots, grad_r, panel, dvec, seq, dq, dk_part, dv_part):
+        c = q.shape[-2]
+        dq.zero_()
+        for j in range(k_slots.shape[0]):
+            pt = panel[0][..., j * c:(j + 1) * c]
+            ds = self._ds(pt, grad_r, v_slots[j:j + 1], dvec)
+            dq[0] += ds @ k_slots[j]
+            dk_part[j] = ds.transpose(-1, -2) @ q[0]
+            dv_part[j] = pt.transpose(-1, -2) @ grad_r[0]
+
+    def kv_stream_hop(self, q, k_j, v_j, grad_r, rowmax, dvec, seq, origin, dk_acc, dv_acc, accumulate):
+        pt = torch.exp(self._s(q, k_j) - rowmax[0][..., None])
+        ds = self._ds(pt, grad_r, v_j, dvec)
+        dk, dv = ds.transpose(-1, -2) @ q[0], pt.transpose(-1, -2) @ grad_r[0]
+        dk_acc[0] = dk_acc[0] + dk if accumulate else dk
+        dv_acc[0] = dv_acc[0] + dv if accumulate else dv
+
+    def q_stream_hop(self, q, k_j, v_j, grad_r, rowmax, dvec, seq, origin, dq_acc, accumulate, dq_out):
+        pt = torch.exp(self._s(q, k_j) - rowmax[0][..., None])
+        t = self._ds(pt, grad_r, v_j, dvec) @ k_j[0]
         dq_acc[0] = dq_acc[0] + t if accumulate else t
         if dq_out is not None:
             dq_out.copy_(dq_acc)
@@ -78,7 +97,7 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, shape, seed, mode, overlap, results):
+def _worker(rank, world, port, shape, seed, mode, overlap, attn, results):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -89,26 +108,34 @@ def _worker(rank, world, port, shape, seed, mode, overlap, results):
         rng = orc.make_rng(seed)
         q, k, v, g = (rng.standard_normal((b, z, seq, a)) for _ in range(4))
         ch = lambda x: torch.from_numpy(orc.chunks_of(x, world)[rank][None].copy())  # noqa: E731
-        ring = SpmdRing(kernels=CpuHopKernels(), mode=mode, overlap=overlap)
+        ring = SpmdRing(kernels=CpuHopKernels(), mode=mode, overlap=overlap, attn=attn)
         out, ctx = ring.forward(ch(q), ch(k), ch(v))
         dq, dk, dv = ring.backward(ctx, ch(g))
+        st = ctx.extra["state"]
+        panel = None if ctx.panel is None else (ctx.panel[0] * st["rowscale"][0][..., None]).numpy()
         results[rank] = {
-            "out": out[0].numpy(), "panel": ctx.panel[0].numpy(),
+            "out": out[0].numpy(), "panel": panel,
             "dq": dq[0].numpy(), "dk": dk[0].numpy(), "dv": dv[0].numpy(),
             "ring": ring.ledger.devices[rank].ring_p2p_elements,
             "ar": ring.ledger.devices[rank].allreduce_elements,
+            "wire": ring.ledger.devices[rank].wire_bytes,
         }
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,mode,overlap", [(2, "reduce_scatter", True), (3, "paper", False), (2, "paper", True)])
-def test_spmd_ring_matches_oracle(world, mode, overlap):
+@pytest.mark.parametrize("world,mode,overlap,attn", [(2, "reduce_scatter", True, "panel"), (3, "paper", False, "panel"),
+                                                     (2, "paper", True, "panel"), (2, "reduce_scatter", True, "stream"),
+                                                     (3, "paper", True, "stream"), (4, "reduce_scatter", True, "stream")])
+def test_spmd_ring_matches_oracle(world, mode, overlap, attn):
+    """The ring schedule (K/V pair ring with single-pass factored hops; panel mode: cached
+    slots and a ring-free backward with reduced partials; stream mode: re-circulated K/V
+    with travelling dK/dV sums) against the oracle, ledgers in the reference convention."""
     shape = (1, 2, 6 * world, 4)
     seed = 17 + world
     mgr = mp.get_context("spawn").Manager()
     results = mgr.dict()
-    mp.start_processes(_worker, args=(world, _free_port(), shape, seed, mode, overlap, results), nprocs=world,
+    mp.start_processes(_worker, args=(world, _free_port(), shape, seed, mode, overlap, attn, results), nprocs=world,
                        join=True, start_method="spawn")
     b, z, seq, a = shape
     rng = orc.make_rng(seed)
@@ -119,13 +146,22 @@ def test_spmd_ring_matches_oracle(world, mode, overlap):
     for d in range(world):
         r = results[d]
         assert np.max(np.abs(r["out"] - outs[d])) <= 1e-12
-        assert np.max(np.abs(r["panel"] - probs[d])) <= 1e-12
+        if attn == "panel":
+            assert np.max(np.abs(r["panel"] - probs[d])) <= 1e-12
+        else:
+            assert r["panel"] is None
         assert np.max(np.abs(r["dq"] - dq[d])) <= 1e-12
         assert np.max(np.abs(r["dk"] - dk[d])) <= 1e-12
         assert np.max(np.abs(r["dv"] - dv[d])) <= 1e-12
         # forward K+V rings, backward V+K rings: 4(N-1) chunks; two all-reduces
         assert r["ring"] == ring_f + ring_b
         assert r["ar"] == ar_b
+        c_bytes = b * z * (seq // world) * a * 8  # float64 chunk
+        ring_wire = 2 * (world - 1) * c_bytes  # the forward's K/V pair ring
+        if attn == "stream":  # the backward K/V ring plus N hops of the two fp64 sums
+            assert r["wire"] == 2 * ring_wire + 2 * world * c_bytes
+        elif mode == "paper":  # all-reduce of two (N*C) partials
+            assert r["wire"] == ring_wire + 2 * (2 * world * c_bytes * (world - 1) // world)
 
 
 class CpuLinformerKernels(CpuHopKernels):

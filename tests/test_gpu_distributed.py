@@ -36,22 +36,28 @@ def _inputs(b, z, seq, a, seed):
     return [orc.bf16_round(rng.standard_normal((b, z, seq, a))) for _ in range(4)]
 
 
-def _worker(rank, world, port, shape, seed, mode, results):
+def _worker(rank, world, port, shape, seed, mode, attn, results, backend="gloo"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":  # one GPU per rank: the real NCCL device transport
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    else:  # ranks share cuda:0, hops staged through host memory over gloo
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import sys
 
         sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from paper_2105_13120_b200 import engine
         from paper_2105_13120_b200.distributed import SpmdRing
 
-        torch.cuda.set_device(0)
-        dev = torch.device("cuda", 0)
         b, z, seq, a = shape
         q, k, v, g = _inputs(b, z, seq, a, seed)
         ch = lambda x: torch.from_numpy(orc.chunks_of(x, world)[rank][None].copy()).to(dev, torch.bfloat16)  # noqa
-        ring = SpmdRing(mode=mode, transport="host")
+        ring = SpmdRing(mode=mode, transport="host" if backend == "gloo" else "device", attn=attn)
         out, ctx = ring.forward(ch(q), ch(k), ch(v))
         dq, dk, dv = ring.backward(ctx, ch(g))
         # Linformer: this rank's column blocks of E / F
@@ -64,7 +70,9 @@ def _worker(rank, world, port, shape, seed, mode, results):
         lin = ring.linformer_forward(ch(q), ch(k), ch(v), cols(e), cols(f))
         torch.cuda.synchronize()
         f64 = lambda t: t.float().cpu().numpy().astype(np.float64)  # noqa: E731
-        results[rank] = {"out": f64(out[0]), "panel": f64(ctx.panel[0]), "dq": f64(dq[0]), "dk": f64(dk[0]),
+        st = ctx.extra["state"]
+        panel = None if ctx.panel is None else f64(engine.normalized_panel(ctx.panel[0], st["rowscale"][0]))
+        results[rank] = {"out": f64(out[0]), "panel": panel, "dq": f64(dq[0]), "dk": f64(dk[0]),
                          "dv": f64(dv[0]), "lin": f64(lin[0] if lin.dim() == 5 else lin),
                          "ring": ring.ledger.devices[rank].ring_p2p_elements,
                          "flag": int(ctx.extra["flag"].item())}
@@ -76,14 +84,13 @@ def _rel(x, y):
     return np.linalg.norm(x - y) / np.linalg.norm(y)
 
 
-@pytest.mark.parametrize("world,mode,shape", [(2, "reduce_scatter", (1, 2, 256, 64)), (3, "paper", (1, 2, 384, 64)),
-                                              (2, "paper", (2, 1, 400, 64))])
-def test_spmd_ring_cuda_kernels_match_oracle(world, mode, shape):
-    seed = 40 + world
-    mgr = mp.get_context("spawn").Manager()
-    results = mgr.dict()
-    mp.start_processes(_worker, args=(world, _free_port(), shape, seed, mode, results), nprocs=world, join=True,
-                       start_method="spawn")
+SPMD_CASES = [(2, "reduce_scatter", "panel", (1, 2, 256, 64)), (3, "paper", "panel", (1, 2, 384, 64)),
+              (2, "paper", "panel", (2, 1, 400, 64)), (2, "reduce_scatter", "panel", (1, 2, 2048, 64)),
+              (2, "reduce_scatter", "stream", (1, 2, 256, 64)), (3, "paper", "stream", (2, 1, 384, 64)),
+              (2, "paper", "stream", (1, 2, 2048, 64))]
+
+
+def _check_spmd(world, mode, attn, shape, seed, results):
     b, z, seq, a = shape
     q, k, v, g = _inputs(b, z, seq, a, seed)
     ch = lambda x: orc.chunks_of(x, world)  # noqa: E731
@@ -97,10 +104,38 @@ def test_spmd_ring_cuda_kernels_match_oracle(world, mode, shape):
         r = results[d]
         assert r["flag"] == 0
         assert _rel(r["out"], outs[d]) <= 1e-2
-        assert np.max(np.abs(r["panel"] - probs[d])) <= 4e-3
+        if attn == "panel":
+            assert np.max(np.abs(r["panel"] - probs[d])) <= 4e-3
         for name, want in (("dq", dq[d]), ("dk", dk[d]), ("dv", dv[d]), ("lin", lin[d])):
             assert _rel(r[name], want) <= 1e-2, (d, name, _rel(r[name], want))
         assert r["ring"] == 4 * (world - 1) * b * z * (seq // world) * a + 2 * (world - 1) * b * z * 32 * a
+
+
+@pytest.mark.parametrize("world,mode,attn,shape", SPMD_CASES)
+def test_spmd_ring_cuda_kernels_match_oracle(world, mode, attn, shape):
+    """SpmdRing with its real kernels: the K/V pair ring with one rsa_fwd_factored_ex per hop;
+    panel mode's ring-free backward over the cached slots (rsa_bwd_fused for c <= 512, else
+    rsa_bwd_dkdv + rsa_bwd_dq) with reduced partials; stream mode's re-circulated K/V with
+    travelling dK/dV sums (rsa_bwd_kv_stream / rsa_bwd_q_stream per hop)."""
+    seed = 40 + world
+    mgr = mp.get_context("spawn").Manager()
+    results = mgr.dict()
+    mp.start_processes(_worker, args=(world, _free_port(), shape, seed, mode, attn, results), nprocs=world, join=True,
+                       start_method="spawn")
+    _check_spmd(world, mode, attn, shape, seed, results)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs for the NCCL device transport")
+@pytest.mark.parametrize("mode,attn", [("reduce_scatter", "panel"), ("paper", "panel"), ("reduce_scatter", "stream")])
+def test_spmd_ring_nccl_two_gpus(mode, attn):
+    """The product transport: NCCL send/recv of device buffers between two GPUs, the NCCL
+    reduce-scatter / all-reduce of the dK/dV partials, and the Linformer all-reduce."""
+    world, shape, seed = 2, (1, 2, 512, 64), 90
+    mgr = mp.get_context("spawn").Manager()
+    results = mgr.dict()
+    mp.start_processes(_worker, args=(world, _free_port(), shape, seed, mode, attn, results, "nccl"), nprocs=world,
+                       join=True, start_method="spawn")
+    _check_spmd(world, mode, attn, shape, seed, results)
 
 
 def _peer_worker(rank, world, port, shape, seed, results):
