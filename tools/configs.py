@@ -39,19 +39,60 @@ def timed(fn, iters, warmup=2):
     return statistics.median(ts)
 
 
-def rsa_layer(n, b, z, seq, a, iters, dev):
+def layer_closure(q, k, v, g, mode, single_pass=None):
+    """One RSA layer fwd+bwd on preallocated buffers (graph-capturable)."""
+    n, b, z, c, a = q.shape
+    dev = q.device
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    out = torch.empty_like(q)
+    rs = torch.empty((n, b, z, c), dtype=torch.float32, device=dev)
+    grads = tuple(torch.empty_like(q) for _ in range(3))
+    dvec = torch.empty((n, b, z, c), dtype=torch.float32, device=dev)
+    gs = torch.empty_like(q)
+    if mode == "stream":
+        m = torch.empty_like(rs)
+
+        def step():
+            engine.forward_stream(q, k, v, flag=flag, out=out, rowscale=rs, rowmax=m)
+            engine.backward_stream(q, k, v, g, out, rs, m, grads=grads, dvec=dvec, grad_scaled=gs)
+        return step
+    panel = torch.empty((n, b, z, c, n * c), dtype=torch.bfloat16, device=dev)
+
+    def step():
+        engine.forward(q, k, v, path="fused", flag=flag, out=out, panel=panel, rowscale=rs)
+        engine.backward(q, k, v, panel, g, outputs=out, rowscale=rs, path="fused", grads=grads, dvec=dvec,
+                        grad_scaled=gs, single_pass=single_pass)
+    return step
+
+
+def graphed(fn):
+    fn()
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        fn()
+    return gr.replay
+
+
+def rsa_layer(n, b, z, seq, a, iters, dev, graph=False):
     c = seq // n
     gen = torch.Generator(device=dev).manual_seed(seq)
     q, k, v, g = (torch.randn((n, b, z, c, a), generator=gen, device=dev).to(torch.bfloat16) for _ in range(4))
-
-    def step():
-        fwd = engine.forward(q, k, v, path="fused")
-        engine.backward(q, k, v, fwd.panel, g, outputs=fwd.out, rowscale=fwd.rowscale, path="fused")
-
-    ms = timed(step, iters)
-    return {"ms_per_layer_fwd_bwd": ms, "tokens_per_s": b * seq / (ms / 1e3),
-            "fused_backward": "rsa_bwd_fused" if engine.single_pass_supported(n, b, z, c, a) else
-            "rsa_bwd_dkdv + rsa_bwd_dq"}
+    res = {}
+    variants = [("panel", None), ("stream", None)]
+    if engine.single_pass_supported(n, b, z, c, a):
+        variants = [("panel", True), ("panel", False), ("stream", None)]
+    for mode, sp in variants:
+        name = mode if sp is None else f"{mode}_{'bwd_fused' if sp else 'bwd_dkdv_dq'}"
+        fn = layer_closure(q, k, v, g, mode, sp)
+        ms = timed(fn, iters)
+        res[name] = {"ms_per_layer_fwd_bwd": ms, "tokens_per_s": b * seq / (ms / 1e3)}
+        if graph:
+            ms_g = timed(graphed(fn), iters)
+            res[name]["graph_ms_per_layer_fwd_bwd"] = ms_g
+            res[name]["graph_tokens_per_s"] = b * seq / (ms_g / 1e3)
+        torch.cuda.empty_cache()
+    return res
 
 
 def linformer(n, b, z, seq, a, kp, iters, dev):
@@ -66,8 +107,21 @@ def linformer(n, b, z, seq, a, kp, iters, dev):
     cfg = SparseAttentionConfig(base=base, proj_dim=kp)
     fwd_ms = timed(lambda: sparse_ring_attention_forward(ch[0], ch[1], ch[2], w, cfg), iters)
     bwd_ms = timed(lambda: sparse_ring_attention_backward(ch[0], ch[1], ch[2], w, cfg, ch[3]), iters)
-    return {"ms_fwd": fwd_ms, "ms_bwd_incl_recompute": bwd_ms, "tokens_per_s_fwd": b * seq / (fwd_ms / 1e3),
-            "tokens_per_s_fwd_bwd": b * seq / ((fwd_ms + bwd_ms) / 1e3)}
+    # the device path without the list API's chunk stacking: projections, then the fused attention
+    from paper_2105_13120_b200 import sparse_attention as spm
+
+    q, k, v = (torch.stack(x) for x in ch[:3])
+    proj_ms = timed(lambda: spm._project(q, k, v, w.key_proj, w.value_proj, kp), iters)
+    k16, v16 = spm._project(q, k, v, w.key_proj, w.value_proj, kp)
+    attn_ms = timed(lambda: spm.low_rank_attention(q, k16, v16), iters)
+    # algorithmic HBM bytes of the forward: read q, k, v and write O (bf16), E/F blocks
+    fwd_bytes = 4 * 2 * b * z * seq * a + 2 * 2 * kp * seq
+    return {"ms_fwd_api": fwd_ms, "ms_bwd_api_incl_recompute": bwd_ms,
+            "tokens_per_s_fwd_api": b * seq / (fwd_ms / 1e3),
+            "tokens_per_s_fwd_bwd_api": b * seq / ((fwd_ms + bwd_ms) / 1e3),
+            "ms_fwd_projections": proj_ms, "ms_fwd_low_rank_attention": attn_ms,
+            "fwd_device_ms": proj_ms + attn_ms, "fwd_alg_bytes": fwd_bytes,
+            "fwd_hbm_frac": fwd_bytes / ((proj_ms + attn_ms) / 1e3) / 6539.9e9}
 
 
 def main():
@@ -77,7 +131,8 @@ def main():
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     res = {}
-    res["config1"] = {"shape": "B4 Z12 A64 L512, N=4 logical ranks", **rsa_layer(4, 4, 12, 512, 64, args.iters, dev)}
+    res["config1"] = {"shape": "B4 Z12 A64 L512, N=4 logical ranks",
+                      **rsa_layer(4, 4, 12, 512, 64, max(args.iters, 20), dev, graph=True)}
     print(json.dumps(res["config1"]), flush=True)
     res["config4"] = {"shape": "BERT-large attention Z16 A64 L16384 B4, N=8 logical ranks (c=2048)",
                       **rsa_layer(8, 4, 16, 16384, 64, args.iters, dev)}
