@@ -222,13 +222,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kv_stream_kernel(const __grid
         uint32_t w[32];
         mbar_wait(s_full, sq.i & 1);
         tc_fence_after();
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          float v[32];
+        {  // both 32-column loads in flight before one wait: TMEM loads are latency-bound
+          float v[64];
           __syncwarp();
-          tmem_ld32(tmem + lane_base + KS_COL_S + half * 64 + cc * 32, v);
+          tmem_ld32(tmem + lane_base + KS_COL_S + half * 64, v);
+          tmem_ld32(tmem + lane_base + KS_COL_S + half * 64 + 32, v + 32);
           tmem_ld_wait();
-          exp2_pack32(v, nvalid - cc * 32, sl, msl, w + cc * 16);
+          exp2_pack32(v, nvalid, sl, msl, w);
+          exp2_pack32(v + 32, nvalid - 32, sl, msl, w + 16);
         }
         tc_fence_before();
         __syncwarp();
@@ -248,14 +249,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kv_stream_kernel(const __grid
         mbar_wait(&dp_full[db], dpq.phase(2));
         tc_fence_after();
         const uint64_t nd = neg_pair(dval);
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          float dp[32];
+        {
+          float dp[64];
           __syncwarp();
-          tmem_ld32(tmem + lane_base + KS_COL_DP + db * TK + half * 64 + cc * 32, dp);
+          tmem_ld32(tmem + lane_base + KS_COL_DP + db * TK + half * 64, dp);
+          tmem_ld32(tmem + lane_base + KS_COL_DP + db * TK + half * 64 + 32, dp + 32);
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) w[cc * 16 + e] = ds_pair(w[cc * 16 + e], dp[2 * e], dp[2 * e + 1], nd);
+          for (int e = 0; e < 32; ++e) w[e] = ds_pair(w[e], dp[2 * e], dp[2 * e + 1], nd);
         }
         tc_fence_before();
         __syncwarp();
@@ -451,13 +452,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_q_stream_kernel(const __grid_
         uint32_t w[32];
         mbar_wait(s_full, sq.i & 1);
         tc_fence_after();
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          float v[32];
+        {  // both 32-column loads in flight before one wait: TMEM loads are latency-bound
+          float v[64];
           __syncwarp();
-          tmem_ld32(tmem + lane_base + QS_COL_S + half * 64 + cc * 32, v);
+          tmem_ld32(tmem + lane_base + QS_COL_S + half * 64, v);
+          tmem_ld32(tmem + lane_base + QS_COL_S + half * 64 + 32, v + 32);
           tmem_ld_wait();
-          exp2_pack32(v, nvalid - cc * 32, sl, msl, w + cc * 16);
+          exp2_pack32(v, nvalid, sl, msl, w);
+          exp2_pack32(v + 32, nvalid - 32, sl, msl, w + 16);
         }
         tc_fence_before();
         __syncwarp();
@@ -466,14 +468,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_q_stream_kernel(const __grid_
         const uint32_t db = dpq.slot(2);
         mbar_wait(&dp_full[db], dpq.phase(2));
         tc_fence_after();
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          float dp[32];
+        {
+          float dp[64];
           __syncwarp();
-          tmem_ld32(tmem + lane_base + QS_COL_DP + db * TK + half * 64 + cc * 32, dp);
+          tmem_ld32(tmem + lane_base + QS_COL_DP + db * TK + half * 64, dp);
+          tmem_ld32(tmem + lane_base + QS_COL_DP + db * TK + half * 64 + 32, dp + 32);
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) w[cc * 16 + e] = ds_pair(w[cc * 16 + e], dp[2 * e], dp[2 * e + 1], nd);
+          for (int e = 0; e < 32; ++e) w[e] = ds_pair(w[e], dp[2 * e], dp[2 * e + 1], nd);
         }
         tc_fence_before();
         __syncwarp();
