@@ -26,6 +26,7 @@ N*C elements backward.  Multi-GPU rings (one process per GPU, NCCL) live in
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import torch
@@ -69,6 +70,27 @@ class RingAttentionBackward:
     ledger: CommLedger
 
 
+RESULTS_ENV_VAR = "RSA_B200_RESULTS"
+RESULT_MODES = ("device", "numpy")
+
+
+def _results_mode(results: str | None) -> str:
+    """'device' (CUDA bf16 tensors, the default) or 'numpy' (float64 ndarrays, as the
+    reference returns them): argument, then $RSA_B200_RESULTS, then 'device'."""
+    mode = results or os.environ.get(RESULTS_ENV_VAR) or "device"
+    if mode not in RESULT_MODES:
+        raise ValueError(f"results must be one of {RESULT_MODES}, got {mode!r}")
+    return mode
+
+
+def _host(t):
+    return t.double().cpu().numpy()
+
+
+def _out_list(stacked, n, mode):
+    return [_host(stacked[d]) if mode == "numpy" else stacked[d] for d in range(n)]
+
+
 class ProbPanels(list):
     """The ``probs`` list returned by the forward: one (B, Z, c, L) panel per rank.
 
@@ -97,6 +119,7 @@ class ProbPanels(list):
         # a caller that replaces a panel (probs[d] = X) gets reference semantics: the
         # backward then uses the given panels, not the saved stack
         self.dirty = False
+        self.as_numpy = False  # results="numpy": items materialise as float64 ndarrays
 
     def __setitem__(self, i, value):
         list.__setitem__(self, i, value)
@@ -108,6 +131,8 @@ class ProbPanels(list):
             scale = None if self.rowscale is None else self.rowscale[d]
             item = engine.normalized_panel(self.stacked[d], scale, torch.float32 if scale is not None else
                                            self.stacked.dtype)
+            if self.as_numpy:
+                item = _host(item)
             list.__setitem__(self, d, item)
         return item
 
@@ -141,13 +166,21 @@ class StreamPanels(ProbPanels):
         self.panel_shape = tuple(panel_shape)
         self.inputs = inputs
         self.dirty = False
+        self.as_numpy = False
 
     def _get(self, d: int):
         item = list.__getitem__(self, d)
         if item is None:
             item = engine.stream_panel(self.q, self.k, self.v, self.rowmax, self.rowscale, d)
+            if self.as_numpy:
+                item = _host(item)
             list.__setitem__(self, d, item)
         return item
+
+
+def _panels(p: ProbPanels, rmode: str) -> ProbPanels:
+    p.as_numpy = rmode == "numpy"
+    return p
 
 
 def _shape_of(x) -> tuple:
@@ -291,7 +324,7 @@ MODES = ("panel", "stream")
 
 
 def ring_attention_forward(q_chunks, k_chunks, v_chunks, cfg: AttentionConfig, *, executor: str | None = None,
-                           path: str = "auto", mode: str = "panel") -> RingAttentionForward:
+                           path: str = "auto", mode: str = "panel", results: str | None = None) -> RingAttentionForward:
     """Distributed attention forward over per-rank (B, Z, L/N, A) chunks.
 
     ringseq/ring_attention.py:124-147.  ``path`` ('auto' | 'fused' | 'staged')
@@ -302,7 +335,11 @@ def ring_attention_forward(q_chunks, k_chunks, v_chunks, cfg: AttentionConfig, *
     query row; ``probs`` is then a ``StreamPanels`` list that recomputes any rank's
     panel on access, and the backward recomputes probability tiles on chip -- memory
     grows as L/N, so the trainable length grows linearly with the rank count.
+
+    ``results="numpy"`` (or $RSA_B200_RESULTS=numpy) returns float64 ndarrays, as the
+    reference does; the default returns CUDA bf16 tensors (no host round trip).
     """
+    rmode = _results_mode(results)
     if mode not in MODES:
         raise ValueError(f"unknown mode {mode!r}; expected one of {MODES}")
     resolve_executor(executor)
@@ -319,27 +356,28 @@ def ring_attention_forward(q_chunks, k_chunks, v_chunks, cfg: AttentionConfig, *
             raise ShapeError(f"stream mode needs head_size 64 and chunk_len % 8 == 0 (got {cfg.head_size}, "
                              f"{cfg.chunk_len})")
         res = _stream_checked(q, k, v)
-        return RingAttentionForward(
-            outputs=[res.out[d] for d in range(cfg.num_devices)],
-            probs=StreamPanels(q, k, v, res.out, res.rowscale, res.rowmax, saved, cfg.panel_shape()),
-            ledger=forward_ledger(cfg),
-        )
+        probs = StreamPanels(q, k, v, res.out, res.rowscale, res.rowmax, saved, cfg.panel_shape())
+        probs.as_numpy = rmode == "numpy"
+        return RingAttentionForward(outputs=_out_list(res.out, cfg.num_devices, rmode), probs=probs,
+                                    ledger=forward_ledger(cfg))
     out, panel, rowscale, _ = _forward_checked(q, k, v, path)
     return RingAttentionForward(
-        outputs=[out[d] for d in range(cfg.num_devices)],
-        probs=ProbPanels(panel, out, rowscale, saved),
+        outputs=_out_list(out, cfg.num_devices, rmode),
+        probs=_panels(ProbPanels(panel, out, rowscale, saved), rmode),
         ledger=forward_ledger(cfg),
     )
 
 
 def ring_attention_backward(q_chunks, k_chunks, v_chunks, probs, grad_chunks, cfg: AttentionConfig, *,
-                            executor: str | None = None, path: str = "auto") -> RingAttentionBackward:
+                            executor: str | None = None, path: str = "auto",
+                            results: str | None = None) -> RingAttentionBackward:
     """Gradients of ring_attention_forward w.r.t. the q/k/v chunks.
 
     ringseq/ring_attention.py:150-217.  ``probs`` are the panels saved by the
     forward (StateError when missing, ShapeError when mis-shaped).
     """
     resolve_executor(executor)
+    rmode = _results_mode(results)
     shape = cfg.chunk_shape()
     q_chunks = _check_chunks("q_chunks", q_chunks, cfg, shape)
     k_chunks = _check_chunks("k_chunks", k_chunks, cfg, shape)
@@ -368,8 +406,8 @@ def ring_attention_backward(q_chunks, k_chunks, v_chunks, probs, grad_chunks, cf
     if isinstance(probs, StreamPanels) and not probs.dirty and q_saved and k_saved and v_saved:
         # the forward's own state: recompute probability tiles on chip, no panel anywhere
         dq, dk, dv = engine.backward_stream(q, k, v, g, probs.outputs, probs.rowscale, probs.rowmax)
-        return RingAttentionBackward(grad_q=[dq[d] for d in range(n)], grad_k=[dk[d] for d in range(n)],
-                                     grad_v=[dv[d] for d in range(n)], ledger=backward_ledger(cfg))
+        return RingAttentionBackward(grad_q=_out_list(dq, n, rmode), grad_k=_out_list(dk, n, rmode),
+                                     grad_v=_out_list(dv, n, rmode), ledger=backward_ledger(cfg))
     panel = _stack(probs, dev)
     own = isinstance(probs, ProbPanels) and panel is probs.stacked
     # the forward's O = P V is reused for D = rowsum(dP * P) = rowsum(dO * O) only when the
@@ -381,9 +419,9 @@ def ring_attention_backward(q_chunks, k_chunks, v_chunks, probs, grad_chunks, cf
         outputs = None
     dq, dk, dv = engine.backward(q, k, v, panel, g, outputs=outputs, rowscale=rowscale, path=path)
     return RingAttentionBackward(
-        grad_q=[dq[d] for d in range(n)],
-        grad_k=[dk[d] for d in range(n)],
-        grad_v=[dv[d] for d in range(n)],
+        grad_q=_out_list(dq, n, rmode),
+        grad_k=_out_list(dk, n, rmode),
+        grad_v=_out_list(dv, n, rmode),
         ledger=backward_ledger(cfg),
     )
 
@@ -414,7 +452,7 @@ def _layer_forward(x, ws, cfg: AttentionConfig, path: str):
 
 
 def sequence_parallel_attention(x_chunks, weights, cfg: AttentionConfig, *, executor: str | None = None,
-                                path: str = "auto"):
+                                path: str = "auto", results: str | None = None):
     """Multi-head attention layer on sequence-partitioned (B, L/N, H) inputs.
 
     ringseq/ring_attention.py:220-241: replicated projections are local
@@ -428,7 +466,7 @@ def sequence_parallel_attention(x_chunks, weights, cfg: AttentionConfig, *, exec
     x = _stack(x_chunks, dev)  # [N][B][c][H]
     _, _, _, res = _layer_forward(x, ws, cfg, path)
     y = ops.matmul(_merge_heads(res.out), ws[3])
-    return [y[d] for d in range(cfg.num_devices)], forward_ledger(cfg)
+    return _out_list(y, cfg.num_devices, _results_mode(results)), forward_ledger(cfg)
 
 
 def sequence_parallel_attention_backward(x_chunks, weights, cfg: AttentionConfig, grad_chunks, *,

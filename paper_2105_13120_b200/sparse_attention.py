@@ -168,7 +168,7 @@ def low_rank_attention(q, k_low, v_low) -> torch.Tensor:
 
 
 def sparse_ring_attention_forward(q_chunks, k_chunks, v_chunks, weights, cfg: SparseAttentionConfig, *,
-                                  executor: str | None = None) -> SparseRingForward:
+                                  executor: str | None = None, results: str | None = None) -> SparseRingForward:
     """Projected attention on sequence-partitioned (B, Z, L/N, A) chunks (ringseq/sparse_attention.py:74-133)."""
     resolve_executor(executor)
     base = cfg.base
@@ -195,7 +195,9 @@ def sparse_ring_attention_forward(q_chunks, k_chunks, v_chunks, weights, cfg: Sp
         logs.append(log)
         if n > 1:
             ledger.record_ring_send(d, 2 * (n - 1) * b * z * kdim * a)
-    return SparseRingForward(outputs=[out[d] for d in range(n)], shape_logs=logs, ledger=ledger)
+    from .ring_attention import _out_list, _results_mode
+
+    return SparseRingForward(outputs=_out_list(out, n, _results_mode(results)), shape_logs=logs, ledger=ledger)
 
 
 def sparse_ring_attention_backward(q_chunks, k_chunks, v_chunks, weights, cfg: SparseAttentionConfig,
