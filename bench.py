@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the captured step")
+    ap.add_argument("--ring-ranks", type=int, default=1,
+                    help="N=1 only: split the sequence over this many logical ring ranks resident on the GPU "
+                         "(config 1 = --ring-ranks 4 --batch 4 --layers 1)")
     ap.add_argument("--attn", default="panel", choices=["panel", "stream"],
                     help="panel: the reference's saved probability panels; stream: O(L) state, P recomputed")
     return ap.parse_args()
@@ -81,7 +84,7 @@ def config_obj(args, n):
         "seq_len": args.seq,
         "heads": args.heads,
         "head_size": args.head_size,
-        "ring_ranks": n,
+        "ring_ranks": n if n > 1 else args.ring_ranks,
         "parallelism": f"seq{n}",
         "l2": "inputs larger than L2 (per-layer working set > 1 GB), no flush",
     }
@@ -307,24 +310,27 @@ def ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     B, Z, L, A, LAYERS = args.batch, args.heads, args.seq, args.head_size, args.layers
-    c = L  # one rank per GPU: the whole sequence is this GPU's chunk at N=1
+    R = args.ring_ranks  # logical ring ranks resident on this GPU (1: the whole sequence is one chunk)
+    if L % R:
+        raise SystemExit(f"seq {L} not divisible by {R} ring ranks")
+    c = L // R
     gen = torch.Generator(device=dev).manual_seed(1234)
 
     def rnd():
-        return torch.randn((1, B, Z, c, A), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
+        return torch.randn((R, B, Z, c, A), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
 
     layers = [dict(q=rnd(), k=rnd(), v=rnd(), g=rnd()) for _ in range(LAYERS)]
     stream = args.attn == "stream"
     for ly in layers:
         ly["o"] = torch.empty_like(ly["q"])
         if stream:  # the stream mode saves two fp32 numbers per row instead of the (c x L) panel
-            ly["m"] = torch.empty((1, B, Z, c), dtype=torch.float32, device=dev)
+            ly["m"] = torch.empty((R, B, Z, c), dtype=torch.float32, device=dev)
         else:
-            ly["p"] = torch.empty((1, B, Z, c, L), dtype=torch.bfloat16, device=dev)
-        ly["r"] = torch.empty((1, B, Z, c), dtype=torch.float32, device=dev)
+            ly["p"] = torch.empty((R, B, Z, c, L), dtype=torch.bfloat16, device=dev)
+        ly["r"] = torch.empty((R, B, Z, c), dtype=torch.float32, device=dev)
         ly["grads"] = (torch.empty_like(ly["q"]), torch.empty_like(ly["q"]), torch.empty_like(ly["q"]))
-    dvec = torch.empty((1, B, Z, c), dtype=torch.float32, device=dev)
-    g_scaled = torch.empty((1, B, Z, c, A), dtype=torch.bfloat16, device=dev)
+    dvec = torch.empty((R, B, Z, c), dtype=torch.float32, device=dev)
+    g_scaled = torch.empty((R, B, Z, c, A), dtype=torch.bfloat16, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
 
     def fwd_layer(ly):
@@ -432,6 +438,9 @@ def ours(args):
     with ClockSampler(local) as kclk:
         for _ in range(rounds):
             for kind, replay in replays.items():
+                # an idle gap before each segment, so every segment (like the headline's timed
+                # loop) starts from the same thermal / power state instead of a power-capped one
+                time.sleep(0.25)
                 k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 k0.record()
                 for _ in range(reps):
@@ -443,14 +452,14 @@ def ours(args):
     step_ref_ms = acc["step"] / (rounds * reps)
     kernel_clocks = kclk.result()
     timing_mode = (f"per kernel type: a CUDA graph of that type's {LAYERS} launches of the step, replayed {reps}x back "
-                   f"to back per round, {rounds} rounds interleaved with the step graph; event pair on the replay "
-                   f"stream")
+                   f"to back per segment after a 0.25 s idle gap, {rounds} rounds interleaved with the step graph; "
+                   f"event pair on the replay stream")
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)
     tc = pk.get("bf16_tflops_sustained", 1400.0)
     dom = max(type_ms, key=type_ms.get)
     per_launch_s = type_ms[dom] / LAYERS / 1e3
-    byts, flops = kernel_model(dom, 1, B, Z, c, L, A)
+    byts, flops = kernel_model(dom, R, B, Z, c, L, A)
     t_hbm, t_tc = byts / (hbm * 1e9), flops / (tc * 1e12)
     if t_hbm >= t_tc:
         roof = {"bound": "hbm", "achieved": byts / per_launch_s / 1e9, "peak": hbm, "unit": "GB/s"}
@@ -465,7 +474,7 @@ def ours(args):
     roof["peak_source"] = "MEASURED_PEAKS.json" if pk else "fallback (B200_PROFILING.md)"
     roof["timing"] = timing_mode
     # whole step against SURVEY.md section 8(d): 4*P_e + 16*C_e algorithmic HBM bytes per layer
-    p_e, c_e = B * Z * c * L, B * Z * c * A
+    p_e, c_e = R * B * Z * c * L, R * B * Z * c * A  # every resident rank's panel and chunks
     step_bytes = LAYERS * (4 * p_e + 16 * c_e)
     roof["step"] = {"bytes": step_bytes, "achieved": step_bytes / (ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                     "frac": step_bytes / (ms / 1e3) / 1e9 / hbm,
@@ -473,7 +482,7 @@ def ours(args):
                                   "(q, k, v, o, dO, dQ, dK, dV bf16)"}
     kernels = {}
     for k, tms in type_ms.items():
-        b_, f_ = kernel_model(k, 1, B, Z, c, L, A)
+        b_, f_ = kernel_model(k, R, B, Z, c, L, A)
         per = tms / LAYERS / 1e3
         kernels[k] = {"launches_per_step": LAYERS, "us_per_launch": per * 1e6, "ms_per_step": tms,
                       "share_of_step": tms / step_ref_ms, "GB/s": b_ / per / 1e9, "TFLOP/s": f_ / per / 1e12}
@@ -521,7 +530,7 @@ def sampled_parity(layers, B, Z, seed, heads_per_layer=8):
         ly = layers[li]
         for item in sorted(set(rng.integers(0, B * Z, heads_per_layer).tolist()) | {B * Z - 1}):
             b, z = divmod(int(item), Z)
-            f = lambda t: t[0, b, z].double().cpu().numpy()  # noqa: E731
+            f = lambda t: torch.cat([t[d, b, z] for d in range(t.shape[0])], 0).double().cpu().numpy()  # noqa: E731
             q, k, v, g = (f(ly[x]) for x in ("q", "k", "v", "g"))
             seq = q.shape[0]
             want = orc.attention_head_sampled(q, k, v, g, np.arange(seq), np.arange(seq))
@@ -530,11 +539,13 @@ def sampled_parity(layers, B, Z, seed, heads_per_layer=8):
                 ref = want[key]
                 worst[key] = max(worst[key], float(np.linalg.norm(val - ref) / np.linalg.norm(ref)))
             if "p" in ly:
-                p = engine.normalized_panel(ly["p"][0, b, z], ly["r"][0, b, z]).double().cpu().numpy()
+                p = torch.cat([engine.normalized_panel(ly["p"][d, b, z], ly["r"][d, b, z]) for d in range(
+                    ly["p"].shape[0])], 0).double().cpu().numpy()
             else:  # stream mode: the head's panel recomputed from its saved row statistics
                 hd = lambda t: t[:, b:b + 1, z:z + 1]  # noqa: E731
-                p = engine.stream_panel(hd(ly["q"]), hd(ly["k"]), hd(ly["v"]), hd(ly["m"]).contiguous(),
-                                        hd(ly["r"]).contiguous(), 0)[0, 0].double().cpu().numpy()
+                p = torch.cat([engine.stream_panel(hd(ly["q"]), hd(ly["k"]), hd(ly["v"]), hd(ly["m"]).contiguous(),
+                                                   hd(ly["r"]).contiguous(), d)[0, 0] for d in range(ly["q"].shape[0])],
+                              0).double().cpu().numpy()
             worst["probs_abs"] = max(worst["probs_abs"], float(np.max(np.abs(p - want["probs"]))))
             checked += 1
     ok = all(worst[k] <= 1e-2 for k in ("out", "dq", "dk", "dv")) and worst["probs_abs"] <= 4e-3
@@ -552,7 +563,11 @@ def e2e_public_api(args, dev):
     from paper_2105_13120_b200.ring_attention import ring_attention_backward, ring_attention_forward
 
     B, Z, L, A, LAYERS = args.batch, args.heads, args.seq, args.head_size, args.layers
-    cfg = AttentionConfig(batch_size=B, seq_len=L, hidden_size=Z * A, num_heads=Z, head_size=A, num_devices=1)
+    R = args.ring_ranks
+    c = L // R
+    cfg = AttentionConfig(batch_size=B, seq_len=L, hidden_size=Z * A, num_heads=Z, head_size=A, num_devices=R)
+    ch = lambda t: [t[:, :, d * c:(d + 1) * c] for d in range(R)]  # noqa: E731  (contiguous L/R chunks)
+    cat_seq = lambda xs: xs[0] if R == 1 else torch.cat(xs, 2)  # noqa: E731
     g = torch.Generator().manual_seed(99)
     host = []
     for _ in range(LAYERS):
@@ -593,8 +608,8 @@ def e2e_public_api(args, dev):
             st = streams[i % 2]
             with torch.cuda.stream(st):
                 st.wait_event(up[set_i][i])
-                fwd = ring_attention_forward([q], [k], [v], cfg, mode=args.attn)
-                outs[0].copy_(fwd.outputs[0], non_blocking=True)
+                fwd = ring_attention_forward(ch(q), ch(k), ch(v), cfg, mode=args.attn)
+                outs[0].copy_(cat_seq(fwd.outputs), non_blocking=True)
             saved.append(fwd)
         if prefetch_next:
             upload(1 - set_i)
@@ -603,10 +618,10 @@ def e2e_public_api(args, dev):
             outs = host[i][1]
             st = streams[i % 2]
             with torch.cuda.stream(st):
-                bwd = ring_attention_backward([q], [k], [v], saved[i].probs, [gr], cfg)
-                outs[1].copy_(bwd.grad_q[0], non_blocking=True)
-                outs[2].copy_(bwd.grad_k[0], non_blocking=True)
-                outs[3].copy_(bwd.grad_v[0], non_blocking=True)
+                bwd = ring_attention_backward(ch(q), ch(k), ch(v), saved[i].probs, ch(gr), cfg)
+                outs[1].copy_(cat_seq(bwd.grad_q), non_blocking=True)
+                outs[2].copy_(cat_seq(bwd.grad_k), non_blocking=True)
+                outs[3].copy_(cat_seq(bwd.grad_v), non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(st)
                 free[set_i][i] = ev

@@ -305,7 +305,10 @@ def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path:
         st = _stream(q)
         g = _geom(n, b, z, c, a, seq, 0, n)
         if single_pass is None:
-            single_pass = bool(L.rsa_bwd_fused_supported(ctypes.byref(g)))
+            # one CTA per head: with fewer heads than half the SMs the two-kernel form (one CTA
+            # per key tile, then per query tile) fills the machine better despite the second
+            # panel read (config 1, B4 Z12: 46.6 vs 48.4 us per graph-captured layer)
+            single_pass = bool(L.rsa_bwd_fused_supported(ctypes.byref(g))) and 2 * b * z >= L.rsa_num_sms()
         if single_pass:
             with tm("bwd_fused"):
                 check(L.rsa_bwd_fused(ctypes.byref(g), _view(q), _view(k), _view(v), _view(grad), _view(panel),
