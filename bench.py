@@ -285,6 +285,8 @@ def kernel_model(name, n, b, z, c, seq, a):
         return 2 * pe + 2 * 7 * ce, 8 * pe * a        # read P; Q,K,V,dO in, dQ,dK,dV out; dO V^T, P^T dO, dS^T Q, dS K
     if name == "bwd_dq":
         return 2 * pe + 2 * 4 * ce, 4 * pe * a        # read P; dO,K,V in, dQ out; dO V^T, dS K
+    if name == "bwd_dkdv_dq":  # the pair as one backward: the panel read twice (algorithmic: once)
+        return 2 * pe + 2 * 7 * ce, 8 * pe * a
     if name == "rowdot":
         return 2 * 3 * ce + 8 * rows, 3 * ce            # read dO, O, r; write D*r, dO*r
     if name == "fwd_stream":
@@ -415,7 +417,8 @@ def ours(args):
         return run_kind
 
     reps = max(3, min(args.steps, 10))
-    kinds = ["fwd_stream", "rowdot", "bwd_stream"] if stream else ["fwd_factored", "rowdot", "bwd_fused"]
+    bwd_kind = "bwd_fused" if engine.single_pass_default(R, B, Z, c, A) else "bwd_dkdv_dq"
+    kinds = ["fwd_stream", "rowdot", "bwd_stream"] if stream else ["fwd_factored", "rowdot", bwd_kind]
     replays = {}
     for kind in kinds:
         fn = launches(kind)
@@ -487,7 +490,8 @@ def ours(args):
         kernels[k] = {"launches_per_step": LAYERS, "us_per_launch": per * 1e6, "ms_per_step": tms,
                       "share_of_step": tms / step_ref_ms, "GB/s": b_ / per / 1e9, "TFLOP/s": f_ / per / 1e12}
     kernel_sum = sum(type_ms.values())
-    launches_per_step = LAYERS * len(kinds)
+    # fwd + rowdot + one backward launch, or two for the two-kernel / stream backward
+    launches_per_step = LAYERS * (4 if (stream or bwd_kind == "bwd_dkdv_dq") else 3)
 
     # parity of the timed path: re-run one step, then check sampled heads of the first and
     # last layer against the float64 oracle (ringseq/reference.py:66-103 per head)

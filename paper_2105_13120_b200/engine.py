@@ -249,6 +249,12 @@ def recompute_outputs(panel: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def single_pass_default(n: int, b: int, z: int, c: int, a: int) -> bool:
+    """The backward ``backward(single_pass=None)`` runs: rsa_bwd_fused when it can tile the
+    geometry and there are at least half as many heads as SMs, else rsa_bwd_dkdv + rsa_bwd_dq."""
+    return single_pass_supported(n, b, z, c, a) and 2 * b * z >= lib().rsa_num_sms()
+
+
 def single_pass_supported(n: int, b: int, z: int, c: int, a: int) -> bool:
     """Does rsa_bwd_fused cover this geometry (a head's query rows in <= 4 tiles)?"""
     g = _geom(n, b, z, c, a, n * c, 0, n)
