@@ -280,6 +280,22 @@ __global__ void __launch_bounds__(256) panel_normalize_kernel(const __nv_bfloat1
 }
 
 
+// y[i] = sum_d x[d * rank_stride + i] over d = 0..n_rank-1 in ascending order (fp32, then
+// fp32 or bf16 out): the per-rank partial projections summed across ranks -- the Linformer's
+// ring-accumulate (ringseq/sparse_attention.py:59-71) when every rank is resident.
+template <typename TO>
+__global__ void __launch_bounds__(256) sum_ranks_kernel(const float* __restrict__ x, int64_t n_rank, int64_t count,
+                                                        int64_t rank_stride, TO* __restrict__ y) {
+  for (int64_t i = (int64_t(blockIdx.x) * 256 + threadIdx.x) * 4; i < count; i += int64_t(gridDim.x) * 256 * 4) {
+    float4 acc = *reinterpret_cast<const float4*>(x + i);
+    for (int64_t d = 1; d < n_rank; ++d) {
+      const float4 t = *reinterpret_cast<const float4*>(x + d * rank_stride + i);
+      acc.x += t.x, acc.y += t.y, acc.z += t.z, acc.w += t.w;
+    }
+    st4(y + i, reinterpret_cast<const float*>(&acc));
+  }
+}
+
 // Exact GELU (ringseq/tensor_ops.py:87-90): y = x * Phi(x), Phi(x) = (1 + erf(x / sqrt 2)) / 2,
 // and its backward dx = dy * (Phi(x) + x * phi(x)).  Grid-stride, 4 elements per thread
 // per iteration when the pointers allow it.
@@ -477,6 +493,26 @@ int rsa_panel_normalize(const void* p, int64_t ld_p, const float* scale, int64_t
   else
     return fail(RSA_ERR_INVALID, "panel_normalize: bad output dtype");
   return check_launch("panel_normalize_kernel");
+}
+
+int rsa_sum_ranks(const float* x, int64_t n_rank, int64_t count, int64_t rank_stride, void* y, int y_dtype,
+                  void* stream) {
+  using namespace rsa;
+  if (!x || !y || n_rank < 1 || count < 0 || rank_stride < count)
+    return fail(RSA_ERR_INVALID, "sum_ranks: bad arguments");
+  if (count % 4 || rank_stride % 4 || !aligned16(x) || !aligned16(y))
+    return fail(RSA_ERR_UNSUPPORTED, "sum_ranks: needs 16-byte aligned rows of 4-element multiples");
+  if (count == 0) return RSA_OK;
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  const int grid = elementwise_grid(count);
+  if (y_dtype == RSA_F32)
+    sum_ranks_kernel<float><<<grid, 256, 0, st>>>(x, n_rank, count, rank_stride, static_cast<float*>(y));
+  else if (y_dtype == RSA_BF16)
+    sum_ranks_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(x, n_rank, count, rank_stride,
+                                                          static_cast<__nv_bfloat16*>(y));
+  else
+    return fail(RSA_ERR_INVALID, "sum_ranks: bad output dtype");
+  return check_launch("sum_ranks_kernel");
 }
 
 int rsa_gelu(const void* x, int x_dtype, int64_t n, void* y, int y_dtype, void* stream) {

@@ -37,6 +37,7 @@ import torch
 
 from . import engine
 from . import tensor_ops as ops
+from ._native import BF16, check, lib
 from .cluster import CommLedger, resolve_executor
 from .config import SparseAttentionConfig
 from .errors import NumericError, ShapeError
@@ -119,17 +120,24 @@ def _check_inputs(name_chunks, weights, cfg: SparseAttentionConfig):
 
 
 def _project(q, k, v, e, f, kdim):
-    """K' = sum_d E_d K_d, V' = sum_d F_d V_d as bf16 [B][Z][K][A]: rsa_gemm with the projection
-    block shared by the B*Z heads (stride-0 batch), accumulated in fp32 over the ranks in
-    ascending order -- the reference's ring-accumulate (:59-71) when every rank is resident."""
+    """K' = sum_d E_d K_d, V' = sum_d F_d V_d as bf16 [B][Z][K][A].
+
+    One rsa_gemm launch per projection covers every (rank, head) pair: rank d's column block
+    E_d is a strided view of E (batch stride c) shared by the B*Z heads (batch stride 0),
+    each product K = c deep, into fp32 per-rank partials; rsa_sum_ranks then adds the
+    partials in ascending rank order -- the reference's ring-accumulate (:59-71) when every
+    rank is resident -- straight to bf16."""
     n, b, z, c, a = q.shape
-    k_low = torch.empty((b, z, kdim, a), dtype=torch.float32, device=q.device)
-    v_low = torch.empty_like(k_low)
-    for d in range(n):
-        cols = slice(d * c, (d + 1) * c)
-        ops.matmul(e[:, cols], k[d], out=k_low, accumulate=d > 0)
-        ops.matmul(f[:, cols], v[d], out=v_low, accumulate=d > 0)
-    return k_low.to(torch.bfloat16), v_low.to(torch.bfloat16)
+    out = []
+    for proj, x in ((e, k), (f, v)):
+        blocks = proj.reshape(kdim, n, c).permute(1, 0, 2).unsqueeze(1)  # [N][1][K][c], row stride L
+        part = ops.matmul(blocks, x.reshape(n, b * z, c, a))             # [N][B*Z][K][A] fp32
+        low = torch.empty((b, z, kdim, a), dtype=torch.bfloat16, device=q.device)
+        per_rank = b * z * kdim * a
+        check(lib().rsa_sum_ranks(part.data_ptr(), n, per_rank, per_rank, low.data_ptr(), BF16,
+                                  torch.cuda.current_stream(q.device).cuda_stream), "rsa_sum_ranks")
+        out.append(low)
+    return out[0], out[1]
 
 
 def _fused_ok(a: int, c: int, kdim: int) -> bool:
