@@ -148,7 +148,8 @@ int rsa_gelu_bwd(const void* x, int x_dtype, const void* dy, int dy_dtype, int64
  * y[i] = sum over d = 0..n_rank-1 (ascending) of x[d * rank_stride + i], i < count; fp32 in,
  * fp32 or bf16 out per y_dtype.  The cross-rank sum of per-rank partial projections: the
  * Linformer's ring-accumulate (ringseq/sparse_attention.py:59-71) when every rank is
- * resident on one GPU.  count and rank_stride multiples of 4, 16-byte aligned buffers.
+ * resident on one GPU.  Vectorised when count and rank_stride are multiples of 4 and the
+ * buffers 16-byte aligned; any layout otherwise.
  */
 int rsa_sum_ranks(const float* x, int64_t n_rank, int64_t count, int64_t rank_stride, void* y, int y_dtype,
                   void* stream);

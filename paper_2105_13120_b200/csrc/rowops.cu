@@ -296,6 +296,16 @@ __global__ void __launch_bounds__(256) sum_ranks_kernel(const float* __restrict_
   }
 }
 
+template <typename TO>
+__global__ void __launch_bounds__(256) sum_ranks_scalar_kernel(const float* __restrict__ x, int64_t n_rank,
+                                                               int64_t count, int64_t rank_stride, TO* __restrict__ y) {
+  for (int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x; i < count; i += int64_t(gridDim.x) * 256) {
+    float acc = x[i];
+    for (int64_t d = 1; d < n_rank; ++d) acc += x[d * rank_stride + i];
+    st1(y, i, acc);
+  }
+}
+
 // Exact GELU (ringseq/tensor_ops.py:87-90): y = x * Phi(x), Phi(x) = (1 + erf(x / sqrt 2)) / 2,
 // and its backward dx = dy * (Phi(x) + x * phi(x)).  Grid-stride, 4 elements per thread
 // per iteration when the pointers allow it.
@@ -500,11 +510,19 @@ int rsa_sum_ranks(const float* x, int64_t n_rank, int64_t count, int64_t rank_st
   using namespace rsa;
   if (!x || !y || n_rank < 1 || count < 0 || rank_stride < count)
     return fail(RSA_ERR_INVALID, "sum_ranks: bad arguments");
-  if (count % 4 || rank_stride % 4 || !aligned16(x) || !aligned16(y))
-    return fail(RSA_ERR_UNSUPPORTED, "sum_ranks: needs 16-byte aligned rows of 4-element multiples");
   if (count == 0) return RSA_OK;
   auto st = reinterpret_cast<cudaStream_t>(stream);
   const int grid = elementwise_grid(count);
+  if (count % 4 || rank_stride % 4 || !aligned16(x) || !aligned16(y)) {  // any layout, one element per step
+    if (y_dtype == RSA_F32)
+      sum_ranks_scalar_kernel<float><<<grid * 4, 256, 0, st>>>(x, n_rank, count, rank_stride, static_cast<float*>(y));
+    else if (y_dtype == RSA_BF16)
+      sum_ranks_scalar_kernel<__nv_bfloat16><<<grid * 4, 256, 0, st>>>(x, n_rank, count, rank_stride,
+                                                                       static_cast<__nv_bfloat16*>(y));
+    else
+      return fail(RSA_ERR_INVALID, "sum_ranks: bad output dtype");
+    return check_launch("sum_ranks_scalar_kernel");
+  }
   if (y_dtype == RSA_F32)
     sum_ranks_kernel<float><<<grid, 256, 0, st>>>(x, n_rank, count, rank_stride, static_cast<float*>(y));
   else if (y_dtype == RSA_BF16)
