@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--heads", type=int, default=12)
     ap.add_argument("--head-size", type=int, default=64)
     ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-checks", default="deferred", choices=["sync", "deferred"],
+                    help="RSA_B200_CHECK for the e2e leg: deferred reads each forward's status flag at its "
+                         "backward instead of a host sync per forward call")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the captured step")
     ap.add_argument("--ring-ranks", type=int, default=1,
@@ -561,6 +564,14 @@ def sampled_parity(layers, B, Z, seed, heads_per_layer=8):
 
 def e2e_public_api(args, dev):
     """Same step through ring_attention_forward/backward with pinned host buffers."""
+    os.environ["RSA_B200_CHECK"] = args.e2e_checks
+    try:
+        return _e2e_public_api(args, dev)
+    finally:
+        os.environ.pop("RSA_B200_CHECK", None)
+
+
+def _e2e_public_api(args, dev):
     import torch
 
     from paper_2105_13120_b200 import AttentionConfig
@@ -651,7 +662,7 @@ def e2e_public_api(args, dev):
             "d2h_bytes_per_step": d2h,
             "path": "ring_attention_forward/backward (public API) on device chunks uploaded every step from "
                     "pinned host bf16 (q, k, v, dO) on a copy stream one step ahead; O, dQ, dK, dV copied to "
-                    "pinned host; layers alternate over 2 compute streams"}
+                    "pinned host; layers alternate over 2 compute streams; status flags: " + args.e2e_checks}
 
 
 def main():

@@ -48,6 +48,7 @@ __all__ = [
     "sequence_parallel_mlp_backward",
     "ProbPanels",
     "StreamPanels",
+    "check_forward",
 ]
 
 
@@ -120,6 +121,7 @@ class ProbPanels(list):
         # backward then uses the given panels, not the saved stack
         self.dirty = False
         self.as_numpy = False  # results="numpy": items materialise as float64 ndarrays
+        self.pending = None  # a deferred status-flag check (RSA_B200_CHECK=deferred)
 
     def __setitem__(self, i, value):
         list.__setitem__(self, i, value)
@@ -167,6 +169,7 @@ class StreamPanels(ProbPanels):
         self.inputs = inputs
         self.dirty = False
         self.as_numpy = False
+        self.pending = None
 
     def _get(self, d: int):
         item = list.__getitem__(self, d)
@@ -262,6 +265,46 @@ def _chunk_elements(cfg: AttentionConfig) -> int:
     return cfg.batch_size * cfg.num_heads * cfg.chunk_len * cfg.head_size
 
 
+CHECK_ENV_VAR = "RSA_B200_CHECK"
+
+
+def _deferred_checks() -> bool:
+    """$RSA_B200_CHECK=deferred: the forward does not wait for its status flag (a host sync
+    per call); the flag travels to pinned host memory behind an event and is read by the
+    backward that consumes the forward's panels (or by ``check_forward``).  Default "sync":
+    the forward raises NumericError itself, as ringseq/tensor_ops.py:80-81 does."""
+    mode = os.environ.get(CHECK_ENV_VAR, "sync")
+    if mode not in ("sync", "deferred"):
+        raise ValueError(f"${CHECK_ENV_VAR} must be 'sync' or 'deferred', got {mode!r}")
+    return mode == "deferred"
+
+
+class _PendingCheck:
+    """A forward's status flag, copied to pinned host memory behind an event on its stream."""
+
+    def __init__(self, flag: torch.Tensor):
+        self.host = torch.empty(1, dtype=torch.int32, pin_memory=True)
+        self.host.copy_(flag, non_blocking=True)
+        self.event = torch.cuda.Event()
+        self.event.record()
+
+    def raise_if_bad(self) -> None:
+        self.event.synchronize()  # waits for this forward only, not the whole device
+        status = int(self.host[0])
+        if status & 1:
+            raise NumericError("softmax_rows requires finite inputs")
+        if status & 2:
+            raise NumericError("a row exceeded the single-pass panel's headroom in a forward with deferred checks; "
+                               f"rerun it with ${CHECK_ENV_VAR}=sync")
+
+
+def check_forward(fwd) -> None:
+    """Raise the NumericError a forward with deferred checks found (no-op otherwise)."""
+    pending = getattr(fwd.probs, "pending", None)
+    if pending is not None:
+        pending.raise_if_bad()
+
+
 def _forward_checked(q, k, v, path: str) -> engine.Forward:
     """engine.forward plus the host-side status check.
 
@@ -271,6 +314,8 @@ def _forward_checked(q, k, v, path: str) -> engine.Forward:
     recomputes the whole launch (never seen for real attention logits).
     """
     res = engine.forward(q, k, v, path=path)
+    if _deferred_checks():
+        return res
     status = int(res.flag.item())
     if status == 2:
         res.flag.zero_()
@@ -309,6 +354,8 @@ def _stream_checked(q, k, v) -> engine.StreamForward:
     """engine.forward_stream plus the status check (bit 0 NumericError; bit 1 reruns the
     launch on every row's true maximum, as _forward_checked does for the panel)."""
     res = engine.forward_stream(q, k, v)
+    if _deferred_checks():
+        return res
     status = int(res.flag.item())
     if status == 2:
         res.flag.zero_()
@@ -358,12 +405,15 @@ def ring_attention_forward(q_chunks, k_chunks, v_chunks, cfg: AttentionConfig, *
         res = _stream_checked(q, k, v)
         probs = StreamPanels(q, k, v, res.out, res.rowscale, res.rowmax, saved, cfg.panel_shape())
         probs.as_numpy = rmode == "numpy"
+        probs.pending = _PendingCheck(res.flag) if _deferred_checks() else None
         return RingAttentionForward(outputs=_out_list(res.out, cfg.num_devices, rmode), probs=probs,
                                     ledger=forward_ledger(cfg))
-    out, panel, rowscale, _ = _forward_checked(q, k, v, path)
+    out, panel, rowscale, flag = _forward_checked(q, k, v, path)
+    probs = _panels(ProbPanels(panel, out, rowscale, saved), rmode)
+    probs.pending = _PendingCheck(flag) if _deferred_checks() else None
     return RingAttentionForward(
         outputs=_out_list(out, cfg.num_devices, rmode),
-        probs=_panels(ProbPanels(panel, out, rowscale, saved), rmode),
+        probs=probs,
         ledger=forward_ledger(cfg),
     )
 
@@ -386,6 +436,8 @@ def ring_attention_backward(q_chunks, k_chunks, v_chunks, probs, grad_chunks, cf
     if probs is None:
         raise StateError("ring_attention_backward needs the probability panels saved by ring_attention_forward")
     probs = _check_chunks("probs", probs, cfg, cfg.panel_shape())
+    if getattr(probs, "pending", None) is not None:  # the forward's deferred status check
+        probs.pending.raise_if_bad()
     dev = _device_of(q_chunks, k_chunks, v_chunks, grad_chunks, probs)
     saved = probs.inputs if isinstance(probs, ProbPanels) else []
 

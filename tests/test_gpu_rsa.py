@@ -499,6 +499,30 @@ def test_backward_follows_given_values_and_panels(rsa, as_torch):
         _gate(name, _np(pkg.gather_sequence(got)), np.concatenate(ref, -2))
 
 
+def test_deferred_checks_raise_at_the_backward(rsa, monkeypatch):
+    """RSA_B200_CHECK=deferred: the forward returns without a host sync; the NumericError
+    for a non-finite score surfaces at check_forward and at the backward that consumes the
+    panels; ordinary inputs pass through unchanged."""
+    pkg, ra = rsa
+    monkeypatch.setenv("RSA_B200_CHECK", "deferred")
+    b, z, seq, a, n = 1, 2, 256, 64, 2
+    q, k, v, g = _inputs(b, z, seq, a, seed=21)
+    cfg = _cfg(pkg, b, z, seq, a, n)
+    ch = lambda x: orc.chunks_of(x, n)  # noqa: E731
+    fwd = ra.ring_attention_forward(ch(q), ch(k), ch(v), cfg)
+    ra.check_forward(fwd)
+    bwd = ra.ring_attention_backward(ch(q), ch(k), ch(v), fwd.probs, ch(g), cfg)
+    _check_all(pkg, fwd, bwd, _oracle(q, k, v, g, n))
+    bad = q.copy()
+    bad[0, 0, 3, 0] = np.nan
+    for mode in ("panel", "stream"):
+        fwd = ra.ring_attention_forward(ch(bad), ch(k), ch(v), cfg, mode=mode)  # no raise here
+        with pytest.raises(pkg.NumericError):
+            ra.check_forward(fwd)
+        with pytest.raises(pkg.NumericError):
+            ra.ring_attention_backward(ch(bad), ch(k), ch(v), fwd.probs, ch(g), cfg)
+
+
 @pytest.mark.parametrize("key", [50, 300])
 def test_negative_overflow_score_raises_numeric_error(rsa, key):
     """A score that overflows the fp32 range to -inf while every other score of its row
