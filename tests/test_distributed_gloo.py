@@ -156,12 +156,16 @@ def test_spmd_ring_matches_oracle(world, mode, overlap, attn):
         # forward K+V rings, backward V+K rings: 4(N-1) chunks; two all-reduces
         assert r["ring"] == ring_f + ring_b
         assert r["ar"] == ar_b
-        c_bytes = b * z * (seq // world) * a * 8  # float64 chunk
-        ring_wire = 2 * (world - 1) * c_bytes  # the forward's K/V pair ring
-        if attn == "stream":  # the backward K/V ring plus N hops of the two fp64 sums
-            assert r["wire"] == 2 * ring_wire + 2 * world * c_bytes
-        elif mode == "paper":  # all-reduce of two (N*C) partials
-            assert r["wire"] == ring_wire + 2 * (2 * world * c_bytes * (world - 1) // world)
+        # the bytes on the wire are the cost report's plan (float64 here: 8-byte elements);
+        # gloo has no reduce-scatter, so both panel modes all-reduce the partials
+        from paper_2105_13120_b200 import AttentionConfig
+        from paper_2105_13120_b200.cost_report import wire_bytes
+
+        cfg = AttentionConfig(batch_size=b, seq_len=seq, hidden_size=z * a, num_heads=z, head_size=a,
+                              num_devices=world)
+        plan = "stream" if attn == "stream" else "panel_paper"
+        want = wire_bytes(cfg, plan, kv_bytes=8, grad_bytes=8)
+        assert r["wire"] == want["forward"] + want["backward"]
 
 
 class CpuLinformerKernels(CpuHopKernels):

@@ -75,6 +75,7 @@ def _worker(rank, world, port, shape, seed, mode, attn, results, backend="gloo")
         results[rank] = {"out": f64(out[0]), "panel": panel, "dq": f64(dq[0]), "dk": f64(dk[0]),
                          "dv": f64(dv[0]), "lin": f64(lin[0] if lin.dim() == 5 else lin),
                          "ring": ring.ledger.devices[rank].ring_p2p_elements,
+                         "wire": ring.ledger.devices[rank].wire_bytes,
                          "flag": int(ctx.extra["flag"].item())}
     finally:
         dist.destroy_process_group()
@@ -90,7 +91,10 @@ SPMD_CASES = [(2, "reduce_scatter", "panel", (1, 2, 256, 64)), (3, "paper", "pan
               (2, "paper", "stream", (1, 2, 2048, 64))]
 
 
-def _check_spmd(world, mode, attn, shape, seed, results):
+def _check_spmd(world, mode, attn, shape, seed, results, backend="gloo"):
+    from paper_2105_13120_b200 import AttentionConfig
+    from paper_2105_13120_b200.cost_report import wire_bytes
+
     b, z, seq, a = shape
     q, k, v, g = _inputs(b, z, seq, a, seed)
     ch = lambda x: orc.chunks_of(x, world)  # noqa: E731
@@ -109,6 +113,14 @@ def _check_spmd(world, mode, attn, shape, seed, results):
         for name, want in (("dq", dq[d]), ("dk", dk[d]), ("dv", dv[d]), ("lin", lin[d])):
             assert _rel(r[name], want) <= 1e-2, (d, name, _rel(r[name], want))
         assert r["ring"] == 4 * (world - 1) * b * z * (seq // world) * a + 2 * (world - 1) * b * z * 32 * a
+        # bytes on the wire = the cost report's plan + the Linformer's fp32 [K'; V'] all-reduce
+        cfg = AttentionConfig(batch_size=b, seq_len=seq, hidden_size=z * a, num_heads=z, head_size=a,
+                              num_devices=world)
+        plan = "stream" if attn == "stream" else (
+            "panel" if backend == "nccl" and mode == "reduce_scatter" else "panel_paper")
+        want = wire_bytes(cfg, plan)
+        lin = 2 * (2 * b * z * 32 * a * 4) * (world - 1) // world
+        assert r["wire"] == want["forward"] + want["backward"] + lin, (r["wire"], want, lin)
 
 
 @pytest.mark.parametrize("world,mode,attn,shape", SPMD_CASES)
@@ -135,7 +147,7 @@ def test_spmd_ring_nccl_two_gpus(mode, attn):
     results = mgr.dict()
     mp.start_processes(_worker, args=(world, _free_port(), shape, seed, mode, attn, results, "nccl"), nprocs=world,
                        join=True, start_method="spawn")
-    _check_spmd(world, mode, attn, shape, seed, results)
+    _check_spmd(world, mode, attn, shape, seed, results, backend="nccl")
 
 
 def _peer_worker(rank, world, port, shape, seed, results):

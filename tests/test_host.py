@@ -79,3 +79,29 @@ def test_executor_resolution(monkeypatch):
     assert resolve_executor("sequential") == "sequential"
     with pytest.raises(pkg.ConfigError):
         resolve_executor("threads")
+
+
+def test_cost_report_reconciles_model_and_ledgers():
+    """The reference's communication model (ringseq/cost_model.py:122-159, restated in
+    cost_report) equals the ledgers the API charges, element for element, including the
+    BERT-base points of tests/test_acceptance.py:183-204 (B2 Z12 L512 A64 N4)."""
+    from fractions import Fraction
+
+    from paper_2105_13120_b200 import AttentionConfig, SparseAttentionConfig
+    from paper_2105_13120_b200.cost_report import comm_volume, reconcile, sparse_comm_volume, wire_bytes
+
+    for b, z, seq, a, n in [(2, 12, 512, 64, 4), (1, 2, 8, 4, 4), (4, 12, 512, 64, 8), (3, 2, 12, 4, 3)]:
+        cfg = AttentionConfig(batch_size=b, seq_len=seq, hidden_size=z * a, num_heads=z, head_size=a, num_devices=n)
+        rep = reconcile(cfg)
+        assert rep["ledger_matches_model"], rep
+    cfg = AttentionConfig(batch_size=2, seq_len=512, hidden_size=768, num_heads=12, head_size=64, num_devices=4)
+    assert comm_volume(cfg, "forward") == 1179648 and comm_volume(cfg, "backward") == 3538944
+    assert comm_volume(cfg) == 4718592
+    sp = SparseAttentionConfig(base=AttentionConfig(batch_size=2, seq_len=40, hidden_size=15, num_heads=3,
+                                                    head_size=5, num_devices=4), proj_dim=7)
+    assert sparse_comm_volume(sp) == Fraction(3 * 2 * 2 * 3 * 7 * 5)
+    # the plans: panel mode sends less than the paper's plan, stream mode more than panel mode
+    w = {p: sum(wire_bytes(cfg, p).values()) for p in ("paper", "panel", "stream")}
+    assert w["panel"] < w["paper"] and w["panel"] < w["stream"]
+    rep = reconcile(cfg, measured=wire_bytes(cfg, "panel"), plan="panel")
+    assert rep["measured"]["matches_plan"]
