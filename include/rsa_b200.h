@@ -302,6 +302,25 @@ int rsa_bwd_q_stream(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_
                      const float* rowmax, const float* dvec, rsa_view dq_acc, int accumulate, rsa_view dq_out,
                      void* stream);
 
+/* ------------------------------------------ BERT harness */
+
+/*
+ * Not on the RSA path: the embedding lookup and masked-LM loss that turn the encoder stack
+ * into the paper's whole-model BERT training step; the reference has
+ * neither.  Rows are laid out [rank][b][i], rank d holding positions d*chunk + i (the
+ * contiguous chunk layout of ringseq/cluster.py:73-88).
+ *   rsa_embed:        x[row] = tok[ids[row]] + pos[position(row)]        (bf16, hidden % 8 == 0)
+ *   rsa_embed_bwd:    dtok[ids[row]] += dx[row], dpos[position(row)] += dx[row]  (fp32 atomics)
+ *   rsa_softmax_xent: loss[r] = logsumexp(logits[r]) - logits[r][targets[r]] and
+ *                     dlogits[r] = (softmax(logits[r]) - onehot(targets[r])) * grad_scale (bf16)
+ */
+int rsa_embed(const int* ids, int64_t n_rank, int64_t batch, int64_t chunk, const void* tok, const void* pos,
+              int64_t hidden, void* x, void* stream);
+int rsa_embed_bwd(const int* ids, int64_t n_rank, int64_t batch, int64_t chunk, const void* dx, int64_t hidden,
+                  float* dtok, float* dpos, void* stream);
+int rsa_softmax_xent(const float* logits, int64_t ld, const int* targets, int64_t rows, int64_t vocab, float* loss,
+                     void* dlogits, int64_t ld_d, float grad_scale, void* stream);
+
 /* --------------------------------------------- peer-resident origins (NVLink) */
 
 #define RSA_MAX_PEERS 8

@@ -123,6 +123,10 @@ EXPORTS = {
     "rsa_fused_supported": (c_int, [_GEOM]),
     "rsa_bwd_fused": (c_int, [_GEOM, _V, _V, _V, _V, _V, c_void_p, _V, c_int, _V, _V, _V, c_int, c_int, c_void_p]),
     "rsa_bwd_fused_supported": (c_int, [_GEOM]),
+    "rsa_embed": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
+    "rsa_embed_bwd": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "rsa_softmax_xent": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_int64, c_float,
+                                 c_void_p]),
     "rsa_fwd_factored_ex": (c_int, [_GEOM, _V, _V, _V, _P(RsaFwdExt), _V, c_void_p, c_void_p, c_void_p]),
     "rsa_bwd_kv_stream": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, c_void_p, _V, _V, c_int, c_int, c_void_p]),
     "rsa_bwd_q_stream": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, c_void_p, _V, c_int, _V, c_void_p]),

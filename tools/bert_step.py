@@ -5,7 +5,12 @@ reference has none) forward then backward with saved activations, synthetic bf16
 inputs and output gradient, random weights at the reference's scales.  Reports tokens/s
 and the share of the step spent in the RSA kernels (timed on their own, same shapes).
 
-usage: python tools/bert_step.py [--model base|large] [--batch 64] [--seq 512] [--ranks 1]
+usage: python tools/bert_step.py [--model base|large] [--batch 64] [--seq 512] [--ranks 1] [--mlm]
+
+--mlm times the whole masked-LM model step instead (paper_2105_13120_b200.bert.BertMLM):
+token + position embeddings, the encoder stack, the tied-weight MLM head over the 15%
+masked positions, mean cross-entropy, and every gradient -- the paper's BERT training step
+ on synthetic token ids.
 """
 import argparse
 import json
@@ -29,7 +34,11 @@ def main():
     ap.add_argument("--ranks", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--out", default="")
+    ap.add_argument("--mlm", action="store_true")
+    ap.add_argument("--vocab", type=int, default=30522)
     args = ap.parse_args()
+    if args.mlm:
+        return mlm(args)
     layers_n, h, z = MODELS[args.model]
     n, b, seq = args.ranks, args.batch, args.seq
     cfg = AttentionConfig(batch_size=b, seq_len=seq, hidden_size=h, num_heads=z, head_size=h // z, num_devices=n)
@@ -83,6 +92,44 @@ def main():
            "ring_ranks": n, "ms_per_step": ms, "tokens_per_s": b * seq / (ms / 1e3),
            "rsa_ms_per_step": rsa_ms, "rsa_share": rsa_ms / ms,
            "note": "training step = every layer fwd then bwd with saved activations; synthetic data, random init"}
+    print(json.dumps(res), flush=True)
+    if args.out:
+        Path(args.out).write_text(json.dumps(res, indent=1))
+
+
+def mlm(args):
+    from paper_2105_13120_b200.bert import BertMLM
+
+    layers_n, h, z = MODELS[args.model]
+    n, b, seq = args.ranks, args.batch, args.seq
+    cfg = AttentionConfig(batch_size=b, seq_len=seq, hidden_size=h, num_heads=z, head_size=h // z, num_devices=n)
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev).manual_seed(0)
+    model = BertMLM(cfg, layers_n, vocab=args.vocab, device=dev, generator=gen)
+    ids = torch.randint(1000, args.vocab, (n, b, seq // n), generator=gen, device=dev, dtype=torch.int32)
+    rows = ids.numel()
+    n_mask = max(1, int(0.15 * rows))
+    mask_rows = torch.randperm(rows, generator=gen, device=dev)[:n_mask].sort().values
+    targets = ids.view(-1)[mask_rows].clone()
+    ids.view(-1)[mask_rows] = 103  # [MASK]
+    for _ in range(2):
+        loss, _ = model.step(ids, mask_rows, targets)
+    torch.cuda.synchronize()
+    losses = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        loss, grads = model.step(ids, mask_rows, targets)
+        losses.append(loss)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    lv = [float(x) for x in losses]
+    res = {"model": f"BERT-{args.model} masked LM ({layers_n} layers, H={h}, Z={z}, vocab {args.vocab})", "batch": b,
+           "seq_len": seq, "ring_ranks": n, "masked_tokens": n_mask, "ms_per_step": ms,
+           "tokens_per_s": b * seq / (ms / 1e3), "loss": lv[-1], "loss_finite": all(x == x and abs(x) < 1e4 for x in lv),
+           "note": "whole training step: embeddings, encoder (RSA + MLP), MLM head on masked rows, cross-entropy, "
+                   "every gradient; synthetic ids, random init (no optimizer update)"}
     print(json.dumps(res), flush=True)
     if args.out:
         Path(args.out).write_text(json.dumps(res, indent=1))
