@@ -53,14 +53,16 @@ def embed_backward(ids: torch.Tensor, dx: torch.Tensor, dtok: torch.Tensor, dpos
                               dpos.data_ptr(), _stream(ids)), "rsa_embed_bwd")
 
 
-def softmax_xent(logits: torch.Tensor, targets: torch.Tensor, grad_scale: float):
+def softmax_xent(logits: torch.Tensor, targets: torch.Tensor, grad_scale: float, vocab: int | None = None):
     """Per-row cross-entropy of fp32 logits [M][V] against int32 targets, and
-    dlogits = (softmax - onehot) * grad_scale as bf16."""
-    m, v = logits.shape
+    dlogits = (softmax - onehot) * grad_scale as bf16.  ``vocab`` < V: only the first
+    ``vocab`` columns take part (padded columns get a zero gradient)."""
+    m, width = logits.shape
+    v = width if vocab is None else vocab
     loss = torch.empty(m, dtype=torch.float32, device=logits.device)
-    dl = torch.empty((m, v), dtype=torch.bfloat16, device=logits.device)
+    dl = (torch.empty if v == width else torch.zeros)((m, width), dtype=torch.bfloat16, device=logits.device)
     check(lib().rsa_softmax_xent(logits.data_ptr(), logits.stride(0), targets.data_ptr(), m, v, loss.data_ptr(),
-                                 dl.data_ptr(), v, float(grad_scale), _stream(logits)), "rsa_softmax_xent")
+                                 dl.data_ptr(), width, float(grad_scale), _stream(logits)), "rsa_softmax_xent")
     return loss, dl
 
 
@@ -71,7 +73,12 @@ class BertMLM:
         self.cfg, self.vocab = cfg, vocab
         h = cfg.hidden_size
         s = h ** -0.5
-        self.tok = (torch.randn((vocab, h), generator=generator, device=device) * s).to(torch.bfloat16)
+        # the table is padded to a multiple of 64 rows so every head GEMM operand row is
+        # 16-byte aligned (the tcgen05 / TMA path); padded rows are zero, and the softmax
+        # runs over the real vocabulary only
+        self.vocab_padded = (vocab + 63) // 64 * 64
+        self.tok = torch.zeros((self.vocab_padded, h), dtype=torch.bfloat16, device=device)
+        self.tok[:vocab] = (torch.randn((vocab, h), generator=generator, device=device) * s).to(torch.bfloat16)
         self.pos = (torch.randn((cfg.seq_len, h), generator=generator, device=device) * s).to(torch.bfloat16)
         rs = (2 * n_layers) ** -0.5
         self.layers = [EncoderLayer(cfg, EncoderWeights.random(cfg, device, generator, residual_scale=rs))
@@ -100,9 +107,9 @@ class BertMLM:
             ly.unchecked = False
         flat = x.view(-1, h)
         xm = flat.index_select(0, mask_rows)                         # [M][H] bf16
-        logits = ops.matmul(xm, self.tok.transpose(0, 1))             # [M][V] fp32
+        logits = ops.matmul(xm, self.tok.transpose(0, 1))             # [M][V_pad] fp32
         m = mask_rows.numel()
-        rows_loss, dlogits = softmax_xent(logits, targets, 1.0 / m)
+        rows_loss, dlogits = softmax_xent(logits, targets, 1.0 / m, vocab=self.vocab)
         loss = rows_loss.mean()
         # head backward (tied weights): dx_m = dlogits tok, dtok = dlogits^T x_m
         dxm = ops.matmul(dlogits, self.tok, out_dtype=torch.bfloat16)
@@ -116,7 +123,7 @@ class BertMLM:
             grads.append(gw)
         dpos = torch.zeros((cfg.seq_len, h), dtype=torch.float32, device=x.device)
         embed_backward(ids, g, dtok, dpos)
-        return loss, {"tok": dtok, "pos": dpos, "layers": grads[::-1]}
+        return loss, {"tok": dtok[:self.vocab], "pos": dpos, "layers": grads[::-1]}
 
     def flags(self) -> list:
         return [int(ly.flag.item()) for ly in self.layers]

@@ -68,7 +68,7 @@ def test_mlm_step_runs_and_head_matches_torch():
     for ly in model.layers:
         x = ly.forward(x)
     xm = x.view(-1, 128).index_select(0, mask_rows).float()
-    want = torch.nn.functional.cross_entropy(xm @ model.tok.float().t(), targets.long())
+    want = torch.nn.functional.cross_entropy(xm @ model.tok[:1000].float().t(), targets.long())
     assert torch.isfinite(loss) and abs(float(loss) - float(want)) <= 2e-3 * max(1.0, float(want))
     assert grads["tok"].shape == (1000, 128) and torch.isfinite(grads["tok"]).all()
     assert torch.isfinite(grads["pos"]).all() and len(grads["layers"]) == 2

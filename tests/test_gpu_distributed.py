@@ -119,8 +119,8 @@ def _check_spmd(world, mode, attn, shape, seed, results, backend="gloo"):
         plan = "stream" if attn == "stream" else (
             "panel" if backend == "nccl" and mode == "reduce_scatter" else "panel_paper")
         want = wire_bytes(cfg, plan)
-        lin = 2 * (2 * b * z * 32 * a * 4) * (world - 1) // world
-        assert r["wire"] == want["forward"] + want["backward"] + lin, (r["wire"], want, lin)
+        lin_bytes = 2 * (2 * b * z * 32 * a * 4) * (world - 1) // world
+        assert r["wire"] == want["forward"] + want["backward"] + lin_bytes, (r["wire"], want, lin_bytes)
 
 
 @pytest.mark.parametrize("world,mode,attn,shape", SPMD_CASES)
