@@ -145,14 +145,15 @@ int rsa_gelu_bwd(const void* x, int x_dtype, const void* dy, int dy_dtype, int64
                  void* stream);
 
 /*
- * y[i] = sum over d = 0..n_rank-1 (ascending) of x[d * rank_stride + i], i < count; fp32 in,
- * fp32 or bf16 out per y_dtype.  The cross-rank sum of per-rank partial projections: the
- * Linformer's ring-accumulate (ringseq/sparse_attention.py:59-71) when every rank is
- * resident on one GPU.  Vectorised when count and rank_stride are multiples of 4 and the
- * buffers 16-byte aligned; any layout otherwise.
+ * y[i] = sum over d = 0..n_rank-1 (ascending) of x[d * rank_stride + i], i < count; x and y
+ * fp32 or bf16 per x_dtype / y_dtype, fp32 accumulation.  The cross-rank sum of per-rank
+ * partial projections: the Linformer's ring-accumulate (ringseq/sparse_attention.py:59-71)
+ * when every rank is resident on one GPU (also the BERT harness's position-embedding
+ * gradient, a sum over the batch).  Vectorised when count and rank_stride are multiples
+ * of 4 and the buffers 16-byte aligned; any layout otherwise.
  */
-int rsa_sum_ranks(const float* x, int64_t n_rank, int64_t count, int64_t rank_stride, void* y, int y_dtype,
-                  void* stream);
+int rsa_sum_ranks(const void* x, int x_dtype, int64_t n_rank, int64_t count, int64_t rank_stride, void* y,
+                  int y_dtype, void* stream);
 
 /* --------------------------------------------------- fused RSA kernels */
 
@@ -310,7 +311,8 @@ int rsa_bwd_q_stream(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_
  * neither.  Rows are laid out [rank][b][i], rank d holding positions d*chunk + i (the
  * contiguous chunk layout of ringseq/cluster.py:73-88).
  *   rsa_embed:        x[row] = tok[ids[row]] + pos[position(row)]        (bf16, hidden % 8 == 0)
- *   rsa_embed_bwd:    dtok[ids[row]] += dx[row], dpos[position(row)] += dx[row]  (fp32 atomics)
+ *   rsa_embed_bwd:    dtok[ids[row]] += dx[row] (fp32 atomics); dpos[position(row)] += dx[row] when
+ *                     dpos is not NULL (fp32 atomics; the harness sums positions with rsa_sum_ranks)
  *   rsa_softmax_xent: loss[r] = logsumexp(logits[r]) - logits[r][targets[r]] and
  *                     dlogits[r] = (softmax(logits[r]) - onehot(targets[r])) * grad_scale (bf16)
  */

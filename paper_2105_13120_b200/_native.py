@@ -105,7 +105,7 @@ EXPORTS = {
         [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_int64, c_void_p],
     ),
     "rsa_gelu": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int, c_void_p]),
-    "rsa_sum_ranks": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int, c_void_p]),
+    "rsa_sum_ranks": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int64, c_void_p, c_int, c_void_p]),
     "rsa_gelu_bwd": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int64, c_void_p, c_int, c_void_p]),
     "rsa_panel_normalize": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_int, c_int64, c_void_p]),
     "rsa_fwd_stats": (c_int, [_GEOM, _V, _V, c_void_p, c_int, c_void_p, c_void_p]),

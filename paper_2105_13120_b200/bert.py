@@ -24,7 +24,7 @@ from __future__ import annotations
 import torch
 
 from . import tensor_ops as ops
-from ._native import check, lib
+from ._native import BF16, F32, check, lib
 from .config import AttentionConfig
 from .encoder import EncoderLayer, EncoderWeights
 
@@ -46,11 +46,16 @@ def embed(ids: torch.Tensor, tok: torch.Tensor, pos: torch.Tensor) -> torch.Tens
 
 
 def embed_backward(ids: torch.Tensor, dx: torch.Tensor, dtok: torch.Tensor, dpos: torch.Tensor) -> None:
-    """dtok[ids] += dx, dpos[positions] += dx (fp32 accumulators, added into)."""
+    """dtok[ids] += dx (fp32 atomics); dpos[positions] = sum over the batch of dx (fp32,
+    written; a deterministic rsa_sum_ranks per rank -- atomics would contend B-way)."""
     n, b, c = ids.shape
+    h = dx.shape[-1]
     dx = dx.contiguous()
-    check(lib().rsa_embed_bwd(ids.data_ptr(), n, b, c, dx.data_ptr(), dx.shape[-1], dtok.data_ptr(),
-                              dpos.data_ptr(), _stream(ids)), "rsa_embed_bwd")
+    st = _stream(ids)
+    check(lib().rsa_embed_bwd(ids.data_ptr(), n, b, c, dx.data_ptr(), h, dtok.data_ptr(), None, st), "rsa_embed_bwd")
+    for d in range(n):  # rank d holds positions d*c .. d*c + c - 1 of every sequence
+        check(lib().rsa_sum_ranks(dx[d].data_ptr(), BF16, b, c * h, c * h, dpos[d * c:(d + 1) * c].data_ptr(), F32,
+                                  st), "rsa_sum_ranks")
 
 
 def softmax_xent(logits: torch.Tensor, targets: torch.Tensor, grad_scale: float, vocab: int | None = None):
@@ -121,7 +126,7 @@ class BertMLM:
         for ly in reversed(self.layers):
             g, gw = ly.backward(g)
             grads.append(gw)
-        dpos = torch.zeros((cfg.seq_len, h), dtype=torch.float32, device=x.device)
+        dpos = torch.empty((cfg.seq_len, h), dtype=torch.float32, device=x.device)
         embed_backward(ids, g, dtok, dpos)
         return loss, {"tok": dtok[:self.vocab], "pos": dpos, "layers": grads[::-1]}
 

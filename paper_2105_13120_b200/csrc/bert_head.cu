@@ -7,9 +7,10 @@
 //   rsa_embed        x[row] = tok[ids[row]] + pos[position(row)] for rows laid out
 //                    [rank][b][i] (rank d holds positions d*c .. d*c + c - 1: the
 //                    contiguous chunk layout of ringseq/cluster.py:73-88)
-//   rsa_embed_bwd    dtok[ids[row]] += dx[row], dpos[position(row)] += dx[row]
-//                    (fp32 atomics: the one non-deterministic sum in this repository,
-//                    confined to the harness's embedding gradient)
+//   rsa_embed_bwd    dtok[ids[row]] += dx[row] (fp32 atomics: the one non-deterministic
+//                    sum in this repository, confined to the harness's token-embedding
+//                    gradient); dpos likewise when given (the harness instead sums the
+//                    batch with rsa_sum_ranks: 64-way contention per address otherwise)
 //   rsa_softmax_xent per masked row: loss = logsumexp(logits) - logits[target] and
 //                    dlogits = (softmax(logits) - onehot(target)) * grad_scale, one CTA
 //                    per row, one read pass (online max / sum) and one write pass
@@ -56,11 +57,11 @@ __global__ void __launch_bounds__(256) embed_bwd_kernel(const int* __restrict__ 
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
   float* t = dtok + int64_t(ids[row]) * h;
-  float* p = dpos + embed_position(row, per_rank, c) * h;
+  float* p = dpos ? dpos + embed_position(row, per_rank, c) * h : nullptr;
   for (int64_t col = lane * 2; col < h; col += 64) {
     const float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dx + row * h + col));
     atomicAdd(t + col, g.x), atomicAdd(t + col + 1, g.y);
-    atomicAdd(p + col, g.x), atomicAdd(p + col + 1, g.y);
+    if (p) atomicAdd(p + col, g.x), atomicAdd(p + col + 1, g.y);
   }
 }
 
@@ -126,7 +127,7 @@ int rsa_embed_bwd(const int* ids, int64_t n_rank, int64_t batch, int64_t chunk, 
                   float* dtok, float* dpos, void* stream) {
   using namespace rsa;
   const int64_t rows = n_rank * batch * chunk;
-  if (!ids || !dx || !dtok || !dpos || hidden % 2 || rows < 0) return fail(RSA_ERR_INVALID, "rsa_embed_bwd: bad arguments");
+  if (!ids || !dx || !dtok || hidden % 2 || rows < 0) return fail(RSA_ERR_INVALID, "rsa_embed_bwd: bad arguments");
   if (rows == 0) return RSA_OK;
   embed_bwd_kernel<<<(rows + 7) / 8, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       ids, rows, static_cast<const __nv_bfloat16*>(dx), hidden, batch * chunk, chunk, dtok, dpos);

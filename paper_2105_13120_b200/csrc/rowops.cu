@@ -283,25 +283,39 @@ __global__ void __launch_bounds__(256) panel_normalize_kernel(const __nv_bfloat1
 // y[i] = sum_d x[d * rank_stride + i] over d = 0..n_rank-1 in ascending order (fp32, then
 // fp32 or bf16 out): the per-rank partial projections summed across ranks -- the Linformer's
 // ring-accumulate (ringseq/sparse_attention.py:59-71) when every rank is resident.
-template <typename TO>
-__global__ void __launch_bounds__(256) sum_ranks_kernel(const float* __restrict__ x, int64_t n_rank, int64_t count,
+template <typename TI>
+__device__ __forceinline__ float4 ld4(const TI* p);
+template <>
+__device__ __forceinline__ float4 ld4<float>(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+template <>
+__device__ __forceinline__ float4 ld4<__nv_bfloat16>(const __nv_bfloat16* p) {
+  const uint2 w = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256) sum_ranks_kernel(const TI* __restrict__ x, int64_t n_rank, int64_t count,
                                                         int64_t rank_stride, TO* __restrict__ y) {
   for (int64_t i = (int64_t(blockIdx.x) * 256 + threadIdx.x) * 4; i < count; i += int64_t(gridDim.x) * 256 * 4) {
-    float4 acc = *reinterpret_cast<const float4*>(x + i);
+    float4 acc = ld4<TI>(x + i);
     for (int64_t d = 1; d < n_rank; ++d) {
-      const float4 t = *reinterpret_cast<const float4*>(x + d * rank_stride + i);
+      const float4 t = ld4<TI>(x + d * rank_stride + i);
       acc.x += t.x, acc.y += t.y, acc.z += t.z, acc.w += t.w;
     }
     st4(y + i, reinterpret_cast<const float*>(&acc));
   }
 }
 
-template <typename TO>
-__global__ void __launch_bounds__(256) sum_ranks_scalar_kernel(const float* __restrict__ x, int64_t n_rank,
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256) sum_ranks_scalar_kernel(const TI* __restrict__ x, int64_t n_rank,
                                                                int64_t count, int64_t rank_stride, TO* __restrict__ y) {
   for (int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x; i < count; i += int64_t(gridDim.x) * 256) {
-    float acc = x[i];
-    for (int64_t d = 1; d < n_rank; ++d) acc += x[d * rank_stride + i];
+    float acc = ld1<TI>(x, i);
+    for (int64_t d = 1; d < n_rank; ++d) acc += ld1<TI>(x, d * rank_stride + i);
     st1(y, i, acc);
   }
 }
@@ -421,6 +435,17 @@ int softmax_bwd_launch(const void* p, int64_t ldp, const float* dp, int64_t lddp
   return check_launch("softmax_bwd_kernel");
 }
 
+template <typename TI, typename TO>
+int sum_ranks_launch(const void* x, int64_t n_rank, int64_t count, int64_t rank_stride, void* y, int vec,
+                     cudaStream_t st) {
+  const int grid = elementwise_grid(count);
+  const auto* xi = static_cast<const TI*>(x);
+  auto* yo = static_cast<TO*>(y);
+  if (vec) sum_ranks_kernel<TI, TO><<<grid, 256, 0, st>>>(xi, n_rank, count, rank_stride, yo);
+  else sum_ranks_scalar_kernel<TI, TO><<<grid * 4, 256, 0, st>>>(xi, n_rank, count, rank_stride, yo);
+  return check_launch("sum_ranks_kernel");
+}
+
 }  // namespace
 }  // namespace rsa
 
@@ -505,32 +530,20 @@ int rsa_panel_normalize(const void* p, int64_t ld_p, const float* scale, int64_t
   return check_launch("panel_normalize_kernel");
 }
 
-int rsa_sum_ranks(const float* x, int64_t n_rank, int64_t count, int64_t rank_stride, void* y, int y_dtype,
-                  void* stream) {
+int rsa_sum_ranks(const void* x, int x_dtype, int64_t n_rank, int64_t count, int64_t rank_stride, void* y,
+                  int y_dtype, void* stream) {
   using namespace rsa;
-  if (!x || !y || n_rank < 1 || count < 0 || rank_stride < count)
+  if (!x || !y || n_rank < 1 || count < 0 || rank_stride < count || (x_dtype != RSA_F32 && x_dtype != RSA_BF16) ||
+      (y_dtype != RSA_F32 && y_dtype != RSA_BF16))
     return fail(RSA_ERR_INVALID, "sum_ranks: bad arguments");
   if (count == 0) return RSA_OK;
   auto st = reinterpret_cast<cudaStream_t>(stream);
-  const int grid = elementwise_grid(count);
-  if (count % 4 || rank_stride % 4 || !aligned16(x) || !aligned16(y)) {  // any layout, one element per step
-    if (y_dtype == RSA_F32)
-      sum_ranks_scalar_kernel<float><<<grid * 4, 256, 0, st>>>(x, n_rank, count, rank_stride, static_cast<float*>(y));
-    else if (y_dtype == RSA_BF16)
-      sum_ranks_scalar_kernel<__nv_bfloat16><<<grid * 4, 256, 0, st>>>(x, n_rank, count, rank_stride,
-                                                                       static_cast<__nv_bfloat16*>(y));
-    else
-      return fail(RSA_ERR_INVALID, "sum_ranks: bad output dtype");
-    return check_launch("sum_ranks_scalar_kernel");
-  }
-  if (y_dtype == RSA_F32)
-    sum_ranks_kernel<float><<<grid, 256, 0, st>>>(x, n_rank, count, rank_stride, static_cast<float*>(y));
-  else if (y_dtype == RSA_BF16)
-    sum_ranks_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(x, n_rank, count, rank_stride,
-                                                          static_cast<__nv_bfloat16*>(y));
-  else
-    return fail(RSA_ERR_INVALID, "sum_ranks: bad output dtype");
-  return check_launch("sum_ranks_kernel");
+  const int vec = count % 4 == 0 && rank_stride % 4 == 0 && aligned16(x) && aligned16(y);
+  if (x_dtype == RSA_F32)
+    return y_dtype == RSA_F32 ? sum_ranks_launch<float, float>(x, n_rank, count, rank_stride, y, vec, st)
+                              : sum_ranks_launch<float, __nv_bfloat16>(x, n_rank, count, rank_stride, y, vec, st);
+  return y_dtype == RSA_F32 ? sum_ranks_launch<__nv_bfloat16, float>(x, n_rank, count, rank_stride, y, vec, st)
+                            : sum_ranks_launch<__nv_bfloat16, __nv_bfloat16>(x, n_rank, count, rank_stride, y, vec, st);
 }
 
 int rsa_gelu(const void* x, int x_dtype, int64_t n, void* y, int y_dtype, void* stream) {

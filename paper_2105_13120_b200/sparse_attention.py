@@ -37,7 +37,7 @@ import torch
 
 from . import engine
 from . import tensor_ops as ops
-from ._native import BF16, check, lib
+from ._native import BF16, F32, check, lib
 from .cluster import CommLedger, resolve_executor
 from .config import SparseAttentionConfig
 from .errors import NumericError, ShapeError
@@ -134,7 +134,7 @@ def _project(q, k, v, e, f, kdim):
         part = ops.matmul(blocks, x.reshape(n, b * z, c, a))             # [N][B*Z][K][A] fp32
         low = torch.empty((b, z, kdim, a), dtype=torch.bfloat16, device=q.device)
         per_rank = b * z * kdim * a
-        check(lib().rsa_sum_ranks(part.data_ptr(), n, per_rank, per_rank, low.data_ptr(), BF16,
+        check(lib().rsa_sum_ranks(part.data_ptr(), F32, n, per_rank, per_rank, low.data_ptr(), BF16,
                                   torch.cuda.current_stream(q.device).cuda_stream), "rsa_sum_ranks")
         out.append(low)
     return out[0], out[1]

@@ -24,7 +24,7 @@ def test_embed_and_backward_match_torch():
     assert torch.allclose(x.float(), want, atol=2e-2, rtol=1e-2)
     dx = torch.randn((n, b, c, h), generator=g, device=dev).to(torch.bfloat16)
     dtok = torch.zeros((vocab, h), device=dev)
-    dpos = torch.zeros((n * c, h), device=dev)
+    dpos = torch.empty((n * c, h), device=dev)
     bert.embed_backward(ids, dx, dtok, dpos)
     wt = torch.zeros_like(dtok).index_add_(0, ids.reshape(-1).long(), dx.reshape(-1, h).float())
     wp = torch.zeros_like(dpos).index_add_(0, positions.reshape(-1), dx.reshape(-1, h).float())
