@@ -28,6 +28,7 @@ namespace {
 
 struct StreamArgs {
   CUtensorMap tq, tk, tv, tdo;  // q / dO': query rows (chunk); k / v: key rows (key_chunk)
+  CUtensorMap tm, td;           // rowmax / dvec as 128-row boxes (bwd_kv_stream)
   Geo g;
   int ck;    // keys per origin chunk
   float sl;  // scale * log2(e)
@@ -42,17 +43,28 @@ __device__ __forceinline__ int64_t row_index(const Geo& g, int d, int b, int z, 
 }
 
 // ============================================================ dK / dV
+//
+// The transposed formulation: a CTA owns a key tile, so every product is written with the
+// keys on the TMEM lanes.  S^T = K Q^T and dP'^T = V dO'^T come from shared memory; the
+// epilogue thread of key k turns its row of S^T into P~^T (the forward's exp2 of the same
+// score, with each query's own reference point) and, with dP'^T, into
+// dS^T = P~^T (dP'^T - D') -- and writes both straight back to TMEM (tcgen05.st), where
+// they are the A operands of dV += P~^T dO' and dK += dS^T Q (the "TS" tcgen05.mma form:
+// A from TMEM, so a 128 x 64 x 16 product reads only its 2 KB B operand from shared memory
+// and runs at the 32-clk math rate instead of 48).  Nothing the epilogue produces goes
+// through shared memory: no proxy fence, no write-after-read hazard on a P slot.
+// The per-query statistics (m, D') arrive by TMA with their query tile.
 
-constexpr int KS_ST = 3;                     // (Q, dO') stages
-constexpr int KS_P = 2;                      // P~ / dS slots
+constexpr int KS_ST = 3;                     // (Q, dO', m, D') stages
+constexpr uint32_t KS_STAGE = 2 * TILE + 2 * TR * 4;
 constexpr uint32_t KS_OFF_KV = 0;            // [buffer][K | V]
-constexpr uint32_t KS_OFF_ST = 4 * TILE;     // [stage][Q | dO']
-constexpr uint32_t KS_OFF_P = KS_OFF_ST + KS_ST * 2 * TILE;
-constexpr uint32_t KS_OFF_BAR = KS_OFF_P + KS_P * PTILE;
+constexpr uint32_t KS_OFF_ST = 4 * TILE;     // [stage][Q | dO' | m | D']
+constexpr uint32_t KS_OFF_BAR = KS_OFF_ST + KS_ST * KS_STAGE;
 constexpr uint32_t KS_SMEM = KS_OFF_BAR + 512 + 1024;
 static_assert(KS_SMEM <= 232448, "bwd_kv_stream smem over the sm_100 per-CTA limit");
-// TMEM: S [0,128), dP' x 2 [128,384), dV [384,448), dK [448,512)
-constexpr uint32_t KS_COL_S = 0, KS_COL_DP = 128, KS_COL_DV = 384, KS_COL_DK = 448;
+// TMEM: S^T [0,128), dP'^T [128,256), P~^T bf16 [256,320), dS^T bf16 [320,384), dV [384,448), dK [448,512)
+constexpr uint32_t KS_COL_S = 0, KS_COL_DP = 128, KS_COL_P = 256, KS_COL_DS = 320, KS_COL_DV = 384,
+                   KS_COL_DK = 448;
 
 __global__ void __launch_bounds__(NTHREADS, 1) bwd_kv_stream_kernel(const __grid_constant__ StreamArgs p) {
   uint8_t* smem = smem_base();
@@ -60,9 +72,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kv_stream_kernel(const __grid
   uint64_t *kv_full = bar, *kv_empty = bar + 2;
   uint64_t *ld_full = bar + 4, *ld_empty = ld_full + KS_ST;
   uint64_t *s_full = ld_empty + KS_ST, *s_empty = s_full + 1;
-  uint64_t *dp_full = s_empty + 1, *dp_empty = dp_full + 2;
-  uint64_t *p_full = dp_empty + 2, *p_read = p_full + KS_P, *ds_full = p_read + KS_P, *ps_empty = ds_full + KS_P;
-  uint64_t *acc_full = ps_empty + KS_P, *acc_empty = acc_full + 1;
+  uint64_t *dp_full = s_empty + 1, *dp_empty = dp_full + 1;
+  uint64_t *p_full = dp_empty + 1, *p_empty = p_full + 1, *ds_full = p_empty + 1, *ds_empty = ds_full + 1;
+  uint64_t *acc_full = ds_empty + 1, *acc_empty = acc_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
 
   const Geo& g = p.g;
@@ -74,19 +86,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kv_stream_kernel(const __grid
 
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&kv_full[s], 1), mbar_init(&kv_empty[s], 1);
-      mbar_init(&dp_full[s], 1), mbar_init(&dp_empty[s], EPI_WARPS);
-    }
+    for (int s = 0; s < 2; ++s) mbar_init(&kv_full[s], 1), mbar_init(&kv_empty[s], 1);
     for (int s = 0; s < KS_ST; ++s) mbar_init(&ld_full[s], 1), mbar_init(&ld_empty[s], 1);
-    for (int s = 0; s < KS_P; ++s) {
-      mbar_init(&p_full[s], EPI_WARPS), mbar_init(&p_read[s], 1);
-      mbar_init(&ds_full[s], EPI_WARPS), mbar_init(&ps_empty[s], 1);
-    }
     mbar_init(s_full, 1), mbar_init(s_empty, EPI_WARPS);
+    mbar_init(dp_full, 1), mbar_init(dp_empty, EPI_WARPS);
+    mbar_init(p_full, EPI_WARPS), mbar_init(p_empty, 1);
+    mbar_init(ds_full, EPI_WARPS), mbar_init(ds_empty, 1);
     mbar_init(acc_full, 1), mbar_init(acc_empty, EPI_WARPS);
     fence_barrier_init();
     tma_prefetch(&p.tq), tma_prefetch(&p.tk), tma_prefetch(&p.tv), tma_prefetch(&p.tdo);
+    tma_prefetch(&p.tm), tma_prefetch(&p.td);
   }
   tc_fence_before();
   __syncthreads();
@@ -110,77 +119,77 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kv_stream_kernel(const __grid
         for (int t = 0, d = 0, r0 = 0; t < T; ++t, r0 = r0 + TR >= nrt * TR ? (++d, 0) : r0 + TR) {
           const uint32_t s = lq.slot(KS_ST);
           mbar_wait(&ld_empty[s], lq.phase(KS_ST) ^ 1);
-          mbar_arrive_expect_tx(&ld_full[s], 2 * TILE);
-          uint8_t* st = smem + KS_OFF_ST + s * 2 * TILE;
+          mbar_arrive_expect_tx(&ld_full[s], KS_STAGE);
+          uint8_t* st = smem + KS_OFF_ST + s * KS_STAGE;
           tma_load_4d(st, &p.tq, &ld_full[s], 0, r0, z, d * g.B + b);
           tma_load_4d(st + TILE, &p.tdo, &ld_full[s], 0, r0, z, d * g.B + b);
+          tma_load_3d(st + 2 * TILE, &p.tm, &ld_full[s], r0, z, d * g.B + b);
+          tma_load_3d(st + 2 * TILE + TR * 4, &p.td, &ld_full[s], r0, z, d * g.B + b);
           ++lq.i;
         }
       }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
-    const uint32_t idesc_s = idesc_bf16_f32(TR, TK, 0, 0);   // Q (K-major) x K (K-major) -> 128 x 128
-    const uint32_t idesc_kv = idesc_bf16_f32(TK, HD, 1, 1);  // P~^T / dS^T (MN) x dO' / Q (MN) -> 128 x 64
-    Pos lq_s, lq_d, lq_v, lq_k, dpq, pq_v, pq_k;
-    uint32_t it = 0;
+    const uint32_t idesc_s = idesc_bf16_f32(TK, TR, 0, 0);   // K (K-major) x Q (K-major) -> keys x queries
+    const uint32_t idesc_ts = idesc_bf16_f32(TK, HD, 0, 1);  // P~^T / dS^T (TMEM) x dO' / Q (MN-major)
+    Pos lq_s, lq_d, lq_v, lq_k;
+    uint32_t n_s = 0, n_d = 0, n_p = 0, n_ds = 0, it = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
       const uint32_t kb = it & 1;
       const uint32_t ka = smem_u32(smem + KS_OFF_KV + kb * 2 * TILE), va = ka + TILE;
       mbar_wait(&kv_full[kb], (it >> 1) & 1);
       mbar_wait(acc_empty, (it & 1) ^ 1);
-      auto issue_s = [&]() {  // S(t) = Q K^T into the single S buffer
+      auto issue_s = [&]() {  // S^T(t) = K Q^T
         const uint32_t s = lq_s.slot(KS_ST);
         mbar_wait(&ld_full[s], lq_s.phase(KS_ST));
-        mbar_wait(s_empty, (lq_s.i & 1) ^ 1);
+        mbar_wait(s_empty, (n_s & 1) ^ 1);
         tc_fence_after();
-        const uint32_t qa = smem_u32(smem + KS_OFF_ST + s * 2 * TILE);
+        const uint32_t qa = smem_u32(smem + KS_OFF_ST + s * KS_STAGE);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
-          umma_bf16_ws(tmem + KS_COL_S, smem_desc_sw128(qa + k * 32, 0, 1024), smem_desc_sw128(ka + k * 32, 0, 1024),
+          umma_bf16_ws(tmem + KS_COL_S, smem_desc_sw128(ka + k * 32, 0, 1024), smem_desc_sw128(qa + k * 32, 0, 1024),
                        idesc_s, k > 0);
         umma_commit_ws(s_full);
-        ++lq_s.i;
+        ++lq_s.i, ++n_s;
       };
-      auto issue_dp = [&]() {  // dP'(t) = dO' V^T
-        const uint32_t s = lq_d.slot(KS_ST), db = dpq.slot(2);
+      auto issue_dp = [&]() {  // dP'^T(t) = V dO'^T
+        const uint32_t s = lq_d.slot(KS_ST);
         mbar_wait(&ld_full[s], lq_d.phase(KS_ST));
-        mbar_wait(&dp_empty[db], dpq.phase(2) ^ 1);
+        mbar_wait(dp_empty, (n_d & 1) ^ 1);
         tc_fence_after();
-        const uint32_t doa = smem_u32(smem + KS_OFF_ST + s * 2 * TILE) + TILE;
+        const uint32_t doa = smem_u32(smem + KS_OFF_ST + s * KS_STAGE) + TILE;
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
-          umma_bf16_ws(tmem + KS_COL_DP + db * TK, smem_desc_sw128(doa + k * 32, 0, 1024),
-                       smem_desc_sw128(va + k * 32, 0, 1024), idesc_s, k > 0);
-        umma_commit_ws(&dp_full[db]);
-        ++lq_d.i, ++dpq.i;
+          umma_bf16_ws(tmem + KS_COL_DP, smem_desc_sw128(va + k * 32, 0, 1024), smem_desc_sw128(doa + k * 32, 0, 1024),
+                       idesc_s, k > 0);
+        umma_commit_ws(dp_full);
+        ++lq_d.i, ++n_d;
       };
-      auto issue_dv = [&](int t) {  // dV += P~^T dO' once the epilogue has written P~(t)
-        const uint32_t s = lq_v.slot(KS_ST), ps = pq_v.slot(KS_P);
-        mbar_wait(&p_full[ps], pq_v.phase(KS_P));
+      auto issue_dv = [&](int t) {  // dV += P~^T dO' (A from TMEM) once the epilogue has stored P~^T(t)
+        const uint32_t s = lq_v.slot(KS_ST);
+        mbar_wait(p_full, n_p & 1);
         tc_fence_after();
-        const uint32_t pa = smem_u32(smem + KS_OFF_P + ps * PTILE);
-        const uint32_t doa = smem_u32(smem + KS_OFF_ST + s * 2 * TILE) + TILE;
+        const uint32_t doa = smem_u32(smem + KS_OFF_ST + s * KS_STAGE) + TILE;
+#pragma unroll
+        for (int k = 0; k < TR / 16; ++k)  // 16 queries per step: 8 TMEM columns of A, 2 KB of B
+          umma_bf16_ts_ws(tmem + KS_COL_DV, tmem + KS_COL_P + 8 * k, smem_desc_sw128(doa + k * 2048, ATOM, 1024),
+                          idesc_ts, (t | k) != 0);
+        umma_commit_ws(p_empty);  // P~^T consumed: the next step's may be stored
+        ++lq_v.i, ++n_p;
+      };
+      auto issue_dk = [&](int t) {  // dK += dS^T Q (A from TMEM) once the epilogue has stored dS^T(t)
+        const uint32_t s = lq_k.slot(KS_ST);
+        mbar_wait(ds_full, n_ds & 1);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(smem + KS_OFF_ST + s * KS_STAGE);
 #pragma unroll
         for (int k = 0; k < TR / 16; ++k)
-          umma_bf16_ws(tmem + KS_COL_DV, smem_desc_sw128(pa + k * 2048, ATOM, 1024),
-                       smem_desc_sw128(doa + k * 2048, ATOM, 1024), idesc_kv, (t | k) != 0);
-        umma_commit_ws(&p_read[ps]);  // P~ consumed: dS may overwrite it
-        ++lq_v.i, ++pq_v.i;
-      };
-      auto issue_dk = [&](int t) {  // dK += dS^T Q once the epilogue has written dS(t)
-        const uint32_t s = lq_k.slot(KS_ST), ps = pq_k.slot(KS_P);
-        mbar_wait(&ds_full[ps], pq_k.phase(KS_P));
-        tc_fence_after();
-        const uint32_t dsa = smem_u32(smem + KS_OFF_P + ps * PTILE);
-        const uint32_t qa = smem_u32(smem + KS_OFF_ST + s * 2 * TILE);
-#pragma unroll
-        for (int k = 0; k < TR / 16; ++k)
-          umma_bf16_ws(tmem + KS_COL_DK, smem_desc_sw128(dsa + k * 2048, ATOM, 1024),
-                       smem_desc_sw128(qa + k * 2048, ATOM, 1024), idesc_kv, (t | k) != 0);
-        umma_commit_ws(&ld_empty[s]);
-        umma_commit_ws(&ps_empty[ps]);
-        ++lq_k.i, ++pq_k.i;
+          umma_bf16_ts_ws(tmem + KS_COL_DK, tmem + KS_COL_DS + 8 * k, smem_desc_sw128(qa + k * 2048, ATOM, 1024),
+                          idesc_ts, (t | k) != 0);
+        umma_commit_ws(ds_empty);
+        umma_commit_ws(&ld_empty[s]);  // the stage's last readers: dK (Q) and the epilogue (m, D', before ds_full)
+        ++lq_k.i, ++n_ds;
       };
       issue_s();
       issue_dp();
@@ -195,81 +204,75 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kv_stream_kernel(const __grid
     }
   } else {
     // ------------------------------------------------------------ epilogue
+    // warp w: TMEM lanes 32*(w%4).. = keys of the tile; query columns half*64 .. +63
     const uint32_t quad = warp & 3;
     const int half = (warp - 2) >> 2;
     const int r = quad * 32 + lane;
     const uint32_t lane_base = (quad * 32u) << 16;
     const float sl = p.sl;
-    Pos sq, dpq, pq;
-    uint32_t it = 0;
+    Pos lq;
+    uint32_t n_s = 0, n_d = 0, n_p = 0, n_ds = 0, it = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
       const int kt = item % ntk, bz = (item / ntk) % BZ, jo = item / (ntk * BZ);
       const int b = bz / g.Z, z = bz % g.Z, k0 = kt * TK;
-      const int nvalid = min(TK, p.ck - k0) - half * 64;
-      int d = 0, r0 = 0;
-      float m_next = r < g.c ? __ldg(p.rowmax + row_index(g, 0, b, z, r)) : 0.f;
-      float d_next = r < g.c ? __ldg(p.dvec + row_index(g, 0, b, z, r)) : 0.f;
-      for (int t = 0; t < T; ++t) {
-        const float msl = m_next, dval = d_next;
-        if (r0 + TR >= nrt * TR) r0 = 0, ++d;
-        else r0 += TR;
-        if (t + 1 < T) {  // the next step's row statistics now: their latency hides behind this step
-          const int nrow = r0 + r;
-          m_next = nrow < g.c ? __ldg(p.rowmax + row_index(g, d, b, z, nrow)) : 0.f;
-          d_next = nrow < g.c ? __ldg(p.dvec + row_index(g, d, b, z, nrow)) : 0.f;
-        }
-        // S -> P~ (the forward's values, zero past the last key)
+      for (int t = 0, r0 = 0; t < T; ++t, r0 = r0 + TR >= nrt * TR ? 0 : r0 + TR) {
+        const int nvalid = min(TR, g.c - r0) - half * 64;  // valid query columns of this half
+        const uint32_t s = lq.slot(KS_ST);
+        const uint32_t stat = smem_u32(smem + KS_OFF_ST + s * KS_STAGE + 2 * TILE) + half * 64 * 4;
+        mbar_wait(&ld_full[s], lq.phase(KS_ST));  // m and D' of the step's queries
+        // S^T -> P~^T (the forward's values), back to TMEM as bf16 pairs along the queries
         uint32_t w[32];
-        mbar_wait(s_full, sq.i & 1);
-        tc_fence_after();
-        {  // both 32-column loads in flight before one wait: TMEM loads are latency-bound
-          float v[64];
+        {
+          float v[64], m[64];
+          mbar_wait(s_full, n_s & 1);
+          tc_fence_after();
           __syncwarp();
           tmem_ld32(tmem + lane_base + KS_COL_S + half * 64, v);
           tmem_ld32(tmem + lane_base + KS_COL_S + half * 64 + 32, v + 32);
-          tmem_ld_wait();
-          exp2_pack32(v, nvalid, sl, msl, w);
-          exp2_pack32(v + 32, nvalid - 32, sl, msl, w + 16);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(s_empty);
-        ++sq.i;
-        const uint32_t ps = pq.slot(KS_P);
-        const uint32_t pt = smem_u32(smem + KS_OFF_P + ps * PTILE) + half * ATOM;
-        mbar_wait(&ps_empty[ps], pq.phase(KS_P) ^ 1);  // dK(t-2) has read this slot's dS
 #pragma unroll
-        for (int q4 = 0; q4 < 8; ++q4)
-          st_shared_v4(pt + sw128_offset(r, q4), w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2], w[4 * q4 + 3]);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[ps]);
-        // dP' -> dS = P~ (dP' - D'), over P~ once dV has read it
-        const uint32_t db = dpq.slot(2);
-        mbar_wait(&dp_full[db], dpq.phase(2));
-        tc_fence_after();
-        const uint64_t nd = neg_pair(dval);
-        {
-          float dp[64];
+          for (int j = 0; j < 64; j += 4) ld_shared_f4(stat + j * 4, m + j);
+          tmem_ld_wait();
+          tc_fence_before();
           __syncwarp();
-          tmem_ld32(tmem + lane_base + KS_COL_DP + db * TK + half * 64, dp);
-          tmem_ld32(tmem + lane_base + KS_COL_DP + db * TK + half * 64 + 32, dp + 32);
-          tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) w[e] = ds_pair(w[e], dp[2 * e], dp[2 * e + 1], nd);
+          if (lane == 0) mbar_arrive(s_empty);
+          ++n_s;
+          exp2_pack32_cols(v, nvalid, sl, m, w);
+          exp2_pack32_cols(v + 32, nvalid - 32, sl, m + 32, w + 16);
         }
+        mbar_wait(p_empty, (n_p & 1) ^ 1);  // dV(t-1) has read the previous P~^T
+        tc_fence_after();
+        tmem_st32(tmem + lane_base + KS_COL_P + half * 32, w);
+        tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&dp_empty[db]);
-        ++dpq.i;
-        mbar_wait(&p_read[ps], pq.phase(KS_P));
+        if (lane == 0) mbar_arrive(p_full);
+        ++n_p;
+        // dP'^T -> dS^T = P~^T (dP'^T - D') (the 1/sqrt(A) scale is applied to dK at the end)
+        {
+          float dp[64], dd[64];
+          mbar_wait(dp_full, n_d & 1);
+          tc_fence_after();
+          __syncwarp();
+          tmem_ld32(tmem + lane_base + KS_COL_DP + half * 64, dp);
+          tmem_ld32(tmem + lane_base + KS_COL_DP + half * 64 + 32, dp + 32);
 #pragma unroll
-        for (int q4 = 0; q4 < 8; ++q4)
-          st_shared_v4(pt + sw128_offset(r, q4), w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2], w[4 * q4 + 3]);
-        fence_proxy_async_smem();
+          for (int j = 0; j < 64; j += 4) ld_shared_f4(stat + TR * 4 + j * 4, dd + j);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dp_empty);
+          ++n_d;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) w[e] = ds_pair2(w[e], dp[2 * e], dp[2 * e + 1], dd[2 * e], dd[2 * e + 1]);
+        }
+        mbar_wait(ds_empty, (n_ds & 1) ^ 1);  // dK(t-1) has read the previous dS^T
+        tc_fence_after();
+        tmem_st32(tmem + lane_base + KS_COL_DS + half * 32, w);
+        tmem_st_wait();
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&ds_full[ps]);
-        ++pq.i;
+        if (lane == 0) mbar_arrive(ds_full);
+        ++n_ds, ++lq.i;
       }
       mbar_wait(acc_full, it & 1);
       tc_fence_after();
@@ -517,6 +520,7 @@ bool stream_args(StreamArgs* a, const rsa_geom* g, rsa_view q, rsa_view k, rsa_v
   if (!head_map(&a->tq, q, g, g->n_rank) || !head_map(&a->tdo, dout, g, g->n_rank) ||
       !head_map(&a->tk, k, g, g->n_org, key_chunk(g)) || !head_map(&a->tv, v, g, g->n_org, key_chunk(g)))
     return false;
+  if (!rows_map(&a->tm, rowmax, g, g->n_rank) || !rows_map(&a->td, dvec, g, g->n_rank)) return false;
   a->g = to_geo(g);
   a->ck = key_chunk(g);
   a->sl = g->scale * LOG2E;

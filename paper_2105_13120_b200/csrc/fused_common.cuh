@@ -72,6 +72,24 @@ __device__ __forceinline__ uint32_t ds_pair(uint32_t pw, float dp0, float dp1, u
   return pack_bf16(a, b);
 }
 
+// ds_pair with a different D for each of the two elements (the transposed backward walks a
+// key across queries, each query with its own D): the same roundings element for element.
+__device__ __forceinline__ uint32_t ds_pair2(uint32_t pw, float dp0, float dp1, float d0, float d1) {
+  uint64_t x, pp, nd;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(dp0), "f"(dp1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(nd) : "f"(-d0), "f"(-d1));
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(nd));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pp) : "f"(__uint_as_float(pw << 16)), "f"(__uint_as_float(pw & 0xFFFF0000u)));
+  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(pp));
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x));
+  return pack_bf16(a, b);
+}
+
+__device__ __forceinline__ void ld_shared_f4(uint32_t addr, float* v) {
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(addr));
+}
+
 // dS = P * (dP - D) for 32 keys of row r in place over the bf16 P tile (columns
 // col0..col0+31 of a SWIZZLE_128B [64-col atom][128 rows] tile); dp: the fp32 dP row
 // chunk, nd: (-D, -D).
@@ -129,24 +147,52 @@ __device__ __forceinline__ void minmax32(const float* v, int nvalid, float& mx_o
 }
 
 // The factored panel's values: 32 scores of one row (32 consecutive keys starting at a
-// multiple of 32) -> 16 packed bf16 pairs of P~ = 2^(v*sl - msl), zero past nvalid.  One
-// exp2 in four runs on the FMA pipe (exp2_poly<3>), the rest on MUFU.  The forward that
-// writes the panel (rsa_fwd_factored) and the stream-mode backward that recomputes it
-// (bwd_stream.cu) both call this, on bitwise-identical tensor-core scores, so the
-// recomputed P~ equals the stored panel bit for bit.
+// multiple of 32) -> 16 packed bf16 pairs of P~ = 2^(v*sl - msl), zero past nvalid, every
+// exp2 on MUFU.  The forward that writes the panel (rsa_fwd_factored) and the stream-mode
+// backward that recomputes it (bwd_stream.cu, which walks a KEY's scores across queries)
+// apply this same per-element rounding to bitwise-identical tensor-core scores, so the
+// recomputed P~ equals the stored panel bit for bit.  (An FMA-pipe polynomial for one exp2
+// in four was measured neutral in the forward, and its key-position pattern cannot be
+// followed by the transposed backward without computing both forms.)
 __device__ __forceinline__ void exp2_pack32(const float* v, int nvalid, float sl, float msl, uint32_t* w) {
   if (nvalid >= 32) {
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const float x0 = fmaf(v[2 * e], sl, -msl), x1 = fmaf(v[2 * e + 1], sl, -msl);
-      w[e] = pack_bf16(fast_exp2(x0), (e & 1) ? exp2_poly<3>(x1) : fast_exp2(x1));
-    }
+    for (int e = 0; e < 16; ++e)
+      w[e] = pack_bf16(fast_exp2(fmaf(v[2 * e], sl, -msl)), fast_exp2(fmaf(v[2 * e + 1], sl, -msl)));
   } else {
 #pragma unroll
     for (int e = 0; e < 16; ++e)
       w[e] = pack_bf16(2 * e < nvalid ? fast_exp2(fmaf(v[2 * e], sl, -msl)) : 0.f,
                        2 * e + 1 < nvalid ? fast_exp2(fmaf(v[2 * e + 1], sl, -msl)) : 0.f);
   }
+}
+
+// The transposed form: 32 scores of one KEY against 32 consecutive queries, each with its
+// own reference point msl[j] (one per query row), zero past nvalid queries.  Element for
+// element the same arithmetic as exp2_pack32.
+__device__ __forceinline__ void exp2_pack32_cols(const float* v, int nvalid, float sl, const float* msl, uint32_t* w) {
+  if (nvalid >= 32) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      w[e] = pack_bf16(fast_exp2(fmaf(v[2 * e], sl, -msl[2 * e])), fast_exp2(fmaf(v[2 * e + 1], sl, -msl[2 * e + 1])));
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      w[e] = pack_bf16(2 * e < nvalid ? fast_exp2(fmaf(v[2 * e], sl, -msl[2 * e])) : 0.f,
+                       2 * e + 1 < nvalid ? fast_exp2(fmaf(v[2 * e + 1], sl, -msl[2 * e + 1])) : 0.f);
+  }
+}
+
+// fp32 row statistics [rank][b][z][row] as a 3-D TMA map (row, z, b*rank) with 128-row boxes:
+// a query tile's 512 bytes land in shared memory next to its Q / dO tiles, rows past the
+// chunk zero-filled.
+inline bool rows_map(CUtensorMap* m, const float* base, const rsa_geom* g, int nrank) {
+  if (!base || (reinterpret_cast<uintptr_t>(base) & 15) || (g->chunk * 4) % 16)
+    return fail(RSA_ERR_UNSUPPORTED, "row statistics must be 16-byte aligned with chunk %% 4 == 0"), false;
+  uint64_t dims[3] = {uint64_t(g->chunk), uint64_t(g->heads), uint64_t(g->batch) * nrank};
+  uint64_t str[2] = {uint64_t(g->chunk) * 4, uint64_t(g->heads) * g->chunk * 4};
+  uint32_t box[3] = {uint32_t(TR), 1, 1};
+  return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
 struct OutView {  // strided output [rank][b][z][row][a]
