@@ -305,17 +305,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kv_stream_kernel(const __grid
 }
 
 // ================================================================== dQ
+//
+// Query rows on the TMEM lanes (the forward's orientation): the epilogue turns S into P~ and,
+// with dP', into dS, and writes dS straight to TMEM, where it is the A operand of
+// dQ += dS K (TS form: only the K tile is read from shared memory).
 
-constexpr int QS_ST = 3;                    // (K, V) stages
-constexpr int QS_DS = 2;                    // dS slots
+constexpr int QS_ST = 4;                    // (K, V) stages
 constexpr uint32_t QS_OFF_QD = 0;           // [buffer][Q | dO']
 constexpr uint32_t QS_OFF_ST = 4 * TILE;    // [stage][K | V]
-constexpr uint32_t QS_OFF_DS = QS_OFF_ST + QS_ST * 2 * TILE;
-constexpr uint32_t QS_OFF_BAR = QS_OFF_DS + QS_DS * PTILE;
+constexpr uint32_t QS_OFF_BAR = QS_OFF_ST + QS_ST * 2 * TILE;
 constexpr uint32_t QS_SMEM = QS_OFF_BAR + 512 + 1024;
 static_assert(QS_SMEM <= 232448, "bwd_q_stream smem over the sm_100 per-CTA limit");
-// TMEM: S [0,128), dP' x 2 [128,384), dQ x 2 [384,512)
-constexpr uint32_t QS_COL_S = 0, QS_COL_DP = 128, QS_COL_DQ = 384;
+// TMEM: S [0,128), dP' [128,256), dS bf16 [256,320), dQ x 2 [320,448)
+constexpr uint32_t QS_COL_S = 0, QS_COL_DP = 128, QS_COL_DS = 256, QS_COL_DQ = 320;
 
 __global__ void __launch_bounds__(NTHREADS, 1) bwd_q_stream_kernel(const __grid_constant__ StreamArgs p) {
   uint8_t* smem = smem_base();
@@ -323,9 +325,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_q_stream_kernel(const __grid_
   uint64_t *qd_full = bar, *qd_empty = bar + 2;
   uint64_t *ld_full = bar + 4, *ld_empty = ld_full + QS_ST;
   uint64_t *s_full = ld_empty + QS_ST, *s_empty = s_full + 1;
-  uint64_t *dp_full = s_empty + 1, *dp_empty = dp_full + 2;
-  uint64_t *ds_full = dp_empty + 2, *ds_empty = ds_full + QS_DS;
-  uint64_t *acc_full = ds_empty + QS_DS, *acc_empty = acc_full + 2;
+  uint64_t *dp_full = s_empty + 1, *dp_empty = dp_full + 1;
+  uint64_t *ds_full = dp_empty + 1, *ds_empty = ds_full + 1;
+  uint64_t *acc_full = ds_empty + 1, *acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const Geo& g = p.g;
@@ -339,12 +341,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_q_stream_kernel(const __grid_
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(&qd_full[s], 1), mbar_init(&qd_empty[s], 1);
-      mbar_init(&dp_full[s], 1), mbar_init(&dp_empty[s], EPI_WARPS);
       mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], EPI_WARPS);
     }
     for (int s = 0; s < QS_ST; ++s) mbar_init(&ld_full[s], 1), mbar_init(&ld_empty[s], 1);
-    for (int s = 0; s < QS_DS; ++s) mbar_init(&ds_full[s], EPI_WARPS), mbar_init(&ds_empty[s], 1);
     mbar_init(s_full, 1), mbar_init(s_empty, EPI_WARPS);
+    mbar_init(dp_full, 1), mbar_init(dp_empty, EPI_WARPS);
+    mbar_init(ds_full, EPI_WARPS), mbar_init(ds_empty, 1);
     fence_barrier_init();
     tma_prefetch(&p.tq), tma_prefetch(&p.tk), tma_prefetch(&p.tv), tma_prefetch(&p.tdo);
   }
@@ -379,9 +381,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_q_stream_kernel(const __grid_
     }
   } else if (warp == 1) {
     const uint32_t idesc_s = idesc_bf16_f32(TR, TK, 0, 0);   // Q x K^T, dO' x V^T (K-major both)
-    const uint32_t idesc_dq = idesc_bf16_f32(TR, HD, 0, 1);  // dS (K-major over keys) x K (MN-major)
-    Pos lq_s, lq_d, lq_q, dpq, dsq;
-    uint32_t it = 0;
+    const uint32_t idesc_ts = idesc_bf16_f32(TR, HD, 0, 1);  // dS (TMEM) x K (MN-major)
+    Pos lq_s, lq_d, lq_q;
+    uint32_t n_s = 0, n_d = 0, n_ds = 0, it = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
       const uint32_t qb = it & 1;
       const uint32_t qa = smem_u32(smem + QS_OFF_QD + qb * 2 * TILE), doa = qa + TILE;
@@ -390,7 +392,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_q_stream_kernel(const __grid_
       auto issue_s = [&]() {
         const uint32_t s = lq_s.slot(QS_ST);
         mbar_wait(&ld_full[s], lq_s.phase(QS_ST));
-        mbar_wait(s_empty, (lq_s.i & 1) ^ 1);
+        mbar_wait(s_empty, (n_s & 1) ^ 1);
         tc_fence_after();
         const uint32_t ka = smem_u32(smem + QS_OFF_ST + s * 2 * TILE);
 #pragma unroll
@@ -398,34 +400,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_q_stream_kernel(const __grid_
           umma_bf16_ws(tmem + QS_COL_S, smem_desc_sw128(qa + k * 32, 0, 1024), smem_desc_sw128(ka + k * 32, 0, 1024),
                        idesc_s, k > 0);
         umma_commit_ws(s_full);
-        ++lq_s.i;
+        ++lq_s.i, ++n_s;
       };
       auto issue_dp = [&]() {
-        const uint32_t s = lq_d.slot(QS_ST), db = dpq.slot(2);
+        const uint32_t s = lq_d.slot(QS_ST);
         mbar_wait(&ld_full[s], lq_d.phase(QS_ST));
-        mbar_wait(&dp_empty[db], dpq.phase(2) ^ 1);
+        mbar_wait(dp_empty, (n_d & 1) ^ 1);
         tc_fence_after();
         const uint32_t va = smem_u32(smem + QS_OFF_ST + s * 2 * TILE) + TILE;
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
-          umma_bf16_ws(tmem + QS_COL_DP + db * TK, smem_desc_sw128(doa + k * 32, 0, 1024),
-                       smem_desc_sw128(va + k * 32, 0, 1024), idesc_s, k > 0);
-        umma_commit_ws(&dp_full[db]);
-        ++lq_d.i, ++dpq.i;
+          umma_bf16_ws(tmem + QS_COL_DP, smem_desc_sw128(doa + k * 32, 0, 1024), smem_desc_sw128(va + k * 32, 0, 1024),
+                       idesc_s, k > 0);
+        umma_commit_ws(dp_full);
+        ++lq_d.i, ++n_d;
       };
       auto issue_dq = [&](int t) {
-        const uint32_t s = lq_q.slot(QS_ST), ds = dsq.slot(QS_DS);
-        mbar_wait(&ds_full[ds], dsq.phase(QS_DS));
+        const uint32_t s = lq_q.slot(QS_ST);
+        mbar_wait(ds_full, n_ds & 1);
         tc_fence_after();
-        const uint32_t dsa = smem_u32(smem + QS_OFF_DS + ds * PTILE);
         const uint32_t ka = smem_u32(smem + QS_OFF_ST + s * 2 * TILE);
 #pragma unroll
-        for (int k = 0; k < TK / 16; ++k)
-          umma_bf16_ws(tmem + QS_COL_DQ + qb * HD, smem_desc_sw128(dsa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
-                       smem_desc_sw128(ka + k * 2048, ATOM, 1024), idesc_dq, (t | k) != 0);
+        for (int k = 0; k < TK / 16; ++k)  // 16 keys per step: 8 TMEM columns of dS, 2 KB of K
+          umma_bf16_ts_ws(tmem + QS_COL_DQ + qb * HD, tmem + QS_COL_DS + 8 * k,
+                          smem_desc_sw128(ka + k * 2048, ATOM, 1024), idesc_ts, (t | k) != 0);
+        umma_commit_ws(ds_empty);
         umma_commit_ws(&ld_empty[s]);
-        umma_commit_ws(&ds_empty[ds]);
-        ++lq_q.i, ++dsq.i;
+        ++lq_q.i, ++n_ds;
       };
       issue_s();
       issue_dp();
@@ -442,8 +443,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_q_stream_kernel(const __grid_
     const int r = quad * 32 + lane;
     const uint32_t lane_base = (quad * 32u) << 16;
     const float sl = p.sl;
-    Pos sq, dpq, dsq;
-    uint32_t it = 0;
+    uint32_t n_s = 0, n_d = 0, n_ds = 0, it = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
       const int rt = item % nrt, bz = (item / nrt) % BZ, d = item / (nrt * BZ);
       const int b = bz / g.Z, z = bz % g.Z, row = rt * TR + r;
@@ -453,47 +453,44 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_q_stream_kernel(const __grid_
       for (int t = 0, k0 = 0; t < T; ++t, k0 = k0 + TK >= ntk * TK ? 0 : k0 + TK) {
         const int nvalid = min(TK, p.ck - k0) - half * 64;
         uint32_t w[32];
-        mbar_wait(s_full, sq.i & 1);
-        tc_fence_after();
-        {  // both 32-column loads in flight before one wait: TMEM loads are latency-bound
+        {
           float v[64];
+          mbar_wait(s_full, n_s & 1);
+          tc_fence_after();
           __syncwarp();
           tmem_ld32(tmem + lane_base + QS_COL_S + half * 64, v);
           tmem_ld32(tmem + lane_base + QS_COL_S + half * 64 + 32, v + 32);
           tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(s_empty);
+          ++n_s;
           exp2_pack32(v, nvalid, sl, msl, w);
           exp2_pack32(v + 32, nvalid - 32, sl, msl, w + 16);
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(s_empty);
-        ++sq.i;
-        const uint32_t db = dpq.slot(2);
-        mbar_wait(&dp_full[db], dpq.phase(2));
-        tc_fence_after();
         {
           float dp[64];
+          mbar_wait(dp_full, n_d & 1);
+          tc_fence_after();
           __syncwarp();
-          tmem_ld32(tmem + lane_base + QS_COL_DP + db * TK + half * 64, dp);
-          tmem_ld32(tmem + lane_base + QS_COL_DP + db * TK + half * 64 + 32, dp + 32);
+          tmem_ld32(tmem + lane_base + QS_COL_DP + half * 64, dp);
+          tmem_ld32(tmem + lane_base + QS_COL_DP + half * 64 + 32, dp + 32);
           tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dp_empty);
+          ++n_d;
 #pragma unroll
           for (int e = 0; e < 32; ++e) w[e] = ds_pair(w[e], dp[2 * e], dp[2 * e + 1], nd);
         }
+        mbar_wait(ds_empty, (n_ds & 1) ^ 1);  // dQ(t-1) has read the previous dS
+        tc_fence_after();
+        tmem_st32(tmem + lane_base + QS_COL_DS + half * 32, w);
+        tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&dp_empty[db]);
-        ++dpq.i;
-        const uint32_t ds = dsq.slot(QS_DS);
-        const uint32_t dst = smem_u32(smem + QS_OFF_DS + ds * PTILE) + half * ATOM;
-        mbar_wait(&ds_empty[ds], dsq.phase(QS_DS) ^ 1);
-#pragma unroll
-        for (int q4 = 0; q4 < 8; ++q4)
-          st_shared_v4(dst + sw128_offset(r, q4), w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2], w[4 * q4 + 3]);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ds_full[ds]);
-        ++dsq.i;
+        if (lane == 0) mbar_arrive(ds_full);
+        ++n_ds;
       }
       const uint32_t ab = it & 1;
       mbar_wait(&acc_full[ab], (it >> 1) & 1);
