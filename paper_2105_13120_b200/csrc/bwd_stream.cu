@@ -15,7 +15,7 @@
 // from query rows per rank, which serves the Linformer's projected keys too.
 //
 // Two persistent, warp-specialised kernels (warp 0 TMA producer, warp 1 tcgen05.mma issuer,
-// warps 2..9 epilogue: warp w owns TMEM lanes 32*(w%4).. and column half (w-2)/4), each
+// warps 2..17 epilogue: warp w owns TMEM lanes 32*(w%4).. and column quarter (w-2)/4), each
 // accumulating in TMEM in a fixed order (deterministic, no atomics):
 //   bwd_kv_stream_kernel  item = (origin, b, z, key tile); walks every query tile:
 //                         S, dP' -> P~ to smem -> dV += P~^T dO' -> dS in place -> dK += dS^T Q
@@ -37,6 +37,13 @@ struct StreamArgs {
   OutView dk, dv, dq_acc, dq_out;
   int dkv_bf16, accumulate;
 };
+
+// 16 epilogue warps: each thread owns one TMEM lane (a key of the tile in bwd_kv_stream, a
+// query in bwd_q_stream) and a quarter of the 128 columns, so four warps per SM
+// sub-partition share the MUFU-bound exp2 and hide each other's TMEM / barrier latencies.
+constexpr int SE_WARPS = 16;
+constexpr int SE_THREADS = 64 + 32 * SE_WARPS;  // 576: at most 112 registers per thread
+constexpr int SE_COLS = 32;                     // columns per thread (128 / (SE_WARPS / 4))
 
 __device__ __forceinline__ int64_t row_index(const Geo& g, int d, int b, int z, int row) {
   return (int64_t(d * g.B + b) * g.Z + z) * g.c + row;
@@ -66,7 +73,7 @@ static_assert(KS_SMEM <= 232448, "bwd_kv_stream smem over the sm_100 per-CTA lim
 constexpr uint32_t KS_COL_S = 0, KS_COL_DP = 128, KS_COL_P = 256, KS_COL_DS = 320, KS_COL_DV = 384,
                    KS_COL_DK = 448;
 
-__global__ void __launch_bounds__(NTHREADS, 1) bwd_kv_stream_kernel(const __grid_constant__ StreamArgs p) {
+__global__ void __maxnreg__(112) bwd_kv_stream_kernel(const __grid_constant__ StreamArgs p) {
   uint8_t* smem = smem_base();
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + KS_OFF_BAR);
   uint64_t *kv_full = bar, *kv_empty = bar + 2;
@@ -88,11 +95,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kv_stream_kernel(const __grid
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) mbar_init(&kv_full[s], 1), mbar_init(&kv_empty[s], 1);
     for (int s = 0; s < KS_ST; ++s) mbar_init(&ld_full[s], 1), mbar_init(&ld_empty[s], 1);
-    mbar_init(s_full, 1), mbar_init(s_empty, EPI_WARPS);
-    mbar_init(dp_full, 1), mbar_init(dp_empty, EPI_WARPS);
-    mbar_init(p_full, EPI_WARPS), mbar_init(p_empty, 1);
-    mbar_init(ds_full, EPI_WARPS), mbar_init(ds_empty, 1);
-    mbar_init(acc_full, 1), mbar_init(acc_empty, EPI_WARPS);
+    mbar_init(s_full, 1), mbar_init(s_empty, SE_WARPS);
+    mbar_init(dp_full, 1), mbar_init(dp_empty, SE_WARPS);
+    mbar_init(p_full, SE_WARPS), mbar_init(p_empty, 1);
+    mbar_init(ds_full, SE_WARPS), mbar_init(ds_empty, 1);
+    mbar_init(acc_full, 1), mbar_init(acc_empty, SE_WARPS);
     fence_barrier_init();
     tma_prefetch(&p.tq), tma_prefetch(&p.tk), tma_prefetch(&p.tv), tma_prefetch(&p.tdo);
     tma_prefetch(&p.tm), tma_prefetch(&p.td);
@@ -204,9 +211,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kv_stream_kernel(const __grid
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    // warp w: TMEM lanes 32*(w%4).. = keys of the tile; query columns half*64 .. +63
+    // warp w: TMEM lanes 32*(w%4).. = keys of the tile; query columns part*32 .. +31
     const uint32_t quad = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int part = (warp - 2) >> 2;
     const int r = quad * 32 + lane;
     const uint32_t lane_base = (quad * 32u) << 16;
     const float sl = p.sl;
@@ -216,32 +223,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kv_stream_kernel(const __grid
       const int kt = item % ntk, bz = (item / ntk) % BZ, jo = item / (ntk * BZ);
       const int b = bz / g.Z, z = bz % g.Z, k0 = kt * TK;
       for (int t = 0, r0 = 0; t < T; ++t, r0 = r0 + TR >= nrt * TR ? 0 : r0 + TR) {
-        const int nvalid = min(TR, g.c - r0) - half * 64;  // valid query columns of this half
+        const int nvalid = min(TR, g.c - r0) - part * SE_COLS;  // valid query columns of this part
         const uint32_t s = lq.slot(KS_ST);
-        const uint32_t stat = smem_u32(smem + KS_OFF_ST + s * KS_STAGE + 2 * TILE) + half * 64 * 4;
+        const uint32_t stat = smem_u32(smem + KS_OFF_ST + s * KS_STAGE + 2 * TILE) + part * SE_COLS * 4;
         mbar_wait(&ld_full[s], lq.phase(KS_ST));  // m and D' of the step's queries
         // S^T -> P~^T (the forward's values), back to TMEM as bf16 pairs along the queries
-        uint32_t w[32];
+        uint32_t w[16];
         {
-          float v[64], m[64];
+          float v[32], m[32];
           mbar_wait(s_full, n_s & 1);
           tc_fence_after();
           __syncwarp();
-          tmem_ld32(tmem + lane_base + KS_COL_S + half * 64, v);
-          tmem_ld32(tmem + lane_base + KS_COL_S + half * 64 + 32, v + 32);
+          tmem_ld32(tmem + lane_base + KS_COL_S + part * SE_COLS, v);
 #pragma unroll
-          for (int j = 0; j < 64; j += 4) ld_shared_f4(stat + j * 4, m + j);
+          for (int j = 0; j < 32; j += 4) ld_shared_f4(stat + j * 4, m + j);
           tmem_ld_wait();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(s_empty);
           ++n_s;
           exp2_pack32_cols(v, nvalid, sl, m, w);
-          exp2_pack32_cols(v + 32, nvalid - 32, sl, m + 32, w + 16);
         }
         mbar_wait(p_empty, (n_p & 1) ^ 1);  // dV(t-1) has read the previous P~^T
         tc_fence_after();
-        tmem_st32(tmem + lane_base + KS_COL_P + half * 32, w);
+        tmem_st16(tmem + lane_base + KS_COL_P + part * 16, w);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -249,53 +254,52 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kv_stream_kernel(const __grid
         ++n_p;
         // dP'^T -> dS^T = P~^T (dP'^T - D') (the 1/sqrt(A) scale is applied to dK at the end)
         {
-          float dp[64], dd[64];
+          float dp[32], dd[32];
           mbar_wait(dp_full, n_d & 1);
           tc_fence_after();
           __syncwarp();
-          tmem_ld32(tmem + lane_base + KS_COL_DP + half * 64, dp);
-          tmem_ld32(tmem + lane_base + KS_COL_DP + half * 64 + 32, dp + 32);
+          tmem_ld32(tmem + lane_base + KS_COL_DP + part * SE_COLS, dp);
 #pragma unroll
-          for (int j = 0; j < 64; j += 4) ld_shared_f4(stat + TR * 4 + j * 4, dd + j);
+          for (int j = 0; j < 32; j += 4) ld_shared_f4(stat + TR * 4 + j * 4, dd + j);
           tmem_ld_wait();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(dp_empty);
           ++n_d;
 #pragma unroll
-          for (int e = 0; e < 32; ++e) w[e] = ds_pair2(w[e], dp[2 * e], dp[2 * e + 1], dd[2 * e], dd[2 * e + 1]);
+          for (int e = 0; e < 16; ++e) w[e] = ds_pair2(w[e], dp[2 * e], dp[2 * e + 1], dd[2 * e], dd[2 * e + 1]);
         }
         mbar_wait(ds_empty, (n_ds & 1) ^ 1);  // dK(t-1) has read the previous dS^T
         tc_fence_after();
-        tmem_st32(tmem + lane_base + KS_COL_DS + half * 32, w);
+        tmem_st16(tmem + lane_base + KS_COL_DS + part * 16, w);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(ds_full);
         ++n_ds, ++lq.i;
       }
+      // the key tile's dV (parts 0, 1) and dK (parts 2, 3): 32 columns per thread
       mbar_wait(acc_full, it & 1);
       tc_fence_after();
-      float dvv[32], dkv[32];
+      float acc[32];
+      const bool is_dk = part >= 2;
+      const int col = (part & 1) * 32;
       __syncwarp();
-      tmem_ld32(tmem + lane_base + KS_COL_DV + half * 32, dvv);
-      tmem_ld32(tmem + lane_base + KS_COL_DK + half * 32, dkv);
+      tmem_ld32(tmem + lane_base + (is_dk ? KS_COL_DK : KS_COL_DV) + col, acc);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty);
+      if (is_dk) {
 #pragma unroll
-      for (int e = 0; e < 32; ++e) dkv[e] *= g.scale;
+        for (int e = 0; e < 32; ++e) acc[e] *= g.scale;
+      }
       const int key = k0 + r;
       if (key < p.ck) {
         const OutView none{nullptr, 0, 0, 0, 0};
-        if (p.dkv_bf16) {
-          store_row32(none, p.dv, 0, jo, b, z, key, half * 32, dvv);
-          store_row32(none, p.dk, 0, jo, b, z, key, half * 32, dkv);
-        } else {
-          store_row32(p.dv, none, p.accumulate, jo, b, z, key, half * 32, dvv);
-          store_row32(p.dk, none, p.accumulate, jo, b, z, key, half * 32, dkv);
-        }
+        const OutView& dst = is_dk ? p.dk : p.dv;
+        if (p.dkv_bf16) store_row32(none, dst, 0, jo, b, z, key, col, acc);
+        else store_row32(dst, none, p.accumulate, jo, b, z, key, col, acc);
       }
     }
   }
@@ -319,7 +323,7 @@ static_assert(QS_SMEM <= 232448, "bwd_q_stream smem over the sm_100 per-CTA limi
 // TMEM: S [0,128), dP' [128,256), dS bf16 [256,320), dQ x 2 [320,448)
 constexpr uint32_t QS_COL_S = 0, QS_COL_DP = 128, QS_COL_DS = 256, QS_COL_DQ = 320;
 
-__global__ void __launch_bounds__(NTHREADS, 1) bwd_q_stream_kernel(const __grid_constant__ StreamArgs p) {
+__global__ void __maxnreg__(112) bwd_q_stream_kernel(const __grid_constant__ StreamArgs p) {
   uint8_t* smem = smem_base();
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + QS_OFF_BAR);
   uint64_t *qd_full = bar, *qd_empty = bar + 2;
@@ -341,12 +345,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_q_stream_kernel(const __grid_
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(&qd_full[s], 1), mbar_init(&qd_empty[s], 1);
-      mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], EPI_WARPS);
+      mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], SE_WARPS);
     }
     for (int s = 0; s < QS_ST; ++s) mbar_init(&ld_full[s], 1), mbar_init(&ld_empty[s], 1);
-    mbar_init(s_full, 1), mbar_init(s_empty, EPI_WARPS);
-    mbar_init(dp_full, 1), mbar_init(dp_empty, EPI_WARPS);
-    mbar_init(ds_full, EPI_WARPS), mbar_init(ds_empty, 1);
+    mbar_init(s_full, 1), mbar_init(s_empty, SE_WARPS);
+    mbar_init(dp_full, 1), mbar_init(dp_empty, SE_WARPS);
+    mbar_init(ds_full, SE_WARPS), mbar_init(ds_empty, 1);
     fence_barrier_init();
     tma_prefetch(&p.tq), tma_prefetch(&p.tk), tma_prefetch(&p.tv), tma_prefetch(&p.tdo);
   }
@@ -439,7 +443,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_q_stream_kernel(const __grid_
     }
   } else {
     const uint32_t quad = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int part = (warp - 2) >> 2;
     const int r = quad * 32 + lane;
     const uint32_t lane_base = (quad * 32u) << 16;
     const float sl = p.sl;
@@ -451,60 +455,62 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_q_stream_kernel(const __grid_
       const float dval = row < g.c ? __ldg(p.dvec + row_index(g, d, b, z, row)) : 0.f;
       const uint64_t nd = neg_pair(dval);
       for (int t = 0, k0 = 0; t < T; ++t, k0 = k0 + TK >= ntk * TK ? 0 : k0 + TK) {
-        const int nvalid = min(TK, p.ck - k0) - half * 64;
-        uint32_t w[32];
+        const int nvalid = min(TK, p.ck - k0) - part * SE_COLS;
+        uint32_t w[16];
         {
-          float v[64];
+          float v[32];
           mbar_wait(s_full, n_s & 1);
           tc_fence_after();
           __syncwarp();
-          tmem_ld32(tmem + lane_base + QS_COL_S + half * 64, v);
-          tmem_ld32(tmem + lane_base + QS_COL_S + half * 64 + 32, v + 32);
+          tmem_ld32(tmem + lane_base + QS_COL_S + part * SE_COLS, v);
           tmem_ld_wait();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(s_empty);
           ++n_s;
           exp2_pack32(v, nvalid, sl, msl, w);
-          exp2_pack32(v + 32, nvalid - 32, sl, msl, w + 16);
         }
         {
-          float dp[64];
+          float dp[32];
           mbar_wait(dp_full, n_d & 1);
           tc_fence_after();
           __syncwarp();
-          tmem_ld32(tmem + lane_base + QS_COL_DP + half * 64, dp);
-          tmem_ld32(tmem + lane_base + QS_COL_DP + half * 64 + 32, dp + 32);
+          tmem_ld32(tmem + lane_base + QS_COL_DP + part * SE_COLS, dp);
           tmem_ld_wait();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(dp_empty);
           ++n_d;
 #pragma unroll
-          for (int e = 0; e < 32; ++e) w[e] = ds_pair(w[e], dp[2 * e], dp[2 * e + 1], nd);
+          for (int e = 0; e < 16; ++e) w[e] = ds_pair(w[e], dp[2 * e], dp[2 * e + 1], nd);
         }
         mbar_wait(ds_empty, (n_ds & 1) ^ 1);  // dQ(t-1) has read the previous dS
         tc_fence_after();
-        tmem_st32(tmem + lane_base + QS_COL_DS + half * 32, w);
+        tmem_st16(tmem + lane_base + QS_COL_DS + part * 16, w);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(ds_full);
         ++n_ds;
       }
+      // dQ: parts 0 and 1 read out 32 columns each
       const uint32_t ab = it & 1;
       mbar_wait(&acc_full[ab], (it >> 1) & 1);
       tc_fence_after();
       float o[32];
       __syncwarp();
-      tmem_ld32(tmem + lane_base + QS_COL_DQ + ab * HD + half * 32, o);
-      tmem_ld_wait();
+      if (part < 2) {
+        tmem_ld32(tmem + lane_base + QS_COL_DQ + ab * HD + part * 32, o);
+        tmem_ld_wait();
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[ab]);
+      if (part < 2) {
 #pragma unroll
-      for (int e = 0; e < 32; ++e) o[e] *= g.scale;
-      if (row < g.c) store_row32(p.dq_acc, p.dq_out, p.accumulate, d, b, z, row, half * 32, o);
+        for (int e = 0; e < 32; ++e) o[e] *= g.scale;
+        if (row < g.c) store_row32(p.dq_acc, p.dq_out, p.accumulate, d, b, z, row, part * 32, o);
+      }
     }
   }
   tc_fence_before();
@@ -546,7 +552,7 @@ int rsa_bwd_kv_stream(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa
   a.dkv_bf16 = dkv_dtype == RSA_BF16;
   a.accumulate = accumulate;
   const int items = g->n_org * g->batch * g->heads * ((key_chunk(g) + TK - 1) / TK);
-  return launch(bwd_kv_stream_kernel, items, KS_SMEM, a, stream, "bwd_kv_stream_kernel");
+  return launch(bwd_kv_stream_kernel, items, KS_SMEM, a, stream, "bwd_kv_stream_kernel", SE_THREADS);
 }
 
 int rsa_bwd_q_stream(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view dout_scaled,
@@ -562,7 +568,7 @@ int rsa_bwd_q_stream(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_
   a.dq_out = to_out(dq_out);
   a.accumulate = accumulate;
   const int items = g->n_rank * g->batch * g->heads * ((g->chunk + TR - 1) / TR);
-  return launch(bwd_q_stream_kernel, items, QS_SMEM, a, stream, "bwd_q_stream_kernel");
+  return launch(bwd_q_stream_kernel, items, QS_SMEM, a, stream, "bwd_q_stream_kernel", SE_THREADS);
 }
 
 }  // extern "C"
