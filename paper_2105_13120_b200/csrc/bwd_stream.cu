@@ -42,7 +42,7 @@ struct StreamArgs {
 // query in bwd_q_stream) and a quarter of the 128 columns, so four warps per SM
 // sub-partition share the MUFU-bound exp2 and hide each other's TMEM / barrier latencies.
 constexpr int SE_WARPS = 16;
-constexpr int SE_THREADS = 64 + 32 * SE_WARPS;  // 576: at most 112 registers per thread
+constexpr int SE_THREADS = 64 + 32 * SE_WARPS;  // 576: 18 warps, 5 on some SMSP (16K registers each): at most 96 registers per thread
 constexpr int SE_COLS = 32;                     // columns per thread (128 / (SE_WARPS / 4))
 
 __device__ __forceinline__ int64_t row_index(const Geo& g, int d, int b, int z, int row) {
@@ -73,7 +73,7 @@ static_assert(KS_SMEM <= 232448, "bwd_kv_stream smem over the sm_100 per-CTA lim
 constexpr uint32_t KS_COL_S = 0, KS_COL_DP = 128, KS_COL_P = 256, KS_COL_DS = 320, KS_COL_DV = 384,
                    KS_COL_DK = 448;
 
-__global__ void __maxnreg__(112) bwd_kv_stream_kernel(const __grid_constant__ StreamArgs p) {
+__global__ void __maxnreg__(96) bwd_kv_stream_kernel(const __grid_constant__ StreamArgs p) {
   uint8_t* smem = smem_base();
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + KS_OFF_BAR);
   uint64_t *kv_full = bar, *kv_empty = bar + 2;
@@ -323,7 +323,7 @@ static_assert(QS_SMEM <= 232448, "bwd_q_stream smem over the sm_100 per-CTA limi
 // TMEM: S [0,128), dP' [128,256), dS bf16 [256,320), dQ x 2 [320,448)
 constexpr uint32_t QS_COL_S = 0, QS_COL_DP = 128, QS_COL_DS = 256, QS_COL_DQ = 320;
 
-__global__ void __maxnreg__(112) bwd_q_stream_kernel(const __grid_constant__ StreamArgs p) {
+__global__ void __maxnreg__(96) bwd_q_stream_kernel(const __grid_constant__ StreamArgs p) {
   uint8_t* smem = smem_base();
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + QS_OFF_BAR);
   uint64_t *qd_full = bar, *qd_empty = bar + 2;
