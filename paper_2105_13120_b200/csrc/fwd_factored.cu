@@ -7,9 +7,10 @@
 //
 // Why factored and single-pass.  A normalised panel needs the full row max
 // AND sum before the first probability can be written, i.e. a second pass
-// over S = Q K^T.  On sm_100 the binding resource of that pass is the TMEM
-// read port (tcgen05.ld moves 64 B/clk per SM: one 128x128 fp32 S tile costs
-// 1024 clk), not the tensor core or the exp2 unit.  Softmax is invariant to
+// over S = Q K^T: another GEMM, another tcgen05.ld of every fp32 score (a
+// per-warp latency chain: tools/membench/tmem_ld measures 53 B/clk per SM for
+// 4 warps with one load in flight, 467 B/clk for 16 warps with four) and
+// another exp2 per element.  Softmax is invariant to
 // the reference point, so any per-row m_ref works as long as 2^(s*sl - m_ref)
 // neither overflows nor flushes the row: here m_ref is the max of the row's
 // FIRST key tile (exact, read once), and every later tile reuses it.  The row

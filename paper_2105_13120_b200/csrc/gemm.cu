@@ -1,11 +1,14 @@
 // Batched GEMM for `matmul` (ringseq/tensor_ops.py:44-72) and the staged
 // RSA path.
 //
-// tcgen05 path: one CTA per 128 x BN output tile, four warps.  Warp 0 lane 0
-// streams A/B k-blocks (64 bf16 = one 128-byte swizzle row) through a
-// 4-stage TMA ring; warp 1 lane 0 issues tcgen05.mma (M=128, N=BN, K=16)
-// into a TMEM accumulator; after the last commit all four warps drain TMEM
-// (warp w owns lanes 32w..32w+31 = tile rows) and store fp32/bf16.
+// tcgen05 path: a persistent, warp-specialised kernel (one CTA per SM, 6 warps)
+// walking (split, batch, 128 x BN tile) work items.  Warp 0 lane 0 streams A/B
+// k-blocks (64 bf16 = one 128-byte swizzle row) through a 4-stage TMA ring;
+// warp 1 issues tcgen05.mma (M=128, N=BN, K=16) into one of two TMEM
+// accumulators while warps 2..5 drain the other (warp w owns TMEM lanes
+// 32*(w%4).. = tile rows) and store fp32/bf16 rows with 256-bit accesses.
+// fp32 outputs may split K: the slices of a tile add into C in slice order,
+// gated by per-tile counters (deterministic, no atomics on the data).
 // Operand majors are runtime: K-major tiles are single TMA boxes of
 // 64 x rows; MN-major tiles are 64-wide boxes stacked 8 KB apart, which the
 // UMMA MN-major descriptor walks with LBO = 8 KB, SBO = 1 KB.
