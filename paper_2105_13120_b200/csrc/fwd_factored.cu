@@ -35,6 +35,7 @@
 // epilogue moves it to registers at once, so one buffer suffices) and the
 // O~ accumulator at +128 (64 columns).
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 
 #include "fused_common.cuh"
@@ -75,11 +76,16 @@ constexpr int FF_THREADS = 32 * (FF_PV_WARP + 1);       // 608
 #ifndef FF_QST
 #define FF_QST 1  // Q tiles per group (2: the next unit's Q loads during this unit)
 #endif
+#ifndef FF_TS_LD2
+#define FF_TS_LD2 1  // TS form: load all 64 columns of S before the first exp2 (frees S sooner)
+#endif
 #ifndef FF_KSTAGES
 #define FF_KSTAGES 4
 #endif
 constexpr int FF_KST = FF_KSTAGES, FF_VST = FF_ONES ? 2 : 3;
 constexpr int PV_N = FF_ONES ? HD + 16 : HD;  // O columns (+ 16 row-sum columns)
+constexpr uint32_t TS_COL_P = 256, TS_COL_O = 320;  // TS form: shared P~ buffer, O~ of group g at +80 g
+static_assert(TS_COL_O + FF_GROUPS * PV_N <= 512, "TS-form TMEM layout over 512 columns");
 constexpr float FF_HEADROOM = 96.f;
     // max (row max - m_ref) * sl before the two-pass fallback
 constexpr uint32_t FF_OFF_Q = 0;                                  // one tile per group
@@ -117,8 +123,17 @@ __device__ __forceinline__ Unit unit_of(int u, int units_per_head, int nq) {
 // 96 registers: 19 warps put 5 warps on three SM sub-partitions, each with a 16K-register file.
 // EXT: the rsa_fwd_factored_ex features (stream mode, given reference points, ring-hop
 // accumulation, key_chunk != chunk); the plain instantiation is the hot forward.
-template <bool EXT>
+//
+// TS (stream mode, no panel written): P~ never touches shared memory.  The epilogue
+// writes it to TMEM as packed bf16 pairs (tcgen05.st) and O~ += P~ [V | 1] runs as a
+// TS-form product (A from TMEM, B from shared memory), which removes the P~ stores
+// and the A-operand reads (64 + 64 KB per 256 x 128 step) from the shared-memory port
+// and the store -> proxy fence -> barrier chain from the epilogue.  TMEM: S of group g
+// at 128 g, ONE P~ buffer (64 columns) at 256 that the two groups take in turn (P~V of
+// one group frees it for the next), O~ of group g at 320 + 80 g: 480 columns.
+template <bool EXT, bool TS>
 __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfArgs p) {
+  static_assert(!TS || EXT, "the TS form is a stream-mode (EXT) variant");
   uint8_t* smem = smem_base();
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FF_OFF_BAR);
   uint64_t *q_full = bar, *q_empty = q_full + 2 * FF_QST;  // [group][stage]
@@ -157,6 +172,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
       mbar_init(&p_full[s], 8), mbar_init(&p_empty[s], 1);
       mbar_init(&o_full[s], 1), mbar_init(&o_empty[s], 8);
     }
+    if (TS) mbar_arrive(&p_empty[0]);  // group 0's first use of the shared P~ buffer has no predecessor
     for (int s = 0; s < FF_KST; ++s) mbar_init(&k_full[s], 1), mbar_init(&k_empty[s], 1);
     for (int s = 0; s < FF_VST; ++s) mbar_init(&v_full[s], 1), mbar_init(&v_empty[s], 1);
     fence_barrier_init();
@@ -171,6 +187,23 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
+    if (TS && lane == 31 && p.trace && blockIdx.x == 0) {
+      // timeline experiments (RSA_FF_TRACE): completion times of group 0's S (event 50) and
+      // of every P~V (event 51), observed from a lane that is otherwise idle
+      uint32_t ns = 0, np0 = 0, np1 = 0;
+      for (int i = 0; i < 4000 && tr_i < 4000; ++i) {
+        if (mbar_try_wait(&s_full[0], ns & 1)) {
+          p.trace[tr_i++] = (50ll << 48) | (clock64() - tr0), ++ns;
+        }
+        if (mbar_try_wait(&p_empty[1], np1 & 1)) {  // P~V of group 0 done (frees P~ for group 1)
+          p.trace[tr_i++] = (51ll << 48) | (clock64() - tr0), ++np1;
+        }
+        if (mbar_try_wait(&p_empty[0], np0 & 1)) {  // phase 0 is the pre-arrive; then P~V of group 1
+          if (np0) p.trace[tr_i++] = (52ll << 48) | (clock64() - tr0);
+          ++np0;
+        }
+      }
+    }
     if (lane == 0) {
       Pos kq, vq;
       uint32_t qn[2] = {0, 0}, kgen = 0;
@@ -240,8 +273,8 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
           const uint32_t qa = smem_u32(smem + FF_OFF_Q + (gi * FF_QST + qn[gi] % FF_QST) * TILE);
 #pragma unroll
           for (int k = 0; k < HD / 16; ++k)
-            umma_bf16_ws(tmem + gi * 256, smem_desc_sw128(qa + k * 32, 0, 1024), smem_desc_sw128(ka + k * 32, 0, 1024),
-                         idesc_s, k > 0);
+            umma_bf16_ws(tmem + gi * (TS ? 128 : 256), smem_desc_sw128(qa + k * 32, 0, 1024),
+                         smem_desc_sw128(ka + k * 32, 0, 1024), idesc_s, k > 0);
           umma_commit_ws(&s_full[gi]);
           FF_TRACE(10 + gi);
           if (last) umma_commit_ws(&q_empty[gi * FF_QST + qn[gi] % FF_QST]), ++qn[gi];
@@ -272,12 +305,21 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
           if (t == 0) mbar_wait(&o_empty[gi], (on[gi] & 1) ^ 1);
           mbar_wait(&p_full[gi], pn[gi] & 1);
           tc_fence_after();
-          const uint32_t pa = smem_u32(smem + FF_OFF_P + gi * PTILE);
+          if (TS) {
 #pragma unroll
-          for (int k = 0; k < TK / 16; ++k)
-            umma_bf16_ws(tmem + gi * 256 + 128, smem_desc_sw128(pa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
-                         smem_desc_sw128(va + k * 2048, lbo, 1024), idesc_o, (t | k) != 0);
-          umma_commit_ws(&p_empty[gi]);
+            for (int k = 0; k < TK / 16; ++k)  // A: 8 TMEM columns (16 keys as bf16 pairs) per k step
+              umma_bf16_ts_ws(tmem + TS_COL_O + gi * PV_N, tmem + TS_COL_P + 8 * k,
+                              smem_desc_sw128(va + k * 2048, lbo, 1024), idesc_o, (t | k) != 0);
+            // the shared P~ buffer passes to the next user: the other group, or group 0 of the next step
+            umma_commit_ws(&p_empty[gi + 1 < un.n ? gi + 1 : 0]);
+          } else {
+            const uint32_t pa = smem_u32(smem + FF_OFF_P + gi * PTILE);
+#pragma unroll
+            for (int k = 0; k < TK / 16; ++k)
+              umma_bf16_ws(tmem + gi * 256 + 128, smem_desc_sw128(pa + (k >> 2) * ATOM + (k & 3) * 32, 0, 1024),
+                           smem_desc_sw128(va + k * 2048, lbo, 1024), idesc_o, (t | k) != 0);
+            umma_commit_ws(&p_empty[gi]);
+          }
           FF_TRACE(12 + gi);
           ++pn[gi];
         }
@@ -295,8 +337,8 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
     const int et = (threadIdx.x - 64) & 255;         // thread index within the group
     const bool storer = (lane == 0) && (quad == 2);  // first warp of each (group, half)
     const uint32_t lane_base = (quad * 32u) << 16;
-    const uint32_t t_s = tmem + lane_base + gi * 256 + half * 64;
-    const uint32_t t_o = tmem + lane_base + gi * 256 + 128;
+    const uint32_t t_s = tmem + lane_base + gi * (TS ? 128 : 256) + half * 64;
+    const uint32_t t_o = tmem + lane_base + (TS ? TS_COL_O + gi * PV_N : gi * 256 + 128);
     const uint32_t xbase = smem_u32(smem + FF_OFF_X) + gi * 3 * 256 * 4;
     const uint32_t ptile = smem_u32(smem + FF_OFF_P + gi * PTILE);
     uint8_t* ptile_gen = smem + FF_OFF_P + gi * PTILE + half * ATOM;
@@ -347,6 +389,23 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
           msl = (mref == -INFINITY || !(fabsf(mref) <= 3.402823466e38f)) ? 0.f : mref * sl;
           exp2_pack32(v, nvalid, sl, msl, w);
           exp2_pack32(v + 32, nvalid - 32, sl, msl, w + 16);
+        } else if (TS && FF_TS_LD2) {  // both chunks in flight, then S is free before any exp2
+          float v[64];
+          tmem_ld32(t_s, v);
+          tmem_ld32(t_s + 32, v + 32);
+          tmem_ld_wait();
+          FF_TRACE(40);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_empty[gi]);
+          FF_TRACE(41);
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            // no per-score check: the row sum l bounds every P~ (headroom) and is non-finite
+            // iff a score is +inf / NaN; -inf scores come only from non-finite keys, which
+            // rsa_fwd_factored_ex scans for before the launch (k_scan_kernel)
+            exp2_pack32(v + cc * 32, nvalid - cc * 32, sl, msl, w + cc * 16);
+          }
         } else {
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc) {  // two 32-column chunks (register budget of 18 warps)
@@ -370,6 +429,21 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
         for (int e = 0; e < 32; ++e) lsum += __uint_as_float(w[e] << 16) + __uint_as_float(w[e] & 0xFFFF0000u);
 #endif
         FF_TRACE(4);
+        if (TS) {  // P~ -> the shared TMEM buffer once the previous user's P~ V has read it
+          mbar_wait(&p_empty[gi], pn & 1);
+          FF_TRACE(5);
+          tc_fence_after();
+          tmem_st32(tmem + lane_base + TS_COL_P + half * 32, w);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[gi]);
+          FF_TRACE(6);
+          ++pn;
+          if (k0 + TK >= ck) k0 = 0, ++jo;
+          else k0 += TK;
+          continue;
+        }
         mbar_wait(&p_empty[gi], (pn & 1) ^ 1);  // the previous P~ V product has read the tile
         FF_TRACE(5);
         // Each warp stores its own 32 rows x 64 keys (4 KB, 1024-byte aligned, so the
@@ -397,7 +471,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
       if (!(m == -INFINITY && mi == INFINITY))  // this thread saw at least one valid key in tile 0
         bad |= !(fabsf(m) <= 3.402823466e38f) || !(fabsf(mi) <= 3.402823466e38f);
       bad |= !(am <= 3.402823466e38f);
-      if (!(EXT && p.rm_exact)) redo |= (FF_ABSMAX ? am : m) * sl - msl > FF_HEADROOM;  // |s| >= s: conservative
+      if (!TS && !(EXT && p.rm_exact)) redo |= (FF_ABSMAX ? am : m) * sl - msl > FF_HEADROOM;  // |s| >= s: conservative
       // ---- O = O~ / l, r = 1 / l (l >= 1 unless the row needs the fallback)
       mbar_wait(&o_full[gi], un_n & 1);
       FF_TRACE(7);
@@ -451,7 +525,8 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
         continue;
       }
       const float rinv = 1.f / l;
-      redo |= !(l >= 1.f && l <= 3.402823466e38f);
+      // TS: l >= every P~ of the row, so l <= 2^FF_HEADROOM is the headroom check (conservative)
+      redo |= !(l >= 1.f && l <= (TS && !p.rm_exact ? 7.9228162514e28f : 3.402823466e38f));
       // O -> the group's P~ buffer (atom 0, swizzled like a TMA tile) -> one TMA store
       if (lane == 0) tma_store_wait_read<0>();  // every warp's last P~ store has left the buffer
       bar_named(bar_grp_id, 256);
@@ -489,6 +564,26 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
 namespace rsa {
 namespace {
 
+// Any non-finite bf16 among the keys [org][b][z][row][64] (16-byte chunks, strided rows) ->
+// bit 0 of *flag (NumericError), as the reference's softmax_rows would raise on the scores.
+// grid (row blocks, heads): no index division per element.
+__global__ void __launch_bounds__(256) k_scan_kernel(const uint4* __restrict__ k, int64_t s_org, int64_t s_b,
+                                                     int64_t s_z, int64_t s_row, int B, int Z, int ck, int* flag) {
+  const int h = blockIdx.y, z = h % Z, ob = h / Z, b = ob % B, o = ob / B;
+  const uint4* base = k + (o * s_org + b * s_b + z * s_z) / 8;
+  const int chunks = ck * (HD / 8);
+  bool bad = false;
+  for (int i = blockIdx.x * 1024 + threadIdx.x, e = 0; e < 4; ++e, i += 256) {
+    if (i >= chunks) break;
+    const uint4 x = __ldg(base + ((i >> 3) * s_row) / 8 + (i & 7));
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      bad |= (w[j] & 0x7F80u) == 0x7F80u || (w[j] & 0x7F800000u) == 0x7F800000u;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 int ff_launch(FfArgs& a, const rsa_geom* g, rsa_view q, rsa_view panel, rsa_view o_out, float* rowscale, int* flag,
               void* stream) {
   const bool final_hop = !a.o_acc.ptr || a.final_hop;
@@ -524,7 +619,8 @@ int ff_launch(FfArgs& a, const rsa_geom* g, rsa_view q, rsa_view panel, rsa_view
   const int units = g->batch * g->heads * ((nq + 1) / 2);
   if (units <= 0) return RSA_OK;
   const bool ext = a.no_panel || a.rowmax || a.rowmax_in || a.o_acc.ptr || a.ck != g->chunk;
-  auto kernel = ext ? fwd_factored_kernel<true> : fwd_factored_kernel<false>;
+  auto kernel = a.no_panel ? fwd_factored_kernel<true, true>
+                           : ext ? fwd_factored_kernel<true, false> : fwd_factored_kernel<false, false>;
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FF_SMEM);
   cudaFuncAttributes fa{};
   if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess && fa.maxThreadsPerBlock < FF_THREADS)
@@ -561,6 +657,18 @@ int rsa_fwd_factored_ex(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, c
   using namespace rsa;
   if (!ext) return fail(RSA_ERR_INVALID, "rsa_fwd_factored_ex: options missing");
   if (!geom_ok_keys(g)) return fail(RSA_ERR_INVALID, "rsa_fwd_factored_ex: unsupported geometry");
+  if (!ext->panel.ptr && !ext->rowmax_exact && flag) {
+    // the TS form checks no score after the first key tile: a non-finite key sets bit 0 here
+    const int heads = g->n_org * g->batch * g->heads;
+    if (heads > 0 && heads < 65536 && k.ptr && aligned16(k.ptr) && k.s_row % 8 == 0 && k.s_z % 8 == 0 &&
+        k.s_b % 8 == 0 && k.s_rank % 8 == 0) {
+      const dim3 grid((key_chunk(g) * (HD / 8) + 1023) / 1024, heads);
+      k_scan_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+          reinterpret_cast<const uint4*>(k.ptr), k.s_rank, k.s_b, k.s_z, k.s_row, g->batch, g->heads, key_chunk(g),
+          flag);
+      if (int rc = check_launch("k_scan_kernel")) return rc;
+    }
+  }
   FfArgs a{};
   if (!head_map(&a.tk, k, g, g->n_org, key_chunk(g)) || !head_map(&a.tv, v, g, g->n_org, key_chunk(g)))
     return RSA_ERR_UNSUPPORTED;

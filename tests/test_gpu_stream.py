@@ -149,6 +149,25 @@ def test_stream_fallback_on_far_row_max(rsa):
     _gate("dv", _np(pkg.gather_sequence(bwd.grad_v)), cat(dv))
 
 
+def test_stream_nonfinite_key_beyond_first_tile(rsa):
+    """A -inf key entry outside the first key tile, against queries that are all positive in
+    that dimension: every row scores -inf there, so P~ = 0 and the row sum stays finite.  The
+    stream forward checks no score after the first tile (the row sum bounds the rest), and
+    the key scan in rsa_fwd_factored_ex must still raise NumericError, as the reference's
+    softmax_rows does on non-finite scores (ringseq/tensor_ops.py:80-81)."""
+    pkg, ra = rsa
+    b, z, seq, a, n = 1, 2, 512, 64, 2
+    q, k, v, _ = _inputs(b, z, seq, a, seed=79)
+    q[..., :, 5] = np.abs(q[..., :, 5]) + 0.5
+    k[..., 300, 5] = -np.inf
+    cfg = pkg.AttentionConfig(batch_size=b, seq_len=seq, hidden_size=z * a, num_heads=z, head_size=a, num_devices=n)
+    ch = lambda x: orc.chunks_of(x, n)  # noqa: E731
+    with pytest.raises(pkg.NumericError):
+        ra.ring_attention_forward(ch(q), ch(k), ch(v), cfg, mode="stream")
+    k[..., 300, 5] = 1.0  # finite again: no error
+    ra.ring_attention_forward(ch(q), ch(k), ch(v), cfg, mode="stream")
+
+
 def test_stream_mode_long_chunk_sampled(rsa):
     """c = 2048 per rank with 8 resident ranks (L = 16K, config 4's chunk): sampled rows and
     keys of two heads against the blockwise oracle; the saved state is O(L) per head."""
