@@ -79,6 +79,9 @@ constexpr int FF_THREADS = 32 * (FF_PV_WARP + 1);       // 608
 #ifndef FF_TS_LD2
 #define FF_TS_LD2 1  // TS form: load all 64 columns of S before the first exp2 (frees S sooner)
 #endif
+#ifndef FF_PANEL_TS
+#define FF_PANEL_TS 1  // panel forward: P~V from a TMEM copy of P~ (TS form); the smem tile only feeds the store
+#endif
 #ifndef FF_KSTAGES
 #define FF_KSTAGES 4
 #endif
@@ -133,7 +136,10 @@ __device__ __forceinline__ Unit unit_of(int u, int units_per_head, int nq) {
 // one group frees it for the next), O~ of group g at 320 + 80 g: 480 columns.
 template <bool EXT, bool TS>
 __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfArgs p) {
-  static_assert(!TS || EXT, "the TS form is a stream-mode (EXT) variant");
+  // stream mode (TS with EXT): no per-score check after the first key tile, the row sum
+  // bounds the rest; the panel forward in TS form keeps the max|s| check
+  constexpr bool LCHK = TS && EXT;
+  constexpr bool NOPANEL = TS && EXT;  // ff_launch picks <true, true> exactly for p.no_panel
   uint8_t* smem = smem_base();
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FF_OFF_BAR);
   uint64_t *q_full = bar, *q_empty = q_full + 2 * FF_QST;  // [group][stage]
@@ -389,7 +395,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
           msl = (mref == -INFINITY || !(fabsf(mref) <= 3.402823466e38f)) ? 0.f : mref * sl;
           exp2_pack32(v, nvalid, sl, msl, w);
           exp2_pack32(v + 32, nvalid - 32, sl, msl, w + 16);
-        } else if (TS && FF_TS_LD2) {  // both chunks in flight, then S is free before any exp2
+        } else if (LCHK && FF_TS_LD2) {  // both chunks in flight, then S is free before any exp2
           float v[64];
           tmem_ld32(t_s, v);
           tmem_ld32(t_s + 32, v + 32);
@@ -440,12 +446,15 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
           if (lane == 0) mbar_arrive(&p_full[gi]);
           FF_TRACE(6);
           ++pn;
-          if (k0 + TK >= ck) k0 = 0, ++jo;
-          else k0 += TK;
-          continue;
+          if (NOPANEL) {
+            if (k0 + TK >= ck) k0 = 0, ++jo;
+            else k0 += TK;
+            continue;
+          }
+        } else {
+          mbar_wait(&p_empty[gi], (pn & 1) ^ 1);  // the previous P~ V product has read the tile
+          FF_TRACE(5);
         }
-        mbar_wait(&p_empty[gi], (pn & 1) ^ 1);  // the previous P~ V product has read the tile
-        FF_TRACE(5);
         // Each warp stores its own 32 rows x 64 keys (4 KB, 1024-byte aligned, so the
         // 128-byte swizzle pattern is the tile's): no cross-warp barrier on this path.
         if (lane == 0) tma_store_wait_read<0>();  // this warp's previous store has read its rows
@@ -457,21 +466,21 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(&p_full[gi]);
-          if (nvalid > 0 && !(EXT && p.no_panel))  // the panel is read back only by the backward: evict-first in L2
+          if (!TS) mbar_arrive(&p_full[gi]);  // TS: the P~V product reads TMEM, the tile only feeds the store
+          if (nvalid > 0 && !NOPANEL)  // the panel is read back only by the backward: evict-first in L2
             tma_store_5d_hint(&p.tp, ptile_gen + quad * 4096, k0 + half * 64, g.org_lo + jo, rt * TR + quad * 32, z,
                               d * g.B + b, pol);
           tma_store_commit();
         }
         FF_TRACE(6);
-        ++pn;
+        if (!TS) ++pn;
         if (k0 + TK >= ck) k0 = 0, ++jo;
         else k0 += TK;
       }
       if (!(m == -INFINITY && mi == INFINITY))  // this thread saw at least one valid key in tile 0
         bad |= !(fabsf(m) <= 3.402823466e38f) || !(fabsf(mi) <= 3.402823466e38f);
       bad |= !(am <= 3.402823466e38f);
-      if (!TS && !(EXT && p.rm_exact)) redo |= (FF_ABSMAX ? am : m) * sl - msl > FF_HEADROOM;  // |s| >= s: conservative
+      if (!LCHK && !(EXT && p.rm_exact)) redo |= (FF_ABSMAX ? am : m) * sl - msl > FF_HEADROOM;  // |s| >= s: conservative
       // ---- O = O~ / l, r = 1 / l (l >= 1 unless the row needs the fallback)
       mbar_wait(&o_full[gi], un_n & 1);
       FF_TRACE(7);
@@ -526,7 +535,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
       }
       const float rinv = 1.f / l;
       // TS: l >= every P~ of the row, so l <= 2^FF_HEADROOM is the headroom check (conservative)
-      redo |= !(l >= 1.f && l <= (TS && !p.rm_exact ? 7.9228162514e28f : 3.402823466e38f));
+      redo |= !(l >= 1.f && l <= (LCHK && !p.rm_exact ? 7.9228162514e28f : 3.402823466e38f));
       // O -> the group's P~ buffer (atom 0, swizzled like a TMA tile) -> one TMA store
       if (lane == 0) tma_store_wait_read<0>();  // every warp's last P~ store has left the buffer
       bar_named(bar_grp_id, 256);
@@ -620,7 +629,7 @@ int ff_launch(FfArgs& a, const rsa_geom* g, rsa_view q, rsa_view panel, rsa_view
   if (units <= 0) return RSA_OK;
   const bool ext = a.no_panel || a.rowmax || a.rowmax_in || a.o_acc.ptr || a.ck != g->chunk;
   auto kernel = a.no_panel ? fwd_factored_kernel<true, true>
-                           : ext ? fwd_factored_kernel<true, false> : fwd_factored_kernel<false, false>;
+                           : ext ? fwd_factored_kernel<true, false> : fwd_factored_kernel<false, FF_PANEL_TS != 0>;
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FF_SMEM);
   cudaFuncAttributes fa{};
   if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess && fa.maxThreadsPerBlock < FF_THREADS)
