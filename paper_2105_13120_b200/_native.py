@@ -130,6 +130,8 @@ EXPORTS = {
     "rsa_fwd_factored_ex": (c_int, [_GEOM, _V, _V, _V, _P(RsaFwdExt), _V, c_void_p, c_void_p, c_void_p]),
     "rsa_bwd_kv_stream": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, c_void_p, _V, _V, c_int, c_int, c_void_p]),
     "rsa_bwd_q_stream": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, c_void_p, _V, c_int, _V, c_void_p]),
+    "rsa_bwd_stream_fused": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, c_void_p, _V, _V, c_int, c_int, c_void_p, c_int,
+                                     _V, c_void_p]),
 }
 
 _lib = None

@@ -21,6 +21,8 @@
 //                         S, dP' -> P~ to smem -> dV += P~^T dO' -> dS in place -> dK += dS^T Q
 //   bwd_q_stream_kernel   item = (rank, b, z, query tile); walks every key tile:
 //                         S, dP' -> dS to smem -> dQ += dS K
+#include <cstdlib>
+
 #include "fused_common.cuh"
 
 namespace rsa {
@@ -29,6 +31,7 @@ namespace {
 struct StreamArgs {
   CUtensorMap tq, tk, tv, tdo;  // q / dO': query rows (chunk); k / v: key rows (key_chunk)
   CUtensorMap tm, td;           // rowmax / dvec as 128-row boxes (bwd_kv_stream)
+  CUtensorMap tdq;              // fp32 dQ accumulator, 16-column x 32-row boxes (bwd_stream_fused)
   Geo g;
   int ck;    // keys per origin chunk
   float sl;  // scale * log2(e)
@@ -36,6 +39,7 @@ struct StreamArgs {
   const float* dvec;    // D * r per query row
   OutView dk, dv, dq_acc, dq_out;
   int dkv_bf16, accumulate;
+  int dbg;  // RSA_FS_DBG experiment bits (bwd_stream_fused): 1 no reduce, 2 no staging, 4 no dQ product
 };
 
 // 16 epilogue warps: each thread owns one TMEM lane (a key of the tile in bwd_kv_stream, a
@@ -518,6 +522,368 @@ __global__ void __maxnreg__(96) bwd_q_stream_kernel(const __grid_constant__ Stre
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// ====================================================== dQ, dK and dV in one pass
+//
+// The dK / dV kernel above plus dQ, so S, dP' and every exp2 are computed once instead of
+// twice.  Per step (key tile x query tile), keys on the TMEM lanes:
+//   S^T = K Q^T                            SS form, issued a step ahead (as bwd_kv_stream)
+//   dV += P~^T dO'                         TS form, A = P~^T (bf16) in TMEM
+//   dP'^T = V dO'^T                        SS form
+//   dK += dS^T Q                           TS form, A = dS^T (bf16) in TMEM
+//   dQ_part = dS K_j                       SS form, A = dS in shared memory (MN-major)
+// The epilogue writes dS^T over the dP'^T columns it has just read (each thread its own
+// lanes and columns, so no other warp's operand is touched) and to shared memory with the
+// queries contiguous.  tcgen05.mma executes in issue order, so dP'^T(t+1), issued after
+// dK(t), overwrites dS^T(t) only after dK(t) has read it; dQ_part(t), issued last, is read
+// out at the end of step t+1, when it is long done.  The epilogue scales dQ_part, stages it
+// per warp (32 rows x 16 columns, SWIZZLE_64B) and the
+// TMA unit adds it into an fp32 dQ accumulator in L2 (cp.reduce.async.bulk.tensor .add;
+// tools/membench/red_bulk: ~5.9 TB/s chip-wide).  So dQ's sum over key tiles is taken in
+// arrival order -- not bitwise reproducible, unlike dK / dV (TMEM, fixed order) and the
+// two-kernel form.  Items walk the query tiles from their own starting tile (kt mod T) so
+// concurrent items of a head add into different dQ tiles.
+// (Measured on the way, L = 8192, B4 Z12, against 3016 us for the two kernels: P~^T and
+// dS^T taking one TMEM buffer in turn, 3085 us; dS^T in shared memory only, read by dK as a
+// K-major SS operand, 2424 us; P~^T / dS^T written over S^T / dP'^T, so S^T(t+1) waits for
+// dV(t), 2474 us; P~^T(t) then dQ_part(t) in one buffer, read out before P~^T(t+1) is
+// written, 2402 us, with the epilogue waiting on dQ_part at every step.)
+
+constexpr int FS_ST = 3;                                    // (Q, dO', m, D') stages
+constexpr uint32_t FS_OFF_KV = 0;                           // K | V (one buffer)
+constexpr uint32_t FS_OFF_ST = 2 * TILE;                    // [stage][Q | dO' | m | D']
+constexpr uint32_t FS_OFF_DS = FS_OFF_ST + FS_ST * KS_STAGE;  // dS: [8-key group][64-query atom][8 keys][128 B]
+constexpr uint32_t FS_OFF_STG = FS_OFF_DS + PTILE;          // dQ_part staging: [epilogue warp][32 rows][64 B]
+constexpr uint32_t FS_OFF_BAR = FS_OFF_STG + SE_WARPS * 2048;
+constexpr uint32_t FS_SMEM = FS_OFF_BAR + 512 + 1024;
+static_assert(FS_OFF_DS % 1024 == 0 && FS_OFF_STG % 1024 == 0, "swizzled tiles need 1024-byte alignment");
+static_assert(FS_SMEM <= 232448, "bwd_stream_fused smem over the sm_100 per-CTA limit");
+// TMEM: S^T [0,128), dP'^T then dS^T [128,256), P~^T [256,320), dQ_part [320,384), dV [384,448), dK [448,512)
+constexpr uint32_t FS_COL_S = 0, FS_COL_DP = 128, FS_COL_P = 256, FS_COL_DQ = 320, FS_COL_DV = 384,
+                   FS_COL_DK = 448;
+
+// Key k's 32 dS values for queries part*32.. (bf16 pairs) into the MN-major SWIZZLE_128B dS
+// tile: row k of its 8-key group, 16-byte chunks XOR-swizzled by k % 8.
+__device__ __forceinline__ void st_ds_mn(uint32_t tile, uint32_t key, int part, const uint32_t* w) {
+  const uint32_t kr = key & 7;
+  const uint32_t row = tile + (key >> 3) * 2048 + (part >> 1) * 1024 + kr * 128;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    st_shared_v4(row + ((((part & 1) * 4 + j) ^ kr) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+}
+
+__global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ StreamArgs p) {
+  uint8_t* smem = smem_base();
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FS_OFF_BAR);
+  uint64_t *kv_full = bar, *kv_empty = bar + 1;
+  uint64_t *ld_full = bar + 2, *ld_empty = ld_full + FS_ST;
+  uint64_t *s_full = ld_empty + FS_ST, *s_empty = s_full + 1, *dp_full = s_empty + 1, *p_full = dp_full + 1;
+  uint64_t *p_empty = p_full + 1, *ds_full = p_empty + 1, *dq_full = ds_full + 1, *dq_empty = dq_full + 1;
+  uint64_t *acc_full = dq_empty + 1, *acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+  const Geo& g = p.g;
+  const int ntk = (p.ck + TK - 1) / TK, nrt = (g.c + TR - 1) / TR;
+  const int T = g.n_rank * nrt;  // query tiles walked per key tile
+  const int BZ = g.B * g.Z;
+  const int items = g.n_org * BZ * ntk;
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1), mbar_init(kv_empty, 1);
+    for (int s = 0; s < FS_ST; ++s) mbar_init(&ld_full[s], 1), mbar_init(&ld_empty[s], 1);
+    mbar_init(s_full, 1), mbar_init(s_empty, SE_WARPS), mbar_init(dp_full, 1), mbar_init(p_full, SE_WARPS);
+    mbar_init(p_empty, 1), mbar_init(ds_full, SE_WARPS), mbar_init(dq_full, 1), mbar_init(dq_empty, SE_WARPS);
+    mbar_init(acc_full, 1), mbar_init(acc_empty, SE_WARPS);
+    fence_barrier_init();
+    tma_prefetch(&p.tq), tma_prefetch(&p.tk), tma_prefetch(&p.tv), tma_prefetch(&p.tdo);
+    tma_prefetch(&p.tm), tma_prefetch(&p.td), tma_prefetch(&p.tdq);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      Pos lq;
+      uint32_t it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        const int kt = item % ntk, bz = (item / ntk) % BZ, jo = item / (ntk * BZ);
+        const int b = bz / g.Z, z = bz % g.Z;
+        mbar_wait(kv_empty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(kv_full, 2 * TILE);
+        uint8_t* kv = smem + FS_OFF_KV;
+        tma_load_4d(kv, &p.tk, kv_full, 0, kt * TK, z, jo * g.B + b);
+        tma_load_4d(kv + TILE, &p.tv, kv_full, 0, kt * TK, z, jo * g.B + b);
+        const int t0 = kt % T;
+        int d = t0 / nrt, r0 = (t0 % nrt) * TR;
+        for (int t = 0; t < T; ++t) {
+          const uint32_t s = lq.slot(FS_ST);
+          mbar_wait(&ld_empty[s], lq.phase(FS_ST) ^ 1);
+          mbar_arrive_expect_tx(&ld_full[s], KS_STAGE);
+          uint8_t* st = smem + FS_OFF_ST + s * KS_STAGE;
+          tma_load_4d(st, &p.tq, &ld_full[s], 0, r0, z, d * g.B + b);
+          tma_load_4d(st + TILE, &p.tdo, &ld_full[s], 0, r0, z, d * g.B + b);
+          tma_load_3d(st + 2 * TILE, &p.tm, &ld_full[s], r0, z, d * g.B + b);
+          tma_load_3d(st + 2 * TILE + TR * 4, &p.td, &ld_full[s], r0, z, d * g.B + b);
+          ++lq.i;
+          if ((r0 += TR) >= nrt * TR) r0 = 0, d = d + 1 == g.n_rank ? 0 : d + 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    const uint32_t idesc_s = idesc_bf16_f32(TK, TR, 0, 0);   // K x Q^T, V x dO'^T -> keys x queries
+    const uint32_t idesc_ts = idesc_bf16_f32(TK, HD, 0, 1);  // P~^T / dS^T (TMEM) x dO' / Q (MN-major)
+    const uint32_t idesc_dq = idesc_bf16_f32(TR, HD, 1, 1);  // dS (smem, MN-major) x K (MN-major)
+    const uint32_t ka = smem_u32(smem + FS_OFF_KV), va = ka + TILE, dsa = smem_u32(smem + FS_OFF_DS);
+    Pos lq_s, lq_d, lq_v, lq_k;
+    uint32_t n_s = 0, n_p = 0, n_ds = 0, n_dq = 0, it = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      mbar_wait(kv_full, it & 1);
+      auto issue_s = [&]() {  // S^T(t) = K Q^T once the epilogue has read S^T(t-1)
+        const uint32_t s = lq_s.slot(FS_ST);
+        mbar_wait(&ld_full[s], lq_s.phase(FS_ST));
+        mbar_wait(s_empty, (n_s & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(smem + FS_OFF_ST + s * KS_STAGE);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+          umma_bf16_ws(tmem + FS_COL_S, smem_desc_sw128(ka + k * 32, 0, 1024), smem_desc_sw128(qa + k * 32, 0, 1024),
+                       idesc_s, k > 0);
+        umma_commit_ws(s_full);
+        ++lq_s.i, ++n_s;
+      };
+      auto issue_dp = [&]() {  // dP'^T(t) = V dO'^T over dS^T(t-1), which dK(t-1) (issued before) has read
+        const uint32_t s = lq_d.slot(FS_ST);
+        mbar_wait(&ld_full[s], lq_d.phase(FS_ST));
+        tc_fence_after();
+        const uint32_t doa = smem_u32(smem + FS_OFF_ST + s * KS_STAGE) + TILE;
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+          umma_bf16_ws(tmem + FS_COL_DP, smem_desc_sw128(va + k * 32, 0, 1024), smem_desc_sw128(doa + k * 32, 0, 1024),
+                       idesc_s, k > 0);
+        umma_commit_ws(dp_full);
+        ++lq_d.i;
+      };
+      // A columns of K-step k (16 queries) in dS^T: part k/2's 16 packed columns over its dP'^T
+      auto ds_col = [](int k) { return uint32_t((k >> 1) * SE_COLS + (k & 1) * 8); };
+      auto issue_dv = [&](int t) {  // dV += P~^T dO' (A from TMEM)
+        const uint32_t s = lq_v.slot(FS_ST);
+        mbar_wait(p_full, n_p & 1);
+        if (t == 0) mbar_wait(acc_empty, (it & 1) ^ 1);  // the previous item's dK / dV are read out
+        tc_fence_after();
+        const uint32_t doa = smem_u32(smem + FS_OFF_ST + s * KS_STAGE) + TILE;
+#pragma unroll
+        for (int k = 0; k < TR / 16; ++k)
+          umma_bf16_ts_ws(tmem + FS_COL_DV, tmem + FS_COL_P + 8 * k, smem_desc_sw128(doa + k * 2048, ATOM, 1024),
+                          idesc_ts, (t | k) != 0);
+        umma_commit_ws(p_empty);
+        ++lq_v.i, ++n_p;
+      };
+      auto issue_dk = [&](int t) {  // dK += dS^T Q (A from TMEM)
+        const uint32_t s = lq_k.slot(FS_ST);
+        mbar_wait(ds_full, n_ds & 1);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(smem + FS_OFF_ST + s * KS_STAGE);
+#pragma unroll
+        for (int k = 0; k < TR / 16; ++k)
+          umma_bf16_ts_ws(tmem + FS_COL_DK, tmem + FS_COL_DP + ds_col(k), smem_desc_sw128(qa + k * 2048, ATOM, 1024),
+                          idesc_ts, (t | k) != 0);
+        umma_commit_ws(&ld_empty[s]);  // the stage's last readers: dK (Q), dV (dO'), the epilogue (m, D')
+        ++lq_k.i, ++n_ds;
+      };
+      auto issue_dq = [&]() {  // dQ_part = dS K (A = the smem dS tile) once dQ_part(t-1) is read out
+        mbar_wait(dq_empty, (n_dq & 1) ^ 1);
+        tc_fence_after();
+        if (!(p.dbg & 4)) {
+#pragma unroll
+          for (int k = 0; k < TK / 16; ++k)  // 16 keys per product: two 8-key groups of dS, 2 KB of K
+            umma_bf16_ws(tmem + FS_COL_DQ, smem_desc_sw128(dsa + k * 4096, 1024, 2048),
+                         smem_desc_sw128(ka + k * 2048, ATOM, 1024), idesc_dq, k > 0);
+        }
+        umma_commit_ws(dq_full);
+        ++n_dq;
+      };
+      issue_s();
+      issue_dp();
+      for (int t = 0; t < T; ++t) {
+        if (t + 1 < T) issue_s();
+        issue_dv(t);
+        issue_dk(t);
+        if (t + 1 < T) issue_dp();
+        issue_dq();
+      }
+      umma_commit_ws(kv_empty);
+      umma_commit_ws(acc_full);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    // warp w: TMEM lanes 32*(w%4).. = keys of the tile (queries for dQ_part); query columns
+    // part*32 .. +31 (dQ_part columns part*16 .. +15)
+    const uint32_t quad = warp & 3;
+    const int part = (warp - 2) >> 2;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_base = (quad * 32u) << 16;
+    const float sl = p.sl;
+    const uint32_t dsa = smem_u32(smem + FS_OFF_DS);
+    uint8_t* stg = smem + FS_OFF_STG + (warp - 2) * 2048;
+    const uint32_t stg_row = smem_u32(stg) + lane * 64, sw = (lane >> 1) & 3;
+    Pos lq;
+    uint32_t n_s = 0, n_d = 0, n_p = 0, n_dq = 0, it = 0;
+    // dQ_part of the previous step (lanes = queries): read out, scaled and staged; the TMA
+    // reduce is issued after the step's proxy fence
+    auto dq_stage = [&]() {
+      float o[16];
+      mbar_wait(dq_full, n_dq & 1);
+      tc_fence_after();
+      __syncwarp();
+      tmem_ld16(tmem + lane_base + FS_COL_DQ + part * 16, o);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_empty);
+      ++n_dq;
+      if (p.dbg & 2) return;
+      if (lane == 0) tma_store_wait_read<0>();  // this warp's previous reduce has read its staging
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        st_shared_v4(stg_row + ((j ^ sw) << 4), __float_as_uint(o[4 * j] * g.scale),
+                     __float_as_uint(o[4 * j + 1] * g.scale), __float_as_uint(o[4 * j + 2] * g.scale),
+                     __float_as_uint(o[4 * j + 3] * g.scale));
+    };
+    auto dq_reduce = [&](int d, int b, int z, int r0) {
+      if (lane == 0 && !(p.dbg & 3)) {
+        tma_reduce_add_4d(&p.tdq, stg, part * 16, r0 + int(quad) * 32, z, d * g.B + b);
+        tma_store_commit();
+      }
+    };
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      const int kt = item % ntk, bz = (item / ntk) % BZ, jo = item / (ntk * BZ);
+      const int b = bz / g.Z, z = bz % g.Z, k0 = kt * TK;
+      const int t0 = kt % T;
+      int d = t0 / nrt, r0 = (t0 % nrt) * TR, pd = 0, pr0 = 0;
+      for (int t = 0; t < T; ++t) {
+        const int nvalid = min(TR, g.c - r0) - part * SE_COLS;  // valid query columns of this part
+        const uint32_t s = lq.slot(FS_ST);
+        const uint32_t stat = smem_u32(smem + FS_OFF_ST + s * KS_STAGE + 2 * TILE) + part * SE_COLS * 4;
+        mbar_wait(&ld_full[s], lq.phase(FS_ST));  // m and D' of the step's queries
+        uint32_t w[16];
+        {  // S^T -> P~^T
+          float v[32], m[32];
+          mbar_wait(s_full, n_s & 1);
+          tc_fence_after();
+          __syncwarp();
+          tmem_ld32(tmem + lane_base + FS_COL_S + part * SE_COLS, v);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) ld_shared_f4(stat + j * 4, m + j);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(s_empty);
+          ++n_s;
+          exp2_pack32_cols(v, nvalid, sl, m, w);
+        }
+        mbar_wait(p_empty, (n_p & 1) ^ 1);  // dV(t-1) has read P~^T(t-1)
+        ++n_p;
+        tc_fence_after();
+        tmem_st16(tmem + lane_base + FS_COL_P + part * 16, w);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+        {  // dP'^T -> dS^T = P~^T (dP'^T - D')
+          float dp[32], dd[32];
+          mbar_wait(dp_full, n_d & 1);
+          tc_fence_after();
+          __syncwarp();
+          tmem_ld32(tmem + lane_base + FS_COL_DP + part * SE_COLS, dp);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) ld_shared_f4(stat + TR * 4 + j * 4, dd + j);
+          tmem_ld_wait();
+          ++n_d;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) w[e] = ds_pair2(w[e], dp[2 * e], dp[2 * e + 1], dd[2 * e], dd[2 * e + 1]);
+        }
+        tmem_st16(tmem + lane_base + FS_COL_DP + part * SE_COLS, w);  // over this thread's own dP'^T
+        if (t > 0) dq_stage();
+        st_ds_mn(dsa, r, part, w);  // dQ_part(t-1), complete above, was the previous dS's last reader
+        fence_proxy_async_smem();
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ds_full);
+        if (t > 0) dq_reduce(pd, b, z, pr0);
+        ++lq.i;
+        pd = d, pr0 = r0;
+        if ((r0 += TR) >= nrt * TR) r0 = 0, d = d + 1 == g.n_rank ? 0 : d + 1;
+      }
+      dq_stage();
+      fence_proxy_async_smem();
+      __syncwarp();
+      dq_reduce(pd, b, z, pr0);
+      // the key tile's dV (parts 0, 1) and dK (parts 2, 3): 32 columns per thread
+      mbar_wait(acc_full, it & 1);
+      tc_fence_after();
+      float acc[32];
+      const bool is_dk = part >= 2;
+      const int col = (part & 1) * 32;
+      __syncwarp();
+      tmem_ld32(tmem + lane_base + (is_dk ? FS_COL_DK : FS_COL_DV) + col, acc);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);
+      if (is_dk) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) acc[e] *= g.scale;
+      }
+      const int key = k0 + r;
+      if (key < p.ck) {
+        const OutView none{nullptr, 0, 0, 0, 0};
+        const OutView& dst = is_dk ? p.dk : p.dv;
+        if (p.dkv_bf16) store_row32(none, dst, 0, jo, b, z, key, col, acc);
+        else store_row32(dst, none, p.accumulate, jo, b, z, key, col, acc);
+      }
+    }
+    if (lane == 0) tma_store_wait_all<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// dQ = bf16(dq_acc): fp32 [rank][b][z][row][64] contiguous into a strided bf16 view, 8
+// columns per thread.
+__global__ void dq_cast_kernel(const float* __restrict__ acc, OutView out, int c, int Z, int B, int64_t rows) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows * 8; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = i >> 3;
+    const int col = int(i & 7) * 8;
+    const int rr = int(row % c);
+    int64_t hb = row / c;
+    const int z = int(hb % Z);
+    hb /= Z;
+    const int b = int(hb % B), d = int(hb / B);
+    const float4 x = *reinterpret_cast<const float4*>(acc + row * HD + col);
+    const float4 y = *reinterpret_cast<const float4*>(acc + row * HD + col + 4);
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out.ptr) + out_off(out, d, b, z, rr) + col) =
+        make_uint4(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w), pack_bf16(y.x, y.y), pack_bf16(y.z, y.w));
+  }
+}
+
+// fp32 dQ accumulator [rank][b][z][row][64] (contiguous) as a 4-D map (col, row, z, b*rank)
+// with 16-column x 32-row boxes, SWIZZLE_64B (the staging layout of bwd_stream_fused).
+inline bool dq_acc_map(CUtensorMap* m, float* base, const rsa_geom* g) {
+  if (!base || !aligned16(base)) return fail(RSA_ERR_UNSUPPORTED, "dq_acc must be 16-byte aligned"), false;
+  uint64_t dims[4] = {uint64_t(HD), uint64_t(g->chunk), uint64_t(g->heads), uint64_t(g->batch) * g->n_rank};
+  uint64_t str[3] = {uint64_t(HD) * 4, uint64_t(g->chunk) * HD * 4, uint64_t(g->heads) * g->chunk * HD * 4};
+  uint32_t box[4] = {16, 32, 1, 1};
+  return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B);
+}
+
 bool stream_args(StreamArgs* a, const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view dout,
                  const float* rowmax, const float* dvec) {
   if (!head_map(&a->tq, q, g, g->n_rank) || !head_map(&a->tdo, dout, g, g->n_rank) ||
@@ -569,6 +935,39 @@ int rsa_bwd_q_stream(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_
   a.accumulate = accumulate;
   const int items = g->n_rank * g->batch * g->heads * ((g->chunk + TR - 1) / TR);
   return launch(bwd_q_stream_kernel, items, QS_SMEM, a, stream, "bwd_q_stream_kernel", SE_THREADS);
+}
+
+int rsa_bwd_stream_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view dout_scaled,
+                         const float* rowmax, const float* dvec, rsa_view dk, rsa_view dv, int dkv_dtype,
+                         int accumulate_dkv, float* dq_acc, int accumulate_dq, rsa_view dq_out, void* stream) {
+  using namespace rsa;
+  if (!geom_ok_keys(g) || !rowmax || !dvec) return fail(RSA_ERR_INVALID, "rsa_bwd_stream_fused: unsupported geometry");
+  const int esz = dkv_dtype == RSA_BF16 ? 2 : 4;
+  if (!dk.ptr || !dv.ptr || !out_ok(dk, esz) || !out_ok(dv, esz) || !out_ok(dq_out, 2))
+    return fail(RSA_ERR_UNSUPPORTED, "rsa_bwd_stream_fused: output views missing or misaligned");
+  StreamArgs a{};
+  if (!stream_args(&a, g, q, k, v, dout_scaled, rowmax, dvec) || !dq_acc_map(&a.tdq, dq_acc, g))
+    return RSA_ERR_UNSUPPORTED;
+  a.dk = to_out(dk);
+  a.dv = to_out(dv);
+  a.dkv_bf16 = dkv_dtype == RSA_BF16;
+  a.accumulate = accumulate_dkv;
+  static const int dbg = [] {  // experiment switch (tools/fs_exp.py), read once
+    const char* e = getenv("RSA_FS_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  a.dbg = dbg;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t rows = int64_t(g->n_rank) * g->batch * g->heads * g->chunk;
+  if (!accumulate_dq && cudaMemsetAsync(dq_acc, 0, size_t(rows) * HD * 4, st) != cudaSuccess)
+    return check_launch("rsa_bwd_stream_fused: dq_acc memset");
+  const int items = g->n_org * g->batch * g->heads * ((key_chunk(g) + TK - 1) / TK);
+  const int rc = launch(bwd_stream_fused_kernel, items, FS_SMEM, a, stream, "bwd_stream_fused_kernel", SE_THREADS);
+  if (rc != RSA_OK || !dq_out.ptr) return rc;
+  const int64_t work = rows * 8;
+  const int blocks = int(std::min<int64_t>((work + 255) / 256, int64_t(num_sms()) * 8));
+  dq_cast_kernel<<<blocks, 256, 0, st>>>(dq_acc, to_out(dq_out), g->chunk, g->heads, g->batch, rows);
+  return check_launch("dq_cast_kernel");
 }
 
 }  // extern "C"

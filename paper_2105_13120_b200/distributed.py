@@ -141,6 +141,18 @@ class CudaHopKernels:
                                                dvec.data_ptr(), V(dq_acc), int(accumulate), V(dq_out), self._st(q)),
                    "rsa_bwd_q_stream")
 
+    def fused_stream_hop(self, q, k_j, v_j, grad_r, rowmax, dvec, seq, origin, dk_acc, dv_acc, dq_acc, accumulate,
+                         dq_out):
+        """kv_stream_hop + q_stream_hop in one launch (rsa_bwd_stream_fused): fp32 dK/dV of
+        origin j (accumulating), dQ partials added into the fp32 dq_acc (zeroed on the first
+        hop), bf16 dq_out on the last."""
+        g = self._g(q, seq, origin)
+        V = self.engine._view
+        self.check(self.lib().rsa_bwd_stream_fused(ctypes.byref(g), V(q), V(k_j), V(v_j), V(grad_r),
+                                                   rowmax.data_ptr(), dvec.data_ptr(), V(dk_acc), V(dv_acc), self.F32,
+                                                   int(accumulate), dq_acc.data_ptr(), int(accumulate), V(dq_out),
+                                                   self._st(q)), "rsa_bwd_stream_fused")
+
     def project_pair(self, e_cols, k, f_cols, v):
         """[E_d K_d ; F_d V_d] as one fp32 [2][B][Z][K][A] buffer (tcgen05 GEMMs)."""
         from . import tensor_ops
@@ -398,16 +410,21 @@ class SpmdRing:
         acc = torch.empty((2, 2, 1, b, z, c, a), dtype=_acc_dtype(grad), device=dev)  # [buf][dk|dv]
         kv[0, 0].copy_(ctx.extra["k_local"])
         kv[0, 1].copy_(ctx.v_local)
-        dq_acc = torch.empty((1, b, z, c, a), dtype=_acc_dtype(grad), device=dev)
+        fused = hasattr(kern, "fused_stream_hop") and not kern.engine.deterministic()
+        dq_acc = torch.empty((1, b, z, c, a), dtype=torch.float32 if fused else _acc_dtype(grad), device=dev)
         dq = torch.empty((1, b, z, c, a), dtype=grad.dtype, device=dev)
         for h in range(n):
             j = (d - h) % n
             cur, nxt = h % 2, (h + 1) % 2
             pend_kv = self._post([(kv[cur], kv[nxt])]) if h + 1 < n and n > 1 else None
-            kern.kv_stream_hop(ctx.q, kv[cur, 0], kv[cur, 1], grad_r, st["rowmax"], dvec, seq, j, acc[cur, 0],
-                               acc[cur, 1], h > 0)
-            kern.q_stream_hop(ctx.q, kv[cur, 0], kv[cur, 1], grad_r, st["rowmax"], dvec, seq, j, dq_acc, h > 0,
-                              dq if h == n - 1 else None)
+            if fused:
+                kern.fused_stream_hop(ctx.q, kv[cur, 0], kv[cur, 1], grad_r, st["rowmax"], dvec, seq, j, acc[cur, 0],
+                                      acc[cur, 1], dq_acc, h > 0, dq if h == n - 1 else None)
+            else:
+                kern.kv_stream_hop(ctx.q, kv[cur, 0], kv[cur, 1], grad_r, st["rowmax"], dvec, seq, j, acc[cur, 0],
+                                   acc[cur, 1], h > 0)
+                kern.q_stream_hop(ctx.q, kv[cur, 0], kv[cur, 1], grad_r, st["rowmax"], dvec, seq, j, dq_acc, h > 0,
+                                  dq if h == n - 1 else None)
             # origin j's dK/dV sum moves on with it; after the last hop it arrives home complete
             pend_acc = self._post([(acc[cur], acc[nxt])], charge=False) if n > 1 else None
             self._wait(pend_kv)

@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from typing import NamedTuple
 
 import torch
@@ -37,6 +38,7 @@ from .errors import ShapeError
 
 __all__ = ["fused_supported", "forward", "backward", "Forward", "normalized_panel", "recompute_outputs", "NULL_VIEW",
            "KernelTimer", "StreamForward", "forward_stream", "backward_stream", "stream_backward_kernels", "stream_panel",
+           "deterministic",
            "stream_supported"]
 
 NULL_VIEW = RsaView(None, 0, 0, 0, 0)
@@ -446,14 +448,22 @@ def stream_panel(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, rowmax: torc
     return normalized_panel(panel[0], rowscale[d], dtype)
 
 
+def deterministic() -> bool:
+    """RSA_B200_DETERMINISTIC=1 selects the stream backward's two-kernel form, whose sums are
+    all taken in a fixed order (bitwise reproducible and bitwise equal to the panel mode);
+    the default one-pass kernel adds dQ's key-tile partials in arrival order."""
+    return os.environ.get("RSA_B200_DETERMINISTIC", "0") not in ("", "0")
+
+
 def backward_stream(q, k, v, grad, out, rowscale, rowmax, *, grads: tuple | None = None,
                     dvec: torch.Tensor | None = None, grad_scaled: torch.Tensor | None = None,
-                    dkv_f32: bool = False, timer=None):
+                    dkv_f32: bool = False, timer=None, fused: bool | None = None, dq_acc: torch.Tensor | None = None):
     """Stream-mode RSA backward: (dq, dk, dv) from q, k, v, dO and the forward's O, r, m.
 
-    rsa_rowdot_scale forms D*r and dO*r; rsa_bwd_kv_stream walks every query tile per key
-    tile (dK, dV); rsa_bwd_q_stream every key tile per query tile (dQ).  Both recompute
-    P~ on chip.  dk / dv are bf16 [N_org][B][Z][ck][A] (fp32 with ``dkv_f32``)."""
+    rsa_rowdot_scale forms D*r and dO*r; then either rsa_bwd_stream_fused (default: one pass
+    per key tile, dQ partials added in L2) or, with ``fused=False`` / RSA_B200_DETERMINISTIC=1,
+    rsa_bwd_kv_stream (dK, dV) and rsa_bwd_q_stream (dQ).  Every kernel recomputes P~ on
+    chip.  dk / dv are bf16 [N_org][B][Z][ck][A] (fp32 with ``dkv_f32``)."""
     n, b, z, c, a = q.shape
     norg, ck = k.shape[0], k.shape[3]
     dev = q.device
@@ -467,12 +477,18 @@ def backward_stream(q, k, v, grad, out, rowscale, rowmax, *, grads: tuple | None
         dq, dk, dv = grads
     with tm("rowdot"):
         dvec, gsc = ops.rowdot_scale(grad, out, rowscale, out=dvec, a_scaled=grad_scaled)
-    return stream_backward_kernels(q, k, v, gsc, rowmax, dvec, (dq, dk, dv), timer=timer)
+    return stream_backward_kernels(q, k, v, gsc, rowmax, dvec, (dq, dk, dv), timer=timer, fused=fused, dq_acc=dq_acc)
 
 
-def stream_backward_kernels(q, k, v, grad_scaled, rowmax, dvec, grads, timer=None):
-    """The two stream-mode backward launches on prepared dO*r (``grad_scaled``) and D*r
-    (``dvec``): rsa_bwd_kv_stream into grads[1:] (bf16 or fp32), rsa_bwd_q_stream into grads[0]."""
+def stream_backward_kernels(q, k, v, grad_scaled, rowmax, dvec, grads, timer=None, fused: bool | None = None,
+                            dq_acc: torch.Tensor | None = None):
+    """The stream-mode backward launches on prepared dO*r (``grad_scaled``) and D*r (``dvec``)
+    into grads = (dq bf16, dk, dv bf16 or fp32).
+
+    ``fused`` (default: not ``deterministic()``): rsa_bwd_stream_fused, one launch computing
+    S, dP and the exp2 once, with ``dq_acc`` (fp32 [N][B][Z][c][A], allocated if None) as its
+    dQ accumulator, then the bf16 cast of dQ.  Otherwise rsa_bwd_kv_stream then
+    rsa_bwd_q_stream."""
     n, b, z, c, a = q.shape
     norg, ck = k.shape[0], k.shape[3]
     dq, dk, dv = grads
@@ -480,10 +496,21 @@ def stream_backward_kernels(q, k, v, grad_scaled, rowmax, dvec, grads, timer=Non
     g = _geom(n, b, z, c, a, norg * ck, 0, norg, 0 if ck == c else ck)
     L = lib()
     st = _stream(q)
+    kdt = F32 if dk.dtype == torch.float32 else BF16
+    if fused is None:
+        fused = not deterministic()
+    if fused:
+        if dq_acc is None:
+            dq_acc = torch.empty((n, b, z, c, a), dtype=torch.float32, device=q.device)
+        with tm("bwd_stream_fused"):
+            check(L.rsa_bwd_stream_fused(ctypes.byref(g), _view(q), _view(k), _view(v), _view(grad_scaled),
+                                         rowmax.data_ptr(), dvec.data_ptr(), _view(dk), _view(dv), kdt, 0,
+                                         dq_acc.data_ptr(), 0, _view(dq), st), "rsa_bwd_stream_fused")
+        return dq, dk, dv
     with tm("bwd_kv_stream"):
         check(L.rsa_bwd_kv_stream(ctypes.byref(g), _view(q), _view(k), _view(v), _view(grad_scaled),
-                                  rowmax.data_ptr(), dvec.data_ptr(), _view(dk), _view(dv),
-                                  F32 if dk.dtype == torch.float32 else BF16, 0, st), "rsa_bwd_kv_stream")
+                                  rowmax.data_ptr(), dvec.data_ptr(), _view(dk), _view(dv), kdt, 0, st),
+              "rsa_bwd_kv_stream")
     with tm("bwd_q_stream"):
         check(L.rsa_bwd_q_stream(ctypes.byref(g), _view(q), _view(k), _view(v), _view(grad_scaled),
                                  rowmax.data_ptr(), dvec.data_ptr(), NULL_VIEW, 0, _view(dq), st), "rsa_bwd_q_stream")

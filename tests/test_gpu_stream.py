@@ -61,8 +61,9 @@ STREAM_SHAPES = [  # (B, Z, L, N)
 
 
 @pytest.mark.parametrize("shape", STREAM_SHAPES)
-def test_stream_mode_matches_oracle_and_panel_mode_bitwise(rsa, shape):
+def test_stream_mode_matches_oracle_and_panel_mode_bitwise(rsa, shape, monkeypatch):
     pkg, ra = rsa
+    monkeypatch.setenv("RSA_B200_DETERMINISTIC", "1")  # the fixed-order two-kernel backward
     b, z, seq, n = shape
     a = 64
     q, k, v, g = _inputs(b, z, seq, a, seed=101 + seq + n)
@@ -93,6 +94,17 @@ def test_stream_mode_matches_oracle_and_panel_mode_bitwise(rsa, shape):
     _gate("dk", _np(pkg.gather_sequence(bs.grad_k)), cat(dk))
     _gate("dv", _np(pkg.gather_sequence(bs.grad_v)), cat(dv))
     assert fs.ledger.devices[0].ring_p2p_elements == fp.ledger.devices[0].ring_p2p_elements
+    # the default one-pass backward (rsa_bwd_stream_fused: dQ partials added in L2 in arrival
+    # order, query tiles walked from a per-item offset): oracle gates, and within bf16
+    # rounding of the fixed-order result
+    monkeypatch.setenv("RSA_B200_DETERMINISTIC", "0")
+    bf = ra.ring_attention_backward(ch(q), ch(k), ch(v), fs.probs, ch(g), cfg)
+    torch.cuda.synchronize()
+    for name, got, ref, want in (("dq", bf.grad_q, bs.grad_q, dq), ("dk", bf.grad_k, bs.grad_k, dk),
+                                 ("dv", bf.grad_v, bs.grad_v, dv)):
+        _gate(name, _np(pkg.gather_sequence(got)), cat(want))
+        g_, r_ = _np(pkg.gather_sequence(got)), _np(pkg.gather_sequence(ref))
+        assert np.linalg.norm(g_ - r_) <= 4e-3 * np.linalg.norm(r_), name
 
 
 def test_stream_mode_multi_unit_grid_capped(rsa):
@@ -109,7 +121,8 @@ def test_stream_mode_multi_unit_grid_capped(rsa):
     lib().rsa_set_max_ctas(3)
     try:
         sf = engine.forward_stream(tq, tk, tv)
-        sb = engine.backward_stream(tq, tk, tv, tg, sf.out, sf.rowscale, sf.rowmax)
+        sb = engine.backward_stream(tq, tk, tv, tg, sf.out, sf.rowscale, sf.rowmax, fused=False)
+        sfu = engine.backward_stream(tq, tk, tv, tg, sf.out, sf.rowscale, sf.rowmax, fused=True)
         torch.cuda.synchronize()
     finally:
         lib().rsa_set_max_ctas(0)
@@ -117,6 +130,9 @@ def test_stream_mode_multi_unit_grid_capped(rsa):
     assert torch.equal(sf.out, ref_f.out) and torch.equal(sf.rowscale, ref_f.rowscale)
     for x, y in zip(sb, ref_b):
         assert torch.equal(x, y)
+    for x, y in zip(sfu, ref_b):  # the one-pass form: same sums in another order
+        x, y = x.double(), y.double()
+        assert torch.linalg.norm(x - y) <= 4e-3 * torch.linalg.norm(y)
 
 
 def test_stream_fallback_on_far_row_max(rsa):

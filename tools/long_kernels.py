@@ -23,7 +23,7 @@ def run(L, n=1):
     q, k, v, dO = (torch.randn((n, B, Z, c, A), generator=g, device=dev).to(torch.bfloat16) for _ in range(4))
     pe = B * Z * L * L
     res = {"seq_len": L, "ranks": n}
-    for mode in ("panel", "stream"):
+    for mode in ("panel", "stream", "stream_2k"):
         tm = engine.KernelTimer()
         for it in range(3):
             if it == 1:
@@ -36,7 +36,8 @@ def run(L, n=1):
             else:
                 with tm("fwd_stream"):
                     sf = engine.forward_stream(q, k, v)
-                engine.backward_stream(q, k, v, dO, sf.out, sf.rowscale, sf.rowmax, timer=tm)
+                engine.backward_stream(q, k, v, dO, sf.out, sf.rowscale, sf.rowmax, timer=tm,
+                                       fused=mode == "stream")
         tot = tm.totals()
         ker = {}
         for name, (cnt, ms) in tot.items():
@@ -44,8 +45,9 @@ def run(L, n=1):
             ker[name] = {"us": round(us, 1)}
             if name in ("fwd_factored", "bwd_dkdv", "bwd_dq"):  # 2 bytes per panel element
                 ker[name]["hbm_frac"] = round(2 * pe / HBM * 1e6 / us, 3)
-            if name in ("fwd_stream", "bwd_kv_stream", "bwd_q_stream", "fwd_factored"):
-                prods = {"fwd_stream": 2, "fwd_factored": 2, "bwd_kv_stream": 4, "bwd_q_stream": 3}[name]
+            if name in ("fwd_stream", "bwd_kv_stream", "bwd_q_stream", "fwd_factored", "bwd_stream_fused"):
+                prods = {"fwd_stream": 2, "fwd_factored": 2, "bwd_kv_stream": 4, "bwd_q_stream": 3,
+                         "bwd_stream_fused": 5}[name]
                 ker[name]["tc_frac_incl_recompute"] = round(prods * 2 * pe * A / TC * 1e6 / us, 3)
         res[mode] = {"layer_us": round(sum(v["us"] for v in ker.values()), 1), "kernels": ker}
         torch.cuda.empty_cache()
