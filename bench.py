@@ -330,6 +330,7 @@ def ours(args):
         ly["o"] = torch.empty_like(ly["q"])
         if stream:  # the stream mode saves two fp32 numbers per row instead of the (c x L) panel
             ly["m"] = torch.empty((R, B, Z, c), dtype=torch.float32, device=dev)
+            ly["dq_acc"] = torch.empty((R, B, Z, c, A), dtype=torch.float32, device=dev)
         else:
             ly["p"] = torch.empty((R, B, Z, c, L), dtype=torch.bfloat16, device=dev)
         ly["r"] = torch.empty((R, B, Z, c), dtype=torch.float32, device=dev)
@@ -351,7 +352,8 @@ def ours(args):
 
             if prologue:
                 ops_.rowdot_scale(ly["g"], ly["o"], ly["r"], out=dvec, a_scaled=g_scaled)
-            return engine.stream_backward_kernels(ly["q"], ly["k"], ly["v"], g_scaled, ly["m"], dvec, ly["grads"])
+            return engine.stream_backward_kernels(ly["q"], ly["k"], ly["v"], g_scaled, ly["m"], dvec, ly["grads"],
+                                                  dq_acc=ly["dq_acc"])
         engine.backward(ly["q"], ly["k"], ly["v"], ly["p"], ly["g"], outputs=ly["o"], path="fused",
                         grads=ly["grads"], dvec=dvec, rowscale=ly["r"], grad_scaled=g_scaled, prologue=prologue)
 
@@ -493,7 +495,8 @@ def ours(args):
         kernels[k] = {"launches_per_step": LAYERS, "us_per_launch": per * 1e6, "ms_per_step": tms,
                       "share_of_step": tms / step_ref_ms, "GB/s": b_ / per / 1e9, "TFLOP/s": f_ / per / 1e12}
     kernel_sum = sum(type_ms.values())
-    # fwd + rowdot + one backward launch, or two for the two-kernel / stream backward
+    # fwd + rowdot + one backward launch, or two for the two-kernel backward and the stream
+    # backward (rsa_bwd_stream_fused + dQ's bf16 cast, or the deterministic kv + q pair)
     launches_per_step = LAYERS * (4 if (stream or bwd_kind == "bwd_dkdv_dq") else 3)
 
     # parity of the timed path: re-run one step, then check sampled heads of the first and

@@ -819,8 +819,8 @@ def bench_main(args, metric, unit, config, clock_sampler=None, peaks=None):
         t_hbm = step_bytes / (hbm * 1e9)
         t_link = wire_step / 900e9
         # per layer: n forward hops, rowdot, then one (c <= 512) or two backward launches (panel)
-        # or a kv and a q launch per hop (stream)
-        launches = LAYERS * ((n + 1 + (1 if c <= 512 else 2)) if attn == "panel" else (3 * n + 1))
+        # or one fused launch per hop plus dQ's bf16 cast (stream)
+        launches = LAYERS * ((n + 1 + (1 if c <= 512 else 2)) if attn == "panel" else (2 * n + 2))
         print(json.dumps({
             "metric": metric, "value": value, "unit": unit, "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
