@@ -531,12 +531,14 @@ __global__ void __maxnreg__(96) bwd_q_stream_kernel(const __grid_constant__ Stre
 //   dP'^T = V dO'^T                        SS form
 //   dK += dS^T Q                           TS form, A = dS^T (bf16) in TMEM
 //   dQ_part = dS K_j                       SS form, A = dS in shared memory (MN-major)
-// The epilogue writes dS^T over the dP'^T columns it has just read (each thread its own
-// lanes and columns, so no other warp's operand is touched) and to shared memory with the
-// queries contiguous.  tcgen05.mma executes in issue order, so dP'^T(t+1), issued after
-// dK(t), overwrites dS^T(t) only after dK(t) has read it; dQ_part(t), issued last, is read
-// out at the end of step t+1, when it is long done.  The epilogue scales dQ_part, stages it
-// per warp (32 rows x 16 columns, SWIZZLE_64B) and the
+// The epilogue writes dS^T to TMEM and to shared memory with the queries contiguous.
+// dQ_part(t) lands in the columns dS^T(t) occupied: tcgen05.mma executes in issue order, so
+// it overwrites dS^T(t) only after dK(t) (issued before it) has read it, and the epilogue of
+// step t+1 reads dQ_part(t) out of exactly the columns it then writes dS^T(t+1) into (each
+// thread its own lanes and columns), so the shared buffer needs no barrier beyond
+// dQ_part's own completion -- and dP'^T(t+1) can still be issued as soon as dP'^T(t) is
+// read.  The epilogue scales dQ_part, stages it per warp (32 rows x 16 columns,
+// SWIZZLE_64B) and the
 // TMA unit adds it into an fp32 dQ accumulator in L2 (cp.reduce.async.bulk.tensor .add;
 // tools/membench/red_bulk: ~5.9 TB/s chip-wide).  So dQ's sum over key tiles is taken in
 // arrival order -- not bitwise reproducible, unlike dK / dV (TMEM, fixed order) and the
@@ -546,7 +548,8 @@ __global__ void __maxnreg__(96) bwd_q_stream_kernel(const __grid_constant__ Stre
 // dS^T taking one TMEM buffer in turn, 3085 us; dS^T in shared memory only, read by dK as a
 // K-major SS operand, 2424 us; P~^T / dS^T written over S^T / dP'^T, so S^T(t+1) waits for
 // dV(t), 2474 us; P~^T(t) then dQ_part(t) in one buffer, read out before P~^T(t+1) is
-// written, 2402 us, with the epilogue waiting on dQ_part at every step.)
+// written, 2402 us, with the epilogue waiting on dQ_part at every step; dS^T over dP'^T,
+// so dP'^T(t+1) waits for dK(t), 2407 us.)
 
 constexpr int FS_ST = 3;                                    // (Q, dO', m, D') stages
 constexpr uint32_t FS_OFF_KV = 0;                           // K | V (one buffer)
@@ -557,8 +560,8 @@ constexpr uint32_t FS_OFF_BAR = FS_OFF_STG + SE_WARPS * 2048;
 constexpr uint32_t FS_SMEM = FS_OFF_BAR + 512 + 1024;
 static_assert(FS_OFF_DS % 1024 == 0 && FS_OFF_STG % 1024 == 0, "swizzled tiles need 1024-byte alignment");
 static_assert(FS_SMEM <= 232448, "bwd_stream_fused smem over the sm_100 per-CTA limit");
-// TMEM: S^T [0,128), dP'^T then dS^T [128,256), P~^T [256,320), dQ_part [320,384), dV [384,448), dK [448,512)
-constexpr uint32_t FS_COL_S = 0, FS_COL_DP = 128, FS_COL_P = 256, FS_COL_DQ = 320, FS_COL_DV = 384,
+// TMEM: S^T [0,128), dP'^T [128,256), P~^T [256,320), dS^T then dQ_part [320,384), dV [384,448), dK [448,512)
+constexpr uint32_t FS_COL_S = 0, FS_COL_DP = 128, FS_COL_P = 256, FS_COL_DSQ = 320, FS_COL_DV = 384,
                    FS_COL_DK = 448;
 
 // Key k's 32 dS values for queries part*32.. (bf16 pairs) into the MN-major SWIZZLE_128B dS
@@ -576,9 +579,9 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FS_OFF_BAR);
   uint64_t *kv_full = bar, *kv_empty = bar + 1;
   uint64_t *ld_full = bar + 2, *ld_empty = ld_full + FS_ST;
-  uint64_t *s_full = ld_empty + FS_ST, *s_empty = s_full + 1, *dp_full = s_empty + 1, *p_full = dp_full + 1;
-  uint64_t *p_empty = p_full + 1, *ds_full = p_empty + 1, *dq_full = ds_full + 1, *dq_empty = dq_full + 1;
-  uint64_t *acc_full = dq_empty + 1, *acc_empty = acc_full + 1;
+  uint64_t *s_full = ld_empty + FS_ST, *s_empty = s_full + 1, *dp_full = s_empty + 1, *dp_empty = dp_full + 1;
+  uint64_t *p_full = dp_empty + 1, *p_empty = p_full + 1, *ds_full = p_empty + 1, *dq_full = ds_full + 1;
+  uint64_t *acc_full = dq_full + 1, *acc_empty = acc_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
 
   const Geo& g = p.g;
@@ -592,8 +595,8 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1), mbar_init(kv_empty, 1);
     for (int s = 0; s < FS_ST; ++s) mbar_init(&ld_full[s], 1), mbar_init(&ld_empty[s], 1);
-    mbar_init(s_full, 1), mbar_init(s_empty, SE_WARPS), mbar_init(dp_full, 1), mbar_init(p_full, SE_WARPS);
-    mbar_init(p_empty, 1), mbar_init(ds_full, SE_WARPS), mbar_init(dq_full, 1), mbar_init(dq_empty, SE_WARPS);
+    mbar_init(s_full, 1), mbar_init(s_empty, SE_WARPS), mbar_init(dp_full, 1), mbar_init(dp_empty, SE_WARPS);
+    mbar_init(p_full, SE_WARPS), mbar_init(p_empty, 1), mbar_init(ds_full, SE_WARPS), mbar_init(dq_full, 1);
     mbar_init(acc_full, 1), mbar_init(acc_empty, SE_WARPS);
     fence_barrier_init();
     tma_prefetch(&p.tq), tma_prefetch(&p.tk), tma_prefetch(&p.tv), tma_prefetch(&p.tdo);
@@ -640,7 +643,7 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
     const uint32_t idesc_dq = idesc_bf16_f32(TR, HD, 1, 1);  // dS (smem, MN-major) x K (MN-major)
     const uint32_t ka = smem_u32(smem + FS_OFF_KV), va = ka + TILE, dsa = smem_u32(smem + FS_OFF_DS);
     Pos lq_s, lq_d, lq_v, lq_k;
-    uint32_t n_s = 0, n_p = 0, n_ds = 0, n_dq = 0, it = 0;
+    uint32_t n_s = 0, n_d = 0, n_p = 0, n_ds = 0, it = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
       mbar_wait(kv_full, it & 1);
       auto issue_s = [&]() {  // S^T(t) = K Q^T once the epilogue has read S^T(t-1)
@@ -656,9 +659,10 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
         umma_commit_ws(s_full);
         ++lq_s.i, ++n_s;
       };
-      auto issue_dp = [&]() {  // dP'^T(t) = V dO'^T over dS^T(t-1), which dK(t-1) (issued before) has read
+      auto issue_dp = [&]() {  // dP'^T(t) = V dO'^T once the epilogue has read dP'^T(t-1)
         const uint32_t s = lq_d.slot(FS_ST);
         mbar_wait(&ld_full[s], lq_d.phase(FS_ST));
+        mbar_wait(dp_empty, (n_d & 1) ^ 1);
         tc_fence_after();
         const uint32_t doa = smem_u32(smem + FS_OFF_ST + s * KS_STAGE) + TILE;
 #pragma unroll
@@ -666,10 +670,8 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
           umma_bf16_ws(tmem + FS_COL_DP, smem_desc_sw128(va + k * 32, 0, 1024), smem_desc_sw128(doa + k * 32, 0, 1024),
                        idesc_s, k > 0);
         umma_commit_ws(dp_full);
-        ++lq_d.i;
+        ++lq_d.i, ++n_d;
       };
-      // A columns of K-step k (16 queries) in dS^T: part k/2's 16 packed columns over its dP'^T
-      auto ds_col = [](int k) { return uint32_t((k >> 1) * SE_COLS + (k & 1) * 8); };
       auto issue_dv = [&](int t) {  // dV += P~^T dO' (A from TMEM)
         const uint32_t s = lq_v.slot(FS_ST);
         mbar_wait(p_full, n_p & 1);
@@ -690,30 +692,27 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
         const uint32_t qa = smem_u32(smem + FS_OFF_ST + s * KS_STAGE);
 #pragma unroll
         for (int k = 0; k < TR / 16; ++k)
-          umma_bf16_ts_ws(tmem + FS_COL_DK, tmem + FS_COL_DP + ds_col(k), smem_desc_sw128(qa + k * 2048, ATOM, 1024),
+          umma_bf16_ts_ws(tmem + FS_COL_DK, tmem + FS_COL_DSQ + 8 * k, smem_desc_sw128(qa + k * 2048, ATOM, 1024),
                           idesc_ts, (t | k) != 0);
         umma_commit_ws(&ld_empty[s]);  // the stage's last readers: dK (Q), dV (dO'), the epilogue (m, D')
         ++lq_k.i, ++n_ds;
       };
-      auto issue_dq = [&]() {  // dQ_part = dS K (A = the smem dS tile) once dQ_part(t-1) is read out
-        mbar_wait(dq_empty, (n_dq & 1) ^ 1);
-        tc_fence_after();
+      auto issue_dq = [&]() {  // dQ_part = dS K (A = the smem dS tile) over dS^T, which dK has read
         if (!(p.dbg & 4)) {
 #pragma unroll
           for (int k = 0; k < TK / 16; ++k)  // 16 keys per product: two 8-key groups of dS, 2 KB of K
-            umma_bf16_ws(tmem + FS_COL_DQ, smem_desc_sw128(dsa + k * 4096, 1024, 2048),
+            umma_bf16_ws(tmem + FS_COL_DSQ, smem_desc_sw128(dsa + k * 4096, 1024, 2048),
                          smem_desc_sw128(ka + k * 2048, ATOM, 1024), idesc_dq, k > 0);
         }
         umma_commit_ws(dq_full);
-        ++n_dq;
       };
       issue_s();
       issue_dp();
       for (int t = 0; t < T; ++t) {
         if (t + 1 < T) issue_s();
         issue_dv(t);
-        issue_dk(t);
         if (t + 1 < T) issue_dp();
+        issue_dk(t);
         issue_dq();
       }
       umma_commit_ws(kv_empty);
@@ -740,11 +739,8 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
       mbar_wait(dq_full, n_dq & 1);
       tc_fence_after();
       __syncwarp();
-      tmem_ld16(tmem + lane_base + FS_COL_DQ + part * 16, o);
+      tmem_ld16(tmem + lane_base + FS_COL_DSQ + part * 16, o);
       tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dq_empty);
       ++n_dq;
       if (p.dbg & 2) return;
       if (lane == 0) tma_store_wait_read<0>();  // this warp's previous reduce has read its staging
@@ -804,12 +800,15 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
 #pragma unroll
           for (int j = 0; j < 32; j += 4) ld_shared_f4(stat + TR * 4 + j * 4, dd + j);
           tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dp_empty);
           ++n_d;
 #pragma unroll
           for (int e = 0; e < 16; ++e) w[e] = ds_pair2(w[e], dp[2 * e], dp[2 * e + 1], dd[2 * e], dd[2 * e + 1]);
         }
-        tmem_st16(tmem + lane_base + FS_COL_DP + part * SE_COLS, w);  // over this thread's own dP'^T
-        if (t > 0) dq_stage();
+        if (t > 0) dq_stage();  // frees this thread's DSQ columns (dQ_part(t-1) complete)
+        tmem_st16(tmem + lane_base + FS_COL_DSQ + part * 16, w);
         st_ds_mn(dsa, r, part, w);  // dQ_part(t-1), complete above, was the previous dS's last reader
         fence_proxy_async_smem();
         tmem_st_wait();
