@@ -288,6 +288,8 @@ def kernel_model(name, n, b, z, c, seq, a):
         return 2 * pe + 2 * 7 * ce, 8 * pe * a        # read P; Q,K,V,dO in, dQ,dK,dV out; dO V^T, P^T dO, dS^T Q, dS K
     if name == "bwd_dq":
         return 2 * pe + 2 * 4 * ce, 4 * pe * a        # read P; dO,K,V in, dQ out; dO V^T, dS K
+    if name == "bwd_panel_fused":  # one panel read at any length; dQ partials through L2 (not algorithmic)
+        return 2 * pe + 2 * 7 * ce, 8 * pe * a
     if name == "bwd_dkdv_dq":  # the pair as one backward: the panel read twice (algorithmic: once)
         return 2 * pe + 2 * 7 * ce, 8 * pe * a
     if name == "rowdot":
@@ -333,6 +335,8 @@ def ours(args):
             ly["dq_acc"] = torch.empty((R, B, Z, c, A), dtype=torch.float32, device=dev)
         else:
             ly["p"] = torch.empty((R, B, Z, c, L), dtype=torch.bfloat16, device=dev)
+            if engine.backward_kind(R, B, Z, c, A) == "bwd_panel_fused":  # its dQ accumulator
+                ly["dq_acc"] = torch.empty((R, B, Z, c, A), dtype=torch.float32, device=dev)
         ly["r"] = torch.empty((R, B, Z, c), dtype=torch.float32, device=dev)
         ly["grads"] = (torch.empty_like(ly["q"]), torch.empty_like(ly["q"]), torch.empty_like(ly["q"]))
     dvec = torch.empty((R, B, Z, c), dtype=torch.float32, device=dev)
@@ -355,7 +359,8 @@ def ours(args):
             return engine.stream_backward_kernels(ly["q"], ly["k"], ly["v"], g_scaled, ly["m"], dvec, ly["grads"],
                                                   dq_acc=ly["dq_acc"])
         engine.backward(ly["q"], ly["k"], ly["v"], ly["p"], ly["g"], outputs=ly["o"], path="fused",
-                        grads=ly["grads"], dvec=dvec, rowscale=ly["r"], grad_scaled=g_scaled, prologue=prologue)
+                        grads=ly["grads"], dvec=dvec, rowscale=ly["r"], grad_scaled=g_scaled, prologue=prologue,
+                        dq_acc=ly.get("dq_acc"))
 
     def step():
         for ly in layers:
@@ -422,7 +427,7 @@ def ours(args):
         return run_kind
 
     reps = max(3, min(args.steps, 10))
-    bwd_kind = "bwd_fused" if engine.single_pass_default(R, B, Z, c, A) else "bwd_dkdv_dq"
+    bwd_kind = engine.backward_kind(R, B, Z, c, A)
     kinds = ["fwd_stream", "rowdot", "bwd_stream"] if stream else ["fwd_factored", "rowdot", bwd_kind]
     replays = {}
     for kind in kinds:
@@ -497,7 +502,7 @@ def ours(args):
     kernel_sum = sum(type_ms.values())
     # fwd + rowdot + one backward launch, or two for the two-kernel backward and the stream
     # backward (rsa_bwd_stream_fused + dQ's bf16 cast, or the deterministic kv + q pair)
-    launches_per_step = LAYERS * (4 if (stream or bwd_kind == "bwd_dkdv_dq") else 3)
+    launches_per_step = LAYERS * (4 if (stream or bwd_kind != "bwd_fused") else 3)
 
     # parity of the timed path: re-run one step, then check sampled heads of the first and
     # last layer against the float64 oracle (ringseq/reference.py:66-103 per head)

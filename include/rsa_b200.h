@@ -78,6 +78,13 @@ int rsa_num_sms(void);
  * next-head prefetch, phase flips) that large launches take.  Returns the previous cap. */
 int rsa_set_max_ctas(int max_ctas);
 
+/* Launch option (no reference counterpart): with on != 0 the persistent RSA kernels are
+ * launched with programmatic stream serialization, so a kernel's CTAs start (barrier init,
+ * TMEM allocation, descriptor prefetch) while the previous kernel's last CTAs finish; every
+ * such kernel waits for its predecessor's completion (griddepcontrol.wait) before it reads
+ * or writes global memory.  Off by default.  Returns the previous setting. */
+int rsa_set_pdl(int on);
+
 /* ------------------------------------------------------------ primitives */
 
 /*
@@ -315,6 +322,18 @@ int rsa_bwd_q_stream(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_
 int rsa_bwd_stream_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view dout_scaled,
                          const float* rowmax, const float* dvec, rsa_view dk, rsa_view dv, int dkv_dtype,
                          int accumulate_dkv, float* dq_acc, int accumulate_dq, rsa_view dq_out, void* stream);
+
+/*
+ * The panel-mode backward (ringseq/ring_attention.py:168-209 on the saved probs) in one pass
+ * at ANY length: rsa_bwd_stream_fused's structure with P~ read from the factored panel instead
+ * of recomputed, so the panel is read once where rsa_bwd_dkdv + rsa_bwd_dq read it twice (and
+ * rsa_bwd_fused needs a head's query rows in 4 tiles).  Inputs as rsa_bwd_dkdv (dout_scaled
+ * = dO * r, dvec = D * r from rsa_rowdot_scale); dQ through the fp32 accumulator dq_acc as in
+ * rsa_bwd_stream_fused (arrival-order sum over key tiles).
+ */
+int rsa_bwd_panel_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view dout_scaled, rsa_view panel,
+                        const float* dvec, rsa_view dk, rsa_view dv, int dkv_dtype, int accumulate_dkv, float* dq_acc,
+                        int accumulate_dq, rsa_view dq_out, void* stream);
 
 /* ------------------------------------------ BERT harness */
 

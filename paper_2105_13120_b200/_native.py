@@ -82,6 +82,7 @@ EXPORTS = {
     "rsa_last_error": (ctypes.c_char_p, []),
     "rsa_num_sms": (c_int, []),
     "rsa_set_max_ctas": (c_int, [c_int]),
+    "rsa_set_pdl": (c_int, [c_int]),
     "rsa_gemm": (
         c_int,
         [c_int, c_int, c_int,
@@ -132,6 +133,8 @@ EXPORTS = {
     "rsa_bwd_q_stream": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, c_void_p, _V, c_int, _V, c_void_p]),
     "rsa_bwd_stream_fused": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, c_void_p, _V, _V, c_int, c_int, c_void_p, c_int,
                                      _V, c_void_p]),
+    "rsa_bwd_panel_fused": (c_int, [_GEOM, _V, _V, _V, _V, _V, c_void_p, _V, _V, c_int, c_int, c_void_p, c_int, _V,
+                                    c_void_p]),
 }
 
 _lib = None
@@ -162,6 +165,8 @@ def lib():
         _load_error = f"{LIB_PATH} has ABI version {ver}, expected {ABI_VERSION}; rebuild it"
         raise NativeUnavailable(_load_error)
     _lib = handle
+    if os.environ.get("RSA_B200_PDL", "0") not in ("", "0"):
+        _lib.rsa_set_pdl(1)  # programmatic dependent launch for the persistent kernels
     return _lib
 
 

@@ -31,7 +31,8 @@ namespace {
 struct StreamArgs {
   CUtensorMap tq, tk, tv, tdo;  // q / dO': query rows (chunk); k / v: key rows (key_chunk)
   CUtensorMap tm, td;           // rowmax / dvec as 128-row boxes (bwd_kv_stream)
-  CUtensorMap tdq;              // fp32 dQ accumulator, 16-column x 32-row boxes (bwd_stream_fused)
+  CUtensorMap tdq;              // fp32 dQ accumulator, 16-column x 32-row boxes (bwd_*_fused)
+  CUtensorMap tp;               // the factored panel, 64-key x 128-row boxes (rsa_bwd_panel_fused)
   Geo g;
   int ck;    // keys per origin chunk
   float sl;  // scale * log2(e)
@@ -111,6 +112,8 @@ __global__ void __maxnreg__(96) bwd_kv_stream_kernel(const __grid_constant__ Str
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();  // the next kernel's CTAs may start their prologue on freed SMs
+  pdl_wait();     // the previous kernel's outputs are complete and visible
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
@@ -361,6 +364,8 @@ __global__ void __maxnreg__(96) bwd_q_stream_kernel(const __grid_constant__ Stre
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();  // the next kernel's CTAs may start their prologue on freed SMs
+  pdl_wait();     // the previous kernel's outputs are complete and visible
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
@@ -551,15 +556,31 @@ __global__ void __maxnreg__(96) bwd_q_stream_kernel(const __grid_constant__ Stre
 // written, 2402 us, with the epilogue waiting on dQ_part at every step; dS^T over dP'^T,
 // so dP'^T(t+1) waits for dK(t), 2407 us.)
 
-constexpr int FS_ST = 3;                                    // (Q, dO', m, D') stages
-constexpr uint32_t FS_OFF_KV = 0;                           // K | V (one buffer)
-constexpr uint32_t FS_OFF_ST = 2 * TILE;                    // [stage][Q | dO' | m | D']
-constexpr uint32_t FS_OFF_DS = FS_OFF_ST + FS_ST * KS_STAGE;  // dS: [8-key group][64-query atom][8 keys][128 B]
-constexpr uint32_t FS_OFF_STG = FS_OFF_DS + PTILE;          // dQ_part staging: [epilogue warp][32 rows][64 B]
-constexpr uint32_t FS_OFF_BAR = FS_OFF_STG + SE_WARPS * 2048;
-constexpr uint32_t FS_SMEM = FS_OFF_BAR + 512 + 1024;
-static_assert(FS_OFF_DS % 1024 == 0 && FS_OFF_STG % 1024 == 0, "swizzled tiles need 1024-byte alignment");
-static_assert(FS_SMEM <= 232448, "bwd_stream_fused smem over the sm_100 per-CTA limit");
+// The same kernel serves the panel mode (PANEL = true, rsa_bwd_panel_fused): P~ comes from
+// the saved factored panel instead of S^T and the exp2 -- the producer loads the step's
+// 128 x 128 panel tile with Q and dO', the epilogue reads its key's column of it, and dV is an
+// SS product with A = the panel tile read as MN-major (keys contiguous).  One read of the
+// panel at any length, where rsa_bwd_dkdv + rsa_bwd_dq read it twice.
+// Shared memory: stream stages carry Q | dO' | m | D' (3 deep); panel stages Q | dO' (2 deep)
+// with D' in a small ring of its own, and the panel tiles a 2-deep ring whose slot is freed
+// as soon as dV and the epilogue's column reads have consumed it (early in the step), so
+// two panel tiles are in flight from HBM (with the tile in the Q / dO stage, freed only at
+// the step's end, one was: 2644 us at L = 8192, 0.37 of HBM).
+template <bool PANEL>
+struct FsLayout {
+  static constexpr int ST = PANEL ? 2 : 3;
+  static constexpr uint32_t STAGE = PANEL ? 2 * TILE : KS_STAGE;
+  static constexpr uint32_t OFF_KV = 0;                        // K | V (one buffer)
+  static constexpr uint32_t OFF_ST = 2 * TILE;                 // [stage]
+  static constexpr uint32_t OFF_P = OFF_ST + ST * STAGE;       // panel mode: [slot] P~ tile
+  static constexpr uint32_t OFF_DS = OFF_P + (PANEL ? 2 * PTILE : 0);  // dS: [8-key group][64-query atom][8 keys][128 B]
+  static constexpr uint32_t OFF_STG = OFF_DS + PTILE;          // dQ_part staging: [epilogue warp][32 rows][64 B]
+  static constexpr uint32_t OFF_D = OFF_STG + SE_WARPS * 2048;  // panel mode: [stage][128] D'
+  static constexpr uint32_t OFF_BAR = OFF_D + (PANEL ? ST * TR * 4 : 0);
+  static constexpr uint32_t SMEM = OFF_BAR + 512 + 1024;
+  static_assert(OFF_DS % 1024 == 0 && OFF_STG % 1024 == 0 && STAGE % 1024 == 0, "swizzled tiles: 1024-byte alignment");
+  static_assert(SMEM <= 232448, "bwd_*_fused smem over the sm_100 per-CTA limit");
+};
 // TMEM: S^T [0,128), dP'^T [128,256), P~^T [256,320), dS^T then dQ_part [320,384), dV [384,448), dK [448,512)
 constexpr uint32_t FS_COL_S = 0, FS_COL_DP = 128, FS_COL_P = 256, FS_COL_DSQ = 320, FS_COL_DV = 384,
                    FS_COL_DK = 448;
@@ -574,15 +595,36 @@ __device__ __forceinline__ void st_ds_mn(uint32_t tile, uint32_t key, int part, 
     st_shared_v4(row + ((((part & 1) * 4 + j) ^ kr) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
 }
 
-__global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ StreamArgs p) {
+// Key k's column of a panel tile: P~ of queries part*32 .. +31 as bf16 pairs (the tile is
+// [64-key atom][128 query rows][128 B], SWIZZLE_128B; a warp's 32 keys read 64 contiguous
+// bytes of one row per load).
+__device__ __forceinline__ void ld_col32(uint32_t tile, uint32_t key, int part, uint32_t* w) {
+  const uint32_t base = tile + (key >> 6) * ATOM + (key & 7) * 2, chunk = (key & 63) >> 3;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const uint32_t q0 = part * 32 + 2 * e, q1 = q0 + 1;
+    uint16_t lo, hi;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(lo) : "r"(base + q0 * 128 + ((chunk ^ (q0 & 7)) << 4)));
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(hi) : "r"(base + q1 * 128 + ((chunk ^ (q1 & 7)) << 4)));
+    w[e] = uint32_t(lo) | (uint32_t(hi) << 16);
+  }
+}
+
+template <bool PANEL>
+__global__ void __maxnreg__(96) bwd_onepass_kernel(const __grid_constant__ StreamArgs p) {
+  using Lay = FsLayout<PANEL>;
+  constexpr int FS_ST = Lay::ST;
+  constexpr uint32_t FS_OFF_KV = Lay::OFF_KV, FS_OFF_ST = Lay::OFF_ST, FS_OFF_DS = Lay::OFF_DS,
+                     FS_OFF_STG = Lay::OFF_STG, STAGE = Lay::STAGE;
   uint8_t* smem = smem_base();
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FS_OFF_BAR);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::OFF_BAR);
   uint64_t *kv_full = bar, *kv_empty = bar + 1;
   uint64_t *ld_full = bar + 2, *ld_empty = ld_full + FS_ST;
   uint64_t *s_full = ld_empty + FS_ST, *s_empty = s_full + 1, *dp_full = s_empty + 1, *dp_empty = dp_full + 1;
   uint64_t *p_full = dp_empty + 1, *p_empty = p_full + 1, *ds_full = p_empty + 1, *dq_full = ds_full + 1;
   uint64_t *acc_full = dq_full + 1, *acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t *pp_full = acc_empty + 1, *pp_empty = pp_full + 2;  // panel mode: the P~ tile ring
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pp_empty + 2);
 
   const Geo& g = p.g;
   const int ntk = (p.ck + TK - 1) / TK, nrt = (g.c + TR - 1) / TR;
@@ -594,23 +636,29 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1), mbar_init(kv_empty, 1);
+    for (int s = 0; s < 2; ++s) mbar_init(&pp_full[s], 1), mbar_init(&pp_empty[s], SE_WARPS + 1);
     for (int s = 0; s < FS_ST; ++s) mbar_init(&ld_full[s], 1), mbar_init(&ld_empty[s], 1);
     mbar_init(s_full, 1), mbar_init(s_empty, SE_WARPS), mbar_init(dp_full, 1), mbar_init(dp_empty, SE_WARPS);
     mbar_init(p_full, SE_WARPS), mbar_init(p_empty, 1), mbar_init(ds_full, SE_WARPS), mbar_init(dq_full, 1);
     mbar_init(acc_full, 1), mbar_init(acc_empty, SE_WARPS);
     fence_barrier_init();
     tma_prefetch(&p.tq), tma_prefetch(&p.tk), tma_prefetch(&p.tv), tma_prefetch(&p.tdo);
-    tma_prefetch(&p.tm), tma_prefetch(&p.td), tma_prefetch(&p.tdq);
+    tma_prefetch(&p.td), tma_prefetch(&p.tdq);
+    if (PANEL) tma_prefetch(&p.tp);
+    else tma_prefetch(&p.tm);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();  // the next kernel's CTAs may start their prologue on freed SMs
+  pdl_wait();     // the previous kernel's outputs are complete and visible
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
-      Pos lq;
+      const uint64_t pol = l2_evict_first();  // the panel streams through once
+      Pos lq, lp;
       uint32_t it = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
         const int kt = item % ntk, bz = (item / ntk) % BZ, jo = item / (ntk * BZ);
@@ -623,14 +671,28 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
         const int t0 = kt % T;
         int d = t0 / nrt, r0 = (t0 % nrt) * TR;
         for (int t = 0; t < T; ++t) {
+          if (PANEL) {  // the panel tile first: its slot frees before the stage's
+            const uint32_t ps = lp.slot(2);
+            mbar_wait(&pp_empty[ps], lp.phase(2) ^ 1);
+            mbar_arrive_expect_tx(&pp_full[ps], PTILE);
+            uint8_t* pt = smem + Lay::OFF_P + ps * PTILE;
+            const int k0 = kt * TK;
+            tma_load_5d_hint(pt, &p.tp, &pp_full[ps], k0, g.org_lo + jo, r0, z, d * g.B + b, pol);
+            tma_load_5d_hint(pt + ATOM, &p.tp, &pp_full[ps], k0 + 64, g.org_lo + jo, r0, z, d * g.B + b, pol);
+            ++lp.i;
+          }
           const uint32_t s = lq.slot(FS_ST);
           mbar_wait(&ld_empty[s], lq.phase(FS_ST) ^ 1);
-          mbar_arrive_expect_tx(&ld_full[s], KS_STAGE);
-          uint8_t* st = smem + FS_OFF_ST + s * KS_STAGE;
+          mbar_arrive_expect_tx(&ld_full[s], PANEL ? STAGE + TR * 4 : STAGE);
+          uint8_t* st = smem + FS_OFF_ST + s * STAGE;
           tma_load_4d(st, &p.tq, &ld_full[s], 0, r0, z, d * g.B + b);
           tma_load_4d(st + TILE, &p.tdo, &ld_full[s], 0, r0, z, d * g.B + b);
-          tma_load_3d(st + 2 * TILE, &p.tm, &ld_full[s], r0, z, d * g.B + b);
-          tma_load_3d(st + 2 * TILE + TR * 4, &p.td, &ld_full[s], r0, z, d * g.B + b);
+          if (PANEL) {
+            tma_load_3d(smem + Lay::OFF_D + s * TR * 4, &p.td, &ld_full[s], r0, z, d * g.B + b);
+          } else {
+            tma_load_3d(st + 2 * TILE, &p.tm, &ld_full[s], r0, z, d * g.B + b);
+            tma_load_3d(st + 2 * TILE + TR * 4, &p.td, &ld_full[s], r0, z, d * g.B + b);
+          }
           ++lq.i;
           if ((r0 += TR) >= nrt * TR) r0 = 0, d = d + 1 == g.n_rank ? 0 : d + 1;
         }
@@ -641,8 +703,9 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
     const uint32_t idesc_s = idesc_bf16_f32(TK, TR, 0, 0);   // K x Q^T, V x dO'^T -> keys x queries
     const uint32_t idesc_ts = idesc_bf16_f32(TK, HD, 0, 1);  // P~^T / dS^T (TMEM) x dO' / Q (MN-major)
     const uint32_t idesc_dq = idesc_bf16_f32(TR, HD, 1, 1);  // dS (smem, MN-major) x K (MN-major)
+    const uint32_t idesc_pv = idesc_bf16_f32(TK, HD, 1, 1);  // panel P~^T (smem, MN-major) x dO' (MN-major)
     const uint32_t ka = smem_u32(smem + FS_OFF_KV), va = ka + TILE, dsa = smem_u32(smem + FS_OFF_DS);
-    Pos lq_s, lq_d, lq_v, lq_k;
+    Pos lq_s, lq_d, lq_v, lq_k, lp;
     uint32_t n_s = 0, n_d = 0, n_p = 0, n_ds = 0, it = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
       mbar_wait(kv_full, it & 1);
@@ -651,7 +714,7 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
         mbar_wait(&ld_full[s], lq_s.phase(FS_ST));
         mbar_wait(s_empty, (n_s & 1) ^ 1);
         tc_fence_after();
-        const uint32_t qa = smem_u32(smem + FS_OFF_ST + s * KS_STAGE);
+        const uint32_t qa = smem_u32(smem + FS_OFF_ST + s * STAGE);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
           umma_bf16_ws(tmem + FS_COL_S, smem_desc_sw128(ka + k * 32, 0, 1024), smem_desc_sw128(qa + k * 32, 0, 1024),
@@ -664,7 +727,7 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
         mbar_wait(&ld_full[s], lq_d.phase(FS_ST));
         mbar_wait(dp_empty, (n_d & 1) ^ 1);
         tc_fence_after();
-        const uint32_t doa = smem_u32(smem + FS_OFF_ST + s * KS_STAGE) + TILE;
+        const uint32_t doa = smem_u32(smem + FS_OFF_ST + s * STAGE) + TILE;
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
           umma_bf16_ws(tmem + FS_COL_DP, smem_desc_sw128(va + k * 32, 0, 1024), smem_desc_sw128(doa + k * 32, 0, 1024),
@@ -672,24 +735,36 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
         umma_commit_ws(dp_full);
         ++lq_d.i, ++n_d;
       };
-      auto issue_dv = [&](int t) {  // dV += P~^T dO' (A from TMEM)
+      auto issue_dv = [&](int t) {  // dV += P~^T dO' (A from TMEM, or the panel tile in smem)
         const uint32_t s = lq_v.slot(FS_ST);
-        mbar_wait(p_full, n_p & 1);
+        if (PANEL) mbar_wait(&ld_full[s], lq_v.phase(FS_ST)), mbar_wait(&pp_full[lp.slot(2)], lp.phase(2));
+        else mbar_wait(p_full, n_p & 1);
         if (t == 0) mbar_wait(acc_empty, (it & 1) ^ 1);  // the previous item's dK / dV are read out
         tc_fence_after();
-        const uint32_t doa = smem_u32(smem + FS_OFF_ST + s * KS_STAGE) + TILE;
+        const uint32_t sa = smem_u32(smem + FS_OFF_ST + s * STAGE), doa = sa + TILE;
+        if (PANEL) {
+          const uint32_t ps = lp.slot(2);
+          const uint64_t pd = smem_desc_sw128(smem_u32(smem + Lay::OFF_P + ps * PTILE), ATOM, 1024);
+          const uint64_t dd = smem_desc_sw128(doa, ATOM, 1024);
 #pragma unroll
-        for (int k = 0; k < TR / 16; ++k)
-          umma_bf16_ts_ws(tmem + FS_COL_DV, tmem + FS_COL_P + 8 * k, smem_desc_sw128(doa + k * 2048, ATOM, 1024),
-                          idesc_ts, (t | k) != 0);
-        umma_commit_ws(p_empty);
+          for (int k = 0; k < TR / 16; ++k)  // MN-major: +16 query rows (2048 B) per k step
+            umma_bf16_ws(tmem + FS_COL_DV, pd + 128 * k, dd + 128 * k, idesc_pv, (t | k) != 0);
+          umma_commit_ws(&pp_empty[ps]);  // dV's read of the panel tile (the epilogue arrives too)
+          ++lp.i;
+        } else {
+#pragma unroll
+          for (int k = 0; k < TR / 16; ++k)
+            umma_bf16_ts_ws(tmem + FS_COL_DV, tmem + FS_COL_P + 8 * k, smem_desc_sw128(doa + k * 2048, ATOM, 1024),
+                            idesc_ts, (t | k) != 0);
+          umma_commit_ws(p_empty);
+        }
         ++lq_v.i, ++n_p;
       };
       auto issue_dk = [&](int t) {  // dK += dS^T Q (A from TMEM)
         const uint32_t s = lq_k.slot(FS_ST);
         mbar_wait(ds_full, n_ds & 1);
         tc_fence_after();
-        const uint32_t qa = smem_u32(smem + FS_OFF_ST + s * KS_STAGE);
+        const uint32_t qa = smem_u32(smem + FS_OFF_ST + s * STAGE);
 #pragma unroll
         for (int k = 0; k < TR / 16; ++k)
           umma_bf16_ts_ws(tmem + FS_COL_DK, tmem + FS_COL_DSQ + 8 * k, smem_desc_sw128(qa + k * 2048, ATOM, 1024),
@@ -706,10 +781,10 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
         }
         umma_commit_ws(dq_full);
       };
-      issue_s();
+      if (!PANEL) issue_s();
       issue_dp();
       for (int t = 0; t < T; ++t) {
-        if (t + 1 < T) issue_s();
+        if (!PANEL && t + 1 < T) issue_s();
         issue_dv(t);
         if (t + 1 < T) issue_dp();
         issue_dk(t);
@@ -730,7 +805,7 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
     const uint32_t dsa = smem_u32(smem + FS_OFF_DS);
     uint8_t* stg = smem + FS_OFF_STG + (warp - 2) * 2048;
     const uint32_t stg_row = smem_u32(stg) + lane * 64, sw = (lane >> 1) & 3;
-    Pos lq;
+    Pos lq, lp;
     uint32_t n_s = 0, n_d = 0, n_p = 0, n_dq = 0, it = 0;
     // dQ_part of the previous step (lanes = queries): read out, scaled and staged; the TMA
     // reduce is issued after the step's proxy fence
@@ -765,10 +840,18 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
       for (int t = 0; t < T; ++t) {
         const int nvalid = min(TR, g.c - r0) - part * SE_COLS;  // valid query columns of this part
         const uint32_t s = lq.slot(FS_ST);
-        const uint32_t stat = smem_u32(smem + FS_OFF_ST + s * KS_STAGE + 2 * TILE) + part * SE_COLS * 4;
-        mbar_wait(&ld_full[s], lq.phase(FS_ST));  // m and D' of the step's queries
+        const uint32_t stat = smem_u32(smem + FS_OFF_ST + s * STAGE + 2 * TILE) + part * SE_COLS * 4;  // m | D'
+        const uint32_t dstat = PANEL ? smem_u32(smem + Lay::OFF_D + s * TR * 4) + part * SE_COLS * 4 : stat + TR * 4;
+        mbar_wait(&ld_full[s], lq.phase(FS_ST));  // the step's operands and per-query statistics
         uint32_t w[16];
-        {  // S^T -> P~^T
+        if (PANEL) {  // this key's column of the panel tile
+          const uint32_t ps = lp.slot(2);
+          mbar_wait(&pp_full[ps], lp.phase(2));
+          ld_col32(smem_u32(smem + Lay::OFF_P + ps * PTILE), r, part, w);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&pp_empty[ps]);
+          ++lp.i;
+        } else {  // S^T -> P~^T
           float v[32], m[32];
           mbar_wait(s_full, n_s & 1);
           tc_fence_after();
@@ -783,14 +866,16 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
           ++n_s;
           exp2_pack32_cols(v, nvalid, sl, m, w);
         }
-        mbar_wait(p_empty, (n_p & 1) ^ 1);  // dV(t-1) has read P~^T(t-1)
-        ++n_p;
-        tc_fence_after();
-        tmem_st16(tmem + lane_base + FS_COL_P + part * 16, w);
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(p_full);
+        if (!PANEL) {
+          mbar_wait(p_empty, (n_p & 1) ^ 1);  // dV(t-1) has read P~^T(t-1)
+          ++n_p;
+          tc_fence_after();
+          tmem_st16(tmem + lane_base + FS_COL_P + part * 16, w);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(p_full);
+        }
         {  // dP'^T -> dS^T = P~^T (dP'^T - D')
           float dp[32], dd[32];
           mbar_wait(dp_full, n_d & 1);
@@ -798,7 +883,7 @@ __global__ void __maxnreg__(96) bwd_stream_fused_kernel(const __grid_constant__ 
           __syncwarp();
           tmem_ld32(tmem + lane_base + FS_COL_DP + part * SE_COLS, dp);
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) ld_shared_f4(stat + TR * 4 + j * 4, dd + j);
+          for (int j = 0; j < 32; j += 4) ld_shared_f4(dstat + j * 4, dd + j);
           tmem_ld_wait();
           tc_fence_before();
           __syncwarp();
@@ -883,6 +968,13 @@ inline bool dq_acc_map(CUtensorMap* m, float* base, const rsa_geom* g) {
   return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
+int dq_cast(const float* dq_acc, const rsa_view& dq_out, const rsa_geom* g, int64_t rows, cudaStream_t st) {
+  const int64_t work = rows * 8;
+  const int blocks = int(std::min<int64_t>((work + 255) / 256, int64_t(num_sms()) * 8));
+  dq_cast_kernel<<<blocks, 256, 0, st>>>(dq_acc, to_out(dq_out), g->chunk, g->heads, g->batch, rows);
+  return check_launch("dq_cast_kernel");
+}
+
 bool stream_args(StreamArgs* a, const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view dout,
                  const float* rowmax, const float* dvec) {
   if (!head_map(&a->tq, q, g, g->n_rank) || !head_map(&a->tdo, dout, g, g->n_rank) ||
@@ -961,12 +1053,41 @@ int rsa_bwd_stream_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, 
   if (!accumulate_dq && cudaMemsetAsync(dq_acc, 0, size_t(rows) * HD * 4, st) != cudaSuccess)
     return check_launch("rsa_bwd_stream_fused: dq_acc memset");
   const int items = g->n_org * g->batch * g->heads * ((key_chunk(g) + TK - 1) / TK);
-  const int rc = launch(bwd_stream_fused_kernel, items, FS_SMEM, a, stream, "bwd_stream_fused_kernel", SE_THREADS);
+  const int rc = launch(bwd_onepass_kernel<false>, items, FsLayout<false>::SMEM, a, stream, "bwd_onepass_kernel<stream>",
+                        SE_THREADS);
   if (rc != RSA_OK || !dq_out.ptr) return rc;
-  const int64_t work = rows * 8;
-  const int blocks = int(std::min<int64_t>((work + 255) / 256, int64_t(num_sms()) * 8));
-  dq_cast_kernel<<<blocks, 256, 0, st>>>(dq_acc, to_out(dq_out), g->chunk, g->heads, g->batch, rows);
-  return check_launch("dq_cast_kernel");
+  return dq_cast(dq_acc, dq_out, g, rows, st);
+}
+
+int rsa_bwd_panel_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view dout_scaled, rsa_view panel,
+                        const float* dvec, rsa_view dk, rsa_view dv, int dkv_dtype, int accumulate_dkv, float* dq_acc,
+                        int accumulate_dq, rsa_view dq_out, void* stream) {
+  using namespace rsa;
+  if (!geom_ok(g) || !dvec) return fail(RSA_ERR_INVALID, "rsa_bwd_panel_fused: unsupported geometry");
+  const int esz = dkv_dtype == RSA_BF16 ? 2 : 4;
+  if (!dk.ptr || !dv.ptr || !out_ok(dk, esz) || !out_ok(dv, esz) || !out_ok(dq_out, 2))
+    return fail(RSA_ERR_UNSUPPORTED, "rsa_bwd_panel_fused: output views missing or misaligned");
+  StreamArgs a{};
+  if (!head_map(&a.tq, q, g, g->n_rank) || !head_map(&a.tdo, dout_scaled, g, g->n_rank) ||
+      !head_map(&a.tk, k, g, g->n_org) || !head_map(&a.tv, v, g, g->n_org) || !panel_map(&a.tp, panel, g, g->n_rank) ||
+      !rows_map(&a.td, dvec, g, g->n_rank) || !dq_acc_map(&a.tdq, dq_acc, g))
+    return RSA_ERR_UNSUPPORTED;
+  a.g = to_geo(g);
+  a.ck = g->chunk;
+  a.dvec = dvec;
+  a.dk = to_out(dk);
+  a.dv = to_out(dv);
+  a.dkv_bf16 = dkv_dtype == RSA_BF16;
+  a.accumulate = accumulate_dkv;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t rows = int64_t(g->n_rank) * g->batch * g->heads * g->chunk;
+  if (!accumulate_dq && cudaMemsetAsync(dq_acc, 0, size_t(rows) * HD * 4, st) != cudaSuccess)
+    return check_launch("rsa_bwd_panel_fused: dq_acc memset");
+  const int items = g->n_org * g->batch * g->heads * ((g->chunk + TK - 1) / TK);
+  const int rc = launch(bwd_onepass_kernel<true>, items, FsLayout<true>::SMEM, a, stream, "bwd_onepass_kernel<panel>",
+                        SE_THREADS);
+  if (rc != RSA_OK || !dq_out.ptr) return rc;
+  return dq_cast(dq_acc, dq_out, g, rows, st);
 }
 
 }  // extern "C"

@@ -187,6 +187,8 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();  // the next kernel's CTAs may start their prologue on freed SMs
+  pdl_wait();     // the previous kernel's outputs are complete and visible
   const uint32_t tmem = *tmem_slot;
   const long long tr0 = clock64();
   int tr_i = 0;
@@ -636,7 +638,7 @@ int ff_launch(FfArgs& a, const rsa_geom* g, rsa_view q, rsa_view panel, rsa_view
     return fail(RSA_ERR_CUDA, "rsa_fwd_factored: %d registers/thread allow only %d threads per CTA (need %d)",
                 fa.numRegs, fa.maxThreadsPerBlock, FF_THREADS);
   const int grid = persistent_grid(units);
-  kernel<<<grid, FF_THREADS, FF_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  launch_grid(kernel, grid, FF_THREADS, FF_SMEM, a, stream);
   if (trace_path) {
     static long long host[(FF_THREADS / 32) * 4096];
     cudaMemcpy(host, trace_buf, sizeof(host), cudaMemcpyDeviceToHost);

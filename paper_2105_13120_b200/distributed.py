@@ -19,8 +19,8 @@ logits) sets flag bit 1 and the layer is recomputed two-pass on every row's true
 Backward, ``attn="panel"`` (the reference's saved probability panel): the forward keeps
 every origin's K and V (the slots the ring filled; O(L) per rank, small next to the
 O(c * L) panel), so the backward needs NO ring: one launch over all resident origins
-(rsa_bwd_fused when c <= 512, else rsa_bwd_dkdv + rsa_bwd_dq) writes fp32 dK/dV partials
-for every origin, summed across ranks by ``reduce_scatter`` (default; half the bytes of
+(rsa_bwd_fused when c <= 512, else rsa_bwd_panel_fused, or rsa_bwd_dkdv + rsa_bwd_dq with
+RSA_B200_DETERMINISTIC=1) writes fp32 dK/dV partials for every origin, summed across ranks by ``reduce_scatter`` (default; half the bytes of
 the reference's all-reduce + slice) or ``all_reduce`` (``mode="paper"``,
 ringseq/ring_attention.py:206-209).
 
@@ -121,6 +121,12 @@ class CudaHopKernels:
             self.check(L.rsa_bwd_fused(ctypes.byref(g), V(q), V(k_slots), V(v_slots), V(grad_r), V(panel),
                                        dvec.data_ptr(), self.engine.NULL_VIEW, 0, V(dq), V(dk_part), V(dv_part),
                                        self.F32, 0, self._st(q)), "rsa_bwd_fused")
+            return
+        if not self.engine.deterministic():  # one panel read at any length (rsa_bwd_panel_fused)
+            dq_acc = torch.empty(dq.shape, dtype=torch.float32, device=dq.device)
+            self.check(L.rsa_bwd_panel_fused(ctypes.byref(g), V(q), V(k_slots), V(v_slots), V(grad_r), V(panel),
+                                             dvec.data_ptr(), V(dk_part), V(dv_part), self.F32, 0, dq_acc.data_ptr(),
+                                             0, V(dq), self._st(q)), "rsa_bwd_panel_fused")
             return
         self.check(L.rsa_bwd_dkdv(ctypes.byref(g), V(q), V(v_slots), V(grad_r), V(panel), dvec.data_ptr(),
                                   V(dk_part), V(dv_part), self.F32, 0, self._st(q)), "rsa_bwd_dkdv")

@@ -38,7 +38,7 @@ from .errors import ShapeError
 
 __all__ = ["fused_supported", "forward", "backward", "Forward", "normalized_panel", "recompute_outputs", "NULL_VIEW",
            "KernelTimer", "StreamForward", "forward_stream", "backward_stream", "stream_backward_kernels", "stream_panel",
-           "deterministic",
+           "deterministic", "backward_kind",
            "stream_supported"]
 
 NULL_VIEW = RsaView(None, 0, 0, 0, 0)
@@ -251,9 +251,25 @@ def recompute_outputs(panel: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def backward_kind(n: int, b: int, z: int, c: int, a: int) -> str:
+    """The panel backward ``backward(single_pass=None)`` runs for this geometry:
+    "bwd_fused" (one CTA per head, one panel read) when it tiles the geometry and there are at
+    least half as many heads as SMs; otherwise "bwd_panel_fused" (one CTA per key tile, one
+    panel read at any length) when a head has more than 4 query tiles, and the fixed-order
+    "bwd_dkdv_dq" pair for the small-batch short shapes (config 1: 44.9 against 45.3 us per
+    graph-captured layer for the one-pass kernel with its dQ zero-fill and cast) or under
+    RSA_B200_DETERMINISTIC=1."""
+    if single_pass_default(n, b, z, c, a):
+        return "bwd_fused"
+    if not deterministic() and not single_pass_supported(n, b, z, c, a):
+        return "bwd_panel_fused"
+    return "bwd_dkdv_dq"
+
+
 def single_pass_default(n: int, b: int, z: int, c: int, a: int) -> bool:
     """The backward ``backward(single_pass=None)`` runs: rsa_bwd_fused when it can tile the
-    geometry and there are at least half as many heads as SMs, else rsa_bwd_dkdv + rsa_bwd_dq."""
+    geometry and there are at least half as many heads as SMs, else rsa_bwd_panel_fused (or,
+    with RSA_B200_DETERMINISTIC=1, rsa_bwd_dkdv + rsa_bwd_dq)."""
     return single_pass_supported(n, b, z, c, a) and 2 * b * z >= lib().rsa_num_sms()
 
 
@@ -266,13 +282,17 @@ def single_pass_supported(n: int, b: int, z: int, c: int, a: int) -> bool:
 def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path: str = "auto",
              grads: tuple | None = None, dvec: torch.Tensor | None = None, rowscale: torch.Tensor | None = None,
              grad_scaled: torch.Tensor | None = None, timer=None, single_pass: bool | None = None,
-             prologue: bool = True):
+             prologue: bool = True, dq_acc: torch.Tensor | None = None):
     """RSA backward on stacked chunks; returns (dq, dk, dv) as [N][B][Z][c][A] bf16.
 
     ``grads`` / ``dvec`` optionally supply preallocated output and D buffers
     (the bench reuses them across layers).  On the fused path,
-    ``single_pass`` picks rsa_bwd_fused (one panel read; default when the
-    geometry allows) or the rsa_bwd_dkdv + rsa_bwd_dq pair.
+    ``single_pass`` picks rsa_bwd_fused (one CTA per head, one panel read; default when the
+    geometry allows and there are at least half as many heads as SMs); otherwise, for heads
+    of more than 4 query tiles, rsa_bwd_panel_fused (one CTA per key tile, one panel read at
+    any length, dQ partials added in L2 through ``dq_acc``), else (or with
+    RSA_B200_DETERMINISTIC=1) the fixed-order rsa_bwd_dkdv + rsa_bwd_dq pair, which reads the
+    panel twice (see ``backward_kind``).
 
     ``rowscale`` marks ``panel`` as factored (P = rowscale * panel, see
     ``forward``): rsa_rowdot_scale then forms D*r and dO*r (``grad_scaled``
@@ -313,15 +333,23 @@ def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path:
         st = _stream(q)
         g = _geom(n, b, z, c, a, seq, 0, n)
         if single_pass is None:
-            # one CTA per head: with fewer heads than half the SMs the two-kernel form (one CTA
-            # per key tile, then per query tile) fills the machine better despite the second
-            # panel read (config 1, B4 Z12: 46.6 vs 48.4 us per graph-captured layer)
+            # one CTA per head: with fewer heads than half the SMs the per-key-tile forms
+            # (rsa_bwd_panel_fused, or the two-kernel pair) fill the machine better
+            # (config 1, B4 Z12: 46.6 vs 48.4 us per graph-captured layer for the pair)
             single_pass = bool(L.rsa_bwd_fused_supported(ctypes.byref(g))) and 2 * b * z >= L.rsa_num_sms()
         if single_pass:
             with tm("bwd_fused"):
                 check(L.rsa_bwd_fused(ctypes.byref(g), _view(q), _view(k), _view(v), _view(grad), _view(panel),
                                       dvec.data_ptr(), NULL_VIEW, 0, _view(dq), _view(dk), _view(dv), BF16, 0, st),
                       "rsa_bwd_fused")
+            return dq, dk, dv
+        if not deterministic() and not L.rsa_bwd_fused_supported(ctypes.byref(g)):
+            if dq_acc is None:
+                dq_acc = torch.empty((n, b, z, c, a), dtype=torch.float32, device=dev)
+            with tm("bwd_panel_fused"):
+                check(L.rsa_bwd_panel_fused(ctypes.byref(g), _view(q), _view(k), _view(v), _view(grad), _view(panel),
+                                            dvec.data_ptr(), _view(dk), _view(dv), BF16, 0, dq_acc.data_ptr(), 0,
+                                            _view(dq), st), "rsa_bwd_panel_fused")
             return dq, dk, dv
         with tm("bwd_dkdv"):
             check(L.rsa_bwd_dkdv(ctypes.byref(g), _view(q), _view(v), _view(grad), _view(panel), dvec.data_ptr(),

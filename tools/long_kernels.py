@@ -4,6 +4,7 @@ kernel's own bound: HBM bytes (panel traffic) or tensor flops (stream recompute)
 usage: python tools/long_kernels.py [L ...]        (B=4, Z=12, A=64, every origin resident)
 """
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -23,12 +24,13 @@ def run(L, n=1):
     q, k, v, dO = (torch.randn((n, B, Z, c, A), generator=g, device=dev).to(torch.bfloat16) for _ in range(4))
     pe = B * Z * L * L
     res = {"seq_len": L, "ranks": n}
-    for mode in ("panel", "stream", "stream_2k"):
+    for mode in ("panel", "panel_2k", "stream", "stream_2k"):
+        os.environ["RSA_B200_DETERMINISTIC"] = "1" if mode == "panel_2k" else "0"
         tm = engine.KernelTimer()
         for it in range(3):
             if it == 1:
                 tm.reset()
-            if mode == "panel":
+            if mode.startswith("panel"):
                 out, panel, rs, flag = engine.forward(q, k, v, path="fused", timer=tm)
                 engine.backward(q, k, v, panel, dO, outputs=out, rowscale=rs, path="fused", timer=tm,
                                 single_pass=False)
@@ -43,7 +45,7 @@ def run(L, n=1):
         for name, (cnt, ms) in tot.items():
             us = ms / cnt * 1e3
             ker[name] = {"us": round(us, 1)}
-            if name in ("fwd_factored", "bwd_dkdv", "bwd_dq"):  # 2 bytes per panel element
+            if name in ("fwd_factored", "bwd_dkdv", "bwd_dq", "bwd_panel_fused"):  # 2 bytes per panel element
                 ker[name]["hbm_frac"] = round(2 * pe / HBM * 1e6 / us, 3)
             if name in ("fwd_stream", "bwd_kv_stream", "bwd_q_stream", "fwd_factored", "bwd_stream_fused"):
                 prods = {"fwd_stream": 2, "fwd_factored": 2, "bwd_kv_stream": 4, "bwd_q_stream": 3,
