@@ -78,13 +78,6 @@ int rsa_num_sms(void);
  * next-head prefetch, phase flips) that large launches take.  Returns the previous cap. */
 int rsa_set_max_ctas(int max_ctas);
 
-/* Launch option (no reference counterpart): with on != 0 the persistent RSA kernels are
- * launched with programmatic stream serialization, so a kernel's CTAs start (barrier init,
- * TMEM allocation, descriptor prefetch) while the previous kernel's last CTAs finish; every
- * such kernel waits for its predecessor's completion (griddepcontrol.wait) before it reads
- * or writes global memory.  Off by default.  Returns the previous setting. */
-int rsa_set_pdl(int on);
-
 /* ------------------------------------------------------------ primitives */
 
 /*

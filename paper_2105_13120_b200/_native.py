@@ -82,7 +82,6 @@ EXPORTS = {
     "rsa_last_error": (ctypes.c_char_p, []),
     "rsa_num_sms": (c_int, []),
     "rsa_set_max_ctas": (c_int, [c_int]),
-    "rsa_set_pdl": (c_int, [c_int]),
     "rsa_gemm": (
         c_int,
         [c_int, c_int, c_int,
@@ -165,8 +164,6 @@ def lib():
         _load_error = f"{LIB_PATH} has ABI version {ver}, expected {ABI_VERSION}; rebuild it"
         raise NativeUnavailable(_load_error)
     _lib = handle
-    if os.environ.get("RSA_B200_PDL", "0") not in ("", "0"):
-        _lib.rsa_set_pdl(1)  # programmatic dependent launch for the persistent kernels
     return _lib
 
 

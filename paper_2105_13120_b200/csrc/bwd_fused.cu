@@ -114,8 +114,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  pdl_trigger();  // the next kernel's CTAs may start their prologue on freed SMs
-  pdl_wait();     // the previous kernel's outputs are complete and visible
   const uint32_t tmem = *tmem_slot;
   const long long tr0 = clock64();
   int tr_i = 0;

@@ -112,8 +112,6 @@ __global__ void __maxnreg__(96) bwd_kv_stream_kernel(const __grid_constant__ Str
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  pdl_trigger();  // the next kernel's CTAs may start their prologue on freed SMs
-  pdl_wait();     // the previous kernel's outputs are complete and visible
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
@@ -364,8 +362,6 @@ __global__ void __maxnreg__(96) bwd_q_stream_kernel(const __grid_constant__ Stre
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  pdl_trigger();  // the next kernel's CTAs may start their prologue on freed SMs
-  pdl_wait();     // the previous kernel's outputs are complete and visible
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
@@ -650,8 +646,6 @@ __global__ void __maxnreg__(96) bwd_onepass_kernel(const __grid_constant__ Strea
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  pdl_trigger();  // the next kernel's CTAs may start their prologue on freed SMs
-  pdl_wait();     // the previous kernel's outputs are complete and visible
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {

@@ -78,9 +78,6 @@ int num_sms() {
 }
 
 static int g_max_ctas = 0;  // 0: one CTA per SM (rsa_set_max_ctas)
-static int g_pdl = 0;       // rsa_set_pdl
-
-bool pdl_enabled() { return g_pdl != 0; }
 
 int persistent_grid(int64_t items) {
   int64_t grid = num_sms();
@@ -99,12 +96,6 @@ int rsa_num_sms(void) { return rsa::num_sms(); }
 int rsa_set_max_ctas(int max_ctas) {
   const int prev = rsa::g_max_ctas;
   rsa::g_max_ctas = max_ctas > 0 ? max_ctas : 0;
-  return prev;
-}
-
-int rsa_set_pdl(int on) {
-  const int prev = rsa::g_pdl;
-  rsa::g_pdl = on ? 1 : 0;
   return prev;
 }
 

@@ -33,7 +33,5 @@ int num_sms();
 
 // Grid of a persistent kernel: min(items, SMs, the rsa_set_max_ctas cap).
 int persistent_grid(int64_t items);
-// rsa_set_pdl: launch the persistent kernels with programmatic stream serialization
-bool pdl_enabled();
 
 }  // namespace rsa

@@ -92,8 +92,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) fwd_kernel(const __grid_constant_
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  pdl_trigger();  // the next kernel's CTAs may start their prologue on freed SMs
-  pdl_wait();     // the previous kernel's outputs are complete and visible
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
@@ -393,8 +391,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dkdv_kernel(const __grid_cons
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  pdl_trigger();  // the next kernel's CTAs may start their prologue on freed SMs
-  pdl_wait();     // the previous kernel's outputs are complete and visible
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
@@ -600,8 +596,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dq_kernel(const __grid_consta
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  pdl_trigger();  // the next kernel's CTAs may start their prologue on freed SMs
-  pdl_wait();     // the previous kernel's outputs are complete and visible
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {

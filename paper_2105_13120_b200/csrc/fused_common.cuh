@@ -327,22 +327,10 @@ inline bool out_ok(const rsa_view& v, int esz) {
          (v.s_rank * esz) % 16 == 0;
 }
 
-// One launch of a persistent kernel, with programmatic stream serialization when
-// rsa_set_pdl is on (every kernel launched here calls pdl_wait before touching global memory).
+// One launch of a persistent kernel.
 template <typename K, typename A>
 void launch_grid(K kernel, int grid, int threads, uint32_t smem, const A& args, void* stream) {
-  if (pdl_enabled()) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid), cfg.blockDim = dim3(threads), cfg.dynamicSmemBytes = smem;
-    cfg.stream = reinterpret_cast<cudaStream_t>(stream);
-    cudaLaunchAttribute attr{};
-    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr.val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = &attr, cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kernel, args);
-  } else {
-    kernel<<<grid, threads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(args);
-  }
+  kernel<<<grid, threads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(args);
 }
 
 template <typename K, typename A>

@@ -108,8 +108,6 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  pdl_trigger();  // the next kernel's CTAs may start their prologue on freed SMs
-  pdl_wait();     // the previous kernel's outputs are complete and visible
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {

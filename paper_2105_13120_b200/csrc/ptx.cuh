@@ -194,15 +194,6 @@ __device__ __forceinline__ void tma_store_wait_all() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// ------------------------------------------- programmatic dependent launch
-
-// Let the next kernel in the stream start its CTAs (prologue) while this grid finishes;
-// it still waits for this grid's completion in pdl_wait before touching its outputs.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-// Wait until the preceding grid has completed and its memory is visible (a no-op unless this
-// grid was launched with programmatic stream serialization).
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
 // ------------------------------------------------------- tcgen05 / TMEM
 
 // Allocate `ncols` TMEM columns (power of two >= 32); one full warp calls.
