@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define RSA_ABI_VERSION 3
+#define RSA_ABI_VERSION 4
 
 enum rsa_status {
   RSA_OK = 0,

@@ -21,7 +21,7 @@ from .errors import NativeError, NativeUnavailable, NumericError, ShapeError
 __all__ = ["lib", "check", "RsaView", "RsaGeom", "RsaFwdExt", "LIB_PATH", "ABI_VERSION", "F32", "BF16", "EXPORTS"]
 
 LIB_PATH = Path(os.environ.get("RSA_B200_LIB", Path(__file__).resolve().parent / "librsa_b200.so"))
-ABI_VERSION = 3
+ABI_VERSION = 4
 F32, BF16 = 0, 1
 
 RSA_OK, RSA_ERR_INVALID, RSA_ERR_UNSUPPORTED, RSA_ERR_CUDA, RSA_ERR_NUMERIC = 0, 1, 2, 3, 4
