@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--layers", type=int, default=12)
     ap.add_argument("--heads", type=int, default=12)
     ap.add_argument("--head-size", type=int, default=64)
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--e2e-checks", default="deferred", choices=["sync", "deferred"],
                     help="RSA_B200_CHECK for the e2e leg: deferred reads each forward's status flag at its "
                          "backward instead of a host sync per forward call")
