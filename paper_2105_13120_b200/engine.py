@@ -344,8 +344,7 @@ def backward(q, k, v, panel, grad, *, outputs: torch.Tensor | None = None, path:
                       "rsa_bwd_fused")
             return dq, dk, dv
         if not deterministic() and not L.rsa_bwd_fused_supported(ctypes.byref(g)):
-            if dq_acc is None:
-                dq_acc = torch.empty((n, b, z, c, a), dtype=torch.float32, device=dev)
+            dq_acc = _dq_accumulator(dq_acc, (n, b, z, c, a), dev)
             with tm("bwd_panel_fused"):
                 check(L.rsa_bwd_panel_fused(ctypes.byref(g), _view(q), _view(k), _view(v), _view(grad), _view(panel),
                                             dvec.data_ptr(), _view(dk), _view(dv), BF16, 0, dq_acc.data_ptr(), 0,
@@ -476,6 +475,17 @@ def stream_panel(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, rowmax: torc
     return normalized_panel(panel[0], rowscale[d], dtype)
 
 
+def _dq_accumulator(dq_acc: torch.Tensor | None, shape, device) -> torch.Tensor:
+    """The one-pass backwards' fp32 dQ accumulator: contiguous [N][B][Z][c][A] fp32 (the kernel
+    adds 16-column x 32-row boxes into it by TMA); allocated when not supplied."""
+    if dq_acc is None:
+        return torch.empty(shape, dtype=torch.float32, device=device)
+    if dq_acc.dtype != torch.float32 or tuple(dq_acc.shape) != tuple(shape) or not dq_acc.is_contiguous():
+        raise ShapeError(f"dq_acc must be a contiguous fp32 tensor of shape {tuple(shape)}, got "
+                         f"{dq_acc.dtype} {tuple(dq_acc.shape)}")
+    return dq_acc
+
+
 def deterministic() -> bool:
     """RSA_B200_DETERMINISTIC=1 selects the stream backward's two-kernel form, whose sums are
     all taken in a fixed order (bitwise reproducible and bitwise equal to the panel mode);
@@ -528,8 +538,7 @@ def stream_backward_kernels(q, k, v, grad_scaled, rowmax, dvec, grads, timer=Non
     if fused is None:
         fused = not deterministic()
     if fused:
-        if dq_acc is None:
-            dq_acc = torch.empty((n, b, z, c, a), dtype=torch.float32, device=q.device)
+        dq_acc = _dq_accumulator(dq_acc, (n, b, z, c, a), q.device)
         with tm("bwd_stream_fused"):
             check(L.rsa_bwd_stream_fused(ctypes.byref(g), _view(q), _view(k), _view(v), _view(grad_scaled),
                                          rowmax.data_ptr(), dvec.data_ptr(), _view(dk), _view(dv), kdt, 0,
