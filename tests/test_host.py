@@ -105,3 +105,20 @@ def test_cost_report_reconciles_model_and_ledgers():
     assert w["panel"] < w["paper"] and w["panel"] < w["stream"]
     rep = reconcile(cfg, measured=wire_bytes(cfg, "panel"), plan="panel")
     assert rep["measured"]["matches_plan"]
+
+
+def test_dq_accumulator_validation():
+    """The one-pass backwards' fp32 dQ accumulator: supplied buffers must match the launch."""
+    import torch
+
+    from paper_2105_13120_b200 import engine
+    from paper_2105_13120_b200.errors import ShapeError
+
+    shape = (1, 2, 3, 128, 64)
+    acc = torch.empty(shape, dtype=torch.float32)
+    assert engine._dq_accumulator(acc, shape, acc.device) is acc
+    assert engine._dq_accumulator(None, shape, acc.device).shape == shape
+    for bad in (torch.empty(shape, dtype=torch.bfloat16), torch.empty((1, 2, 3, 64, 64)),
+                torch.empty((1, 2, 3, 64, 128)).transpose(-1, -2)):
+        with pytest.raises(ShapeError):
+            engine._dq_accumulator(bad, shape, acc.device)
