@@ -1,6 +1,7 @@
-"""Experiment driver: rsa_bwd_stream_fused per-launch time under RSA_FS_DBG bits (set by the caller).
+"""Experiment driver: the stream backward's one-pass kernel against the two-kernel form at one
+length (per-launch time and relative difference).
 
-usage: RSA_FS_DBG=<bits> python tools/fs_exp.py [L]"""
+usage: [RSA_FS_DBG=<bits>] python tools/fs_exp.py [L]"""
 import os
 import sys
 from pathlib import Path
@@ -19,6 +20,8 @@ sf = engine.forward_stream(q, k, v)
 dvec, gsc = engine.ops.rowdot_scale(dO, sf.out, sf.rowscale)
 grads = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v))
 acc = torch.empty(q.shape, dtype=torch.float32, device=dev)
+ref = engine.stream_backward_kernels(q, k, v, gsc, sf.rowmax, dvec, tuple(torch.empty_like(x) for x in grads),
+                                     fused=False)
 for fused in (True, False):
     for _ in range(2):
         engine.stream_backward_kernels(q, k, v, gsc, sf.rowmax, dvec, grads, fused=fused, dq_acc=acc)
@@ -28,4 +31,6 @@ for fused in (True, False):
         engine.stream_backward_kernels(q, k, v, gsc, sf.rowmax, dvec, grads, fused=fused, dq_acc=acc)
     e1.record()
     torch.cuda.synchronize()
-    print(f"L={L} dbg={os.environ.get('RSA_FS_DBG', '0')} fused={fused}: {e0.elapsed_time(e1) / 5 * 1e3:.1f} us", flush=True)
+    err = [float((x.double() - y.double()).norm() / y.double().norm()) for x, y in zip(grads, ref)]
+    print(f"L={L} dbg={os.environ.get('RSA_FS_DBG', '0')} fused={fused}: "
+          f"{e0.elapsed_time(e1) / 5 * 1e3:.1f} us, rel diff vs two-kernel {['%.1e' % x for x in err]}", flush=True)
