@@ -127,8 +127,9 @@ def _check_spmd(world, mode, attn, shape, seed, results, backend="gloo"):
 def test_spmd_ring_cuda_kernels_match_oracle(world, mode, attn, shape):
     """SpmdRing with its real kernels: the K/V pair ring with one rsa_fwd_factored_ex per hop;
     panel mode's ring-free backward over the cached slots (rsa_bwd_fused for c <= 512, else
-    rsa_bwd_dkdv + rsa_bwd_dq) with reduced partials; stream mode's re-circulated K/V with
-    travelling dK/dV sums (rsa_bwd_kv_stream / rsa_bwd_q_stream per hop)."""
+    rsa_bwd_panel_fused) with reduced partials; stream mode's re-circulated K/V with
+    travelling dK/dV sums (rsa_bwd_stream_fused per hop: fp32 dK/dV accumulated across hops,
+    dQ partials added into one fp32 accumulator over all hops)."""
     seed = 40 + world
     mgr = mp.get_context("spawn").Manager()
     results = mgr.dict()
