@@ -328,6 +328,19 @@ int rsa_bwd_panel_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, r
                         const float* dvec, rsa_view dk, rsa_view dv, int dkv_dtype, int accumulate_dkv, float* dq_acc,
                         int accumulate_dq, rsa_view dq_out, void* stream);
 
+/*
+ * Linformer K/V projection (ringseq/sparse_attention.py:111-123, the sequence-sharded
+ * K'_d = E_d K_d, V'_d = F_d V_d and their ring-accumulate) for every head at once:
+ * K' = sum over the resident origins [org_lo, org_lo + n_org) of E_d K_d (likewise V'), one
+ * contraction over their n_org * chunk positions.  e / f: bf16 (proj_dim x L) row-major with
+ * leading dimension ld_proj (origin d's columns at d * chunk); k / v: [n_org][B][Z][chunk][64]
+ * bf16 views.  k_acc / v_acc: fp32 [B][Z][proj_dim][64] contiguous outputs (zero-filled
+ * here, then added into by TMA reduce-add); k_low / v_low (optional): bf16 copies of them.
+ * Needs head_dim 64, chunk % 64 == 0, proj_dim % 128 == 0 and B*Z % 4 == 0.
+ */
+int rsa_linformer_project(const rsa_geom* g, int proj_dim, const void* e, const void* f, int64_t ld_proj, rsa_view k,
+                          rsa_view v, float* k_acc, float* v_acc, void* k_low, void* v_low, void* stream);
+
 /* ------------------------------------------ BERT harness */
 
 /*

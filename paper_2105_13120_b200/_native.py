@@ -132,6 +132,8 @@ EXPORTS = {
     "rsa_bwd_q_stream": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, c_void_p, _V, c_int, _V, c_void_p]),
     "rsa_bwd_stream_fused": (c_int, [_GEOM, _V, _V, _V, _V, c_void_p, c_void_p, _V, _V, c_int, c_int, c_void_p, c_int,
                                      _V, c_void_p]),
+    "rsa_linformer_project": (c_int, [_GEOM, c_int, c_void_p, c_void_p, c_int64, _V, _V, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_void_p]),
     "rsa_bwd_panel_fused": (c_int, [_GEOM, _V, _V, _V, _V, _V, c_void_p, _V, _V, c_int, c_int, c_void_p, c_int, _V,
                                     c_void_p]),
 }

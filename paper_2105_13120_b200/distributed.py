@@ -160,11 +160,23 @@ class CudaHopKernels:
                                                    self._st(q)), "rsa_bwd_stream_fused")
 
     def project_pair(self, e_cols, k, f_cols, v):
-        """[E_d K_d ; F_d V_d] as one fp32 [2][B][Z][K][A] buffer (tcgen05 GEMMs)."""
+        """[E_d K_d ; F_d V_d] as one fp32 [2][B][Z][K][A] buffer: rsa_linformer_project (four
+        heads per tensor-core tile, this rank's c positions) when it tiles the shapes, else
+        two rsa_gemm launches."""
         from . import tensor_ops
 
-        b, z, _, a = k.shape
-        out = torch.empty((2, b, z, e_cols.shape[0], a), dtype=torch.float32, device=k.device)
+        b, z, c, a = k.shape
+        kdim = e_cols.shape[0]
+        out = torch.empty((2, b, z, kdim, a), dtype=torch.float32, device=k.device)
+        if (a == 64 and c % 64 == 0 and kdim % 128 == 0 and (b * z) % 4 == 0 and e_cols.dtype == f_cols.dtype ==
+                torch.bfloat16 and e_cols.stride(1) == f_cols.stride(1) == 1 and e_cols.stride(0) == f_cols.stride(0)):
+            g = self.engine._geom(1, b, z, c, a, c, 0, 1)
+            V = self.engine._view
+            self.check(self.lib().rsa_linformer_project(ctypes.byref(g), kdim, e_cols.data_ptr(), f_cols.data_ptr(),
+                                                        e_cols.stride(0), V(k.unsqueeze(0)), V(v.unsqueeze(0)),
+                                                        out[0].data_ptr(), out[1].data_ptr(), None, None,
+                                                        self._st(k)), "rsa_linformer_project")
+            return out
         tensor_ops.matmul(e_cols, k, out=out[0])
         tensor_ops.matmul(f_cols, v, out=out[1])
         return out

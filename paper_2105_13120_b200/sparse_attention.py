@@ -29,6 +29,7 @@ The ledger charges the reference's ring-accumulate convention:
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -122,12 +123,25 @@ def _check_inputs(name_chunks, weights, cfg: SparseAttentionConfig):
 def _project(q, k, v, e, f, kdim):
     """K' = sum_d E_d K_d, V' = sum_d F_d V_d as bf16 [B][Z][K][A].
 
-    One rsa_gemm launch per projection covers every (rank, head) pair: rank d's column block
-    E_d is a strided view of E (batch stride c) shared by the B*Z heads (batch stride 0),
-    each product K = c deep, into fp32 per-rank partials; rsa_sum_ranks then adds the
-    partials in ascending rank order -- the reference's ring-accumulate (:59-71) when every
-    rank is resident -- straight to bf16."""
+    rsa_linformer_project: every head at once, four heads per 128 x 256 tensor-core tile (E_d
+    staged once for four heads), the sum over the resident ranks as one contraction over L in
+    ascending rank order -- the reference's ring-accumulate (:59-71) when every rank is
+    resident -- split over the SMs with fp32 TMA reduce-add, then bf16.  Shapes it cannot tile
+    (A != 64, c % 64, K % 128, B*Z % 4) take the generic path: one rsa_gemm launch per
+    projection over every (rank, head) pair into fp32 per-rank partials, summed in ascending
+    rank order by rsa_sum_ranks."""
     n, b, z, c, a = q.shape
+    if (a == 64 and c % 64 == 0 and kdim % 128 == 0 and (b * z) % 4 == 0 and e.dtype == f.dtype == torch.bfloat16
+            and e.stride(1) == f.stride(1) == 1 and e.stride(0) == f.stride(0)):
+        dev = q.device
+        acc = torch.empty((2, b, z, kdim, a), dtype=torch.float32, device=dev)
+        low = torch.empty((2, b, z, kdim, a), dtype=torch.bfloat16, device=dev)
+        g = engine._geom(n, b, z, c, a, n * c, 0, n)
+        check(lib().rsa_linformer_project(ctypes.byref(g), kdim, e.data_ptr(), f.data_ptr(), e.stride(0),
+                                          engine._view(k), engine._view(v), acc[0].data_ptr(), acc[1].data_ptr(),
+                                          low[0].data_ptr(), low[1].data_ptr(),
+                                          torch.cuda.current_stream(dev).cuda_stream), "rsa_linformer_project")
+        return low[0], low[1]
     out = []
     for proj, x in ((e, k), (f, v)):
         blocks = proj.reshape(kdim, n, c).permute(1, 0, 2).unsqueeze(1)  # [N][1][K][c], row stride L

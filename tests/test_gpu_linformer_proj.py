@@ -1,0 +1,60 @@
+"""rsa_linformer_project (csrc/linformer.cu): the Linformer's sequence-sharded K/V projection
+K' = sum_d E_d K_d, V' = sum_d F_d V_d (ringseq/sparse_attention.py:111-123) for every head
+at once, against a float64 restatement of the same sums and against the generic path
+(rsa_gemm per (rank, head) + rsa_sum_ranks) it replaces."""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("shape", [(8, 1, 4, 128, 128), (8, 4, 12, 1024, 256), (3, 2, 2, 192, 384),
+                                   (1, 2, 6, 512, 128)])
+def test_linformer_projection_matches_float64(shape):
+    from paper_2105_13120_b200 import engine
+    from paper_2105_13120_b200._native import check, lib
+
+    n, b, z, c, kdim = shape
+    a, L = 64, shape[0] * shape[3]
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev).manual_seed(c + kdim)
+    k, v = (torch.randn((n, b, z, c, a), generator=gen, device=dev).to(torch.bfloat16) for _ in range(2))
+    e, f = ((torch.randn((kdim, L), generator=gen, device=dev) / L ** 0.5).to(torch.bfloat16) for _ in range(2))
+    acc = torch.empty((2, b, z, kdim, a), dtype=torch.float32, device=dev)
+    low = torch.empty((2, b, z, kdim, a), dtype=torch.bfloat16, device=dev)
+    g = engine._geom(n, b, z, c, a, L, 0, n)
+    check(lib().rsa_linformer_project(ctypes.byref(g), kdim, e.data_ptr(), f.data_ptr(), e.stride(0), engine._view(k),
+                                      engine._view(v), acc[0].data_ptr(), acc[1].data_ptr(), low[0].data_ptr(),
+                                      low[1].data_ptr(), torch.cuda.current_stream().cuda_stream),
+          "rsa_linformer_project")
+    torch.cuda.synchronize()
+    for j, (p, x) in enumerate(((e, k), (f, v))):
+        pd = p.double().cpu().numpy()
+        xd = x.double().cpu().numpy()
+        want = sum(np.einsum("kc,bzca->bzka", pd[:, d * c:(d + 1) * c], xd[d]) for d in range(n))
+        got = acc[j].double().cpu().numpy()
+        rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+        assert rel <= 1e-5, (j, rel)  # fp32 accumulation of exact bf16 products
+        assert torch.equal(low[j], acc[j].to(torch.bfloat16))
+
+
+def test_linformer_projection_rejects_untileable():
+    from paper_2105_13120_b200 import engine
+    from paper_2105_13120_b200._native import lib
+
+    n, b, z, c, kdim, a = 2, 1, 3, 128, 128, 64  # B*Z = 3: not a multiple of four heads
+    dev = torch.device("cuda", 0)
+    k = torch.zeros((n, b, z, c, a), dtype=torch.bfloat16, device=dev)
+    e = torch.zeros((kdim, n * c), dtype=torch.bfloat16, device=dev)
+    acc = torch.empty((b, z, kdim, a), dtype=torch.float32, device=dev)
+    g = engine._geom(n, b, z, c, a, n * c, 0, n)
+    rc = lib().rsa_linformer_project(ctypes.byref(g), kdim, e.data_ptr(), e.data_ptr(), e.stride(0), engine._view(k),
+                                     engine._view(k), acc.data_ptr(), acc.data_ptr(), None, None,
+                                     torch.cuda.current_stream().cuda_stream)
+    assert rc != 0
