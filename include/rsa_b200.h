@@ -341,6 +341,17 @@ int rsa_bwd_panel_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, r
 int rsa_linformer_project(const rsa_geom* g, int proj_dim, const void* e, const void* f, int64_t ld_proj, rsa_view k,
                           rsa_view v, float* k_acc, float* v_acc, void* k_low, void* v_low, void* stream);
 
+/*
+ * The projections' gradients (the Linformer backward): for every
+ * resident origin d, grad_e[:, d-block] = sum over the B*Z heads of dK'_h K_{d,h}^T, and
+ * grad_f likewise from dV' and V.  dk_low / dv_low: bf16 [B][Z][proj_dim][64] contiguous;
+ * k / v as rsa_linformer_project; grad_e / grad_f: fp32 (proj_dim x L) row-major, leading
+ * dimension ld_grad, written (not accumulated) at origin d's columns d * chunk.  Needs
+ * head_dim 64, chunk % 256 == 0 and proj_dim % 128 == 0.
+ */
+int rsa_linformer_proj_grad(const rsa_geom* g, int proj_dim, const void* dk_low, const void* dv_low, rsa_view k,
+                            rsa_view v, float* grad_e, float* grad_f, int64_t ld_grad, void* stream);
+
 /* ------------------------------------------ BERT harness */
 
 /*

@@ -169,6 +169,142 @@ __global__ void __launch_bounds__(LP_THREADS, 1) linformer_project_kernel(const 
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// ---------------------------------------------------------------- projection gradients
+//
+// dE[:, d-block] = sum_{b,z} dK'_{bz} K_{d,bz}^T (and dF from dV', V): for every rank d's
+// c positions, a (Kp x c) block summed over the B*Z heads -- ringseq/sparse_attention.py's
+// projections differentiated.  Tile: 128 rows of Kp (M) x 256
+// positions (N); the contraction walks the heads, 64 dimensions each: A = dK'_{bz} rows
+// (dims contiguous, K-major), B = K_{d,bz} positions (dims contiguous, K-major), so neither
+// operand is transposed or copied.  The fp32 128 x 256 result leaves by TMA store.
+constexpr int LG_N = 256;                           // positions per tile
+constexpr uint32_t LG_A = TR * HD * 2;              // 16 KB
+constexpr uint32_t LG_B = LG_N * HD * 2;            // 32 KB
+constexpr uint32_t LG_STAGE = LG_A + LG_B;          // 48 KB (= LP_STAGE: same layout of stages)
+
+struct LgArgs {
+  CUtensorMap ta[2], tb[2], to[2];  // dK' / dV' ([b][z][Kp][64]), K / V (heads), fp32 dE / dF (Kp x L)
+  int kp, BZ, Z, B, c, n_org;
+  int nblocks;                      // 256-position blocks per origin chunk
+  int items;
+};
+
+__global__ void __launch_bounds__(LP_THREADS, 1) linformer_grad_kernel(const __grid_constant__ LgArgs p) {
+  uint8_t* smem = smem_base();
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + LP_OFF_BAR);
+  uint64_t *full = bar, *empty = bar + LP_ST, *acc_full = empty + LP_ST, *acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int mblocks = p.kp / TR;
+
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < LP_ST; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    for (int s = 0; s < 2; ++s) mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], 4);
+    fence_barrier_init();
+    for (int j = 0; j < 2; ++j) tma_prefetch(&p.ta[j]), tma_prefetch(&p.tb[j]), tma_prefetch(&p.to[j]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // item -> (projection j, Kp block mb, origin d, position block nb)
+  auto decode = [&](int item, int& j, int& mb, int& d, int& nb) {
+    nb = item % p.nblocks;
+    int rest = item / p.nblocks;
+    d = rest % p.n_org, rest /= p.n_org;
+    mb = rest % mblocks, j = rest / mblocks;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      Pos lq;
+      for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+        int j, mb, d, nb;
+        decode(item, j, mb, d, nb);
+        for (int bz = 0; bz < p.BZ; ++bz) {
+          const uint32_t s = lq.slot(LP_ST);
+          mbar_wait(&empty[s], lq.phase(LP_ST) ^ 1);
+          mbar_arrive_expect_tx(&full[s], LG_STAGE);
+          uint8_t* sa = smem + s * LP_STAGE;
+          tma_load_4d(sa, &p.ta[j], &full[s], 0, mb * TR, bz % p.Z, bz / p.Z);
+          tma_load_4d(sa + LG_A, &p.tb[j], &full[s], 0, nb * LG_N, bz % p.Z, d * p.B + bz / p.Z);
+          ++lq.i;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_bf16_f32(TR, LG_N, 0, 0);  // both K-major (head dims contiguous)
+    Pos lq;
+    uint32_t it = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+      const uint32_t ab = it & 1;
+      mbar_wait(&acc_empty[ab], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      for (int bz = 0; bz < p.BZ; ++bz) {
+        const uint32_t s = lq.slot(LP_ST);
+        mbar_wait(&full[s], lq.phase(LP_ST));
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * LP_STAGE), sb = sa + LG_A;
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+          umma_bf16_ws(tmem + ab * 256, smem_desc_sw128(sa + k * 32, 0, 1024), smem_desc_sw128(sb + k * 32, 0, 1024),
+                       idesc, (bz > 0) || (k > 0));
+        umma_commit_ws(&empty[s]);
+        ++lq.i;
+      }
+      umma_commit_ws(&acc_full[ab]);
+    }
+  } else {
+    const uint32_t quad = warp & 3;
+    const uint32_t lane_base = (quad * 32u) << 16;
+    uint8_t* stg = smem + LP_OFF_STG + (warp - 2) * 8192;
+    uint32_t it = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+      int j, mb, d, nb;
+      decode(item, j, mb, d, nb);
+      const uint32_t ab = it & 1;
+      mbar_wait(&acc_full[ab], (it >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int ch = 0; ch < LG_N / 32; ++ch) {
+        float v[32];
+        __syncwarp();
+        tmem_ld32(tmem + lane_base + ab * 256 + ch * 32, v);
+        tmem_ld_wait();
+        if (ch == LG_N / 32 - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[ab]);
+        }
+        uint8_t* buf = stg + (ch & 1) * 4096;
+        if (lane == 0) tma_store_wait_read<1>();
+        __syncwarp();
+        const uint32_t row = smem_u32(buf) + lane * 128;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          st_shared_v4(row + ((q ^ (lane & 7)) << 4), __float_as_uint(v[4 * q]), __float_as_uint(v[4 * q + 1]),
+                       __float_as_uint(v[4 * q + 2]), __float_as_uint(v[4 * q + 3]));
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                  reinterpret_cast<uint64_t>(&p.to[j])),
+              "r"(smem_u32(buf)), "r"(d * p.c + nb * LG_N + ch * 32), "r"(mb * TR + int(quad) * 32)
+              : "memory");
+          tma_store_commit();
+        }
+      }
+    }
+    if (lane == 0) tma_store_wait_all<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
 __global__ void cast_bf16_kernel(const float4* __restrict__ x, uint2* __restrict__ y, int64_t n4) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
     const float4 v = x[i];
@@ -244,6 +380,50 @@ int rsa_linformer_project(const rsa_geom* g, int proj_dim, const void* e, const 
     if (int rc = check_launch("cast_bf16_kernel")) return rc;
   }
   return RSA_OK;
+}
+
+int rsa_linformer_proj_grad(const rsa_geom* g, int proj_dim, const void* dk_low, const void* dv_low, rsa_view k,
+                            rsa_view v, float* grad_e, float* grad_f, int64_t ld_grad, void* stream) {
+  using namespace rsa;
+  if (!g || g->head_dim != HD || g->chunk % LG_N || proj_dim % TR || g->n_org < 1 || g->org_lo < 0 || !dk_low ||
+      !dv_low || !grad_e || !grad_f || ld_grad < int64_t(g->org_lo + g->n_org) * g->chunk)
+    return fail(RSA_ERR_INVALID, "rsa_linformer_proj_grad: unsupported geometry (A = 64, chunk %% 256, Kp %% 128)");
+  if (!aligned16(dk_low) || !aligned16(dv_low) || !aligned16(grad_e) || !aligned16(grad_f) || (ld_grad * 4) % 16)
+    return fail(RSA_ERR_UNSUPPORTED, "rsa_linformer_proj_grad: buffers not 16-byte aligned");
+  LgArgs a{};
+  const void* low[2] = {dk_low, dv_low};
+  const rsa_view x[2] = {k, v};
+  float* out[2] = {grad_e, grad_f};
+  for (int j = 0; j < 2; ++j) {
+    // dK' / dV': [b][z][Kp][64] bf16 contiguous; 64-dim x 128-row boxes
+    uint64_t ad[4] = {uint64_t(HD), uint64_t(proj_dim), uint64_t(g->heads), uint64_t(g->batch)};
+    uint64_t as[3] = {uint64_t(HD) * 2, uint64_t(proj_dim) * HD * 2, uint64_t(g->heads) * proj_dim * HD * 2};
+    uint32_t ab[4] = {HD, TR, 1, 1};
+    if (!encode_tmap(&a.ta[j], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, low[j], ad, as, ab, CU_TENSOR_MAP_SWIZZLE_128B))
+      return RSA_ERR_UNSUPPORTED;
+    // K / V: [origin][b][z][row][a]; 256-row boxes
+    if (!head_map(&a.tb[j], x[j], g, g->n_org)) return RSA_ERR_UNSUPPORTED;
+    {
+      uint64_t d4[4] = {uint64_t(HD), uint64_t(g->chunk), uint64_t(g->heads), uint64_t(g->batch) * g->n_org};
+      const int64_t sb = (g->batch == 1 && g->n_org > 1) ? x[j].s_rank : x[j].s_b;
+      uint64_t s4[3] = {uint64_t(x[j].s_row) * 2, uint64_t(x[j].s_z) * 2, uint64_t(sb) * 2};
+      uint32_t b4[4] = {HD, LG_N, 1, 1};
+      if (!encode_tmap(&a.tb[j], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, x[j].ptr, d4, s4, b4, CU_TENSOR_MAP_SWIZZLE_128B))
+        return RSA_ERR_UNSUPPORTED;
+    }
+    // fp32 dE / dF (Kp x L), columns from org_lo * c on: 32-column x 32-row boxes
+    float* base = out[j] + int64_t(g->org_lo) * g->chunk;
+    uint64_t od[2] = {uint64_t(g->n_org) * g->chunk, uint64_t(proj_dim)};
+    uint64_t os[1] = {uint64_t(ld_grad) * 4};
+    uint32_t ob[2] = {32, 32};
+    if (!encode_tmap(&a.to[j], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, od, os, ob, CU_TENSOR_MAP_SWIZZLE_128B))
+      return RSA_ERR_UNSUPPORTED;
+  }
+  a.kp = proj_dim, a.BZ = g->batch * g->heads, a.Z = g->heads, a.B = g->batch;
+  a.c = g->chunk, a.n_org = g->n_org;
+  a.nblocks = g->chunk / LG_N;
+  a.items = 2 * (proj_dim / TR) * g->n_org * a.nblocks;
+  return launch(linformer_grad_kernel, a.items, LP_SMEM, a, stream, "linformer_grad_kernel", LP_THREADS);
 }
 
 }  // extern "C"

@@ -273,15 +273,26 @@ def sparse_ring_attention_backward(q_chunks, k_chunks, v_chunks, weights, cfg: S
     dv = torch.empty_like(q)
     grad_e = torch.empty((kdim, base.seq_len), dtype=torch.float32, device=dev)
     grad_f = torch.empty_like(grad_e)
-    # (K, B*Z*A) views of the low-rank gradients for the shared-projection gradients
-    dk_flat = d_klow16.permute(2, 0, 1, 3).reshape(kdim, b * z * a)
-    dv_flat = d_vlow16.permute(2, 0, 1, 3).reshape(kdim, b * z * a)
     for d in range(n):
         cols = slice(d * c, (d + 1) * c)
         ops.matmul(e[:, cols].transpose(0, 1), d_klow16, out=dk[d])
         ops.matmul(f[:, cols].transpose(0, 1), d_vlow16, out=dv[d])
-        ops.matmul(dk_flat, k[d].transpose(-1, -2).reshape(b * z * a, c), out=grad_e[:, cols])
-        ops.matmul(dv_flat, v[d].transpose(-1, -2).reshape(b * z * a, c), out=grad_f[:, cols])
+    if a == 64 and c % 256 == 0 and kdim % 128 == 0:
+        # dE / dF for every rank in one launch: each (Kp x 256-position) tile sums the heads'
+        # dK'_h K_{d,h}^T with both operands read in place (csrc/linformer.cu)
+        g_ = engine._geom(n, b, z, c, a, n * c, 0, n)
+        check(lib().rsa_linformer_proj_grad(ctypes.byref(g_), kdim, d_klow16.data_ptr(), d_vlow16.data_ptr(),
+                                            engine._view(k), engine._view(v), grad_e.data_ptr(), grad_f.data_ptr(),
+                                            grad_e.stride(0), torch.cuda.current_stream(dev).cuda_stream),
+              "rsa_linformer_proj_grad")
+    else:
+        # (K, B*Z*A) views of the low-rank gradients for the shared-projection gradients
+        dk_flat = d_klow16.permute(2, 0, 1, 3).reshape(kdim, b * z * a)
+        dv_flat = d_vlow16.permute(2, 0, 1, 3).reshape(kdim, b * z * a)
+        for d in range(n):
+            cols = slice(d * c, (d + 1) * c)
+            ops.matmul(dk_flat, k[d].transpose(-1, -2).reshape(b * z * a, c), out=grad_e[:, cols])
+            ops.matmul(dv_flat, v[d].transpose(-1, -2).reshape(b * z * a, c), out=grad_f[:, cols])
     ledger = CommLedger(n)
     if n > 1:
         for d in range(n):

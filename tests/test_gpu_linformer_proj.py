@@ -58,3 +58,30 @@ def test_linformer_projection_rejects_untileable():
                                      engine._view(k), acc.data_ptr(), acc.data_ptr(), None, None,
                                      torch.cuda.current_stream().cuda_stream)
     assert rc != 0
+
+
+@pytest.mark.parametrize("shape", [(8, 1, 4, 256, 128), (2, 4, 12, 1024, 256), (3, 1, 3, 512, 384)])
+def test_linformer_projection_gradients_match_float64(shape):
+    """rsa_linformer_proj_grad: dE[:, d-block] = sum_h dK'_h K_{d,h}^T for every rank (and dF)."""
+    from paper_2105_13120_b200 import engine
+    from paper_2105_13120_b200._native import check, lib
+
+    n, b, z, c, kdim = shape
+    a, L = 64, shape[0] * shape[3]
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev).manual_seed(7 * c + kdim)
+    k, v = (torch.randn((n, b, z, c, a), generator=gen, device=dev).to(torch.bfloat16) for _ in range(2))
+    dkl, dvl = (torch.randn((b, z, kdim, a), generator=gen, device=dev).to(torch.bfloat16) for _ in range(2))
+    ge, gf = (torch.full((kdim, L), float("nan"), dtype=torch.float32, device=dev) for _ in range(2))
+    g = engine._geom(n, b, z, c, a, L, 0, n)
+    check(lib().rsa_linformer_proj_grad(ctypes.byref(g), kdim, dkl.data_ptr(), dvl.data_ptr(), engine._view(k),
+                                        engine._view(v), ge.data_ptr(), gf.data_ptr(), ge.stride(0),
+                                        torch.cuda.current_stream().cuda_stream), "rsa_linformer_proj_grad")
+    torch.cuda.synchronize()
+    for got, low, x in ((ge, dkl, k), (gf, dvl, v)):
+        ld, xd = low.double().cpu().numpy(), x.double().cpu().numpy()
+        want = np.concatenate([np.einsum("bzka,bzca->kc", ld, xd[d]) for d in range(n)], axis=1)
+        g64 = got.double().cpu().numpy()
+        assert np.isfinite(g64).all()
+        rel = np.linalg.norm(g64 - want) / np.linalg.norm(want)
+        assert rel <= 1e-5, rel
