@@ -41,6 +41,23 @@ struct StreamArgs {
   OutView dk, dv, dq_acc, dq_out;
   int dkv_bf16, accumulate;
   int dbg;  // RSA_FS_DBG experiment bits (bwd_stream_fused): 1 no reduce, 2 no staging, 4 no dQ product
+  int qsplit;  // one-pass kernels: items per key tile, each over a contiguous share of the query tiles
+};
+
+// item = ((origin * B*Z + head) * ntk + key tile) * qsplit + query share
+struct OpItem {
+  int jo, bz, kt, q0, q1;
+  __device__ __forceinline__ OpItem(int item, int qsplit, int ntk, int BZ, int T) {
+    const int qs = item % qsplit;
+    const int rest = item / qsplit;
+    kt = rest % ntk, bz = (rest / ntk) % BZ, jo = rest / (ntk * BZ);
+    const int tq = (T + qsplit - 1) / qsplit;
+    q0 = qs * tq, q1 = min(T, q0 + tq);
+  }
+  __device__ __forceinline__ int len() const { return q1 - q0; }
+  // the first tile: with one share, each key tile of a head starts at its own tile (kt mod T)
+  // and wraps, so concurrent items add into different dQ tiles; with several, the share's first
+  __device__ __forceinline__ int start(int qsplit, int T) const { return qsplit == 1 ? kt % T : q0; }
 };
 
 // 16 epilogue warps: each thread owns one TMEM lane (a key of the tile in bwd_kv_stream, a
@@ -626,7 +643,7 @@ __global__ void __maxnreg__(96) bwd_onepass_kernel(const __grid_constant__ Strea
   const int ntk = (p.ck + TK - 1) / TK, nrt = (g.c + TR - 1) / TR;
   const int T = g.n_rank * nrt;  // query tiles walked per key tile
   const int BZ = g.B * g.Z;
-  const int items = g.n_org * BZ * ntk;
+  const int items = g.n_org * BZ * ntk * p.qsplit;
   const uint32_t warp = warp_id(), lane = lane_id();
 
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -655,16 +672,16 @@ __global__ void __maxnreg__(96) bwd_onepass_kernel(const __grid_constant__ Strea
       Pos lq, lp;
       uint32_t it = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-        const int kt = item % ntk, bz = (item / ntk) % BZ, jo = item / (ntk * BZ);
-        const int b = bz / g.Z, z = bz % g.Z;
+        const OpItem oi(item, p.qsplit, ntk, BZ, T);
+        const int kt = oi.kt, jo = oi.jo, b = oi.bz / g.Z, z = oi.bz % g.Z;
         mbar_wait(kv_empty, (it & 1) ^ 1);
         mbar_arrive_expect_tx(kv_full, 2 * TILE);
         uint8_t* kv = smem + FS_OFF_KV;
         tma_load_4d(kv, &p.tk, kv_full, 0, kt * TK, z, jo * g.B + b);
         tma_load_4d(kv + TILE, &p.tv, kv_full, 0, kt * TK, z, jo * g.B + b);
-        const int t0 = kt % T;
+        const int t0 = oi.start(p.qsplit, T);
         int d = t0 / nrt, r0 = (t0 % nrt) * TR;
-        for (int t = 0; t < T; ++t) {
+        for (int t = 0; t < oi.len(); ++t) {
           if (PANEL) {  // the panel tile first: its slot frees before the stage's
             const uint32_t ps = lp.slot(2);
             mbar_wait(&pp_empty[ps], lp.phase(2) ^ 1);
@@ -702,6 +719,7 @@ __global__ void __maxnreg__(96) bwd_onepass_kernel(const __grid_constant__ Strea
     Pos lq_s, lq_d, lq_v, lq_k, lp;
     uint32_t n_s = 0, n_d = 0, n_p = 0, n_ds = 0, it = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      const int T = OpItem(item, p.qsplit, ntk, BZ, g.n_rank * nrt).len();  // this item's steps
       mbar_wait(kv_full, it & 1);
       auto issue_s = [&]() {  // S^T(t) = K Q^T once the epilogue has read S^T(t-1)
         const uint32_t s = lq_s.slot(FS_ST);
@@ -827,11 +845,11 @@ __global__ void __maxnreg__(96) bwd_onepass_kernel(const __grid_constant__ Strea
       }
     };
     for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-      const int kt = item % ntk, bz = (item / ntk) % BZ, jo = item / (ntk * BZ);
-      const int b = bz / g.Z, z = bz % g.Z, k0 = kt * TK;
-      const int t0 = kt % T;
+      const OpItem oi(item, p.qsplit, ntk, BZ, T);
+      const int jo = oi.jo, b = oi.bz / g.Z, z = oi.bz % g.Z, k0 = oi.kt * TK;
+      const int t0 = oi.start(p.qsplit, T);
       int d = t0 / nrt, r0 = (t0 % nrt) * TR, pd = 0, pr0 = 0;
-      for (int t = 0; t < T; ++t) {
+      for (int t = 0; t < oi.len(); ++t) {
         const int nvalid = min(TR, g.c - r0) - part * SE_COLS;  // valid query columns of this part
         const uint32_t s = lq.slot(FS_ST);
         const uint32_t stat = smem_u32(smem + FS_OFF_ST + s * STAGE + 2 * TILE) + part * SE_COLS * 4;  // m | D'
@@ -923,8 +941,18 @@ __global__ void __maxnreg__(96) bwd_onepass_kernel(const __grid_constant__ Strea
       if (key < p.ck) {
         const OutView none{nullptr, 0, 0, 0, 0};
         const OutView& dst = is_dk ? p.dk : p.dv;
-        if (p.dkv_bf16) store_row32(none, dst, 0, jo, b, z, key, col, acc);
-        else store_row32(dst, none, p.accumulate, jo, b, z, key, col, acc);
+        if (p.qsplit > 1) {  // several items share this key tile: fp32 adds in L2
+          float* row = reinterpret_cast<float*>(dst.ptr) + out_off(dst, jo, b, z, key) + col;
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + e), "f"(acc[e]),
+                         "f"(acc[e + 1]), "f"(acc[e + 2]), "f"(acc[e + 3])
+                         : "memory");
+        } else if (p.dkv_bf16) {
+          store_row32(none, dst, 0, jo, b, z, key, col, acc);
+        } else {
+          store_row32(dst, none, p.accumulate, jo, b, z, key, col, acc);
+        }
       }
     }
     if (lane == 0) tma_store_wait_all<0>();
@@ -960,6 +988,35 @@ inline bool dq_acc_map(CUtensorMap* m, float* base, const rsa_geom* g) {
   uint64_t str[3] = {uint64_t(HD) * 4, uint64_t(g->chunk) * HD * 4, uint64_t(g->heads) * g->chunk * HD * 4};
   uint32_t box[4] = {16, 32, 1, 1};
   return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B);
+}
+
+// How many items share each key tile of a one-pass backward: 1, unless the launch has fewer
+// key-tile items than SMs (the Linformer's few projected keys: B*Z*2 items over ~10^3 query
+// tiles each) and dK/dV are fp32 outputs laid out contiguously, which the items then add
+// into (red.global.add) after a zero-fill.
+inline int onepass_qsplit(const rsa_geom* g, int dkv_bf16, const rsa_view& dk, const rsa_view& dv) {
+  const int ck = key_chunk(g), ntk = (ck + TK - 1) / TK;
+  const int64_t base = int64_t(g->n_org) * g->batch * g->heads * ntk;
+  const int T = g->n_rank * ((g->chunk + TR - 1) / TR);
+  const int sms = num_sms();
+  if (dkv_bf16 || base >= sms || T < 16) return 1;
+  auto dense = [&](const rsa_view& x) {
+    return x.s_row == HD && x.s_z == int64_t(ck) * HD && x.s_b == int64_t(g->heads) * ck * HD &&
+           (g->n_org == 1 || x.s_rank == int64_t(g->batch) * g->heads * ck * HD);
+  };
+  if (!dense(dk) || !dense(dv)) return 1;
+  int qs = int(std::min<int64_t>((2 * sms + base - 1) / base, T / 8));
+  const int tq = (T + qs - 1) / qs;
+  return (T + tq - 1) / tq;  // no empty share
+}
+
+inline int onepass_zero_dkv(const rsa_geom* g, int qsplit, int accumulate, const rsa_view& dk, const rsa_view& dv,
+                            cudaStream_t st) {
+  if (qsplit == 1 || accumulate) return RSA_OK;
+  const size_t bytes = size_t(g->n_org) * g->batch * g->heads * key_chunk(g) * HD * 4;
+  if (cudaMemsetAsync(dk.ptr, 0, bytes, st) != cudaSuccess || cudaMemsetAsync(dv.ptr, 0, bytes, st) != cudaSuccess)
+    return check_launch("one-pass backward: dK / dV zero-fill");
+  return RSA_OK;
 }
 
 int dq_cast(const float* dq_acc, const rsa_view& dq_out, const rsa_geom* g, int64_t rows, cudaStream_t st) {
@@ -1046,7 +1103,9 @@ int rsa_bwd_stream_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, 
   const int64_t rows = int64_t(g->n_rank) * g->batch * g->heads * g->chunk;
   if (!accumulate_dq && cudaMemsetAsync(dq_acc, 0, size_t(rows) * HD * 4, st) != cudaSuccess)
     return check_launch("rsa_bwd_stream_fused: dq_acc memset");
-  const int items = g->n_org * g->batch * g->heads * ((key_chunk(g) + TK - 1) / TK);
+  a.qsplit = onepass_qsplit(g, a.dkv_bf16, dk, dv);
+  if (int rc = onepass_zero_dkv(g, a.qsplit, accumulate_dkv, dk, dv, st)) return rc;
+  const int items = g->n_org * g->batch * g->heads * ((key_chunk(g) + TK - 1) / TK) * a.qsplit;
   const int rc = launch(bwd_onepass_kernel<false>, items, FsLayout<false>::SMEM, a, stream, "bwd_onepass_kernel<stream>",
                         SE_THREADS);
   if (rc != RSA_OK || !dq_out.ptr) return rc;
@@ -1077,7 +1136,9 @@ int rsa_bwd_panel_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, r
   const int64_t rows = int64_t(g->n_rank) * g->batch * g->heads * g->chunk;
   if (!accumulate_dq && cudaMemsetAsync(dq_acc, 0, size_t(rows) * HD * 4, st) != cudaSuccess)
     return check_launch("rsa_bwd_panel_fused: dq_acc memset");
-  const int items = g->n_org * g->batch * g->heads * ((g->chunk + TK - 1) / TK);
+  a.qsplit = onepass_qsplit(g, a.dkv_bf16, dk, dv);
+  if (int rc = onepass_zero_dkv(g, a.qsplit, accumulate_dkv, dk, dv, st)) return rc;
+  const int items = g->n_org * g->batch * g->heads * ((g->chunk + TK - 1) / TK) * a.qsplit;
   const int rc = launch(bwd_onepass_kernel<true>, items, FsLayout<true>::SMEM, a, stream, "bwd_onepass_kernel<panel>",
                         SE_THREADS);
   if (rc != RSA_OK || !dq_out.ptr) return rc;
