@@ -93,6 +93,27 @@ def _stack(chunks, device) -> torch.Tensor:
     return out
 
 
+def _sequence_view(chunks):
+    """The (1, B, Z, L, A) tensor the chunks are consecutive slices of along the sequence axis
+    (chunk d = tokens [d*c, (d+1)*c) of one bf16 device tensor, the layout scatter_sequence
+    produces), as a zero-copy view -- or None.  Every Linformer product is local to a query row
+    or sums over all ranks' positions, so with every rank resident the whole sequence can run
+    as one rank of L rows; the chunk list is only the reference's calling convention."""
+    if not chunks or not all(isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.bfloat16 for x in chunks):
+        return None
+    c0 = chunks[0]
+    if c0.dim() != 4 or c0.stride(-1) != 1:
+        return None
+    step = c0.shape[-2] * c0.stride(-2) * c0.element_size()
+    base = c0.untyped_storage().data_ptr()
+    for d, x in enumerate(chunks):
+        if (x.shape != c0.shape or x.stride() != c0.stride() or x.untyped_storage().data_ptr() != base
+                or x.data_ptr() != c0.data_ptr() + d * step):
+            return None
+    b, z, c, a = c0.shape
+    return c0.as_strided((1, b, z, c * len(chunks), a), (0,) + tuple(c0.stride()))
+
+
 def _device(chunks):
     for x in chunks:
         if isinstance(x, torch.Tensor) and x.is_cuda:
@@ -202,11 +223,18 @@ def sparse_ring_attention_forward(q_chunks, k_chunks, v_chunks, weights, cfg: Sp
     dev = _device(q_chunks + k_chunks + v_chunks)
     b, z, c, a = expect
     kdim = cfg.proj_dim
-    q, k, v = _stack(q_chunks, dev), _stack(k_chunks, dev), _stack(v_chunks, dev)
+    seq = [_sequence_view(x) for x in (q_chunks, k_chunks, v_chunks)]
     e = ops.to_device(weights.key_proj, dev)  # (K, L) bf16
     f = ops.to_device(weights.value_proj, dev)
-    k_low16, v_low16 = _project(q, k, v, e, f, kdim)
-    out = low_rank_attention(q, k_low16, v_low16)  # [N][B][Z][c][A]
+    if all(x is not None for x in seq):  # zero-copy: the sequence as one resident rank of L rows
+        q, k, v = seq
+        k_low16, v_low16 = _project(q, k, v, e, f, kdim)
+        whole = low_rank_attention(q, k_low16, v_low16)[0]  # (B, Z, L, A)
+        out = [whole[:, :, d * c:(d + 1) * c] for d in range(n)]
+    else:
+        q, k, v = _stack(q_chunks, dev), _stack(k_chunks, dev), _stack(v_chunks, dev)
+        k_low16, v_low16 = _project(q, k, v, e, f, kdim)
+        out = low_rank_attention(q, k_low16, v_low16)  # [N][B][Z][c][A]
 
     chunk, low, rows = (b, z, c, a), (b, z, kdim, a), (b, z, c, kdim)
     logs = []
@@ -245,11 +273,17 @@ def sparse_ring_attention_backward(q_chunks, k_chunks, v_chunks, weights, cfg: S
     dev = _device(q_chunks + k_chunks + v_chunks + grad_chunks)
     b, z, c, a = base.chunk_shape()
     kdim = cfg.proj_dim
-    q, k, v, g = (_stack(x, dev) for x in (q_chunks, k_chunks, v_chunks, grad_chunks))
+    seq = [_sequence_view(x) for x in (q_chunks, k_chunks, v_chunks, grad_chunks)]
+    n_run, c_run = n, c
+    if all(x is not None for x in seq):  # zero-copy: the sequence as one resident rank of L rows
+        q, k, v, g = seq
+        n_run, c_run = 1, n * c
+    else:
+        q, k, v, g = (_stack(x, dev) for x in (q_chunks, k_chunks, v_chunks, grad_chunks))
     e = ops.to_device(weights.key_proj, dev)
     f = ops.to_device(weights.value_proj, dev)
     k_low16, v_low16 = _project(q, k, v, e, f, kdim)
-    res = _low_rank_stream(q, k_low16, v_low16) if _fused_ok(a, c, kdim) else None
+    res = _low_rank_stream(q, k_low16, v_low16) if _fused_ok(a, c_run, kdim) else None
     if res is not None:
         # fused: P recomputed on chip; the kv kernel walks every rank's query rows, so its
         # fp32 dK' / dV' are already the cross-rank sums
@@ -260,27 +294,27 @@ def sparse_ring_attention_backward(q_chunks, k_chunks, v_chunks, weights, cfg: S
         probs, _ = _low_rank_staged(q, k_low16, v_low16)
         # cross-rank sums (fp32 over ranks in ascending order)
         d_vlow = torch.empty((b, z, kdim, a), dtype=torch.float32, device=dev)
-        for d in range(n):
+        for d in range(n_run):
             ops.matmul(probs[d].transpose(-1, -2), g[d], out=d_vlow, accumulate=d > 0)
         dp = ops.matmul(g, v_low16.transpose(-1, -2))  # [N][B][Z][c][K] fp32
         ds = ops.softmax_backward(probs, dp, 1.0 / math.sqrt(a), out_dtype=torch.bfloat16)
         dq = ops.matmul(ds, k_low16, out_dtype=torch.bfloat16)
         d_klow = torch.empty_like(d_vlow)
-        for d in range(n):
+        for d in range(n_run):
             ops.matmul(ds[d].transpose(-1, -2), q[d], out=d_klow, accumulate=d > 0)
     d_klow16, d_vlow16 = d_klow.to(torch.bfloat16), d_vlow.to(torch.bfloat16)
-    dk = torch.empty_like(q)
-    dv = torch.empty_like(q)
+    dk = torch.empty((n_run, b, z, c_run, a), dtype=torch.bfloat16, device=dev)
+    dv = torch.empty_like(dk)
     grad_e = torch.empty((kdim, base.seq_len), dtype=torch.float32, device=dev)
     grad_f = torch.empty_like(grad_e)
-    for d in range(n):
-        cols = slice(d * c, (d + 1) * c)
+    for d in range(n_run):
+        cols = slice(d * c_run, (d + 1) * c_run)
         ops.matmul(e[:, cols].transpose(0, 1), d_klow16, out=dk[d])
         ops.matmul(f[:, cols].transpose(0, 1), d_vlow16, out=dv[d])
-    if a == 64 and c % 256 == 0 and kdim % 128 == 0:
+    if a == 64 and c_run % 256 == 0 and kdim % 128 == 0:
         # dE / dF for every rank in one launch: each (Kp x 256-position) tile sums the heads'
         # dK'_h K_{d,h}^T with both operands read in place (csrc/linformer.cu)
-        g_ = engine._geom(n, b, z, c, a, n * c, 0, n)
+        g_ = engine._geom(n_run, b, z, c_run, a, n * c, 0, n_run)
         check(lib().rsa_linformer_proj_grad(ctypes.byref(g_), kdim, d_klow16.data_ptr(), d_vlow16.data_ptr(),
                                             engine._view(k), engine._view(v), grad_e.data_ptr(), grad_f.data_ptr(),
                                             grad_e.stride(0), torch.cuda.current_stream(dev).cuda_stream),
@@ -289,17 +323,18 @@ def sparse_ring_attention_backward(q_chunks, k_chunks, v_chunks, weights, cfg: S
         # (K, B*Z*A) views of the low-rank gradients for the shared-projection gradients
         dk_flat = d_klow16.permute(2, 0, 1, 3).reshape(kdim, b * z * a)
         dv_flat = d_vlow16.permute(2, 0, 1, 3).reshape(kdim, b * z * a)
-        for d in range(n):
-            cols = slice(d * c, (d + 1) * c)
-            ops.matmul(dk_flat, k[d].transpose(-1, -2).reshape(b * z * a, c), out=grad_e[:, cols])
-            ops.matmul(dv_flat, v[d].transpose(-1, -2).reshape(b * z * a, c), out=grad_f[:, cols])
+        for d in range(n_run):
+            cols = slice(d * c_run, (d + 1) * c_run)
+            ops.matmul(dk_flat, k[d].transpose(-1, -2).reshape(b * z * a, c_run), out=grad_e[:, cols])
+            ops.matmul(dv_flat, v[d].transpose(-1, -2).reshape(b * z * a, c_run), out=grad_f[:, cols])
     ledger = CommLedger(n)
     if n > 1:
         for d in range(n):
             ledger.record_ring_send(d, 2 * (n - 1) * b * z * kdim * a)
-    return SparseRingBackward(grad_q=[dq[d] for d in range(n)], grad_k=[dk[d] for d in range(n)],
-                              grad_v=[dv[d] for d in range(n)], grad_key_proj=grad_e, grad_value_proj=grad_f,
-                              ledger=ledger)
+    per_rank = (lambda t: [t[0][:, :, d * c:(d + 1) * c] for d in range(n)]) if n_run == 1 and n > 1 else (
+        lambda t: [t[d] for d in range(n)])
+    return SparseRingBackward(grad_q=per_rank(dq), grad_k=per_rank(dk), grad_v=per_rank(dv), grad_key_proj=grad_e,
+                              grad_value_proj=grad_f, ledger=ledger)
 
 
 def full_length_dims(shape_logs, cfg: SparseAttentionConfig) -> list:

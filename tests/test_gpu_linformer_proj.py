@@ -85,3 +85,45 @@ def test_linformer_projection_gradients_match_float64(shape):
         assert np.isfinite(g64).all()
         rel = np.linalg.norm(g64 - want) / np.linalg.norm(want)
         assert rel <= 1e-5, rel
+
+
+def test_sparse_api_sequence_views_match_separate_chunks():
+    """Chunks that are consecutive slices of one device tensor run zero-copy as one resident
+    rank of L rows (sparse_attention._sequence_view); the results equal those of the same
+    values passed as separate per-rank tensors (stacked first) to fp32 summation-order noise."""
+    import math
+
+    from paper_2105_13120_b200 import AttentionConfig, SparseAttentionConfig
+    from paper_2105_13120_b200.sparse_attention import (_sequence_view, sparse_ring_attention_backward,
+                                                        sparse_ring_attention_forward)
+    from paper_2105_13120_b200.weights import SparseWeights
+
+    n, b, z, L, a, kdim = 4, 1, 4, 2048, 64, 128
+    c = L // n
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev).manual_seed(3)
+    q, k, v, g = (torch.randn((b, z, L, a), generator=gen, device=dev).to(torch.bfloat16) for _ in range(4))
+    w = SparseWeights(*((torch.randn((kdim, L), generator=gen, device=dev) / math.sqrt(L)).to(torch.bfloat16)
+                        for _ in range(2)))
+    cfg = SparseAttentionConfig(base=AttentionConfig(batch_size=b, seq_len=L, hidden_size=z * a, num_heads=z,
+                                                     head_size=a, num_devices=n), proj_dim=kdim)
+    views = [[t[:, :, d * c:(d + 1) * c] for d in range(n)] for t in (q, k, v, g)]
+    seps = [[x.clone() for x in ch] for ch in views]
+    assert _sequence_view(views[0]) is not None and _sequence_view(seps[0]) is None
+    fv = sparse_ring_attention_forward(*views[:3], w, cfg)
+    fs = sparse_ring_attention_forward(*seps[:3], w, cfg)
+    bv = sparse_ring_attention_backward(*views[:3], w, cfg, views[3])
+    bs = sparse_ring_attention_backward(*seps[:3], w, cfg, seps[3])
+    torch.cuda.synchronize()
+
+    def close(x, y, tol=2e-3):
+        x, y = x.double(), y.double()
+        assert float(torch.linalg.norm(x - y) / torch.linalg.norm(y)) <= tol
+
+    for d in range(n):
+        close(fv.outputs[d], fs.outputs[d])
+        close(bv.grad_q[d], bs.grad_q[d])
+        close(bv.grad_k[d], bs.grad_k[d])
+        close(bv.grad_v[d], bs.grad_v[d])
+    close(bv.grad_key_proj, bs.grad_key_proj)
+    close(bv.grad_value_proj, bs.grad_value_proj)

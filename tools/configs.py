@@ -105,8 +105,17 @@ def linformer(n, b, z, seq, a, kp, iters, dev):
                       (torch.randn((kp, seq), generator=gen, device=dev) * s).to(torch.bfloat16))
     base = AttentionConfig(batch_size=b, seq_len=seq, hidden_size=z * a, num_heads=z, head_size=a, num_devices=n)
     cfg = SparseAttentionConfig(base=base, proj_dim=kp)
-    fwd_ms = timed(lambda: sparse_ring_attention_forward(ch[0], ch[1], ch[2], w, cfg), iters)
-    bwd_ms = timed(lambda: sparse_ring_attention_backward(ch[0], ch[1], ch[2], w, cfg, ch[3]), iters)
+    # chunks as views of whole-sequence tensors (zero copy: the API runs the sequence as one
+    # resident rank) ...
+    seqs = [torch.cat(x, dim=2) for x in ch]
+    sc = [list(t.chunk(n, dim=2)) for t in seqs]
+    fwd_ms = timed(lambda: sparse_ring_attention_forward(sc[0], sc[1], sc[2], w, cfg), iters)
+    bwd_ms = timed(lambda: sparse_ring_attention_backward(sc[0], sc[1], sc[2], w, cfg, sc[3]), iters)
+    # ... and independent contiguous per-rank chunks, as scatter_sequence returns them (stacked
+    # into [N][B][Z][c][A] first)
+    fwd_ms_sep = timed(lambda: sparse_ring_attention_forward(ch[0], ch[1], ch[2], w, cfg), iters)
+    bwd_ms_sep = timed(lambda: sparse_ring_attention_backward(ch[0], ch[1], ch[2], w, cfg, ch[3]), iters)
+    del seqs, sc
     # the device path without the list API's chunk stacking: projections, then the fused attention
     from paper_2105_13120_b200 import sparse_attention as spm
 
@@ -117,6 +126,7 @@ def linformer(n, b, z, seq, a, kp, iters, dev):
     # algorithmic HBM bytes of the forward: read q, k, v and write O (bf16), E/F blocks
     fwd_bytes = 4 * 2 * b * z * seq * a + 2 * 2 * kp * seq
     return {"ms_fwd_api": fwd_ms, "ms_bwd_api_incl_recompute": bwd_ms,
+            "ms_fwd_api_separate_chunks": fwd_ms_sep, "ms_bwd_api_separate_chunks": bwd_ms_sep,
             "tokens_per_s_fwd_api": b * seq / (fwd_ms / 1e3),
             "tokens_per_s_fwd_bwd_api": b * seq / ((fwd_ms + bwd_ms) / 1e3),
             "ms_fwd_projections": proj_ms, "ms_fwd_low_rank_attention": attn_ms,
