@@ -352,6 +352,16 @@ int rsa_linformer_project(const rsa_geom* g, int proj_dim, const void* e, const 
 int rsa_linformer_proj_grad(const rsa_geom* g, int proj_dim, const void* dk_low, const void* dv_low, rsa_view k,
                             rsa_view v, float* grad_e, float* grad_f, int64_t ld_grad, void* stream);
 
+/*
+ * The projections' transposes (the Linformer backward): for every
+ * resident origin d and head h, dk[d][h] = E_d^T dK'_h and dv[d][h] = F_d^T dV'_h.  e / f as
+ * rsa_linformer_project (origin d's columns at (org_lo + d) * chunk); dk_low / dv_low: bf16
+ * [B][Z][proj_dim][64] contiguous; dk / dv: bf16 [n_org][B][Z][chunk][64] views.  Needs
+ * head_dim 64, chunk % 128 == 0, proj_dim % 64 == 0 and B*Z % 4 == 0.
+ */
+int rsa_linformer_proj_back(const rsa_geom* g, int proj_dim, const void* e, const void* f, int64_t ld_proj,
+                            const void* dk_low, const void* dv_low, rsa_view dk, rsa_view dv, void* stream);
+
 /* ------------------------------------------ BERT harness */
 
 /*

@@ -136,6 +136,8 @@ EXPORTS = {
                                       c_void_p, c_void_p]),
     "rsa_linformer_proj_grad": (c_int, [_GEOM, c_int, c_void_p, c_void_p, _V, _V, c_void_p, c_void_p, c_int64,
                                         c_void_p]),
+    "rsa_linformer_proj_back": (c_int, [_GEOM, c_int, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, _V, _V,
+                                        c_void_p]),
     "rsa_bwd_panel_fused": (c_int, [_GEOM, _V, _V, _V, _V, _V, c_void_p, _V, _V, c_int, c_int, c_void_p, c_int, _V,
                                     c_void_p]),
 }

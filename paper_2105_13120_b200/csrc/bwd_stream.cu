@@ -1005,7 +1005,11 @@ inline int onepass_qsplit(const rsa_geom* g, int dkv_bf16, const rsa_view& dk, c
            (g->n_org == 1 || x.s_rank == int64_t(g->batch) * g->heads * ck * HD);
   };
   if (!dense(dk) || !dense(dv)) return 1;
-  int qs = int(std::min<int64_t>((2 * sms + base - 1) / base, T / 8));
+  static const int per_sm = [] {  // experiment switch: items per SM to aim for (RSA_OP_ITEMS_PER_SM)
+    const char* e = getenv("RSA_OP_ITEMS_PER_SM");
+    return e ? std::max(1, atoi(e)) : 4;
+  }();
+  int qs = int(std::min<int64_t>((per_sm * sms + base - 1) / base, T / 8));
   const int tq = (T + qs - 1) / qs;
   return (T + tq - 1) / tq;  // no empty share
 }

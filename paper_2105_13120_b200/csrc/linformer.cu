@@ -305,6 +305,132 @@ __global__ void __launch_bounds__(LP_THREADS, 1) linformer_grad_kernel(const __g
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// ------------------------------------------------------------ the projections' transposes
+//
+// dK_d = E_d^T dK', dV_d = F_d^T dV' (the Linformer backward's gradients of the keys and
+// values) for every rank and head: tile = 128 positions (M) x four
+// heads' 64 dimensions (N = 256), contraction over Kp in 64-row stages.  A = E read as
+// MN-major (positions contiguous), B = the four heads' dK' blocks (dims contiguous), so the
+// E tile staged for a position block feeds four heads; bf16 rows leave straight from TMEM
+// (each thread one row's 32 dimensions per store pair).
+struct LbArgs {
+  CUtensorMap ta[2], tb[2];  // E / F (Kp x L), dK' / dV' ([b][z][Kp][64])
+  OutView out[2];            // dK / dV: [origin][b][z][position][64] bf16
+  int kp, BZ, Z, B, c, n_org, org_lo;
+  int pblocks, items;
+};
+
+__global__ void __launch_bounds__(LP_THREADS, 1) linformer_back_kernel(const __grid_constant__ LbArgs p) {
+  uint8_t* smem = smem_base();
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + LP_OFF_BAR);
+  uint64_t *full = bar, *empty = bar + LP_ST, *acc_full = empty + LP_ST, *acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int hgroups = p.BZ / LP_HEADS, kstages = p.kp / LP_KB;
+
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < LP_ST; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    for (int s = 0; s < 2; ++s) mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], 4);
+    fence_barrier_init();
+    for (int j = 0; j < 2; ++j) tma_prefetch(&p.ta[j]), tma_prefetch(&p.tb[j]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // item -> (projection j, origin d, position block pb, head group hg): head groups fastest,
+  // so consecutive items of a CTA reuse the E tile from L2
+  auto decode = [&](int item, int& j, int& d, int& pb, int& hg) {
+    hg = item % hgroups;
+    int rest = item / hgroups;
+    pb = rest % p.pblocks, rest /= p.pblocks;
+    d = rest % p.n_org, j = rest / p.n_org;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      Pos lq;
+      for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+        int j, d, pb, hg;
+        decode(item, j, d, pb, hg);
+        for (int ks = 0; ks < kstages; ++ks) {
+          const uint32_t s = lq.slot(LP_ST);
+          mbar_wait(&empty[s], lq.phase(LP_ST) ^ 1);
+          mbar_arrive_expect_tx(&full[s], LP_STAGE);
+          uint8_t* sa = smem + s * LP_STAGE;
+          const int col = (p.org_lo + d) * p.c + pb * TR;
+          tma_load_2d(sa, &p.ta[j], &full[s], col, ks * LP_KB);                  // positions col .. +63
+          tma_load_2d(sa + LP_A / 2, &p.ta[j], &full[s], col + 64, ks * LP_KB);  // positions col + 64 .. +127
+#pragma unroll
+          for (int h = 0; h < LP_HEADS; ++h) {
+            const int bz = hg * LP_HEADS + h;
+            tma_load_4d(sa + LP_A + h * LP_BH, &p.tb[j], &full[s], 0, ks * LP_KB, bz % p.Z, bz / p.Z);
+          }
+          ++lq.i;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // A: E^T (positions contiguous: MN-major, two 64-position atoms 8 KB apart); B: dK' blocks
+    // (dims contiguous: MN-major, four 64-dim atoms 8 KB apart); 16 Kp rows (2 KB) per k step
+    const uint32_t idesc = idesc_bf16_f32(TR, LP_HEADS * HD, 1, 1);
+    Pos lq;
+    uint32_t it = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+      const uint32_t ab = it & 1;
+      mbar_wait(&acc_empty[ab], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      for (int ks = 0; ks < kstages; ++ks) {
+        const uint32_t s = lq.slot(LP_ST);
+        mbar_wait(&full[s], lq.phase(LP_ST));
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * LP_STAGE), sb = sa + LP_A;
+#pragma unroll
+        for (int k = 0; k < LP_KB / 16; ++k)
+          umma_bf16_ws(tmem + ab * 256, smem_desc_sw128(sa + k * 2048, LP_A / 2, 1024),
+                       smem_desc_sw128(sb + k * 2048, LP_BH, 1024), idesc, (ks > 0) || (k > 0));
+        umma_commit_ws(&empty[s]);
+        ++lq.i;
+      }
+      umma_commit_ws(&acc_full[ab]);
+    }
+  } else {
+    const uint32_t quad = warp & 3;
+    const uint32_t lane_base = (quad * 32u) << 16;
+    uint32_t it = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+      int j, d, pb, hg;
+      decode(item, j, d, pb, hg);
+      const uint32_t ab = it & 1;
+      const int pos = pb * TR + int(quad) * 32 + int(lane);
+      mbar_wait(&acc_full[ab], (it >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int ch = 0; ch < 2 * LP_HEADS; ++ch) {
+        float v[32];
+        __syncwarp();
+        tmem_ld32(tmem + lane_base + ab * 256 + ch * 32, v);
+        tmem_ld_wait();
+        if (ch == 2 * LP_HEADS - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[ab]);
+        }
+        if (pos < p.c) {
+          const int bz = hg * LP_HEADS + ch / 2;
+          const OutView none{nullptr, 0, 0, 0, 0};
+          store_row32(none, p.out[j], 0, d, bz / p.Z, bz % p.Z, pos, (ch & 1) * 32, v);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
 __global__ void cast_bf16_kernel(const float4* __restrict__ x, uint2* __restrict__ y, int64_t n4) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
     const float4 v = x[i];
@@ -424,6 +550,43 @@ int rsa_linformer_proj_grad(const rsa_geom* g, int proj_dim, const void* dk_low,
   a.nblocks = g->chunk / LG_N;
   a.items = 2 * (proj_dim / TR) * g->n_org * a.nblocks;
   return launch(linformer_grad_kernel, a.items, LP_SMEM, a, stream, "linformer_grad_kernel", LP_THREADS);
+}
+
+int rsa_linformer_proj_back(const rsa_geom* g, int proj_dim, const void* e, const void* f, int64_t ld_proj,
+                            const void* dk_low, const void* dv_low, rsa_view dk, rsa_view dv, void* stream) {
+  using namespace rsa;
+  if (!g || g->head_dim != HD || g->chunk % TR || proj_dim % LP_KB || (g->batch * g->heads) % LP_HEADS ||
+      g->n_org < 1 || g->org_lo < 0 || !e || !f || !dk_low || !dv_low || !dk.ptr || !dv.ptr ||
+      ld_proj < int64_t(g->org_lo + g->n_org) * g->chunk)
+    return fail(RSA_ERR_INVALID, "rsa_linformer_proj_back: unsupported geometry (A = 64, chunk %% 128, Kp %% 64, "
+                                 "B*Z %% 4)");
+  if (!aligned16(e) || !aligned16(f) || (ld_proj * 2) % 16 || !aligned16(dk_low) || !aligned16(dv_low) ||
+      !out_ok(dk, 2) || !out_ok(dv, 2))
+    return fail(RSA_ERR_UNSUPPORTED, "rsa_linformer_proj_back: buffers not 16-byte aligned");
+  LbArgs a{};
+  const void* proj[2] = {e, f};
+  const void* low[2] = {dk_low, dv_low};
+  const rsa_view out[2] = {dk, dv};
+  for (int j = 0; j < 2; ++j) {
+    // E / F: (Kp x L) row-major; 64-position x 64-row boxes (positions contiguous)
+    uint64_t dims[2] = {uint64_t(ld_proj), uint64_t(proj_dim)};
+    uint64_t str[1] = {uint64_t(ld_proj) * 2};
+    uint32_t box[2] = {64, LP_KB};
+    if (!encode_tmap(&a.ta[j], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, proj[j], dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
+      return RSA_ERR_UNSUPPORTED;
+    // dK' / dV': [b][z][Kp][64] bf16 contiguous; 64-dim x 64-row boxes
+    uint64_t bd[4] = {uint64_t(HD), uint64_t(proj_dim), uint64_t(g->heads), uint64_t(g->batch)};
+    uint64_t bs[3] = {uint64_t(HD) * 2, uint64_t(proj_dim) * HD * 2, uint64_t(g->heads) * proj_dim * HD * 2};
+    uint32_t bb[4] = {HD, LP_KB, 1, 1};
+    if (!encode_tmap(&a.tb[j], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, low[j], bd, bs, bb, CU_TENSOR_MAP_SWIZZLE_128B))
+      return RSA_ERR_UNSUPPORTED;
+    a.out[j] = to_out(out[j]);
+  }
+  a.kp = proj_dim, a.BZ = g->batch * g->heads, a.Z = g->heads, a.B = g->batch;
+  a.c = g->chunk, a.n_org = g->n_org, a.org_lo = g->org_lo;
+  a.pblocks = g->chunk / TR;
+  a.items = 2 * g->n_org * a.pblocks * (a.BZ / LP_HEADS);
+  return launch(linformer_back_kernel, a.items, LP_SMEM, a, stream, "linformer_back_kernel", LP_THREADS);
 }
 
 }  // extern "C"

@@ -307,10 +307,19 @@ def sparse_ring_attention_backward(q_chunks, k_chunks, v_chunks, weights, cfg: S
     dv = torch.empty_like(dk)
     grad_e = torch.empty((kdim, base.seq_len), dtype=torch.float32, device=dev)
     grad_f = torch.empty_like(grad_e)
-    for d in range(n_run):
-        cols = slice(d * c_run, (d + 1) * c_run)
-        ops.matmul(e[:, cols].transpose(0, 1), d_klow16, out=dk[d])
-        ops.matmul(f[:, cols].transpose(0, 1), d_vlow16, out=dv[d])
+    if (a == 64 and c_run % 128 == 0 and kdim % 64 == 0 and (b * z) % 4 == 0 and e.stride(1) == f.stride(1) == 1
+            and e.stride(0) == f.stride(0)):
+        # dK_d = E_d^T dK', dV_d = F_d^T dV' for every rank and head in one launch
+        g_ = engine._geom(n_run, b, z, c_run, a, n * c, 0, n_run)
+        check(lib().rsa_linformer_proj_back(ctypes.byref(g_), kdim, e.data_ptr(), f.data_ptr(), e.stride(0),
+                                            d_klow16.data_ptr(), d_vlow16.data_ptr(), engine._view(dk),
+                                            engine._view(dv), torch.cuda.current_stream(dev).cuda_stream),
+              "rsa_linformer_proj_back")
+    else:
+        for d in range(n_run):
+            cols = slice(d * c_run, (d + 1) * c_run)
+            ops.matmul(e[:, cols].transpose(0, 1), d_klow16, out=dk[d])
+            ops.matmul(f[:, cols].transpose(0, 1), d_vlow16, out=dv[d])
     if a == 64 and c_run % 256 == 0 and kdim % 128 == 0:
         # dE / dF for every rank in one launch: each (Kp x 256-position) tile sums the heads'
         # dK'_h K_{d,h}^T with both operands read in place (csrc/linformer.cu)

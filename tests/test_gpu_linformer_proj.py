@@ -127,3 +127,30 @@ def test_sparse_api_sequence_views_match_separate_chunks():
         close(bv.grad_v[d], bs.grad_v[d])
     close(bv.grad_key_proj, bs.grad_key_proj)
     close(bv.grad_value_proj, bs.grad_value_proj)
+
+
+@pytest.mark.parametrize("shape", [(8, 1, 4, 256, 128), (2, 4, 12, 1024, 256), (3, 1, 4, 384, 192)])
+def test_linformer_projection_transposes_match_float64(shape):
+    """rsa_linformer_proj_back: dK_d = E_d^T dK', dV_d = F_d^T dV' for every rank and head."""
+    from paper_2105_13120_b200 import engine
+    from paper_2105_13120_b200._native import check, lib
+
+    n, b, z, c, kdim = shape
+    a, L = 64, shape[0] * shape[3]
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev).manual_seed(5 * c + kdim)
+    e, f = ((torch.randn((kdim, L), generator=gen, device=dev) / L ** 0.5).to(torch.bfloat16) for _ in range(2))
+    dkl, dvl = (torch.randn((b, z, kdim, a), generator=gen, device=dev).to(torch.bfloat16) for _ in range(2))
+    dk, dv = (torch.full((n, b, z, c, a), float("nan"), dtype=torch.bfloat16, device=dev) for _ in range(2))
+    g = engine._geom(n, b, z, c, a, L, 0, n)
+    check(lib().rsa_linformer_proj_back(ctypes.byref(g), kdim, e.data_ptr(), f.data_ptr(), e.stride(0),
+                                        dkl.data_ptr(), dvl.data_ptr(), engine._view(dk), engine._view(dv),
+                                        torch.cuda.current_stream().cuda_stream), "rsa_linformer_proj_back")
+    torch.cuda.synchronize()
+    for got, p, low in ((dk, e, dkl), (dv, f, dvl)):
+        pd, ld = p.double().cpu().numpy(), low.double().cpu().numpy()
+        want = np.stack([np.einsum("kc,bzka->bzca", pd[:, d * c:(d + 1) * c], ld) for d in range(n)])
+        g64 = got.double().cpu().numpy()
+        assert np.isfinite(g64).all()
+        rel = np.linalg.norm(g64 - want) / np.linalg.norm(want)
+        assert rel <= 5e-3, rel  # one bf16 rounding of an fp32 sum
