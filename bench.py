@@ -521,12 +521,35 @@ def ours(args):
         "clocks": clocks, "roofline": roof, "kernels": kernels, "kernel_ms_sum": kernel_sum,
         "kernel_sum_over_step": kernel_sum / step_ref_ms, "step_ms_interleaved": step_ref_ms,
         "kernel_timing_clocks": kernel_clocks, "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
-        "parity": parity,
+        "parity": parity, "max_seq_len": max_seq_len(args, torch.cuda.mem_get_info(dev)[1]),
     }
     if not args.no_cpu_baseline:
         v, cores, sample = cpu_oracle_sample(args, host_threads())
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
     print(json.dumps(line), flush=True)
+
+
+def max_seq_len(args, total_hbm):
+    """The metric's second half, "max seq length per box", for BASELINE config 3's workload
+    (BERT-base attention stack, B = 4, 12 layers, every layer's state saved), DERIVED from
+    the state each mode keeps per token against this GPU's HBM (the sweep that measures it
+    and the proof run at the stream maximum are tools/stream_sweep.py's, in
+    profiles/r2s3_stream_sweep.json: 536,576 tokens run, 12,288 for panels).  Per layer and
+    token: q, k, v, O (4 x Z*A bf16) plus, stream mode, m and r (2 x Z fp32) or, panel
+    mode, its row of the (c x L) panel (Z*L bf16); the backward adds one layer's transient
+    gradient buffers (dQ fp32 accumulator, dO, dO*r, dQ/dK/dV, D).  Max L grows linearly
+    with N in stream mode (state O(L/N) per GPU) and as sqrt(N) with panels."""
+    Z, A, layers, B = args.heads, args.head_size, args.layers, 4
+    per_tok = layers * (4 * Z * A * 2) + (Z * A * 4 + 5 * Z * A * 2 + Z * 4)  # + one layer's backward transients
+    stream = (layers * 2 * Z * 4 + per_tok) * B
+    budget = 0.97 * total_hbm
+    l_stream = int(budget // stream) // 4096 * 4096
+    # panel: B * (per_tok + layers * Z * 2 * L) * L <= budget
+    a_, b_ = B * layers * Z * 2, B * per_tok
+    l_panel = int((-b_ + (b_ * b_ + 4 * a_ * budget) ** 0.5) / (2 * a_)) // 1024 * 1024
+    return {"stream": l_stream, "panel": l_panel, "batch": B, "layers": layers, "method": "derived (bytes per token "
+            "against this GPU's HBM); measured: profiles/r2s3_stream_sweep.json", "stream_per_8_gpus_derived": 8 * l_stream,
+            "panel_per_8_gpus_derived": int(l_panel * 8 ** 0.5)}
 
 
 def sampled_parity(layers, B, Z, seed, heads_per_layer=8):
