@@ -308,8 +308,9 @@ int rsa_bwd_q_stream(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_
  * the V-ring and K-ring backward, without a saved panel): per key tile, walking every query
  * tile, dV_j and dK_j as rsa_bwd_kv_stream and dQ_part = dS K_j added into the fp32
  * accumulator dq_acc ([n_rank][B][Z][chunk][64], contiguous, zeroed first unless
- * accumulate_dq) by TMA reduce-add in L2; S, dP and every exp2 are computed once.
- * dq_out (optional, bf16 view) receives bf16(dq_acc) at the end.  dK / dV are summed in a
+ * accumulate_dq; it holds the sum WITHOUT the 1/sqrt(A) factor) by TMA reduce-add in L2;
+ * S, dP and every exp2 are computed once.  dq_out (optional, bf16 view) receives
+ * bf16(dq_acc / sqrt(A)) at the end.  dK / dV are summed in a
  * fixed order; dQ's sum over key tiles is in arrival order (not bitwise reproducible).
  */
 int rsa_bwd_stream_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_view dout_scaled,

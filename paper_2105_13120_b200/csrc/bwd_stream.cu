@@ -834,9 +834,8 @@ __global__ void __maxnreg__(96) bwd_onepass_kernel(const __grid_constant__ Strea
       __syncwarp();
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        st_shared_v4(stg_row + ((j ^ sw) << 4), __float_as_uint(o[4 * j] * g.scale),
-                     __float_as_uint(o[4 * j + 1] * g.scale), __float_as_uint(o[4 * j + 2] * g.scale),
-                     __float_as_uint(o[4 * j + 3] * g.scale));
+        st_shared_v4(stg_row + ((j ^ sw) << 4), __float_as_uint(o[4 * j]), __float_as_uint(o[4 * j + 1]),
+                     __float_as_uint(o[4 * j + 2]), __float_as_uint(o[4 * j + 3]));  // 1/sqrt(A) at the cast
     };
     auto dq_reduce = [&](int d, int b, int z, int r0) {
       if (lane == 0 && !(p.dbg & 3)) {
@@ -962,9 +961,10 @@ __global__ void __maxnreg__(96) bwd_onepass_kernel(const __grid_constant__ Strea
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
-// dQ = bf16(dq_acc): fp32 [rank][b][z][row][64] contiguous into a strided bf16 view, 8
-// columns per thread.
-__global__ void dq_cast_kernel(const float* __restrict__ acc, OutView out, int c, int Z, int B, int64_t rows) {
+// dQ = bf16(scale * dq_acc): fp32 [rank][b][z][row][64] contiguous (the unscaled sum of the
+// dS K_j partials) into a strided bf16 view, 8 columns per thread.
+__global__ void dq_cast_kernel(const float* __restrict__ acc, OutView out, int c, int Z, int B, int64_t rows,
+                               float scale) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows * 8; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t row = i >> 3;
     const int col = int(i & 7) * 8;
@@ -973,8 +973,9 @@ __global__ void dq_cast_kernel(const float* __restrict__ acc, OutView out, int c
     const int z = int(hb % Z);
     hb /= Z;
     const int b = int(hb % B), d = int(hb / B);
-    const float4 x = *reinterpret_cast<const float4*>(acc + row * HD + col);
-    const float4 y = *reinterpret_cast<const float4*>(acc + row * HD + col + 4);
+    float4 x = *reinterpret_cast<const float4*>(acc + row * HD + col);
+    float4 y = *reinterpret_cast<const float4*>(acc + row * HD + col + 4);
+    x.x *= scale, x.y *= scale, x.z *= scale, x.w *= scale, y.x *= scale, y.y *= scale, y.z *= scale, y.w *= scale;
     *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out.ptr) + out_off(out, d, b, z, rr) + col) =
         make_uint4(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w), pack_bf16(y.x, y.y), pack_bf16(y.z, y.w));
   }
@@ -1026,7 +1027,7 @@ inline int onepass_zero_dkv(const rsa_geom* g, int qsplit, int accumulate, const
 int dq_cast(const float* dq_acc, const rsa_view& dq_out, const rsa_geom* g, int64_t rows, cudaStream_t st) {
   const int64_t work = rows * 8;
   const int blocks = int(std::min<int64_t>((work + 255) / 256, int64_t(num_sms()) * 8));
-  dq_cast_kernel<<<blocks, 256, 0, st>>>(dq_acc, to_out(dq_out), g->chunk, g->heads, g->batch, rows);
+  dq_cast_kernel<<<blocks, 256, 0, st>>>(dq_acc, to_out(dq_out), g->chunk, g->heads, g->batch, rows, g->scale);
   return check_launch("dq_cast_kernel");
 }
 
