@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = tmem_base(tmem_slot);
   const long long tr0 = clock64();
   int tr_i = 0;
 

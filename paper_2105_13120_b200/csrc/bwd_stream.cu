@@ -129,7 +129,7 @@ __global__ void __maxnreg__(96) bwd_kv_stream_kernel(const __grid_constant__ Str
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = tmem_base(tmem_slot);
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -379,7 +379,7 @@ __global__ void __maxnreg__(96) bwd_q_stream_kernel(const __grid_constant__ Stre
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = tmem_base(tmem_slot);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -663,7 +663,7 @@ __global__ void __maxnreg__(96) bwd_onepass_kernel(const __grid_constant__ Strea
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = tmem_base(tmem_slot);
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer

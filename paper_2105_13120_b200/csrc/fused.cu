@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fwd_kernel(const __grid_constant_
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = tmem_base(tmem_slot);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dkdv_kernel(const __grid_cons
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = tmem_base(tmem_slot);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_dq_kernel(const __grid_consta
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = tmem_base(tmem_slot);
 
   if (warp == 0) {
     if (lane == 0) {

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(LP_THREADS, 1) linformer_project_kernel(const 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = tmem_base(tmem_slot);
 
   // item -> (projection j, Kp block mb, head group hg, split ks); stage range [s0, s1)
   auto decode = [&](int item, int& j, int& mb, int& hg, int& s0, int& s1) {
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(LP_THREADS, 1) linformer_grad_kernel(const __g
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = tmem_base(tmem_slot);
 
   // item -> (projection j, Kp block mb, origin d, position block nb)
   auto decode = [&](int item, int& j, int& mb, int& d, int& nb) {
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(LP_THREADS, 1) linformer_back_kernel(const __g
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = tmem_base(tmem_slot);
 
   // item -> (projection j, origin d, position block pb, head group hg): head groups fastest,
   // so consecutive items of a CTA reuse the E tile from L2

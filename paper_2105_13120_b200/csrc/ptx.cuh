@@ -21,7 +21,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
-__device__ __forceinline__ uint32_t warp_id() { return threadIdx.x >> 5; }
+// The warp index, provably warp-uniform (a shuffle from lane 0): role branches on it are
+// uniform branches, so the single-warp roles (TMA producer, MMA issuer) keep their loop
+// counters, addresses and descriptors in uniform registers instead of per-MMA R2UR / elect
+// sequences.  Call at kernel entry, with the whole warp converged.
+__device__ __forceinline__ uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
+
+// The TMEM base address a warp allocated (written to shared memory), warp-uniform likewise.
+__device__ __forceinline__ uint32_t tmem_base(const uint32_t* slot) { return __shfl_sync(0xffffffffu, *slot, 0); }
 
 // ------------------------------------------------------------- mbarriers
 
@@ -63,6 +70,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+
 
 // Busy-poll form (mbarrier.test_wait never suspends the thread).
 __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
