@@ -187,9 +187,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
           tc_fence_after();
           const uint64_t da = smem_desc_sw128(smem_u32(smem + BF_OFF_DO + ds * TILE), 0, 1024);
           const uint64_t db = smem_desc_sw128(smem_u32(smem + BF_OFF_V + vs * TILE), 0, 1024);
-#pragma unroll
-          for (int k = 0; k < HD / 16; ++k)  // K-major: +32 B per 16-wide k step
-            umma_bf16_ws(tmem + COL_DP, da + 2 * k, db + 2 * k, idesc_dp, k > 0);
+          umma_ss_x4<2, 2>(tmem + COL_DP, da, db, idesc_dp, 0);  // K-major: +32 B per 16-wide k step
           if (qt == NQ - 1) {
             umma_commit_ws(&rv.empty[vs]);
             ++v_a.i;
@@ -206,9 +204,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
           tc_fence_after();
           const uint64_t da = smem_desc_sw128(smem_u32(smem + BF_OFF_P + ps * PTILE), ATOM, 1024);
           const uint64_t db = smem_desc_sw128(smem_u32(smem + BF_OFF_DO + ds * TILE), ATOM, 1024);
-#pragma unroll
-          for (int k = 0; k < TR / 16; ++k)  // MN-major: +16 rows (2048 B) per k step
-            umma_bf16_ws(tmem + COL_DV, da + 128 * k, db + 128 * k, idesc_kv, (qt | k) != 0);
+          umma_ss_x4<128, 128>(tmem + COL_DV, da, db, idesc_kv, qt != 0);  // MN-major: +16 rows (2048 B) per k step
+          umma_ss_x4<128, 128>(tmem + COL_DV, da + 512, db + 512, idesc_kv, 1);
           umma_commit_ws(&rdo.empty[ds]);
           umma_commit_ws(&p_read[ps]);
           BF_TRACE(11);
@@ -227,17 +224,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
           const uint64_t dkm = smem_desc_sw128(dsa, 0, 1024);     // dS: K-major A
           const uint64_t qd = smem_desc_sw128(smem_u32(smem + BF_OFF_Q + qs * TILE), ATOM, 1024);
           const uint64_t kd = smem_desc_sw128(smem_u32(smem + BF_OFF_K + ks * TILE), ATOM, 1024);
-#pragma unroll
-          for (int k = 0; k < TR / 16; ++k)
-            umma_bf16_ws(tmem + COL_DK, dmn + 128 * k, qd + 128 * k, idesc_kv, (qt | k) != 0);
+          umma_ss_x4<128, 128>(tmem + COL_DK, dmn, qd, idesc_kv, qt != 0);
+          umma_ss_x4<128, 128>(tmem + COL_DK, dmn + 512, qd + 512, idesc_kv, 1);
           if (kk == 0) {
             mbar_wait(&dq_empty[qt], (head_it & 1) ^ 1);
             tc_fence_after();
           }
-#pragma unroll
-          for (int k = 0; k < TK / 16; ++k)  // dS K-major over keys: 64-key atoms ATOM apart, +32 B per k
-            umma_bf16_ws(tmem + COL_DQ + qt * HD, dkm + (k >> 2) * (ATOM >> 4) + 2 * (k & 3), kd + 128 * k, idesc_dq,
-                         (kk | k) != 0);
+          // dS K-major over keys: 64-key atoms ATOM apart, +32 B per k
+          umma_ss_x4<2, 128>(tmem + COL_DQ + qt * HD, dkm, kd, idesc_dq, kk != 0);
+          umma_ss_x4<2, 128>(tmem + COL_DQ + qt * HD, dkm + (ATOM >> 4), kd + 512, idesc_dq, 1);
           if (!(p.kv_tma && qt == NQ - 1)) umma_commit_ws(&rp.empty[ps]);  // else the epilogue frees it
           umma_commit_ws(&rq.empty[qs]);
           if (qt == NQ - 1) {

@@ -727,10 +727,7 @@ __global__ void __maxnreg__(96) bwd_onepass_kernel(const __grid_constant__ Strea
         mbar_wait(s_empty, (n_s & 1) ^ 1);
         tc_fence_after();
         const uint32_t qa = smem_u32(smem + FS_OFF_ST + s * STAGE);
-#pragma unroll
-        for (int k = 0; k < HD / 16; ++k)
-          umma_bf16_ws(tmem + FS_COL_S, smem_desc_sw128(ka + k * 32, 0, 1024), smem_desc_sw128(qa + k * 32, 0, 1024),
-                       idesc_s, k > 0);
+        umma_ss_x4<2, 2>(tmem + FS_COL_S, smem_desc_sw128(ka, 0, 1024), smem_desc_sw128(qa, 0, 1024), idesc_s, 0);
         umma_commit_ws(s_full);
         ++lq_s.i, ++n_s;
       };
@@ -740,10 +737,7 @@ __global__ void __maxnreg__(96) bwd_onepass_kernel(const __grid_constant__ Strea
         mbar_wait(dp_empty, (n_d & 1) ^ 1);
         tc_fence_after();
         const uint32_t doa = smem_u32(smem + FS_OFF_ST + s * STAGE) + TILE;
-#pragma unroll
-        for (int k = 0; k < HD / 16; ++k)
-          umma_bf16_ws(tmem + FS_COL_DP, smem_desc_sw128(va + k * 32, 0, 1024), smem_desc_sw128(doa + k * 32, 0, 1024),
-                       idesc_s, k > 0);
+        umma_ss_x4<2, 2>(tmem + FS_COL_DP, smem_desc_sw128(va, 0, 1024), smem_desc_sw128(doa, 0, 1024), idesc_s, 0);
         umma_commit_ws(dp_full);
         ++lq_d.i, ++n_d;
       };
@@ -758,16 +752,13 @@ __global__ void __maxnreg__(96) bwd_onepass_kernel(const __grid_constant__ Strea
           const uint32_t ps = lp.slot(2);
           const uint64_t pd = smem_desc_sw128(smem_u32(smem + Lay::OFF_P + ps * PTILE), ATOM, 1024);
           const uint64_t dd = smem_desc_sw128(doa, ATOM, 1024);
-#pragma unroll
-          for (int k = 0; k < TR / 16; ++k)  // MN-major: +16 query rows (2048 B) per k step
-            umma_bf16_ws(tmem + FS_COL_DV, pd + 128 * k, dd + 128 * k, idesc_pv, (t | k) != 0);
+          umma_ss_x4<128, 128>(tmem + FS_COL_DV, pd, dd, idesc_pv, t != 0);  // MN-major: +16 query rows (2048 B) per k step
+          umma_ss_x4<128, 128>(tmem + FS_COL_DV, pd + 512, dd + 512, idesc_pv, 1);
           umma_commit_ws(&pp_empty[ps]);  // dV's read of the panel tile (the epilogue arrives too)
           ++lp.i;
         } else {
-#pragma unroll
-          for (int k = 0; k < TR / 16; ++k)
-            umma_bf16_ts_ws(tmem + FS_COL_DV, tmem + FS_COL_P + 8 * k, smem_desc_sw128(doa + k * 2048, ATOM, 1024),
-                            idesc_ts, (t | k) != 0);
+          umma_ts_x4<128>(tmem + FS_COL_DV, tmem + FS_COL_P, smem_desc_sw128(doa, ATOM, 1024), idesc_ts, t != 0);
+          umma_ts_x4<128>(tmem + FS_COL_DV, tmem + FS_COL_P + 32, smem_desc_sw128(doa + 8192, ATOM, 1024), idesc_ts, 1);
           umma_commit_ws(p_empty);
         }
         ++lq_v.i, ++n_p;
@@ -777,19 +768,18 @@ __global__ void __maxnreg__(96) bwd_onepass_kernel(const __grid_constant__ Strea
         mbar_wait(ds_full, n_ds & 1);
         tc_fence_after();
         const uint32_t qa = smem_u32(smem + FS_OFF_ST + s * STAGE);
-#pragma unroll
-        for (int k = 0; k < TR / 16; ++k)
-          umma_bf16_ts_ws(tmem + FS_COL_DK, tmem + FS_COL_DSQ + 8 * k, smem_desc_sw128(qa + k * 2048, ATOM, 1024),
-                          idesc_ts, (t | k) != 0);
+        umma_ts_x4<128>(tmem + FS_COL_DK, tmem + FS_COL_DSQ, smem_desc_sw128(qa, ATOM, 1024), idesc_ts, t != 0);
+        umma_ts_x4<128>(tmem + FS_COL_DK, tmem + FS_COL_DSQ + 32, smem_desc_sw128(qa + 8192, ATOM, 1024), idesc_ts, 1);
         umma_commit_ws(&ld_empty[s]);  // the stage's last readers: dK (Q), dV (dO'), the epilogue (m, D')
         ++lq_k.i, ++n_ds;
       };
       auto issue_dq = [&]() {  // dQ_part = dS K (A = the smem dS tile) over dS^T, which dK has read
         if (!(p.dbg & 4)) {
-#pragma unroll
-          for (int k = 0; k < TK / 16; ++k)  // 16 keys per product: two 8-key groups of dS, 2 KB of K
-            umma_bf16_ws(tmem + FS_COL_DSQ, smem_desc_sw128(dsa + k * 4096, 1024, 2048),
-                         smem_desc_sw128(ka + k * 2048, ATOM, 1024), idesc_dq, k > 0);
+          // 16 keys per product: two 8-key groups of dS (4 KB), 2 KB of K
+          umma_ss_x4<256, 128>(tmem + FS_COL_DSQ, smem_desc_sw128(dsa, 1024, 2048), smem_desc_sw128(ka, ATOM, 1024),
+                               idesc_dq, 0);
+          umma_ss_x4<256, 128>(tmem + FS_COL_DSQ, smem_desc_sw128(dsa + 16384, 1024, 2048),
+                               smem_desc_sw128(ka + 8192, ATOM, 1024), idesc_dq, 1);
         }
         umma_commit_ws(dq_full);
       };

@@ -260,6 +260,53 @@ __device__ __forceinline__ void umma_bf16_ts_ws(uint32_t d_tmem, uint32_t a_tmem
       : "memory");
 }
 
+// Four K steps of one product from one elected lane: D (+)= sum_k A_k B_k with the shared-memory
+// descriptors advanced by k * AS and k * BS (16-byte units) in their low word -- the start
+// address field, which these tiles never carry out of -- so the issuing warp spends one 32-bit
+// add per descriptor per step instead of rebuilding 64-bit descriptors around every MMA.
+template <uint32_t AS, uint32_t BS>
+__device__ __forceinline__ void umma_ss_x4(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t.reg .b32 al, ah, bl, bh;\n\t.reg .b64 a, b;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 t, %5, 0;\n\t"
+      "mov.b64 {al, ah}, %1;\n\t"
+      "mov.b64 {bl, bh}, %2;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "add.u32 al, al, %6;\n\tadd.u32 bl, bl, %7;\n\tmov.b64 a, {al, ah};\n\tmov.b64 b, {bl, bh};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+      "add.u32 al, al, %6;\n\tadd.u32 bl, bl, %7;\n\tmov.b64 a, {al, ah};\n\tmov.b64 b, {bl, bh};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+      "add.u32 al, al, %6;\n\tadd.u32 bl, bl, %7;\n\tmov.b64 a, {al, ah};\n\tmov.b64 b, {bl, bh};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(1u), "n"(AS), "n"(BS)
+      : "memory");
+}
+
+// The TS form of umma_ss_x4: A from TMEM at a_tmem + 8k columns (K = 16 bf16 per step), B as above.
+template <uint32_t BS>
+__device__ __forceinline__ void umma_ts_x4(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t.reg .b32 ta, bl, bh;\n\t.reg .b64 b;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 t, %5, 0;\n\t"
+      "mov.b64 {bl, bh}, %2;\n\t"
+      "mov.b32 ta, %1;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "add.u32 ta, ta, 8;\n\tadd.u32 bl, bl, %6;\n\tmov.b64 b, {bl, bh};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, t;\n\t"
+      "add.u32 ta, ta, 8;\n\tadd.u32 bl, bl, %6;\n\tmov.b64 b, {bl, bh};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, t;\n\t"
+      "add.u32 ta, ta, 8;\n\tadd.u32 bl, bl, %6;\n\tmov.b64 b, {bl, bh};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, t;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(1u), "n"(BS)
+      : "memory");
+}
+
 __device__ __forceinline__ void umma_commit_ws(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
