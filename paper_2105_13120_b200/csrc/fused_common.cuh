@@ -289,6 +289,21 @@ inline bool head_map(CUtensorMap* m, const rsa_view& v, const rsa_geom* g, int n
   return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, v.ptr, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+// head_map with 32-row x 32-column boxes, SWIZZLE_64B: one warp's rows x one column half
+// (64-byte rows), for per-warp TMA stores of a 128 x 64 tile.
+inline bool head_map_w32(CUtensorMap* m, const rsa_view& v, const rsa_geom* g, int nrank) {
+  if (!v.ptr || !aligned16(v.ptr)) return fail(RSA_ERR_UNSUPPORTED, "fused: tensor not 16-byte aligned"), false;
+  if (nrank > 1 && g->batch > 1 && v.s_rank != int64_t(g->batch) * v.s_b)
+    return fail(RSA_ERR_UNSUPPORTED, "fused: rank stride must equal B * batch stride"), false;
+  const int64_t sb = (g->batch == 1 && nrank > 1) ? v.s_rank : v.s_b;
+  if (!stride_ok(v.s_row * 2) || !stride_ok(v.s_z * 2) || !stride_ok(sb * 2))
+    return fail(RSA_ERR_UNSUPPORTED, "fused: strides must be multiples of 8 elements"), false;
+  uint64_t dims[4] = {uint64_t(HD), uint64_t(g->chunk), uint64_t(g->heads), uint64_t(g->batch) * nrank};
+  uint64_t str[3] = {uint64_t(v.s_row) * 2, uint64_t(v.s_z) * 2, uint64_t(sb) * 2};
+  uint32_t box[4] = {32, 32, 1, 1};
+  return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, v.ptr, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B);
+}
+
 // [rank][b][z][row][col], col = blk * c + key: 5-D (key, blk, row, z, b*rank).
 inline bool panel_map(CUtensorMap* m, const rsa_view& v, const rsa_geom* g, int nrank, uint32_t box_rows = TR) {
   if (!v.ptr || !aligned16(v.ptr)) return fail(RSA_ERR_UNSUPPORTED, "fused: panel not 16-byte aligned"), false;

@@ -341,14 +341,13 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
     const int half = ((warp - 2) >> 2) & 1;
     const int r = quad * 32 + lane;
     const int et = (threadIdx.x - 64) & 255;         // thread index within the group
-    const bool storer = (lane == 0) && (quad == 2);  // first warp of each (group, half)
     const uint32_t lane_base = (quad * 32u) << 16;
     const uint32_t t_s = tmem + lane_base + gi * (TS ? 128 : 256) + half * 64;
     const uint32_t t_o = tmem + lane_base + (TS ? TS_COL_O + gi * PV_N : gi * 256 + 128);
     const uint32_t xbase = smem_u32(smem + FF_OFF_X) + gi * 3 * 256 * 4;
     const uint32_t ptile = smem_u32(smem + FF_OFF_P + gi * PTILE);
     uint8_t* ptile_gen = smem + FF_OFF_P + gi * PTILE + half * ATOM;
-    const uint32_t bar_rows_id = 6 + gi * 4 + quad, bar_grp_id = 14 + gi;
+    const uint32_t bar_rows_id = 6 + gi * 4 + quad;
     const float sl = p.sl;
     uint32_t sn = 0, pn = 0, un_n = 0;
     bool bad = false, redo = false;
@@ -536,23 +535,28 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
       const float rinv = 1.f / l;
       // TS: l >= every P~ of the row, so l <= 2^FF_HEADROOM is the headroom check (conservative)
       redo |= !(l >= 1.f && l <= (LCHK && !p.rm_exact ? 7.9228162514e28f : 3.402823466e38f));
-      // O -> the group's P~ buffer (atom 0, swizzled like a TMA tile) -> one TMA store
-      if (lane == 0) tma_store_wait_read<0>();  // every warp's last P~ store has left the buffer
-      bar_named(bar_grp_id, 256);
+      // O -> this warp's 32 rows x 32 columns, staged in the first 2 KB of its own P~ rows
+      // (64-byte rows, SWIZZLE_64B) -> one TMA store per warp: no group barrier.  The region's
+      // only other user is this warp's own P~ store (waited for here), and the P~V products
+      // that read it (non-TS form) are complete: o_full.
+      if (lane == 0) tma_store_wait_read<0>();
+      __syncwarp();
+      {
+        uint8_t* ostg = ptile_gen + quad * 4096;
+        const uint32_t orow = smem_u32(ostg) + lane * 64, osw = (lane >> 1) & 3;
 #pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4)
-        st_shared_v4(ptile + sw128_offset(r, half * 4 + q4), pack_bf16(o[8 * q4] * rinv, o[8 * q4 + 1] * rinv),
-                     pack_bf16(o[8 * q4 + 2] * rinv, o[8 * q4 + 3] * rinv),
-                     pack_bf16(o[8 * q4 + 4] * rinv, o[8 * q4 + 5] * rinv),
-                     pack_bf16(o[8 * q4 + 6] * rinv, o[8 * q4 + 7] * rinv));
-      fence_proxy_async_smem();
-      bar_named(bar_grp_id, 256);
-      if (storer && half == 0) {
-        tma_store_4d(&p.to, smem + FF_OFF_P + gi * PTILE, 0, rt * TR, z, d * g.B + b);
-        tma_store_commit();
-        tma_store_wait_read<0>();  // other warps' next P~ rows go into this atom
+        for (int q4 = 0; q4 < 4; ++q4)
+          st_shared_v4(orow + ((q4 ^ osw) << 4), pack_bf16(o[8 * q4] * rinv, o[8 * q4 + 1] * rinv),
+                       pack_bf16(o[8 * q4 + 2] * rinv, o[8 * q4 + 3] * rinv),
+                       pack_bf16(o[8 * q4 + 4] * rinv, o[8 * q4 + 5] * rinv),
+                       pack_bf16(o[8 * q4 + 6] * rinv, o[8 * q4 + 7] * rinv));
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_4d(&p.to, ostg, half * 32, rt * TR + int(quad) * 32, z, d * g.B + b);
+          tma_store_commit();
+        }
       }
-      bar_named(bar_grp_id, 256);
       if (row < g.c && half == 0) {
         p.rowscale[ridx] = rinv;
         if (EXT && p.rowmax && !p.rowmax_in) p.rowmax[ridx] = msl;
@@ -608,7 +612,7 @@ int ff_launch(FfArgs& a, const rsa_geom* g, rsa_view q, rsa_view panel, rsa_view
   if (!a.no_panel && key_chunk(g) != g->chunk)
     return fail(RSA_ERR_INVALID, "rsa_fwd_factored_ex: a panel needs key_chunk == chunk");
   if (!head_map(&a.tq, q, g, g->n_rank) || (!a.no_panel && !panel_map(&a.tp, panel, g, g->n_rank, 32)) ||
-      (final_hop && !head_map(&a.to, o_out, g, g->n_rank)))
+      (final_hop && !head_map_w32(&a.to, o_out, g, g->n_rank)))
     return RSA_ERR_UNSUPPORTED;
   if (a.no_panel) a.tp = a.tq;  // never used; keeps the prefetch harmless
   if (!final_hop) a.to = a.tq;
