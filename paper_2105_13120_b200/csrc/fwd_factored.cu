@@ -82,6 +82,9 @@ constexpr int FF_THREADS = 32 * (FF_PV_WARP + 1);       // 608
 #ifndef FF_PANEL_TS
 #define FF_PANEL_TS 1  // panel forward: P~V from a TMEM copy of P~ (TS form); the smem tile only feeds the store
 #endif
+#ifndef FF_DEFER
+#define FF_DEFER 1  // a unit's O readout deferred into the next unit's first step (unit_end)
+#endif
 #ifndef FF_KSTAGES
 #define FF_KSTAGES 4
 #endif
@@ -352,134 +355,19 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
     uint32_t sn = 0, pn = 0, un_n = 0;
     bool bad = false, redo = false;
     const uint64_t pol = l2_evict_first();
-    for (int u = u_begin; u < u_end; ++u) {
-      const Unit un = unit_of(u, UH, NQ);
-      if (int(gi) >= un.n) continue;
-      const int b = un.bz / g.Z, z = un.bz % g.Z;
-      const int qi = un.qi0 + gi, d = qi / nrt, rt = qi % nrt;
+    // DEFER (TS form, row sums from the ones block): the previous unit's end waits for the
+    // next unit's first exp2 (unit_end)
+    constexpr bool DEFER = TS && FF_ONES && FF_DEFER;
+    bool pend = false;
+    int pd_ = 0, pb_ = 0, pz_ = 0, prt_ = 0;
+    float pmsl_ = 0.f;
+    uint32_t ux = 0;  // units begun: parity of the row-max exchange slot
+    // A unit's end: O = O~ / l and r = 1 / l once its last P~ V has landed (o_full), then the
+    // per-warp O store.  DEFER: run during the NEXT unit's first step, after that step's
+    // exp2 and before its P~ store (which frees O~ for the next unit), so the epilogue does
+    // not sit idle while the last P~ V products of the unit drain.
+    auto unit_end = [&](int d, int b, int z, int rt, float msl, float lsum) {
       const int row = rt * TR + r;
-      FF_TRACE(1);
-      // tile 0: raw max and min (the reference point); later tiles: max |s| only, which
-      // bounds the row max (headroom check) and is finite iff every score is
-      float m = -INFINITY, mi = INFINITY, am = 0.f, msl = 0.f;
-      if (EXT && p.rowmax_in)
-        msl = row < g.c ? __ldg(p.rowmax_in + ((int64_t(d * g.B + b) * g.Z + z) * g.c + row) * p.rm_stride) : 0.f;
-#if !FF_ONES
-      float lsum = 0.f;  // this thread's share of sum_k P~[row, k] over the bf16 values stored
-#endif
-      int jo = 0, k0 = 0;
-      for (int t = 0; t < T; ++t) {
-        const int nvalid = min(TK, ck - k0) - half * 64;
-        uint32_t w[32];
-        mbar_wait(&s_full[gi], sn & 1);
-        FF_TRACE(3);
-        tc_fence_after();
-        __syncwarp();
-        if (t == 0 && !(EXT && p.rowmax_in)) {  // first key tile: its row max is the reference
-          float v[64];
-          tmem_ld32(t_s, v);
-          tmem_ld32(t_s + 32, v + 32);
-          tmem_ld_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&s_empty[gi]);
-          minmax32(v, nvalid, m, mi);
-          minmax32(v + 32, nvalid - 32, m, mi);
-          const uint32_t slot = xbase + (un_n & 1) * 256 * 4;  // combine the two column halves
-          asm volatile("st.shared.f32 [%0], %1;" ::"r"(slot + et * 4), "f"(m) : "memory");
-          bar_named(bar_rows_id, 64);
-          float o;
-          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(slot + ((et + 128) & 255) * 4) : "memory");
-          const float mref = fmaxf(m, o);
-          msl = (mref == -INFINITY || !(fabsf(mref) <= 3.402823466e38f)) ? 0.f : mref * sl;
-          exp2_pack32(v, nvalid, sl, msl, w);
-          exp2_pack32(v + 32, nvalid - 32, sl, msl, w + 16);
-        } else if (LCHK && FF_TS_LD2) {  // both chunks in flight, then S is free before any exp2
-          float v[64];
-          tmem_ld32(t_s, v);
-          tmem_ld32(t_s + 32, v + 32);
-          tmem_ld_wait();
-          FF_TRACE(40);
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&s_empty[gi]);
-          FF_TRACE(41);
-#pragma unroll
-          for (int cc = 0; cc < 2; ++cc) {
-            // no per-score check: the row sum l bounds every P~ (headroom) and is non-finite
-            // iff a score is +inf / NaN; -inf scores come only from non-finite keys, which
-            // rsa_fwd_factored_ex scans for before the launch (k_scan_kernel)
-            exp2_pack32(v + cc * 32, nvalid - cc * 32, sl, msl, w + cc * 16);
-          }
-        } else {
-#pragma unroll
-          for (int cc = 0; cc < 2; ++cc) {  // two 32-column chunks (register budget of 18 warps)
-            float v[32];
-            tmem_ld32(t_s + cc * 32, v);
-            tmem_ld_wait();
-            FF_TRACE(40 + cc);
-            if (cc == 1) {  // both chunks are in registers: free S for the next key tile
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&s_empty[gi]);
-            }
-            if (FF_ABSMAX) absmax32(v, nvalid - cc * 32, am);
-            else minmax32(v, nvalid - cc * 32, m, mi);
-            exp2_pack32(v, nvalid - cc * 32, sl, msl, w + cc * 16);
-          }
-        }
-        ++sn;
-#if !FF_ONES
-#pragma unroll
-        for (int e = 0; e < 32; ++e) lsum += __uint_as_float(w[e] << 16) + __uint_as_float(w[e] & 0xFFFF0000u);
-#endif
-        FF_TRACE(4);
-        if (TS) {  // P~ -> the shared TMEM buffer once the previous user's P~ V has read it
-          mbar_wait(&p_empty[gi], pn & 1);
-          FF_TRACE(5);
-          tc_fence_after();
-          tmem_st32(tmem + lane_base + TS_COL_P + half * 32, w);
-          tmem_st_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&p_full[gi]);
-          FF_TRACE(6);
-          ++pn;
-          if (NOPANEL) {
-            if (k0 + TK >= ck) k0 = 0, ++jo;
-            else k0 += TK;
-            continue;
-          }
-        } else {
-          mbar_wait(&p_empty[gi], (pn & 1) ^ 1);  // the previous P~ V product has read the tile
-          FF_TRACE(5);
-        }
-        // Each warp stores its own 32 rows x 64 keys (4 KB, 1024-byte aligned, so the
-        // 128-byte swizzle pattern is the tile's): no cross-warp barrier on this path.
-        if (lane == 0) tma_store_wait_read<0>();  // this warp's previous store has read its rows
-        __syncwarp();
-#pragma unroll
-        for (int q4 = 0; q4 < 8; ++q4)
-          st_shared_v4(ptile + half * ATOM + sw128_offset(r, q4), w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2],
-                       w[4 * q4 + 3]);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          if (!TS) mbar_arrive(&p_full[gi]);  // TS: the P~V product reads TMEM, the tile only feeds the store
-          if (nvalid > 0 && !NOPANEL)  // the panel is read back only by the backward: evict-first in L2
-            tma_store_5d_hint(&p.tp, ptile_gen + quad * 4096, k0 + half * 64, g.org_lo + jo, rt * TR + quad * 32, z,
-                              d * g.B + b, pol);
-          tma_store_commit();
-        }
-        FF_TRACE(6);
-        if (!TS) ++pn;
-        if (k0 + TK >= ck) k0 = 0, ++jo;
-        else k0 += TK;
-      }
-      if (!(m == -INFINITY && mi == INFINITY))  // this thread saw at least one valid key in tile 0
-        bad |= !(fabsf(m) <= 3.402823466e38f) || !(fabsf(mi) <= 3.402823466e38f);
-      bad |= !(am <= 3.402823466e38f);
-      if (!LCHK && !(EXT && p.rm_exact)) redo |= (FF_ABSMAX ? am : m) * sl - msl > FF_HEADROOM;  // |s| >= s: conservative
       // ---- O = O~ / l, r = 1 / l (l >= 1 unless the row needs the fallback)
       mbar_wait(&o_full[gi], un_n & 1);
       FF_TRACE(7);
@@ -530,7 +418,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
           }
         }
         FF_TRACE(21);
-        continue;
+        return;
       }
       const float rinv = 1.f / l;
       // TS: l >= every P~ of the row, so l <= 2^FF_HEADROOM is the headroom check (conservative)
@@ -562,7 +450,151 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
         if (EXT && p.rowmax && !p.rowmax_in) p.rowmax[ridx] = msl;
       }
       FF_TRACE(21);
+    };
+    for (int u = u_begin; u < u_end; ++u) {
+      const Unit un = unit_of(u, UH, NQ);
+      if (int(gi) >= un.n) continue;
+      const int b = un.bz / g.Z, z = un.bz % g.Z;
+      const int qi = un.qi0 + gi, d = qi / nrt, rt = qi % nrt;
+      const int row = rt * TR + r;
+      FF_TRACE(1);
+      // tile 0: raw max and min (the reference point); later tiles: max |s| only, which
+      // bounds the row max (headroom check) and is finite iff every score is
+      float m = -INFINITY, mi = INFINITY, am = 0.f, msl = 0.f;
+      if (EXT && p.rowmax_in)
+        msl = row < g.c ? __ldg(p.rowmax_in + ((int64_t(d * g.B + b) * g.Z + z) * g.c + row) * p.rm_stride) : 0.f;
+#if !FF_ONES
+      float lsum = 0.f;  // this thread's share of sum_k P~[row, k] over the bf16 values stored
+#endif
+      int jo = 0, k0 = 0;
+      for (int t = 0; t < T; ++t) {
+        const int nvalid = min(TK, ck - k0) - half * 64;
+        uint32_t w[32];
+        mbar_wait(&s_full[gi], sn & 1);
+        FF_TRACE(3);
+        tc_fence_after();
+        __syncwarp();
+        if (t == 0 && !(EXT && p.rowmax_in)) {  // first key tile: its row max is the reference
+          float v[64];
+          tmem_ld32(t_s, v);
+          tmem_ld32(t_s + 32, v + 32);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_empty[gi]);
+          minmax32(v, nvalid, m, mi);
+          minmax32(v + 32, nvalid - 32, m, mi);
+          const uint32_t slot = xbase + (ux & 1) * 256 * 4;  // combine the two column halves
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(slot + et * 4), "f"(m) : "memory");
+          bar_named(bar_rows_id, 64);
+          float o;
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(slot + ((et + 128) & 255) * 4) : "memory");
+          const float mref = fmaxf(m, o);
+          msl = (mref == -INFINITY || !(fabsf(mref) <= 3.402823466e38f)) ? 0.f : mref * sl;
+          exp2_pack32(v, nvalid, sl, msl, w);
+          exp2_pack32(v + 32, nvalid - 32, sl, msl, w + 16);
+        } else if (LCHK && FF_TS_LD2) {  // both chunks in flight, then S is free before any exp2
+          float v[64];
+          tmem_ld32(t_s, v);
+          tmem_ld32(t_s + 32, v + 32);
+          tmem_ld_wait();
+          FF_TRACE(40);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_empty[gi]);
+          FF_TRACE(41);
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            // no per-score check: the row sum l bounds every P~ (headroom) and is non-finite
+            // iff a score is +inf / NaN; -inf scores come only from non-finite keys, which
+            // rsa_fwd_factored_ex scans for before the launch (k_scan_kernel)
+            exp2_pack32(v + cc * 32, nvalid - cc * 32, sl, msl, w + cc * 16);
+          }
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {  // two 32-column chunks (register budget of 18 warps)
+            float v[32];
+            tmem_ld32(t_s + cc * 32, v);
+            tmem_ld_wait();
+            FF_TRACE(40 + cc);
+            if (cc == 1) {  // both chunks are in registers: free S for the next key tile
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&s_empty[gi]);
+            }
+            if (FF_ABSMAX) absmax32(v, nvalid - cc * 32, am);
+            else minmax32(v, nvalid - cc * 32, m, mi);
+            exp2_pack32(v, nvalid - cc * 32, sl, msl, w + cc * 16);
+          }
+        }
+        ++sn;
+#if !FF_ONES
+#pragma unroll
+        for (int e = 0; e < 32; ++e) lsum += __uint_as_float(w[e] << 16) + __uint_as_float(w[e] & 0xFFFF0000u);
+#endif
+        FF_TRACE(4);
+        if (DEFER && t == 0 && pend) {  // the previous unit's O~ is read out before this P~ V can overwrite it
+          pend = false;
+          unit_end(pd_, pb_, pz_, prt_, pmsl_, 0.f);
+        }
+        if (TS) {  // P~ -> the shared TMEM buffer once the previous user's P~ V has read it
+          mbar_wait(&p_empty[gi], pn & 1);
+          FF_TRACE(5);
+          tc_fence_after();
+          tmem_st32(tmem + lane_base + TS_COL_P + half * 32, w);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[gi]);
+          FF_TRACE(6);
+          ++pn;
+          if (NOPANEL) {
+            if (k0 + TK >= ck) k0 = 0, ++jo;
+            else k0 += TK;
+            continue;
+          }
+        } else {
+          mbar_wait(&p_empty[gi], (pn & 1) ^ 1);  // the previous P~ V product has read the tile
+          FF_TRACE(5);
+        }
+        // Each warp stores its own 32 rows x 64 keys (4 KB, 1024-byte aligned, so the
+        // 128-byte swizzle pattern is the tile's): no cross-warp barrier on this path.
+        if (lane == 0) tma_store_wait_read<0>();  // this warp's previous store has read its rows
+        __syncwarp();
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4)
+          st_shared_v4(ptile + half * ATOM + sw128_offset(r, q4), w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2],
+                       w[4 * q4 + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (!TS) mbar_arrive(&p_full[gi]);  // TS: the P~V product reads TMEM, the tile only feeds the store
+          if (nvalid > 0 && !NOPANEL)  // the panel is read back only by the backward: evict-first in L2
+            tma_store_5d_hint(&p.tp, ptile_gen + quad * 4096, k0 + half * 64, g.org_lo + jo, rt * TR + quad * 32, z,
+                              d * g.B + b, pol);
+          tma_store_commit();
+        }
+        FF_TRACE(6);
+        if (!TS) ++pn;
+        if (k0 + TK >= ck) k0 = 0, ++jo;
+        else k0 += TK;
+      }
+      if (!(m == -INFINITY && mi == INFINITY))  // this thread saw at least one valid key in tile 0
+        bad |= !(fabsf(m) <= 3.402823466e38f) || !(fabsf(mi) <= 3.402823466e38f);
+      bad |= !(am <= 3.402823466e38f);
+      if (!LCHK && !(EXT && p.rm_exact)) redo |= (FF_ABSMAX ? am : m) * sl - msl > FF_HEADROOM;  // |s| >= s: conservative
+      ++ux;
+      if (DEFER) {
+        pend = true, pd_ = d, pb_ = b, pz_ = z, prt_ = rt, pmsl_ = msl;  // (DEFER implies FF_ONES: no lsum)
+      } else {
+#if FF_ONES
+        unit_end(d, b, z, rt, msl, 0.f);
+#else
+        unit_end(d, b, z, rt, msl, lsum);
+#endif
+      }
     }
+    if (DEFER && pend) unit_end(pd_, pb_, pz_, prt_, pmsl_, 0.f);
     if (p.flag && (bad || redo)) atomicOr(p.flag, (bad ? 1 : 0) | (redo ? 2 : 0));
     if (lane == 0) tma_store_wait_all<0>();
   }
