@@ -143,10 +143,20 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
   // bounds the rest; the panel forward in TS form keeps the max|s| check
   constexpr bool LCHK = TS && EXT;
   constexpr bool NOPANEL = TS && EXT;  // ff_launch picks <true, true> exactly for p.no_panel
+  // Q stages per group: stream mode has no panel to stage, so the second half of each group's
+  // P~ tile holds a second Q stage -- the next unit's Q loads while this unit runs (the O
+  // staging moves to the first half).  A Q tile from a busy HBM takes ~7 k clk, which a unit
+  // of few key tiles (Linformer's K' = 256 keys: two) does not cover.
+  constexpr int QS = NOPANEL ? 2 : FF_QST;
+  auto q_off = [](int qx) -> uint32_t {  // qx = group * QS + stage
+    if (QS == FF_QST) return FF_OFF_Q + qx * TILE;
+    const int gq = qx / QS, sq = qx % QS;
+    return sq < FF_QST ? FF_OFF_Q + (gq * FF_QST + sq) * TILE : FF_OFF_P + gq * PTILE + ATOM;
+  };
   uint8_t* smem = smem_base();
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FF_OFF_BAR);
-  uint64_t *q_full = bar, *q_empty = q_full + 2 * FF_QST;  // [group][stage]
-  uint64_t *k_full = q_empty + 2 * FF_QST, *k_empty = k_full + FF_KST;
+  uint64_t *q_full = bar, *q_empty = q_full + 2 * QS;  // [group][stage]
+  uint64_t *k_full = q_empty + 2 * QS, *k_empty = k_full + FF_KST;
   uint64_t *v_full = k_empty + FF_KST, *v_empty = v_full + FF_VST;
   uint64_t *s_full = v_empty + FF_VST, *s_empty = s_full + 2;
   uint64_t *p_full = s_empty + 2, *p_empty = p_full + 2;
@@ -176,7 +186,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
-      for (int q = 0; q < FF_QST; ++q) mbar_init(&q_full[s * FF_QST + q], 1), mbar_init(&q_empty[s * FF_QST + q], 1);
+      for (int q = 0; q < QS; ++q) mbar_init(&q_full[s * QS + q], 1), mbar_init(&q_empty[s * QS + q], 1);
       mbar_init(&s_full[s], 1), mbar_init(&s_empty[s], 8);
       mbar_init(&p_full[s], 8), mbar_init(&p_empty[s], 1);
       mbar_init(&o_full[s], 1), mbar_init(&o_empty[s], 8);
@@ -222,10 +232,10 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
         const int b = un.bz / g.Z, z = un.bz % g.Z;
         for (int gi = 0; gi < un.n; ++gi) {
           const int qi = un.qi0 + gi, d = qi / nrt, rt = qi % nrt;
-          const int qx = gi * FF_QST + int(qn[gi] % FF_QST);
-          mbar_wait(&q_empty[qx], ((qn[gi] / FF_QST) & 1) ^ 1);
+          const int qx = gi * QS + int(qn[gi] % QS);
+          mbar_wait(&q_empty[qx], ((qn[gi] / QS) & 1) ^ 1);
           mbar_arrive_expect_tx(&q_full[qx], TILE);
-          tma_load_4d(smem + FF_OFF_Q + qx * TILE, &p.tq, &q_full[qx], 0, rt * TR, z, d * g.B + b);
+          tma_load_4d(smem + q_off(qx), &p.tq, &q_full[qx], 0, rt * TR, z, d * g.B + b);
           ++qn[gi];
         }
         if (kres && un.bz != prev_bz) {
@@ -269,7 +279,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
       // resident K: release the slots after the unit's last S unless the next unit reuses them
       const bool k_release = kres && u + 1 < u_end && unit_of(u + 1, UH, NQ).bz != un.bz;
       for (int gi = 0; gi < un.n; ++gi)
-        mbar_wait(&q_full[gi * FF_QST + qn[gi] % FF_QST], (qn[gi] / FF_QST) & 1);
+        mbar_wait(&q_full[gi * QS + qn[gi] % QS], (qn[gi] / QS) & 1);
       // S(g) = Q_g K_t^T for both query tiles of the unit from one K tile
       auto issue_s = [&](int t) {
         const bool last = t + 1 == T;
@@ -279,14 +289,14 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
         for (int gi = 0; gi < un.n; ++gi) {
           mbar_wait(&s_empty[gi], (sn[gi] & 1) ^ 1);
           tc_fence_after();
-          const uint32_t qa = smem_u32(smem + FF_OFF_Q + (gi * FF_QST + qn[gi] % FF_QST) * TILE);
+          const uint32_t qa = smem_u32(smem + q_off(gi * QS + qn[gi] % QS));
 #pragma unroll
           for (int k = 0; k < HD / 16; ++k)
             umma_bf16_ws(tmem + gi * (TS ? 128 : 256), smem_desc_sw128(qa + k * 32, 0, 1024),
                          smem_desc_sw128(ka + k * 32, 0, 1024), idesc_s, k > 0);
           umma_commit_ws(&s_full[gi]);
           FF_TRACE(10 + gi);
-          if (last) umma_commit_ws(&q_empty[gi * FF_QST + qn[gi] % FF_QST]), ++qn[gi];
+          if (last) umma_commit_ws(&q_empty[gi * QS + qn[gi] % QS]), ++qn[gi];
           ++sn[gi];
         }
         if (!kres) umma_commit_ws(&k_empty[ks]), ++kq.i;
@@ -430,7 +440,8 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
       if (lane == 0) tma_store_wait_read<0>();
       __syncwarp();
       {
-        uint8_t* ostg = ptile_gen + quad * 4096;
+        // (stream mode: the first half of the P~ tile, 2 KB per warp; the second half is a Q stage)
+        uint8_t* ostg = NOPANEL ? smem + FF_OFF_P + gi * PTILE + (half * 4 + quad) * 2048 : ptile_gen + quad * 4096;
         const uint32_t orow = smem_u32(ostg) + lane * 64, osw = (lane >> 1) & 3;
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4)
