@@ -37,7 +37,8 @@ namespace {
 constexpr int MAX_QT = 4;  // query tiles per head that fit the dQ columns of TMEM
 
 struct BwdArgs {
-  CUtensorMap tq, tk, tv, tdo, tp, tdk, tdv;
+  CUtensorMap tq, tk, tv, tdo, tp, tdk, tdv, tdq;
+  int dq_tma;  // bf16 dQ only: each query tile staged (BF_OFF_DQS) and TMA-stored
   int kv_tma;  // bf16, non-accumulating dK/dV: staged in the retiring P slot and TMA-stored
   int peer;    // K / V of origin j from pm.k[j] / pm.v[j] (rsa_bwd_fused_peer)
   PeerMaps pm;
@@ -59,13 +60,29 @@ struct BwdArgs {
 // Ring depths.  Each operand is released as soon as its last MMA has read it
 // (dO after P^T dO, V after the key tile's last dO V^T, Q / P / K after the
 // dS products), so the producer runs 1-2 steps ahead of the tensor pipe.
-constexpr int BF_DO = 2, BF_Q = 2, BF_P = 3, BF_K = 2, BF_V = 2;
+#ifndef BF_RDO  // ring depths (experiments: -DBF_RDO=.. -DBF_RQ=.. -DBF_RP=.. -DBF_RK=.. -DBF_RV=..)
+#define BF_RDO 2
+#endif
+#ifndef BF_RQ
+#define BF_RQ 2
+#endif
+#ifndef BF_RP
+#define BF_RP 3
+#endif
+#ifndef BF_RK
+#define BF_RK 2
+#endif
+#ifndef BF_RV
+#define BF_RV 1  // one V tile: V is read by one product per step (dO V^T), and a second slot measured +-0
+#endif
+constexpr int BF_DO = BF_RDO, BF_Q = BF_RQ, BF_P = BF_RP, BF_K = BF_RK, BF_V = BF_RV;
 constexpr uint32_t BF_OFF_DO = 0;
 constexpr uint32_t BF_OFF_Q = BF_OFF_DO + BF_DO * TILE;
 constexpr uint32_t BF_OFF_K = BF_OFF_Q + BF_Q * TILE;
 constexpr uint32_t BF_OFF_V = BF_OFF_K + BF_K * TILE;
 constexpr uint32_t BF_OFF_P = BF_OFF_V + BF_V * TILE;  // [slot] P, then dS in place
-constexpr uint32_t BF_OFF_BAR = BF_OFF_P + BF_P * PTILE;
+constexpr uint32_t BF_OFF_DQS = BF_OFF_P + BF_P * PTILE;  // dQ staging: 2 KB per epilogue warp (32 x 32 bf16, SWIZZLE_64B)
+constexpr uint32_t BF_OFF_BAR = BF_OFF_DQS + TILE;
 constexpr uint32_t BF_SMEM = BF_OFF_BAR + 512 + 1024;
 static_assert(BF_SMEM <= 232448, "bwd_fused smem over the sm_100 per-CTA limit");
 
@@ -110,6 +127,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
     fence_barrier_init();
     tma_prefetch(&p.tq), tma_prefetch(&p.tk), tma_prefetch(&p.tv), tma_prefetch(&p.tdo), tma_prefetch(&p.tp);
     if (p.kv_tma) tma_prefetch(&p.tdk), tma_prefetch(&p.tdv);
+    if (p.dq_tma) tma_prefetch(&p.tdq);
   }
   tc_fence_before();
   __syncthreads();
@@ -336,8 +354,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
       if (lane == 0) mbar_arrive(&dq_empty[qqt]);
 #pragma unroll
       for (int e = 0; e < 32; ++e) o[e] *= g.scale;
-      if (qrow < g.c) store_row32(p.dq_acc, p.dq_out, p.accumulate_dq, qd, qb, qz, qrow, half * 32, o);
       q_on = false;
+      if (p.dq_tma) {  // this warp's 32 rows x 32 columns through its own 2 KB of staging: one TMA store
+        uint8_t* stg = smem + BF_OFF_DQS + (warp - 2) * 2048;
+        const uint32_t srow = smem_u32(stg) + lane * 64, sw = (lane >> 1) & 3;
+        if (lane == 0) tma_store_wait_read<0>();  // this warp's previous dQ store has read it
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          st_shared_v4(srow + ((j ^ sw) << 4), pack_bf16(o[8 * j], o[8 * j + 1]), pack_bf16(o[8 * j + 2], o[8 * j + 3]),
+                       pack_bf16(o[8 * j + 4], o[8 * j + 5]), pack_bf16(o[8 * j + 6], o[8 * j + 7]));
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_4d(&p.tdq, stg, half * 32, qrow - int(lane), qz, qd * g.B + qb);
+          tma_store_commit();
+        }
+        return;
+      }
+      if (qrow < g.c) store_row32(p.dq_acc, p.dq_out, p.accumulate_dq, qd, qb, qz, qrow, half * 32, o);
     };
     auto load_d = [&](int it, float* out) {  // D of this thread's rows of head `it`
       const int hb = it / g.Z, hz = it % g.Z;
@@ -443,6 +478,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_fused_kernel(const __grid_con
     if (rel_pending && threadIdx.x == 64) mbar_arrive(&rp.empty[rel_slot]);
     if (p.kv_tma && threadIdx.x == 64) tma_store_wait_all<0>();
     if (q_on) flush_q();
+    if (p.dq_tma && lane == 0) tma_store_wait_all<0>();  // this warp's dQ stores have left shared memory
   }
   tc_fence_before();
   __syncthreads();
@@ -484,6 +520,7 @@ int rsa_bwd_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_vie
   a.dkv_bf16 = dkv_dtype == RSA_BF16;
   a.accumulate_dkv = accumulate_dkv;
   a.kv_tma = dkv_dtype == RSA_BF16 && head_map(&a.tdk, dk, g, g->n_org) && head_map(&a.tdv, dv, g, g->n_org);
+  a.dq_tma = !dq_acc.ptr && dq_out.ptr && head_map_w32(&a.tdq, dq_out, g, g->n_rank);
   static long long* trace_buf = nullptr;
   const char* trace_path = getenv("RSA_BF_TRACE");
   if (trace_path) {
