@@ -23,7 +23,7 @@
 //
 // Warp roles (10 warps): warp 0 TMA producer, warp 1 tcgen05.mma issuer
 // (owns TMEM), warps 2..9 epilogue (warp w reads TMEM lanes 32*(w%4)..,
-// column half (w-2)/4).  Rings: K, V, dO, Q tiles 2 deep each, panel
+// column half (w-2)/4).  Rings: K, dO, Q tiles 2 deep each, V 1 deep, panel
 // tiles 3 deep (the only HBM stream that matters; dO/Q re-reads are L2 hits).  dS overwrites P in place once P^T dO has consumed it.
 #include <cstdio>
 #include <cstdlib>
