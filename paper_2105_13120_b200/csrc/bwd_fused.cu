@@ -520,7 +520,10 @@ int rsa_bwd_fused(const rsa_geom* g, rsa_view q, rsa_view k, rsa_view v, rsa_vie
   a.dkv_bf16 = dkv_dtype == RSA_BF16;
   a.accumulate_dkv = accumulate_dkv;
   a.kv_tma = dkv_dtype == RSA_BF16 && head_map(&a.tdk, dk, g, g->n_org) && head_map(&a.tdv, dv, g, g->n_org);
-  a.dq_tma = !dq_acc.ptr && dq_out.ptr && head_map_w32(&a.tdq, dq_out, g, g->n_rank);
+  // (the layouts head_map_w32 accepts, checked first so a fallback leaves no error message)
+  a.dq_tma = !dq_acc.ptr && dq_out.ptr &&
+             !(g->n_rank > 1 && g->batch > 1 && dq_out.s_rank != int64_t(g->batch) * dq_out.s_b) &&
+             head_map_w32(&a.tdq, dq_out, g, g->n_rank);
   static long long* trace_buf = nullptr;
   const char* trace_path = getenv("RSA_BF_TRACE");
   if (trace_path) {
