@@ -88,7 +88,10 @@ constexpr int FF_THREADS = 32 * (FF_PV_WARP + 1);       // 608
 #ifndef FF_KSTAGES
 #define FF_KSTAGES 4
 #endif
-constexpr int FF_KST = FF_KSTAGES, FF_VST = FF_ONES ? 2 : 3;
+#ifndef FF_VSTAGES
+#define FF_VSTAGES (FF_ONES ? 2 : 3)
+#endif
+constexpr int FF_KST = FF_KSTAGES, FF_VST = FF_VSTAGES;
 constexpr int PV_N = FF_ONES ? HD + 16 : HD;  // O columns (+ 16 row-sum columns)
 constexpr uint32_t TS_COL_P = 256, TS_COL_O = 320;  // TS form: shared P~ buffer, O~ of group g at +80 g
 static_assert(TS_COL_O + FF_GROUPS * PV_N <= 512, "TS-form TMEM layout over 512 columns");
@@ -367,10 +370,10 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
     const uint64_t pol = l2_evict_first();
     // DEFER (TS form, row sums from the ones block): the previous unit's end waits for the
     // next unit's first exp2 (unit_end)
-    constexpr bool DEFER = TS && FF_ONES && FF_DEFER;
+    constexpr bool DEFER = TS && FF_DEFER;
     bool pend = false;
     int pd_ = 0, pb_ = 0, pz_ = 0, prt_ = 0;
-    float pmsl_ = 0.f;
+    float pmsl_ = 0.f, plsum_ = 0.f;  // plsum_: the pending unit's row-sum share (FF_ONES = 0)
     uint32_t ux = 0;  // units begun: parity of the row-max exchange slot
     // A unit's end: O = O~ / l and r = 1 / l once its last P~ V has landed (o_full), then the
     // per-warp O store.  DEFER: run during the NEXT unit's first step, after that step's
@@ -546,7 +549,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
         FF_TRACE(4);
         if (DEFER && t == 0 && pend) {  // the previous unit's O~ is read out before this P~ V can overwrite it
           pend = false;
-          unit_end(pd_, pb_, pz_, prt_, pmsl_, 0.f);
+          unit_end(pd_, pb_, pz_, prt_, pmsl_, plsum_);
         }
         if (TS) {  // P~ -> the shared TMEM buffer once the previous user's P~ V has read it
           mbar_wait(&p_empty[gi], pn & 1);
@@ -596,7 +599,10 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
       if (!LCHK && !(EXT && p.rm_exact)) redo |= (FF_ABSMAX ? am : m) * sl - msl > FF_HEADROOM;  // |s| >= s: conservative
       ++ux;
       if (DEFER) {
-        pend = true, pd_ = d, pb_ = b, pz_ = z, prt_ = rt, pmsl_ = msl;  // (DEFER implies FF_ONES: no lsum)
+        pend = true, pd_ = d, pb_ = b, pz_ = z, prt_ = rt, pmsl_ = msl;
+#if !FF_ONES
+        plsum_ = lsum;
+#endif
       } else {
 #if FF_ONES
         unit_end(d, b, z, rt, msl, 0.f);
@@ -605,7 +611,7 @@ __global__ void __maxnreg__(96) fwd_factored_kernel(const __grid_constant__ FfAr
 #endif
       }
     }
-    if (DEFER && pend) unit_end(pd_, pb_, pz_, prt_, pmsl_, 0.f);
+    if (DEFER && pend) unit_end(pd_, pb_, pz_, prt_, pmsl_, plsum_);
     if (p.flag && (bad || redo)) atomicOr(p.flag, (bad ? 1 : 0) | (redo ? 2 : 0));
     if (lane == 0) tma_store_wait_all<0>();
   }
